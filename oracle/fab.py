@@ -1,0 +1,106 @@
+"""f(A)b drivers (§3).
+
+  alg4   Algorithm 4 (l.199-209): Alg 2 basis, y by Blendenpik, return
+         ||b|| V_m f(H_m + h_{m+1,m} y e_m^T) e_1
+  ss     Remark 2 (l.249-251): as Alg 4 with y from sketch-and-solve
+         (mathematically sFOM, Eq. (9))
+  alg5   Algorithm 5 (l.219-228): ||b|| V_m f(H_m) e_1, no least squares
+  sfom   the literal Eq. (9) formula (cross-check of `ss`)
+  fom    Eq. (4) with a full Arnoldi basis (the paper's baseline 'Arnoldi')
+  dense  f(A) b formed densely (small n only)
+
+Compression (Eq. (6), l.167-171): V_m^+ A V_m = H_m + h_{m+1,m} (V_m^+ v_{m+1})
+e_m^T, gamma_b = ||b||_2 for Alg 2 (l.172).  f is applied as
+f(alpha C + sigma I) (reading G-17).  Reading G-12: Blendenpik reuses the
+basis sketch Theta (one fab_sketch call), so SV_{m+1} = Theta V_{m+1} feeds
+both the Blendenpik R and sketch-and-solve.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+"""
+import numpy as np
+
+from . import krylov, lsq, matfun
+from .srht import SRHT
+
+MODES = ("blendenpik", "sketch_solve", "none")
+
+
+def compress(dec, SV, mode, lsqr_tol=1e-6, lsqr_iters=None, lsqr_maxit=None):
+    """y and C_m = H_m + h_{m+1,m} y e_m^T from an Alg 2 decomposition."""
+    V, H, m = dec["V"], dec["H"], dec["m_eff"]
+    Hm = H[:m, :m].copy()
+    info = {}
+    if dec["breakdown"] or mode == "none":
+        y = np.zeros(m)
+        R = None
+        if mode != "none" and SV is not None:
+            R, _ = lsq.householder_qr(SV[:, :m])
+    elif mode == "blendenpik":
+        y, R, info = lsq.blendenpik(V[:, :m], V[:, m], SV[:, :m], tol=lsqr_tol,
+                                    maxit=lsqr_maxit, iters=lsqr_iters)
+    elif mode == "sketch_solve":
+        y, R = lsq.sketch_and_solve(SV[:, :m], SV[:, m])
+    else:
+        raise ValueError(mode)
+    C = Hm.copy()
+    if not dec["breakdown"]:
+        C[:, m - 1] += H[m, m - 1] * y                      # Eq. (6)
+    return y, C, R, info
+
+
+def solve(A, b, m, k, s, seed, mode="blendenpik", f="exp", alpha=1.0,
+          sigma=0.0, poly=None, lsqr_tol=1e-6, lsqr_iters=None,
+          lsqr_maxit=None, variant="cgs", keep=True):
+    """One f(A)b approximation by Alg 4 / Remark 2 / Alg 5.  Returns a dict
+    with f_m and every intermediate (V, H, SV, rows, signs, y, C, c)."""
+    dec = krylov.truncated_arnoldi(A, b, m, k, variant=variant)     # Alg 2
+    me = dec["m_eff"]
+    th = SV = None
+    if mode != "none":
+        th = SRHT(b.shape[0], s, seed)                              # Theta
+        if me + 1 > s:
+            raise ValueError("InvalidSketchSize: need s >= m+1")
+        SV = th.apply(dec["V"])                                     # Theta V_{m+1}
+    y, C, R, info = compress(dec, SV, mode, lsqr_tol, lsqr_iters, lsqr_maxit)
+    c = matfun.f_e1(f, C, alpha, sigma, poly)                       # f(C) e_1
+    fm = dec["gamma"] * (dec["V"][:, :me] @ c)                      # ||b|| V_m c
+    out = dict(f_m=fm, H=dec["H"], gamma=dec["gamma"], m_eff=me,
+               breakdown=dec["breakdown"], y=y, C=C, c=c, R=R, lsqr=info)
+    if keep:
+        out.update(V=dec["V"], SV=SV)
+    if th is not None:
+        out.update(rows=th.rows, signs=th.signs)
+    return out
+
+
+def sfom(A, b, m, k, s, seed, f="exp", alpha=1.0, sigma=0.0, poly=None):
+    """Eq. (9) written out: Theta V_m = S_m R_m (thin QR),
+    f_hat = V_m (R_m^{-1} f(S_m^T Theta A V_m R_m^{-1}) S_m^T Theta b)."""
+    dec = krylov.truncated_arnoldi(A, b, m, k)
+    me = dec["m_eff"]
+    Vm = dec["V"][:, :me]
+    th = SRHT(b.shape[0], s, seed)
+    TV = th.apply(Vm)
+    TAV = th.apply(A @ Vm)
+    Tb = th.apply(b)
+    Q, R = np.linalg.qr(TV)
+    sg = np.sign(np.diag(R))
+    Q, R = Q * sg, sg[:, None] * R
+    Rinv = lsq.solve_upper(R, np.eye(me))
+    inner = Q.T @ TAV @ Rinv
+    F = matfun.fmat(f, alpha * inner + sigma * np.eye(me), poly) if f != "invsqrt" \
+        else np.linalg.inv(matfun.fmat("sqrt", alpha * inner + sigma * np.eye(me)))
+    return Vm @ (Rinv @ (F @ (Q.T @ Tb)))
+
+
+def fom(A, b, m, f="exp", alpha=1.0, sigma=0.0, poly=None):
+    """Eq. (4): f_m = ||b|| U_m f(K_m) e_1 with a full Arnoldi basis."""
+    dec = krylov.arnoldi(A, b, m)
+    me = dec["m_eff"]
+    c = matfun.f_e1(f, dec["H"][:me, :me], alpha, sigma, poly)
+    return dec["gamma"] * (dec["V"][:, :me] @ c)
+
+
+def dense(A, b, f="exp", alpha=1.0, sigma=0.0, poly=None):
+    Ad = A.toarray() if hasattr(A, "toarray") else np.asarray(A)
+    return matfun.f_dense_apply(f, Ad, b, alpha, sigma, poly)

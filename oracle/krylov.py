@@ -1,0 +1,95 @@
+"""Krylov bases: Algorithm 2 (truncated orthogonalization, PAPER.md
+l.102-130, §2.1.2) and the Arnoldi decomposition (Eq. (2), l.38-48).
+
+Algorithm 2 as printed (l.118-127):
+    v_1 <- b / ||b||_2
+    for i = 2 .. m+1:
+        w_i <- A v_{i-1}
+        for j = max{1, i-k} .. i-1:
+            h_{j,i-1} <- v_j^T w_i
+            w_i <- w_i - h_{j,i} v_i           (typo, G-1: read h_{j,i-1} v_j)
+        h_{i,i-1} <- ||w||_2                   (read ||w_i||_2)
+        v_i <- w_i / ||w_i||_2
+Reading G-1 restores the evident orthogonalization.  ``variant="mgs"`` is the
+literal sequential loop; ``variant="cgs"`` computes all k window coefficients
+from the un-updated w_i first (one-pass classical GS, equal in exact
+arithmetic because the window is orthonormal, G-2).  Breakdown (G-5): stop
+when h_{i,i-1} <= 1e-14 ||A||_inf; then m_eff = i-1 and K_{m_eff} is an
+invariant subspace.
+
+Indices: code is 0-based, column c of V is the paper's v_{c+1}; H is the
+(m+1) x m matrix underline-H_m with H[c', c] = h_{c'+1, c+1}.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+"""
+import numpy as np
+
+
+def _norm_inf(A):
+    return float(abs(A).sum(axis=1).max())
+
+
+def truncated_arnoldi(A, b, m: int, k: int, variant: str = "mgs",
+                      breakdown_tol: float = 1e-14):
+    """Algorithm 2.  Returns dict(V, H, gamma=||b||_2, m_eff, breakdown):
+    V is n x (m+1) and H (m+1) x m without breakdown; on breakdown at step
+    i, m_eff = i-1, V = [v_1..v_{m_eff}] and H is (m_eff+1) x m_eff."""
+    n = b.shape[0]
+    if k < 1 or m < 1:
+        raise ValueError("need k >= 1, m >= 1")
+    gamma = float(np.linalg.norm(b))
+    V = np.zeros((n, m + 1))
+    H = np.zeros((m + 1, m))
+    V[:, 0] = b / gamma                                   # l.118
+    thresh = breakdown_tol * _norm_inf(A)
+    for i in range(2, m + 2):                             # l.119, paper index i
+        c = i - 1                                          # 0-based new column
+        w = A @ V[:, c - 1]                                # l.120
+        js = range(max(1, i - k), i)                       # l.121, paper j
+        if variant == "mgs":
+            for j in js:
+                H[j - 1, c - 1] = V[:, j - 1] @ w          # l.122
+                w = w - H[j - 1, c - 1] * V[:, j - 1]      # l.123 (G-1)
+        elif variant == "cgs":
+            W = V[:, [j - 1 for j in js]]
+            hc = W.T @ w
+            for t, j in enumerate(js):
+                H[j - 1, c - 1] = hc[t]
+            w = w - W @ hc
+        else:
+            raise ValueError(variant)
+        hn = float(np.linalg.norm(w))                      # l.125
+        H[c, c - 1] = hn
+        if hn <= thresh:                                   # G-5
+            # K_{i-1} is A-invariant: m_eff = i-1; V keeps v_1..v_{i-1} only
+            m_eff = c
+            return dict(V=V[:, :m_eff], H=H[: m_eff + 1, :m_eff],
+                        gamma=gamma, m_eff=m_eff, breakdown=True)
+        V[:, c] = w / hn                                   # l.126
+    return dict(V=V, H=H, gamma=gamma, m_eff=m, breakdown=False)
+
+
+def arnoldi(A, b, m: int, breakdown_tol: float = 1e-14):
+    """Arnoldi decomposition Eq. (2): A U_m = U_{m+1} K_m (underline), U
+    orthonormal; modified Gram-Schmidt with one full reorthogonalization
+    pass (the 'exact' reference of PAPER.md l.358)."""
+    n = b.shape[0]
+    gamma = float(np.linalg.norm(b))
+    U = np.zeros((n, m + 1))
+    K = np.zeros((m + 1, m))
+    U[:, 0] = b / gamma
+    thresh = breakdown_tol * _norm_inf(A)
+    for c in range(1, m + 1):
+        w = A @ U[:, c - 1]
+        for _pass in range(2):
+            for j in range(c):
+                hj = U[:, j] @ w
+                K[j, c - 1] += hj
+                w = w - hj * U[:, j]
+        hn = float(np.linalg.norm(w))
+        K[c, c - 1] = hn
+        if hn <= thresh:
+            return dict(V=U[:, :c], H=K[: c + 1, :c], gamma=gamma,
+                        m_eff=c, breakdown=True)
+        U[:, c] = w / hn
+    return dict(V=U, H=K, gamma=gamma, m_eff=m, breakdown=False)

@@ -1,0 +1,98 @@
+"""Pins for oracle/krylov.py: Algorithm 2 and Arnoldi
+(Eq. (2), l.38-48)."""
+import json
+import os
+
+import numpy as np
+import scipy.sparse as sp
+
+import fab_problems as fp
+from oracle import krylov
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _arnoldi_like_residual(A, V, H):
+    m = H.shape[1]
+    R = A @ V[:, :m] - V[:, : m + 1] @ H
+    return np.linalg.norm(R) / (abs(A).sum(axis=1).max() * np.linalg.norm(V[:, :m]))
+
+
+def test_stencil_matvec_hand_case():
+    # tridiag(-1, 2, -1) (1, 1, 1) = (1, 0, 1)
+    g = json.load(open(os.path.join(GOLD, "spec_examples.json")))["tridiag_matvec"]
+    ip, ix, dv = fp.stencil_csr((3, 1, 1), (2.0, -1.0, -1.0, 0, 0, 0, 0))
+    A = sp.csr_matrix((dv, ix, ip), shape=(3, 3))
+    assert np.array_equal(A @ np.array(g["x"]), np.array(g["y"]))
+
+
+def test_symmetric_k2_is_lanczos():
+    # l.104: for symmetric A and k = 2, Alg 2 coincides with Lanczos: H tridiagonal
+    # and V orthonormal (in exact arithmetic; well-conditioned instance here)
+    n = 400
+    A = sp.diags([-np.ones(n - 1), 2 + np.linspace(0, 1, n), -np.ones(n - 1)], [-1, 0, 1]).tocsr()
+    b = np.random.default_rng(0).standard_normal(n)
+    d = krylov.truncated_arnoldi(A, b, 20, 2, variant="mgs")
+    H, V = d["H"], d["V"]
+    assert np.abs(np.triu(H[:20, :20], 2)).max() <= 1e-10 * np.abs(H).max()
+    assert np.linalg.norm(V.T @ V - np.eye(21)) <= 1e-8
+    assert np.allclose(H[:20, :20], H[:20, :20].T, atol=1e-10 * np.abs(H).max())
+
+
+def test_k_ge_m_equals_full_arnoldi():
+    # k >= m -> truncation inactive -> identical to Arnoldi (single pass MGS)
+    # (well-conditioned Krylov basis, so single-pass MGS keeps orthogonality)
+    p = fp.make("c1", g=20, m=15, k=2, s=40)
+    A, b = p.scipy(), p.b
+    d1 = krylov.truncated_arnoldi(A, b, 15, 15, variant="mgs")
+    d2 = krylov.arnoldi(A, b, 15)
+    assert np.allclose(d1["H"], d2["H"], rtol=0, atol=1e-10 * np.abs(d2["H"]).max())
+    assert np.allclose(d1["V"], d2["V"], atol=1e-10)
+    assert np.linalg.norm(d2["V"].T @ d2["V"] - np.eye(16)) <= 1e-12
+
+
+def test_window_orthogonality_residual_unit_columns():
+    p = fp.make("c3", g=20, m=40, k=4, s=80)
+    A, b = p.scipy(), p.b
+    d = krylov.truncated_arnoldi(A, b, 40, 4)
+    V, H = d["V"], d["H"]
+    G = V.T @ V
+    for i in range(41):
+        for j in range(max(0, i - 4), i):
+            assert abs(G[i, j]) <= 1e-12                    # orthogonal to last k
+    assert np.allclose(np.diag(G), 1.0, atol=1e-14)         # unit columns (l.126)
+    assert _arnoldi_like_residual(A, V, H) <= 1e-12          # Eq. (3)
+    assert np.linalg.norm(V[:, :40], 2) <= np.sqrt(40) + 1e-12   # l.337
+    assert np.abs(np.tril(H, -2)).max() == 0.0               # upper Hessenberg
+    # banded: column c has rows c+1-k..c+1 only (k-truncation)
+    assert np.abs(np.triu(H, 4)).max() == 0.0
+
+
+def test_mgs_equals_cgs_within_window():
+    # G-2: CGS and MGS agree (window is orthonormal)
+    p = fp.make("c1", g=30, m=25, k=2, s=50)
+    A, b = p.scipy(), p.b
+    a = krylov.truncated_arnoldi(A, b, 25, 2, variant="mgs")
+    c = krylov.truncated_arnoldi(A, b, 25, 2, variant="cgs")
+    assert np.abs(a["H"] - c["H"]).max() <= 1e-11 * np.abs(a["H"]).max()
+    assert np.abs(a["V"] - c["V"]).max() <= 1e-10
+
+
+def test_breakdown_eigenvector():
+    # A = diag(1..5), b = e_1 -> breakdown at i = 2, H = [1]
+    A = sp.diags(np.arange(1.0, 6.0)).tocsr()
+    b = np.zeros(5)
+    b[0] = 1
+    d = krylov.truncated_arnoldi(A, b, 3, 2)
+    assert d["breakdown"] and d["m_eff"] == 1
+    assert d["H"][0, 0] == 1.0
+    d = krylov.arnoldi(A, b, 3)
+    assert d["breakdown"] and d["m_eff"] == 1
+
+
+def test_breakdown_distinct_eigenvalues():
+    # diagonal A with d distinct values: Krylov space of dimension d
+    A = sp.diags(np.repeat([1.0, 2.0, 3.0, 4.0], 10)).tocsr()
+    b = np.random.default_rng(1).standard_normal(40)
+    d = krylov.truncated_arnoldi(A, b, 10, 10)
+    assert d["breakdown"] and d["m_eff"] == 4
