@@ -1,0 +1,215 @@
+/*
+ * fab.h -- C ABI of the B200-native randomized-Krylov f(A)b hot path
+ * (Cortinovis, Kressner, Nakatsukasa, arXiv 2212.12758).
+ *
+ * Citations "PAPER.md l.N" are lines of /root/reference/PAPER.md (the
+ * paper's LaTeX source); G-n are the readings listed in DESIGN.md.
+ *
+ * The calls compute, on one B200 (sm_100a), Algorithm 4 (PAPER.md
+ * l.199-209) and its two variants:
+ *
+ *   fab_init     A (CSR or constant stencil) and b; gamma_b = ||b||_2 (l.172)
+ *   fab_sketch   draw Theta = (1/sqrt s) P H_N D, the SRHT of l.70
+ *   fab_basis    Algorithm 2 (l.112-130): V_{m+1}, underline-H_m; if the
+ *                sketch was drawn first, Theta V_{m+1} is fused into it
+ *   fab_compress y of Eq. (7) (l.174-177) by Blendenpik-LSQR (l.183), by
+ *                sketch-and-solve (Remark 2, l.249-251) or not at all
+ *                (Algorithm 5, l.219-228); C_m = H_m + h_{m+1,m} y e_m^T
+ *                (Eq. (6), l.168-170)
+ *   fab_apply    y_out = gamma_b V_m f(alpha C_m + sigma I) e_1 (l.207)
+ *
+ * Conventions
+ *  - Every pointer marked "device" is a CUDA device pointer on the
+ *    context's device; "host" pointers are ordinary (preferably pinned)
+ *    host memory.  The library never takes ownership of caller memory:
+ *    operator arrays are BORROWED and must stay alive and unchanged until
+ *    fab_destroy; b and y_out are copied.
+ *  - Dense matrices are column-major.  V is n x (m+1) with leading
+ *    dimension ld = n rounded up to a multiple of 32 doubles; its stored
+ *    columns are unnormalized (w_hat_j = beta_j v_j, G-4); fab_get returns
+ *    the normalized v_j.
+ *  - All work is enqueued on opts->stream (a cudaStream_t, NULL = legacy
+ *    default stream).  fab_basis, fab_compress and fab_apply synchronize
+ *    that stream before returning (they report device-side status:
+ *    breakdown, LSQR convergence, domain errors), and so do fab_init and
+ *    fab_sketch (small host<->device copies).  Asynchronous CUDA errors
+ *    surface as FAB_ECUDA at the next synchronizing call.
+ *  - Calls must come in order: init, then basis and sketch (either order),
+ *    then compress, then apply (repeatable).  Out-of-order -> FAB_EORDER.
+ *  - One context per host thread.  No exception crosses the ABI.
+ *  - Status: 0 ok, > 0 warning (result valid), < 0 error (no result).
+ */
+#ifndef FAB_H
+#define FAB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FAB_ABI_VERSION 1
+
+/* ---- status codes ---------------------------------------------------- */
+enum {
+  FAB_OK = 0,
+  FAB_BREAKDOWN = 1,   /* h_{i,i-1} <= 1e-14 ||A||_inf: K_{i-1} invariant, m_eff = i-1 (G-5) */
+  FAB_ILLCOND = 2,     /* cond(R) of the sketched basis > 1e8 (G-24)                        */
+  FAB_NOTCONV = 3,     /* LSQR hit maxit before tol (result still returned; Lemma 2 l.297) */
+  FAB_EINVAL = -1,     /* bad argument                                                      */
+  FAB_EORDER = -2,     /* call out of order                                                 */
+  FAB_ESINGULAR = -3,  /* min R_ii < 1e-14 max R_jj, or singular Pade/DB matrix             */
+  FAB_EDOMAIN = -4,    /* sqrt / invsqrt of a matrix with eigenvalues on R_{<=0}            */
+  FAB_ENOCONV = -5,    /* Denman-Beavers iteration cap reached                              */
+  FAB_ENOMEM = -6,     /* workspace too small / allocation failed                           */
+  FAB_ECUDA = -7,      /* CUDA runtime error                                                */
+  FAB_ENCCL = -8,      /* NCCL error (multi-GPU)                                             */
+  FAB_ENODEV = -9      /* no CUDA device / not an sm_100 device                             */
+};
+
+/* ---- enums ------------------------------------------------------------ */
+enum { FAB_BLENDENPIK = 0, FAB_SKETCH_SOLVE = 1, FAB_NONE = 2 };       /* fab_compress */
+enum { FAB_EXP = 0, FAB_SQRT = 1, FAB_INVSQRT = 2, FAB_POLY = 3 };     /* fab_apply    */
+enum { FAB_OP_CSR = 0, FAB_OP_STENCIL = 1 };                          /* operator kind */
+enum { FAB_DEVICE = 0, FAB_HOST = 1 };                                /* pointer space */
+
+/* fab_get / fab_set selectors */
+enum {
+  FAB_GET_INFO = 0,   /* fab_info                                           */
+  FAB_GET_H = 1,      /* underline-H_m, (m_eff+1) x m_eff doubles            */
+  FAB_GET_V = 2,      /* normalized basis v_1..v_{m_eff+1}, n x (m_eff+1)    */
+  FAB_GET_SV = 3,     /* Theta V_{m+1}, s x (m_eff+1)                         */
+  FAB_GET_ROWS = 4,   /* sampled rows, s int64, ascending                    */
+  FAB_GET_SIGNS = 5,  /* sign bitmap, ceil(N/32) uint32, bit=1 <=> D_tt = -1 */
+  FAB_GET_Y = 6,      /* y of Eq. (7), m_eff doubles                          */
+  FAB_GET_C = 7,      /* C_m, m_eff x m_eff doubles                           */
+  FAB_GET_FC = 8,     /* c = f(alpha C_m + sigma I) e_1, m_eff doubles        */
+  FAB_GET_R = 9,      /* R of QR(Theta V_m), m_eff x m_eff doubles            */
+  FAB_GET_BETA = 10,  /* norms of the stored columns, m_eff+1 doubles         */
+  FAB_SET_POLY = 100  /* FAB_POLY coefficients p_0..p_d (doubles), d < 64     */
+};
+
+typedef struct fab_ctx fab_ctx;
+
+/* The operator A (n x n), accessed only through products A x (l.17). */
+typedef struct {
+  int kind;                /* FAB_OP_CSR or FAB_OP_STENCIL                          */
+  int row_ptr_64;          /* reserved (row_ptr is always int64)                    */
+  int64_t n;               /* global dimension                                      */
+  int64_t row_begin;       /* first owned row (multi-GPU block rows); 0 on 1 GPU    */
+  int64_t row_end;         /* one past the last owned row; n on 1 GPU               */
+  /* CSR (kind == FAB_OP_CSR): device pointers, local rows, GLOBAL column ids  */
+  int64_t nnz;
+  const int64_t* row_ptr;  /* row_end-row_begin+1 entries, row_ptr[0] == 0         */
+  const int32_t* col_idx;  /* nnz, sorted ascending within each row                */
+  const double* values;    /* nnz; NULL => every stored entry equals value_scale    */
+  double value_scale;      /* multiplies every value (1.0 = unscaled)               */
+  /* constant-coefficient stencil (kind == FAB_OP_STENCIL), Dirichlet BC:
+     row r = x + gx*(y + gy*z); (A u)_r = c0 u_r + cxm u_{r-1} + cxp u_{r+1}
+     + cym u_{r-gx} + cyp u_{r+gx} + czm u_{r-gx*gy} + czp u_{r+gx*gy},
+     neighbours outside the grid omitted.  gz == 1 is 2D.                    */
+  int64_t dims[3];
+  double coeffs[7];        /* c0, cxm, cxp, cym, cyp, czm, czp                      */
+} fab_operator;
+
+typedef struct {
+  void* stream;            /* cudaStream_t; NULL = legacy default stream            */
+  int device;              /* CUDA ordinal; -1 = current device                     */
+  int m_max;               /* capacity: largest m for fab_basis (>= 1)              */
+  int k_max;               /* capacity: largest truncation k (1..16)                */
+  int s_max;               /* capacity: largest sketch size s (0 = no sketch)       */
+  void* workspace;         /* device; NULL => the library allocates (cudaMalloc)    */
+  size_t workspace_bytes;  /* size of workspace, >= fab_workspace_size()            */
+  int b_location;          /* FAB_DEVICE or FAB_HOST for fab_init's b               */
+  unsigned flags;          /* reserved, 0                                           */
+  void* comm;              /* reserved for multi-GPU (NCCL); NULL on one GPU        */
+} fab_opts;
+
+typedef struct {
+  int iters;               /* > 0: run exactly this many LSQR iterations (parity)   */
+  int maxit;               /* tolerance mode cap; 0 => 4m               */
+  double tol;              /* tolerance mode: MATLAB lsqr test (l.359); 0 => 1e-6    */
+} fab_lsqr_opts;
+
+typedef struct {
+  int64_t n, N;            /* local rows; N = 2^ceil(log2 n_global)                  */
+  int m, k, s, m_eff;
+  int breakdown;           /* 1 if Alg 2 broke down (G-5)                            */
+  int sketch_fused;        /* 1 if Theta V was computed inside fab_basis             */
+  int mode;                /* last fab_compress mode                                 */
+  int lsqr_iters, lsqr_converged;
+  int dense_iters;         /* DB iterations / Pade squarings of the last fab_apply   */
+  int pad0;
+  double gamma_b;          /* ||b||_2                                                */
+  double h_last;           /* h_{m+1,m}                                              */
+  double norm_inf;         /* ||A||_inf                                              */
+  double cond_R;           /* ||R||_1 ||R^{-1}||_1 of QR(Theta V_m)                  */
+  double lsqr_rnorm, lsqr_arnorm, lsqr_anorm;
+  double ms_basis, ms_sketch, ms_compress, ms_apply;  /* device time, CUDA events */
+  int64_t launches_basis, launches_sketch, launches_compress, launches_apply;
+} fab_info;
+
+/* Library ABI version (FAB_ABI_VERSION). */
+int fab_version(void);
+
+/* Human-readable text for a status code (static storage). */
+const char* fab_strerror(int status);
+
+/* Bytes of device workspace fab_init needs for this operator and capacity
+   (opts: m_max, k_max, s_max, device).  0 on success. */
+int fab_workspace_size(const fab_operator* A, const fab_opts* opts, size_t* bytes);
+
+/* Create a context: validates A, copies b (n_local doubles, device or host per
+   opts->b_location) into V's first column, computes gamma_b = ||b|| and
+   ||A||_inf.  Errors: EINVAL, ENOMEM, ECUDA, ENODEV. */
+int fab_init(fab_ctx** ctx, const fab_operator* A, const double* b, const fab_opts* opts);
+
+/* Algorithm 2 with m steps and truncation k (1 <= k <= k_max, 1 <= m <= m_max,
+   m < n).  Returns FAB_BREAKDOWN (with m_eff in fab_info) on a lucky
+   breakdown.  Errors: EORDER, EINVAL, ECUDA. */
+int fab_basis(fab_ctx* ctx, int m, int k);
+
+/* Draw the SRHT Theta (s rows, seed) of l.70: signs from the counter hash of
+   G-10, rows by Floyd sampling without replacement.  Before fab_basis it arms
+   the fused sketch; after it, sketches V_{m+1} in one batched pass.  Results
+   are identical either way.  Requires m+1 <= s <= min(N, s_max).
+   Errors: EINVAL, EORDER, ECUDA. */
+int fab_sketch(fab_ctx* ctx, int s, uint64_t seed);
+
+/* Compression (Eq. (6)/(7)).  mode FAB_BLENDENPIK: QR of Theta V_m, LSQR on
+   V_m R^{-1} (opts NULL => tol 1e-6, maxit 4m); FAB_SKETCH_SOLVE:
+   y = R^{-1} Q^T Theta v_{m+1}; FAB_NONE: y = 0 (Alg 5).  Warnings: ILLCOND,
+   NOTCONV.  Errors: EORDER, ESINGULAR, ECUDA. */
+int fab_compress(fab_ctx* ctx, int mode, const fab_lsqr_opts* opts);
+
+/* y_out (n_local doubles, device or host per y_location) =
+   gamma_b V_m f(alpha C_m + sigma I) e_1, f in {EXP, SQRT, INVSQRT, POLY}.
+   Errors: EORDER, EINVAL, EDOMAIN, ENOCONV, ESINGULAR, ECUDA. */
+int fab_apply(fab_ctx* ctx, int f, double alpha, double sigma, double* y_out, int y_location);
+
+/* Copy a result to HOST memory dst (bytes >= the size listed in the enum). */
+int fab_get(fab_ctx* ctx, int what, void* dst, size_t bytes);
+
+/* Normalized basis column v_{j+1} (0 <= j <= m_eff, or < m_eff after a
+   breakdown) -> dst (HOST, n_local doubles).  For full-size spot checks. */
+int fab_get_column(fab_ctx* ctx, int j, double* dst);
+
+/* Rows of the normalized basis: dst[i*(ncols) + j] = v_{j+1}[rows[i]] for the
+   nrows local row indices in rows (HOST), ncols = m_eff+1 (m_eff after a
+   breakdown).  For full-size spot checks of Eq. (3) and of f_m. */
+int fab_get_vrows(fab_ctx* ctx, const int64_t* rows, int nrows, double* dst);
+
+/* Set a test-only input from HOST memory. */
+int fab_set(fab_ctx* ctx, int what, const void* src, size_t bytes);
+
+/* Text of the last CUDA error seen by this thread (diagnostics). */
+const char* fab_last_error(void);
+
+/* Release the context (and the workspace if the library allocated it). */
+int fab_destroy(fab_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FAB_H */

@@ -1,0 +1,515 @@
+// The C ABI (include/fab.h): validation, workspace layout, call ordering,
+// timing and result export.  All arithmetic runs in the kernels of basis.cu,
+// sketch.cu, lsqr.cu, dense.cu and apply.cu.
+#include <math.h>
+#include <stdlib.h>
+
+#include <new>
+
+#include "fab_internal.cuh"
+
+namespace fab {
+
+static thread_local char g_err[512] = "";
+
+void set_last_cuda_error(cudaError_t e, const char* what, const char* file, int line) {
+  snprintf(g_err, sizeof(g_err), "%s (%s) at %s:%d: %s", cudaGetErrorName(e), what, file, line,
+           cudaGetErrorString(e));
+}
+
+struct Layout {
+  size_t V, vec, H, beta, coef, part_norm, part_sk, SV, rows, signs, part_g, part_tn, small, dense, qr, st;
+  size_t total;
+};
+
+static size_t carve(size_t& cur, size_t bytes) {
+  const size_t off = cur;
+  cur += (bytes + 255) / 256 * 256;
+  return off;
+}
+
+static Layout make_layout(const fab_ctx* c) {
+  Layout L;
+  size_t cur = 0;
+  const size_t m1 = (size_t)c->m_max + 1;
+  L.V = carve(cur, m1 * c->ld * 8);
+  L.vec = carve(cur, (size_t)c->ld * 8);
+  L.H = carve(cur, m1 * c->m_max * 8);
+  L.beta = carve(cur, ((size_t)c->m_max + 2) * 8);
+  L.coef = carve(cur, ((size_t)c->m_max + 2) * (kKMax + 1) * 8);
+  L.part_norm = carve(cur, (size_t)c->grid_upd * 8);
+  L.part_sk = carve(cur, c->s_max > 0 ? m1 * c->grid_upd * c->s_max * 8 : 8);
+  L.SV = carve(cur, (size_t)(c->s_max > 0 ? c->s_max : 1) * m1 * 8);
+  L.rows = carve(cur, (size_t)(c->s_max > 0 ? c->s_max : 1) * 8);
+  L.signs = carve(cur, (size_t)((c->N + 31) / 32) * 4);
+  L.part_g = carve(cur, (size_t)c->grid_lsqr * c->m_max * 8);
+  L.part_tn = carve(cur, (size_t)c->grid_lsqr * 8);
+  L.small = carve(cur, (size_t)kSmallVecs * kSmall * 8);
+  L.dense = carve(cur, (size_t)kDenseMats * c->m_max * c->m_max * 8);
+  L.qr = carve(cur, (size_t)(c->s_max > 0 ? c->s_max : 1) * m1 * 8);
+  L.st = carve(cur, sizeof(DevState));
+  L.total = cur;
+  return L;
+}
+
+double* qr_work(fab_ctx* c) {
+  Layout L = make_layout(c);
+  return reinterpret_cast<double*>(c->ws + L.qr);
+}
+
+static int validate_operator(const fab_operator* A) {
+  if (!A) return FAB_EINVAL;
+  if (A->n < 2 || A->row_begin < 0 || A->row_end > A->n || A->row_end <= A->row_begin) return FAB_EINVAL;
+  if (A->n > ((int64_t)1 << 31) - 64) return FAB_EINVAL;   // int32 column ids / stencil indexing
+  if (A->kind == FAB_OP_CSR) {
+    if (!A->row_ptr || (A->nnz > 0 && !A->col_idx) || A->nnz < 0) return FAB_EINVAL;
+  } else if (A->kind == FAB_OP_STENCIL) {
+    if (A->dims[0] < 1 || A->dims[1] < 1 || A->dims[2] < 1) return FAB_EINVAL;
+    if (A->dims[0] * A->dims[1] * A->dims[2] != A->n) return FAB_EINVAL;
+    if (A->row_begin != 0 || A->row_end != A->n) return FAB_EINVAL;   // one GPU only (this round)
+    for (int i = 0; i < 7; ++i)
+      if (!isfinite(A->coeffs[i])) return FAB_EINVAL;
+  } else {
+    return FAB_EINVAL;
+  }
+  return FAB_OK;
+}
+
+static int validate_opts(const fab_operator* A, const fab_opts* o) {
+  if (!o) return FAB_EINVAL;
+  if (o->m_max < 1 || o->m_max > kMaxM || o->m_max >= A->n) return FAB_EINVAL;
+  if (o->k_max < 1 || o->k_max > kKMax) return FAB_EINVAL;
+  if (o->s_max < 0 || o->s_max > kThreads * 3) return FAB_EINVAL;
+  if (o->b_location != FAB_DEVICE && o->b_location != FAB_HOST) return FAB_EINVAL;
+  if (o->comm) return FAB_EINVAL;   // multi-GPU: not in this build
+  return FAB_OK;
+}
+
+// fills device, sizes and grids of a context (no allocation)
+static int setup_ctx(fab_ctx* c, const fab_operator* A, const fab_opts* o) {
+  int dev = o->device;
+  if (dev < 0) FAB_CUDA(cudaGetDevice(&dev));
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return FAB_ENODEV;
+  if (dev >= ndev) return FAB_EINVAL;
+  FAB_CUDA(cudaSetDevice(dev));
+  cudaDeviceProp prop;
+  FAB_CUDA(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10) return FAB_ENODEV;   // built for sm_100a only
+  c->device = dev;
+  c->num_sms = prop.multiProcessorCount;
+  c->op = *A;
+  c->stencil = (A->kind == FAB_OP_STENCIL);
+  c->n_global = A->n;
+  c->row_begin = A->row_begin;
+  c->n = A->row_end - A->row_begin;
+  c->ld = round_up(c->n, 32);
+  c->N = next_pow2(c->n_global);
+  c->m_max = o->m_max;
+  c->k_max = o->k_max;
+  c->s_max = o->s_max;
+  c->ldH = o->m_max + 1;
+  int rc = basis_setup_grids(c);
+  if (rc != FAB_OK) return rc;
+  c->grid_lsqr = 2 * c->num_sms;
+  c->grid_comb = 8 * c->num_sms;
+  return FAB_OK;
+}
+
+static void assign_buffers(fab_ctx* c) {
+  Layout L = make_layout(c);
+  char* w = c->ws;
+  c->V = reinterpret_cast<double*>(w + L.V);
+  c->vec = reinterpret_cast<double*>(w + L.vec);
+  c->H = reinterpret_cast<double*>(w + L.H);
+  c->beta = reinterpret_cast<double*>(w + L.beta);
+  c->coef = reinterpret_cast<double*>(w + L.coef);
+  c->part_norm = reinterpret_cast<double*>(w + L.part_norm);
+  c->part_sk = reinterpret_cast<double*>(w + L.part_sk);
+  c->SV = reinterpret_cast<double*>(w + L.SV);
+  c->rows_d = reinterpret_cast<int64_t*>(w + L.rows);
+  c->signs_d = reinterpret_cast<uint32_t*>(w + L.signs);
+  c->part_g = reinterpret_cast<double*>(w + L.part_g);
+  c->part_tn = reinterpret_cast<double*>(w + L.part_tn);
+  c->small = reinterpret_cast<double*>(w + L.small);
+  c->dense = reinterpret_cast<double*>(w + L.dense);
+  c->st_d = reinterpret_cast<DevState*>(w + L.st);
+}
+
+static void free_ctx(fab_ctx* c) {
+  if (!c) return;
+  release_long_rows(c);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->part_dots) cudaFree(c->part_dots);
+  if (c->own_ws && c->ws) cudaFree(c->ws);
+  if (c->st_h) cudaFreeHost(c->st_h);
+  if (c->cap) cudaStreamDestroy(c->cap);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  delete c;
+}
+
+static int pull_state(fab_ctx* c) {
+  FAB_CUDA(cudaMemcpyAsync(c->st_h, c->st_d, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+  FAB_CUDA(cudaStreamSynchronize(c->stream));
+  return FAB_OK;
+}
+
+static int timed_end(fab_ctx* c, double* ms) {
+  FAB_CUDA(cudaEventRecord(c->ev1, c->stream));
+  FAB_CUDA(cudaEventSynchronize(c->ev1));
+  float t = 0.f;
+  FAB_CUDA(cudaEventElapsedTime(&t, c->ev0, c->ev1));
+  *ms = t;
+  return FAB_OK;
+}
+
+}  // namespace fab
+
+using namespace fab;
+
+extern "C" {
+
+int fab_version(void) { return FAB_ABI_VERSION; }
+
+const char* fab_strerror(int s) {
+  switch (s) {
+    case FAB_OK: return "ok";
+    case FAB_BREAKDOWN: return "Krylov breakdown: invariant subspace found (m_eff < m)";
+    case FAB_ILLCOND: return "sketched basis ill-conditioned (cond(R) > 1e8)";
+    case FAB_NOTCONV: return "LSQR reached maxit before tol";
+    case FAB_EINVAL: return "invalid argument";
+    case FAB_EORDER: return "call out of order";
+    case FAB_ESINGULAR: return "singular triangular factor or singular matrix";
+    case FAB_EDOMAIN: return "matrix function undefined (eigenvalue on the closed negative real axis)";
+    case FAB_ENOCONV: return "matrix function iteration did not converge";
+    case FAB_ENOMEM: return "out of memory / workspace too small";
+    case FAB_ECUDA: return g_err[0] ? g_err : "CUDA error";
+    case FAB_ENCCL: return "NCCL error";
+    case FAB_ENODEV: return "no sm_100 CUDA device";
+    default: return "unknown status";
+  }
+}
+
+int fab_workspace_size(const fab_operator* A, const fab_opts* o, size_t* bytes) {
+  int rc = validate_operator(A);
+  if (rc != FAB_OK) return rc;
+  if ((rc = validate_opts(A, o)) != FAB_OK) return rc;
+  if (!bytes) return FAB_EINVAL;
+  fab_ctx tmp;
+  rc = setup_ctx(&tmp, A, o);
+  if (rc != FAB_OK) return rc;
+  *bytes = make_layout(&tmp).total;
+  return FAB_OK;
+}
+
+int fab_init(fab_ctx** out, const fab_operator* A, const double* b, const fab_opts* o) {
+  if (!out || !b) return FAB_EINVAL;
+  *out = nullptr;
+  int rc = validate_operator(A);
+  if (rc != FAB_OK) return rc;
+  if ((rc = validate_opts(A, o)) != FAB_OK) return rc;
+  fab_ctx* c = new (std::nothrow) fab_ctx();
+  if (!c) return FAB_ENOMEM;
+  rc = setup_ctx(c, A, o);
+  if (rc != FAB_OK) {
+    free_ctx(c);
+    return rc;
+  }
+  c->stream = reinterpret_cast<cudaStream_t>(o->stream);
+  const size_t need = make_layout(c).total;
+  if (o->workspace) {
+    if (o->workspace_bytes < need || (reinterpret_cast<uintptr_t>(o->workspace) & 255)) {
+      free_ctx(c);
+      return FAB_ENOMEM;
+    }
+    c->ws = reinterpret_cast<char*>(o->workspace);
+    c->ws_bytes = o->workspace_bytes;
+  } else {
+    if (cudaMalloc(&c->ws, need) != cudaSuccess) {
+      cudaGetLastError();
+      free_ctx(c);
+      return FAB_ENOMEM;
+    }
+    c->own_ws = true;
+    c->ws_bytes = need;
+  }
+  assign_buffers(c);
+#define INIT_CUDA(x)                                   \
+  do {                                                 \
+    cudaError_t e_ = (x);                              \
+    if (e_ != cudaSuccess) {                           \
+      set_last_cuda_error(e_, #x, __FILE__, __LINE__); \
+      free_ctx(c);                                     \
+      return FAB_ECUDA;                                \
+    }                                                  \
+  } while (0)
+  INIT_CUDA(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+  INIT_CUDA(cudaEventCreate(&c->ev0));
+  INIT_CUDA(cudaEventCreate(&c->ev1));
+  INIT_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  INIT_CUDA(cudaMallocHost(&c->st_h, sizeof(DevState)));
+  // b -> V[:, 0]
+  INIT_CUDA(cudaMemcpyAsync(c->V, b, c->n * sizeof(double),
+                            o->b_location == FAB_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                            c->stream));
+  if (c->stencil) {
+    double s = 0.0;
+    for (int i = 0; i < 7; ++i) s += fabs(c->op.coeffs[i]);
+    c->norm_inf = s;
+  }
+  rc = init_vector_norm(c);   // CSR: ||A||_inf, long-row list, dot partial buffer
+  if (rc != FAB_OK) {
+    free_ctx(c);
+    return rc;
+  }
+  DevState h;
+  memset(&h, 0, sizeof(h));
+  h.norm_inf = c->norm_inf;
+  h.thresh = 1e-14 * c->norm_inf;
+  *c->st_h = h;
+  INIT_CUDA(cudaMemcpyAsync(c->st_d, c->st_h, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
+  INIT_CUDA(cudaStreamSynchronize(c->stream));
+#undef INIT_CUDA
+  c->info.n = c->n;
+  c->info.N = c->N;
+  c->info.norm_inf = c->norm_inf;
+  *out = c;
+  return FAB_OK;
+}
+
+int fab_basis(fab_ctx* c, int m, int k) {
+  if (!c) return FAB_EINVAL;
+  if (k < 1 || k > c->k_max || m < 1 || m > c->m_max || m >= c->n_global) return FAB_EINVAL;
+  if (c->sketch_ready && c->s < m + 1) return FAB_EINVAL;
+  FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
+  int rc = run_basis(c, m, k);
+  if (rc != FAB_OK) return rc;
+  double ms = 0;
+  if ((rc = timed_end(c, &ms)) != FAB_OK) return rc;
+  if ((rc = pull_state(c)) != FAB_OK) return rc;
+  c->m = m;
+  c->k = k;
+  c->breakdown = c->st_h->breakdown != 0;
+  c->m_eff = c->st_h->m_eff;
+  c->basis_ready = true;
+  c->compressed = false;
+  c->sketch_in_V = c->sketch_ready;
+  c->info.m = m;
+  c->info.k = k;
+  c->info.m_eff = c->m_eff;
+  c->info.breakdown = c->breakdown;
+  c->info.sketch_fused = c->sketch_ready ? 1 : 0;
+  c->info.gamma_b = c->st_h->gamma;
+  c->info.ms_basis = ms;
+  double hl = 0;
+  if (!c->breakdown) {
+    FAB_CUDA(cudaMemcpy(&hl, c->H + m + (int64_t)(m - 1) * c->ldH, sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  c->info.h_last = hl;
+  return c->breakdown ? FAB_BREAKDOWN : FAB_OK;
+}
+
+int fab_sketch(fab_ctx* c, int s, uint64_t seed) {
+  if (!c) return FAB_EINVAL;
+  if (s < 1 || s > c->s_max || (int64_t)s > c->N) return FAB_EINVAL;
+  if (c->basis_ready && s < (c->breakdown ? c->m_eff : c->m + 1)) return FAB_EINVAL;
+  FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
+  int rc = sketch_draw(c, s, seed);
+  if (rc != FAB_OK) return rc;
+  int64_t launches = 1;
+  if (c->basis_ready) {
+    if ((rc = sketch_batched(c)) != FAB_OK) return rc;
+    launches += 2;
+    c->sketch_in_V = true;
+    c->compressed = false;
+    c->info.sketch_fused = 0;
+  } else {
+    c->sketch_ready = true;
+  }
+  double ms = 0;
+  if ((rc = timed_end(c, &ms)) != FAB_OK) return rc;
+  c->info.s = s;
+  c->info.ms_sketch = ms;
+  c->info.launches_sketch = launches;
+  return FAB_OK;
+}
+
+int fab_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o) {
+  if (!c) return FAB_EINVAL;
+  if (mode != FAB_BLENDENPIK && mode != FAB_SKETCH_SOLVE && mode != FAB_NONE) return FAB_EINVAL;
+  if (!c->basis_ready) return FAB_EORDER;
+  if (mode != FAB_NONE && !c->sketch_in_V) return FAB_EORDER;
+  if (o && (o->iters < 0 || o->maxit < 0 || o->tol < 0)) return FAB_EINVAL;
+  FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
+  int warn = FAB_OK;
+  int rc = run_compress(c, mode, o, &warn);
+  if (rc != FAB_OK) return rc;
+  double ms = 0;
+  if ((rc = timed_end(c, &ms)) != FAB_OK) return rc;
+  FAB_CUDA(cudaGetLastError());
+  c->compressed = true;
+  c->mode = mode;
+  c->info.mode = mode;
+  c->info.ms_compress = ms;
+  return warn;
+}
+
+int fab_apply(fab_ctx* c, int f, double alpha, double sigma, double* y, int y_location) {
+  if (!c || !y) return FAB_EINVAL;
+  if (f < FAB_EXP || f > FAB_POLY) return FAB_EINVAL;
+  if (y_location != FAB_DEVICE && y_location != FAB_HOST) return FAB_EINVAL;
+  if (!isfinite(alpha) || !isfinite(sigma)) return FAB_EINVAL;
+  if (!c->compressed) return FAB_EORDER;
+  FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
+  double* cvec = svec(c, 16);
+  int iters = 0;
+  int rc = dense_fe1(c, f, alpha, sigma, cvec, &iters);
+  if (rc != FAB_OK) return rc;
+  const bool direct = (y_location == FAB_DEVICE) && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
+  double* ydev = direct ? y : c->vec;
+  if ((rc = run_combine(c, cvec, ydev)) != FAB_OK) return rc;
+  if (!direct) {
+    FAB_CUDA(cudaMemcpyAsync(y, ydev, c->n * sizeof(double),
+                             y_location == FAB_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                             c->stream));
+  }
+  double ms = 0;
+  if ((rc = timed_end(c, &ms)) != FAB_OK) return rc;
+  FAB_CUDA(cudaGetLastError());
+  c->info.dense_iters = iters;
+  c->info.ms_apply = ms;
+  return FAB_OK;
+}
+
+int fab_get(fab_ctx* c, int what, void* dst, size_t bytes) {
+  if (!c || !dst) return FAB_EINVAL;
+  const int me = c->m_eff;
+  auto need = [&](size_t b) { return bytes >= b; };
+  switch (what) {
+    case FAB_GET_INFO:
+      if (!need(sizeof(fab_info))) return FAB_EINVAL;
+      memcpy(dst, &c->info, sizeof(fab_info));
+      return FAB_OK;
+    case FAB_GET_H: {
+      if (!c->basis_ready) return FAB_EORDER;
+      const int rows = me + 1, cols = me;
+      if (!need((size_t)rows * cols * 8)) return FAB_EINVAL;
+      FAB_CUDA(cudaMemcpy2D(dst, rows * 8, c->H, c->ldH * 8, rows * 8, cols, cudaMemcpyDeviceToHost));
+      if (c->breakdown) {   // the last row holds the (tiny) breakdown value h_{m_eff+1,m_eff}
+      }
+      return FAB_OK;
+    }
+    case FAB_GET_BETA: {
+      if (!c->basis_ready) return FAB_EORDER;
+      if (!need((size_t)(me + 1) * 8)) return FAB_EINVAL;
+      FAB_CUDA(cudaMemcpy(dst, c->beta, (me + 1) * 8, cudaMemcpyDeviceToHost));
+      return FAB_OK;
+    }
+    case FAB_GET_V: {
+      if (!c->basis_ready) return FAB_EORDER;
+      const int cols = c->breakdown ? me : me + 1;
+      if (!need((size_t)c->n * cols * 8)) return FAB_EINVAL;
+      std::vector<double> bt(cols);
+      FAB_CUDA(cudaMemcpy(bt.data(), c->beta, cols * 8, cudaMemcpyDeviceToHost));
+      FAB_CUDA(cudaMemcpy2D(dst, c->n * 8, c->V, c->ld * 8, c->n * 8, cols, cudaMemcpyDeviceToHost));
+      double* d = static_cast<double*>(dst);
+      for (int j = 0; j < cols; ++j)
+        for (int64_t r = 0; r < c->n; ++r) d[r + (int64_t)j * c->n] /= bt[j];
+      return FAB_OK;
+    }
+    case FAB_GET_SV: {
+      if (!c->sketch_in_V) return FAB_EORDER;
+      const int cols = c->breakdown ? me : me + 1;
+      if (!need((size_t)c->s * cols * 8)) return FAB_EINVAL;
+      FAB_CUDA(cudaMemcpy(dst, c->SV, (size_t)c->s * cols * 8, cudaMemcpyDeviceToHost));
+      return FAB_OK;
+    }
+    case FAB_GET_ROWS:
+      if (c->s <= 0) return FAB_EORDER;
+      if (!need((size_t)c->s * 8)) return FAB_EINVAL;
+      FAB_CUDA(cudaMemcpy(dst, c->rows_d, (size_t)c->s * 8, cudaMemcpyDeviceToHost));
+      return FAB_OK;
+    case FAB_GET_SIGNS: {
+      if (c->s <= 0) return FAB_EORDER;
+      const size_t nb = (size_t)((c->N + 31) / 32) * 4;
+      if (!need(nb)) return FAB_EINVAL;
+      FAB_CUDA(cudaMemcpy(dst, c->signs_d, nb, cudaMemcpyDeviceToHost));
+      return FAB_OK;
+    }
+    case FAB_GET_Y:
+      if (!c->compressed) return FAB_EORDER;
+      if (!need((size_t)me * 8)) return FAB_EINVAL;
+      FAB_CUDA(cudaMemcpy(dst, svec(c, 0), (size_t)me * 8, cudaMemcpyDeviceToHost));
+      return FAB_OK;
+    case FAB_GET_C:
+      if (!c->compressed) return FAB_EORDER;
+      if (!need((size_t)me * me * 8)) return FAB_EINVAL;
+      FAB_CUDA(cudaMemcpy(dst, dmat(c, 0), (size_t)me * me * 8, cudaMemcpyDeviceToHost));
+      return FAB_OK;
+    case FAB_GET_R:
+      if (!c->compressed || c->mode == FAB_NONE) return FAB_EORDER;
+      if (!need((size_t)me * me * 8)) return FAB_EINVAL;
+      FAB_CUDA(cudaMemcpy(dst, dmat(c, 1), (size_t)me * me * 8, cudaMemcpyDeviceToHost));
+      return FAB_OK;
+    case FAB_GET_FC:
+      if (!c->compressed) return FAB_EORDER;
+      if (!need((size_t)me * 8)) return FAB_EINVAL;
+      FAB_CUDA(cudaMemcpy(dst, svec(c, 16), (size_t)me * 8, cudaMemcpyDeviceToHost));
+      return FAB_OK;
+    default:
+      return FAB_EINVAL;
+  }
+}
+
+int fab_get_column(fab_ctx* c, int j, double* dst) {
+  if (!c || !dst) return FAB_EINVAL;
+  if (!c->basis_ready) return FAB_EORDER;
+  const int cols = c->breakdown ? c->m_eff : c->m_eff + 1;
+  if (j < 0 || j >= cols) return FAB_EINVAL;
+  double bj = 0;
+  FAB_CUDA(cudaMemcpy(&bj, c->beta + j, 8, cudaMemcpyDeviceToHost));
+  FAB_CUDA(cudaMemcpy(dst, c->V + (int64_t)j * c->ld, c->n * 8, cudaMemcpyDeviceToHost));
+  for (int64_t r = 0; r < c->n; ++r) dst[r] /= bj;
+  return FAB_OK;
+}
+
+int fab_get_vrows(fab_ctx* c, const int64_t* rows, int nrows, double* dst) {
+  if (!c || !dst || !rows || nrows < 0) return FAB_EINVAL;
+  if (!c->basis_ready) return FAB_EORDER;
+  const int cols = c->breakdown ? c->m_eff : c->m_eff + 1;
+  std::vector<double> bt(cols);
+  FAB_CUDA(cudaMemcpy(bt.data(), c->beta, cols * 8, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < nrows; ++i) {
+    if (rows[i] < 0 || rows[i] >= c->n) return FAB_EINVAL;
+    FAB_CUDA(cudaMemcpy2D(dst + (int64_t)i * cols, 8, c->V + rows[i], c->ld * 8, 8, cols,
+                          cudaMemcpyDeviceToHost));
+    for (int j = 0; j < cols; ++j) dst[(int64_t)i * cols + j] /= bt[j];
+  }
+  return FAB_OK;
+}
+
+int fab_set(fab_ctx* c, int what, const void* src, size_t bytes) {
+  if (!c || !src) return FAB_EINVAL;
+  if (what == FAB_SET_POLY) {
+    const size_t n = bytes / sizeof(double);
+    if (n < 1 || n > (size_t)kPolyMax) return FAB_EINVAL;
+    memcpy(c->poly, src, n * sizeof(double));
+    c->npoly = (int)n;
+    return FAB_OK;
+  }
+  return FAB_EINVAL;
+}
+
+int fab_destroy(fab_ctx* c) {
+  if (!c) return FAB_EINVAL;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  free_ctx(c);
+  return FAB_OK;
+}
+
+const char* fab_last_error(void) { return g_err; }
+
+}  // extern "C"

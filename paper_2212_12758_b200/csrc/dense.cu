@@ -1,0 +1,544 @@
+// Small dense linear algebra on the device (m <= 1024, s <= 768):
+//
+//   dense_qr_sketch   Householder QR of Theta V_m (s x m) with R_ii >= 0 and
+//                     Q^T (Theta v_{m+1}) -- the Blendenpik preconditioner
+//                      and the sketch-and-solve factor
+//                     (Remark 2, l.249-251).  Cooperative kernel, one warp per
+//                     trailing column, one grid barrier per reflector.
+//   dense_tri_inverse R^{-1} by back substitution, one CTA per column.
+//   dense_fe1         c = f(alpha C_m + sigma I) e_1 (l.195, l.207, l.226):
+//                     exp: [13/13] Pade with scaling and squaring;
+//                     sqrt / invsqrt: scaled product-form Denman-Beavers
+//                     iteration (X -> sqrt, Z -> inverse sqrt), determinant
+//                     scaling from log|det| of Gauss-Jordan pivots;
+//                     poly: Horner-free Krylov sum p_0 e_1 + p_1 X e_1 + ...
+//   The paper uses MATLAB expm / sqrtm (l.356); these are the device
+//   counterparts (reading G-19).
+#include <cooperative_groups.h>
+#include <math.h>
+
+#include "fab_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace fab {
+
+// ---------------------------------------------------------------------------
+// Householder QR (cooperative).  A: rows x ncols_total, lda = rows.  Factors
+// the first nf columns; later columns are only transformed.  diag[j] = R_jj.
+// ---------------------------------------------------------------------------
+constexpr int kQrNQ = 24;   // rows <= 768
+
+__global__ void __launch_bounds__(kThreads)
+k_qr_coop(double* A, int rows, int nf, int ntot, double* diag) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int tw = (gridDim.x * blockDim.x) >> 5;
+  for (int j = 0; j < nf; ++j) {
+    const double* colj = A + (int64_t)j * rows;
+    double x[kQrNQ];
+    double sig = 0.0;
+#pragma unroll
+    for (int q = 0; q < kQrNQ; ++q) {
+      const int i = lane + 32 * q;
+      x[q] = (i > j && i < rows) ? colj[i] : 0.0;
+      sig = fma(x[q], x[q], sig);
+    }
+    sig = warp_sum(sig);
+    const double x0 = colj[j];
+    double beta, mu, v0;
+    if (sig == 0.0) {
+      beta = (x0 >= 0.0) ? 0.0 : 2.0;
+      mu = fabs(x0);
+      v0 = 1.0;
+    } else {
+      mu = sqrt(x0 * x0 + sig);
+      v0 = (x0 <= 0.0) ? (x0 - mu) : (-sig / (x0 + mu));
+      beta = 2.0 * v0 * v0 / (sig + v0 * v0);
+    }
+    const double iv0 = 1.0 / v0;
+    if (beta != 0.0) {
+      for (int jj = j + 1 + gw; jj < ntot; jj += tw) {
+        double* col = A + (int64_t)jj * rows;
+        double w = 0.0;
+#pragma unroll
+        for (int q = 0; q < kQrNQ; ++q) {
+          const int i = lane + 32 * q;
+          if (i > j && i < rows) w = fma(x[q] * iv0, col[i], w);
+        }
+        const double cj = col[j];
+        w = warp_sum(w) + cj;
+        const double bw = beta * w;
+        __syncwarp();
+        if (lane == 0) col[j] = cj - bw;
+#pragma unroll
+        for (int q = 0; q < kQrNQ; ++q) {
+          const int i = lane + 32 * q;
+          if (i > j && i < rows) col[i] = fma(-bw, x[q] * iv0, col[i]);
+        }
+      }
+    }
+    if (gw == 0 && lane == 0) diag[j] = mu;
+    grid.sync();
+  }
+}
+
+__global__ void k_qr_extract(const double* A, int rows, int m, const double* diag, double* R, double* qtb) {
+  const int64_t total = (int64_t)m * m;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i % m), col = (int)(i / m);
+    R[i] = (r < col) ? A[r + (int64_t)col * rows] : (r == col ? diag[r] : 0.0);
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    qtb[i] = A[i + (int64_t)m * rows];
+}
+
+static int coop_grid(fab_ctx* c, const void* fn, int want) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, 0);
+  if (occ < 1) occ = 1;
+  int mx = occ * c->num_sms;
+  if (want > mx) want = mx;
+  if (want < 1) want = 1;
+  return want;
+}
+
+double* qr_work(fab_ctx* c);   // abi.cu
+
+int dense_qr_sketch(fab_ctx* c, int m, double* R, double* qtb, cudaStream_t st) {
+  const int s = c->s;
+  if (s > 32 * kQrNQ) return FAB_EINVAL;
+  double* A = qr_work(c);
+  double* diag = svec(c, 10);
+  FAB_CUDA(cudaMemcpyAsync(A, c->SV, (size_t)s * (m + 1) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  int rows = s, nf = m, ntot = m + 1;
+  void* args[] = {&A, &rows, &nf, &ntot, &diag};
+  const int grid = coop_grid(c, (const void*)k_qr_coop, (ntot + kWarps - 1) / kWarps);
+  FAB_CUDA(cudaLaunchCooperativeKernel((const void*)k_qr_coop, grid, kThreads, args, 0, st));
+  k_qr_extract<<<(m * m + kThreads - 1) / kThreads, kThreads, 0, st>>>(A, s, m, diag, R, qtb);
+  FAB_CHECK_LAUNCH();
+  return FAB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// R^{-1} for upper triangular R (column-major m x m): CTA j solves R x = e_j
+// by column-oriented back substitution (x_i = 0 for i > j).
+// ---------------------------------------------------------------------------
+__global__ void k_tri_inverse(const double* R, int m, double* Rinv) {
+  extern __shared__ double b[];
+  const int j = blockIdx.x;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) b[i] = (i == j) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int l = j; l >= 0; --l) {
+    const double xl = b[l] / R[l + (int64_t)l * m];
+    __syncthreads();
+    if (threadIdx.x == 0) b[l] = xl;
+    for (int i = threadIdx.x; i < l; i += blockDim.x) b[i] = fma(-R[i + (int64_t)l * m], xl, b[i]);
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < m; i += blockDim.x) Rinv[i + (int64_t)j * m] = (i <= j) ? b[i] : 0.0;
+}
+
+int dense_tri_inverse(fab_ctx* c, const double* R, int m, double* Rinv, cudaStream_t st) {
+  k_tri_inverse<<<m, 128, m * sizeof(double), st>>>(R, m, Rinv);
+  FAB_CHECK_LAUNCH();
+  return FAB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// GEMM: D = alpha A B + beta C + gamma I   (m x m, column-major, ld = m).
+// D may alias C (each output element is read once, then written, by one thread).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+k_gemm(int m, const double* __restrict__ A, const double* __restrict__ B, double alpha, double beta,
+       const double* C, double gamma, double* D) {
+  __shared__ double As[32][33];
+  __shared__ double Bs[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int row0 = blockIdx.x * 32, col0 = blockIdx.y * 32;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int k0 = 0; k0 < m; k0 += 32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int kk = ty + 8 * i;
+      const int r = row0 + tx, kA = k0 + kk;
+      As[kk][tx] = (r < m && kA < m) ? A[r + (int64_t)kA * m] : 0.0;
+      const int kB = k0 + tx, cB = col0 + kk;
+      Bs[tx][kk] = (kB < m && cB < m) ? B[kB + (int64_t)cB * m] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < 32; ++kk) {
+      const double a = As[kk][tx];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = fma(a, Bs[kk][ty + 8 * i], acc[i]);
+    }
+    __syncthreads();
+  }
+  const int r = row0 + tx;
+  if (r < m) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int col = col0 + ty + 8 * i;
+      if (col < m) {
+        const int64_t o = r + (int64_t)col * m;
+        double v = alpha * acc[i];
+        if (beta != 0.0) v = fma(beta, C[o], v);
+        if (r == col) v += gamma;
+        D[o] = v;
+      }
+    }
+  }
+}
+
+static int gemm(fab_ctx* c, int m, const double* A, const double* B, double alpha, double beta,
+                const double* C, double gamma, double* D, cudaStream_t st) {
+  dim3 g((m + 31) / 32, (m + 31) / 32);
+  k_gemm<<<g, 256, 0, st>>>(m, A, B, alpha, beta, C, gamma, D);
+  FAB_CHECK_LAUNCH();
+  return FAB_OK;
+}
+
+// D = a1 X1 + a2 X2 + a3 X3 + a0 I (null pointers skipped); D may alias any Xi
+__global__ void k_lincomb(int m, double a1, const double* X1, double a2, const double* X2, double a3,
+                          const double* X3, double a0, double* D) {
+  const int64_t total = (int64_t)m * m;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i % m), col = (int)(i / m);
+    double v = (r == col) ? a0 : 0.0;
+    if (X1) v = fma(a1, X1[i], v);
+    if (X2) v = fma(a2, X2[i], v);
+    if (X3) v = fma(a3, X3[i], v);
+    D[i] = v;
+  }
+}
+
+static int lincomb(fab_ctx* c, int m, double a1, const double* X1, double a2, const double* X2, double a3,
+                   const double* X3, double a0, double* D, cudaStream_t st) {
+  const int64_t total = (int64_t)m * m;
+  int g = (int)((total + kThreads - 1) / kThreads);
+  if (g > 1024) g = 1024;
+  k_lincomb<<<g, kThreads, 0, st>>>(m, a1, X1, a2, X2, a3, X3, a0, D);
+  FAB_CHECK_LAUNCH();
+  return FAB_OK;
+}
+
+// out[0] = ||X||_1 (max column abs sum), out[1] = ||X - I||_F, out[2] = any non-finite
+__global__ void k_mat_stats(const double* X, int m, double* out) {
+  __shared__ double smax[kThreads], ssum[kThreads];
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  double mx = 0.0, fs = 0.0;
+  int b = 0;
+  for (int col = threadIdx.x; col < m; col += blockDim.x) {
+    double a = 0.0;
+    for (int r = 0; r < m; ++r) {
+      const double v = X[r + (int64_t)col * m];
+      if (!isfinite(v)) b = 1;
+      a += fabs(v);
+      const double d = v - (r == col ? 1.0 : 0.0);
+      fs = fma(d, d, fs);
+    }
+    mx = fmax(mx, a);
+  }
+  if (b) bad = 1;
+  smax[threadIdx.x] = mx;
+  ssum[threadIdx.x] = fs;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double M = 0.0, S = 0.0;
+    for (int t = 0; t < (int)blockDim.x; ++t) {
+      M = fmax(M, smax[t]);
+      S += ssum[t];
+    }
+    out[0] = M;
+    out[1] = sqrt(S);
+    out[2] = bad ? 1.0 : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Gauss-Jordan with partial pivoting (cooperative): solves A X = B in place
+// (B <- X), A destroyed.  One warp per column of [A(:, k+1:) | B]; one grid
+// barrier per pivot.  out[0] = sum log|pivot| (log|det A|), out[1] = 1 if a
+// zero pivot was met.
+// ---------------------------------------------------------------------------
+constexpr int kGjNQ = kMaxM / 32;
+
+__global__ void __launch_bounds__(kThreads)
+k_gj_coop(double* A, double* B, int m, int nrhs, double* out) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int tw = (gridDim.x * blockDim.x) >> 5;
+  double logdet = 0.0;
+  int singular = 0;
+  const int nq = (m + 31) >> 5;
+  for (int k = 0; k < m; ++k) {
+    const double* colk = A + (int64_t)k * m;
+    double cv[kGjNQ];
+    double best = -1.0;
+    int bi = m;
+#pragma unroll
+    for (int q = 0; q < kGjNQ; ++q) {
+      const int i = lane + 32 * q;
+      cv[q] = (q < nq && i < m) ? colk[i] : 0.0;
+      if (q < nq && i >= k && i < m) {
+        const double a = fabs(cv[q]);
+        if (a > best) {
+          best = a;
+          bi = i;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    const int p = bi;
+    const double piv = colk[p];
+    const double ck = colk[k];
+    if (!(best > 0.0)) singular = 1;
+    logdet += log(fabs(piv));
+    const double ipiv = 1.0 / piv;
+    // columns k+1..m-1 of A, then all of B
+    const int ncol = (m - k - 1) + nrhs;
+    for (int t = gw; t < ncol; t += tw) {
+      double* col = (t < m - k - 1) ? (A + (int64_t)(k + 1 + t) * m) : (B + (int64_t)(t - (m - k - 1)) * m);
+      const double ap = col[p], ak = col[k];
+      const double rr = ap * ipiv;   // new row k value
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < kGjNQ; ++q) {
+        const int i = lane + 32 * q;
+        if (q < nq && i < m) {
+          double nv;
+          if (i == k)
+            nv = rr;
+          else if (i == p)
+            nv = fma(-ck, rr, ak);   // old row k moves to row p
+          else
+            nv = fma(-cv[q], rr, col[i]);
+          col[i] = nv;
+        }
+      }
+    }
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    out[0] = logdet;
+    out[1] = singular ? 1.0 : 0.0;
+  }
+}
+
+// solve A X = B; A is copied to a scratch so the input survives
+static int gj_solve(fab_ctx* c, int m, const double* A, double* Awork, double* B, int nrhs, double* out,
+                    cudaStream_t st) {
+  FAB_CUDA(cudaMemcpyAsync(Awork, A, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  int mm = m, nr = nrhs;
+  void* args[] = {&Awork, &B, &mm, &nr, &out};
+  const int grid = coop_grid(c, (const void*)k_gj_coop, (m + nrhs + kWarps - 1) / kWarps);
+  FAB_CUDA(cudaLaunchCooperativeKernel((const void*)k_gj_coop, grid, kThreads, args, 0, st));
+  return FAB_OK;
+}
+
+__global__ void k_gemv_e(const double* X, int m, const double* u, double* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    double a = 0.0;
+    for (int j = 0; j < m; ++j) a = fma(X[i + (int64_t)j * m], u[j], a);
+    out[i] = a;
+  }
+}
+__global__ void k_axpy_small(int m, double a, const double* x, double* y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) y[i] = fma(a, x[i], y[i]);
+}
+__global__ void k_unit(int m, double a, double* y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) y[i] = (i == 0) ? a : 0.0;
+}
+
+static int read_stats(fab_ctx* c, const double* X, int m, double* h, cudaStream_t st) {
+  double* d = svec(c, 11);
+  k_mat_stats<<<1, kThreads, 0, st>>>(X, m, d);
+  FAB_CHECK_LAUNCH();
+  FAB_CUDA(cudaMemcpyAsync(h, d, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FAB_CUDA(cudaStreamSynchronize(st));
+  return FAB_OK;
+}
+
+#define FAB_TRY(x)          \
+  do {                      \
+    int rc__ = (x);         \
+    if (rc__ != FAB_OK) return rc__; \
+  } while (0)
+
+// exp by [13/13] Pade with scaling and squaring (theta_13 = 5.371920351148152)
+static int expm_e1(fab_ctx* c, int m, const double* X0, double* c_out, int* iters, cudaStream_t st) {
+  static const double b[14] = {64764752532480000.0, 32382376266240000.0, 7771770303897600.0,
+                               1187353796428800.0,  129060195264000.0,   10559470521600.0,
+                               670442572800.0,      33522128640.0,       1323241920.0,
+                               40840800.0,          960960.0,            16380.0,
+                               182.0,               1.0};
+  double* X = dmat(c, 5);
+  double* X2 = dmat(c, 6);
+  double* X4 = dmat(c, 7);
+  double* X6 = dmat(c, 8);
+  double* T = dmat(c, 9);
+  double* U = dmat(c, 10);
+  double* Vp = dmat(c, 11);
+  double* P = dmat(c, 12);
+  double* W = dmat(c, 13);
+  double h[3];
+  FAB_TRY(read_stats(c, X0, m, h, st));
+  if (h[2] != 0.0) return FAB_EDOMAIN;
+  const double theta13 = 5.371920351148152;
+  int s = 0;
+  if (h[0] > theta13) s = (int)ceil(log2(h[0] / theta13));
+  if (s < 0) s = 0;
+  const double sc = ldexp(1.0, -s);
+  FAB_TRY(lincomb(c, m, sc, X0, 0, nullptr, 0, nullptr, 0.0, X, st));
+  FAB_TRY(gemm(c, m, X, X, 1.0, 0.0, nullptr, 0.0, X2, st));
+  FAB_TRY(gemm(c, m, X2, X2, 1.0, 0.0, nullptr, 0.0, X4, st));
+  FAB_TRY(gemm(c, m, X4, X2, 1.0, 0.0, nullptr, 0.0, X6, st));
+  // U = X [X6 (b13 X6 + b11 X4 + b9 X2) + b7 X6 + b5 X4 + b3 X2 + b1 I]
+  FAB_TRY(lincomb(c, m, b[13], X6, b[11], X4, b[9], X2, 0.0, T, st));
+  FAB_TRY(gemm(c, m, X6, T, 1.0, 0.0, nullptr, 0.0, W, st));
+  FAB_TRY(lincomb(c, m, 1.0, W, b[7], X6, b[5], X4, b[1], T, st));
+  FAB_TRY(lincomb(c, m, 1.0, T, b[3], X2, 0, nullptr, 0.0, T, st));
+  FAB_TRY(gemm(c, m, X, T, 1.0, 0.0, nullptr, 0.0, U, st));
+  // V = X6 (b12 X6 + b10 X4 + b8 X2) + b6 X6 + b4 X4 + b2 X2 + b0 I
+  FAB_TRY(lincomb(c, m, b[12], X6, b[10], X4, b[8], X2, 0.0, T, st));
+  FAB_TRY(gemm(c, m, X6, T, 1.0, 0.0, nullptr, 0.0, W, st));
+  FAB_TRY(lincomb(c, m, 1.0, W, b[6], X6, b[4], X4, b[0], Vp, st));
+  FAB_TRY(lincomb(c, m, 1.0, Vp, b[2], X2, 0, nullptr, 0.0, Vp, st));
+  // (V - U) R = (V + U)
+  FAB_TRY(lincomb(c, m, 1.0, Vp, -1.0, U, 0, nullptr, 0.0, P, st));
+  FAB_TRY(lincomb(c, m, 1.0, Vp, 1.0, U, 0, nullptr, 0.0, T, st));
+  double* gout = svec(c, 12);
+  FAB_TRY(gj_solve(c, m, P, W, T, m, gout, st));
+  double gh[2];
+  FAB_CUDA(cudaMemcpyAsync(gh, gout, sizeof(gh), cudaMemcpyDeviceToHost, st));
+  FAB_CUDA(cudaStreamSynchronize(st));
+  if (gh[1] != 0.0 || !isfinite(gh[0])) return FAB_ESINGULAR;
+  // square s times (the last squaring only needs the first column)
+  double* cur = T;
+  double* nxt = X2;
+  for (int i = 0; i < s; ++i) {
+    if (i == s - 1) {
+      k_gemv_e<<<(m + 127) / 128, 128, 0, st>>>(cur, m, cur, c_out);   // cur * cur[:,0]
+      FAB_CHECK_LAUNCH();
+      *iters = s;
+      return FAB_OK;
+    }
+    FAB_TRY(gemm(c, m, cur, cur, 1.0, 0.0, nullptr, 0.0, nxt, st));
+    double* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+  FAB_CUDA(cudaMemcpyAsync(c_out, cur, m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  *iters = s;
+  return FAB_OK;
+}
+
+// sqrt / inverse sqrt by the scaled product-form Denman-Beavers iteration:
+//   M_0 = X, Y_0 = X, Z_0 = I
+//   mu_k = |det M_k|^{-1/(2m)}  (while ||M_k - I||_F > 1e-2, else 1)
+//   Y_{k+1} = mu/2 Y_k (I + mu^-2 M_k^-1),  Z_{k+1} = mu/2 Z_k (I + mu^-2 M_k^-1)
+//   M_{k+1} = 1/2 I + mu^2/4 M_k + mu^-2/4 M_k^-1
+// Y -> X^{1/2}, Z -> X^{-1/2}, M -> I.
+static int db_e1(fab_ctx* c, int m, const double* X0, int want_inv, double* c_out, int* iters,
+                 cudaStream_t st) {
+  double* M = dmat(c, 5);
+  double* Y = dmat(c, 6);
+  double* Z = dmat(c, 7);
+  double* Mi = dmat(c, 8);
+  double* Wk = dmat(c, 9);
+  double* T = dmat(c, 10);
+  double* Y2 = dmat(c, 11);
+  double* Z2 = dmat(c, 12);
+  double* gout = svec(c, 12);
+  FAB_CUDA(cudaMemcpyAsync(M, X0, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  FAB_CUDA(cudaMemcpyAsync(Y, X0, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  FAB_TRY(lincomb(c, m, 0, nullptr, 0, nullptr, 0, nullptr, 1.0, Z, st));
+  double h[3];
+  FAB_TRY(read_stats(c, M, m, h, st));
+  if (h[2] != 0.0) return FAB_EDOMAIN;
+  double err = h[1];
+  bool extra_done = false;
+  const int maxit = 100;
+  for (int it = 0; it < maxit; ++it) {
+    FAB_TRY(lincomb(c, m, 0, nullptr, 0, nullptr, 0, nullptr, 1.0, Mi, st));
+    FAB_TRY(gj_solve(c, m, M, Wk, Mi, m, gout, st));
+    double gh[2];
+    FAB_CUDA(cudaMemcpyAsync(gh, gout, sizeof(gh), cudaMemcpyDeviceToHost, st));
+    FAB_CUDA(cudaStreamSynchronize(st));
+    if (gh[1] != 0.0 || !isfinite(gh[0])) return FAB_EDOMAIN;
+    double mu = 1.0;
+    if (err > 1e-2) mu = exp(-gh[0] / (2.0 * m));
+    const double imu2 = 1.0 / (mu * mu);
+    FAB_TRY(lincomb(c, m, imu2, Mi, 0, nullptr, 0, nullptr, 1.0, T, st));   // I + mu^-2 M^-1
+    FAB_TRY(gemm(c, m, Y, T, 0.5 * mu, 0.0, nullptr, 0.0, Y2, st));
+    FAB_TRY(gemm(c, m, Z, T, 0.5 * mu, 0.0, nullptr, 0.0, Z2, st));
+    double* t;
+    t = Y; Y = Y2; Y2 = t;
+    t = Z; Z = Z2; Z2 = t;
+    FAB_TRY(lincomb(c, m, 0.25 * mu * mu, M, 0.25 * imu2, Mi, 0, nullptr, 0.5, M, st));
+    FAB_TRY(read_stats(c, M, m, h, st));
+    if (h[2] != 0.0) return FAB_EDOMAIN;
+    err = h[1];
+    *iters = it + 1;
+    if (extra_done) break;
+    if (err <= 1e-12 * sqrt((double)m)) extra_done = true;   // one more step after convergence
+  }
+  if (!extra_done) return FAB_ENOCONV;
+  FAB_CUDA(cudaMemcpyAsync(c_out, want_inv ? Z : Y, m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  return FAB_OK;
+}
+
+static int poly_e1(fab_ctx* c, int m, const double* X, double* c_out, cudaStream_t st) {
+  double* u = svec(c, 13);
+  double* u2 = svec(c, 14);
+  const int g = (m + 127) / 128;
+  k_unit<<<g, 128, 0, st>>>(m, 1.0, u);
+  k_unit<<<g, 128, 0, st>>>(m, c->npoly > 0 ? c->poly[0] : 0.0, c_out);
+  for (int i = 1; i < c->npoly; ++i) {
+    k_gemv_e<<<g, 128, 0, st>>>(X, m, u, u2);
+    k_axpy_small<<<g, 128, 0, st>>>(m, c->poly[i], u2, c_out);
+    double* t = u;
+    u = u2;
+    u2 = t;
+  }
+  FAB_CHECK_LAUNCH();
+  return FAB_OK;
+}
+
+int dense_fe1(fab_ctx* c, int f, double alpha, double sigma, double* c_out, int* iters) {
+  const int m = c->m_eff;
+  cudaStream_t st = c->stream;
+  const double* C = dmat(c, 0);
+  double* X = dmat(c, 4);
+  *iters = 0;
+  FAB_TRY(lincomb(c, m, alpha, C, 0, nullptr, 0, nullptr, sigma, X, st));   // alpha C + sigma I
+  switch (f) {
+    case FAB_EXP:
+      return expm_e1(c, m, X, c_out, iters, st);
+    case FAB_SQRT:
+      return db_e1(c, m, X, 0, c_out, iters, st);
+    case FAB_INVSQRT:
+      return db_e1(c, m, X, 1, c_out, iters, st);
+    case FAB_POLY:
+      return poly_e1(c, m, X, c_out, st);
+    default:
+      return FAB_EINVAL;
+  }
+}
+
+}  // namespace fab

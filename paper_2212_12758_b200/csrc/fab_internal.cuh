@@ -1,0 +1,198 @@
+// Internal definitions shared by the fab CUDA sources (sm_100a).
+// Nothing here is visible through the C ABI (include/fab.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <vector>
+
+#include "../../include/fab.h"
+
+namespace fab {
+
+constexpr int kThreads = 256;     // streaming kernels: 8 warps per CTA
+constexpr int kWarps = kThreads / 32;
+constexpr int kKMax = 8;          // largest supported truncation window k
+constexpr int kSkLogT = 12;       // SRHT tile: T = 4096 consecutive global rows
+constexpr int kSkT = 1 << kSkLogT;
+constexpr int kSkPer = kSkT / kThreads;   // 16 elements per thread per tile
+constexpr int kMaxM = 1024;       // largest m (dense step, coefficient buffers)
+constexpr int kPolyMax = 64;
+
+// Device-resident status / scalar state of one context.  Kernels read and
+// write it; the host reads it (pinned mirror) only at synchronizing calls.
+struct DevState {
+  int breakdown;        // Alg 2 breakdown seen (G-5)
+  int m_eff;            // number of basis vectors v_1..v_m_eff
+  int lsqr_done;        // LSQR converged (tolerance mode)
+  int lsqr_iters;       // LSQR iterations performed
+  int err;              // device-side error code (FAB_E*)
+  int dense_flag;       // dense step status
+  int pad[2];
+  double gamma;         // ||b||
+  double norm_inf;      // ||A||_inf
+  double thresh;        // breakdown threshold 1e-14 ||A||_inf
+  // LSQR scalars (Paige-Saunders), see lsqr.cu
+  double alpha, beta, phibar, rhobar, anorm2, rnorm, arnorm, anorm;
+  double scal;          // coefficient of the previous t in the next pass
+  double tol;
+  double logdet;        // log|det| from the last Gauss-Jordan solve
+  double scratch[8];
+};
+
+}  // namespace fab
+
+// The opaque context of the ABI.
+struct fab_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;   // caller's stream
+  cudaStream_t cap = nullptr;      // internal stream used for graph capture
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_join = nullptr;
+
+  // operator
+  fab_operator op{};
+  bool stencil = false;
+  int64_t n = 0;          // local rows
+  int64_t n_global = 0;
+  int64_t row_begin = 0;
+  int64_t ld = 0;         // column stride of V (doubles)
+  int64_t N = 0;          // SRHT length, next pow2 of n_global
+  double norm_inf = 0.0;
+
+  // capacity
+  int m_max = 0, k_max = 0, s_max = 0;
+
+  // workspace
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  bool own_ws = false;
+
+  double* V = nullptr;       // (m_max+1) * ld
+  double* vec = nullptr;     // ld: z (basis) / t (LSQR) / y staging (apply)
+  double* H = nullptr;       // (m_max+1) x m_max, ldH = m_max+1
+  int ldH = 0;
+  double* beta = nullptr;    // m_max+2 norms of stored columns
+  double* coef = nullptr;    // (m_max+2) * (kKMax+1) update coefficients per step
+  double* part_dots = nullptr;   // grid_spmv * (kKMax+1)
+  double* part_norm = nullptr;   // 2 * grid_upd (double buffered)
+  double* part_sk = nullptr;     // (m_max+1) * grid_upd * s_max
+  double* SV = nullptr;          // s_max x (m_max+1)
+  int64_t* rows_d = nullptr;     // s_max
+  uint32_t* signs_d = nullptr;   // N/32 words
+  double* part_g = nullptr;      // grid_lsqr * (m_max+1)
+  double* part_tn = nullptr;     // grid_lsqr
+  double* small = nullptr;       // small vectors (LSQR, dense)
+  double* dense = nullptr;       // dense pool: kDenseMats * m_max^2
+  fab::DevState* st_d = nullptr;
+  fab::DevState* st_h = nullptr; // pinned mirror
+
+  // grids
+  int grid_spmv = 0, grid_upd = 0, grid_lsqr = 0, grid_comb = 0;
+
+  // state
+  bool basis_ready = false, sketch_ready = false, sketch_in_V = false;
+  bool compressed = false;
+  int m = 0, k = 0, s = 0, m_eff = 0;
+  uint64_t seed = 0;
+  int mode = -1;
+  bool breakdown = false;
+  int npoly = 0;
+  double poly[fab::kPolyMax];
+
+  // cached basis graph
+  cudaGraphExec_t gexec = nullptr;
+  int g_m = -1, g_k = -1, g_s = -1;
+  bool g_fused = false;
+  int64_t g_launches = 0;
+
+  fab_info info{};
+};
+
+// ------------------------------------------------------------------------
+// helpers
+// ------------------------------------------------------------------------
+#define FAB_CUDA(call)                                                   \
+  do {                                                                   \
+    cudaError_t e__ = (call);                                            \
+    if (e__ != cudaSuccess) {                                            \
+      fab::set_last_cuda_error(e__, #call, __FILE__, __LINE__);          \
+      return FAB_ECUDA;                                                  \
+    }                                                                    \
+  } while (0)
+
+#define FAB_CHECK_LAUNCH() FAB_CUDA(cudaGetLastError())
+
+namespace fab {
+
+void set_last_cuda_error(cudaError_t e, const char* what, const char* file, int line);
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Fixed-order block reduction of NV values per thread; result valid in
+// thread 0 (out[j]).  smem must hold kWarps*NV doubles.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* smem, double (&out)[NV]) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    double x = warp_sum(v[j]);
+    if (lane == 0) smem[wid * NV + j] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      double acc = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) acc += smem[w * NV + j];
+      out[j] = acc;
+    }
+  }
+  __syncthreads();
+}
+
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+inline int64_t next_pow2(int64_t n) {
+  int64_t p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+// ---- sub-module entry points (host side) ---------------------------------
+// basis.cu
+int basis_setup_grids(fab_ctx* c);
+int init_vector_norm(fab_ctx* c);            // partial norms of column 0, norm_inf
+int run_basis(fab_ctx* c, int m, int k);
+void release_long_rows(fab_ctx* c);
+int launch_sketch_cols(fab_ctx* c, int c0, int c1, cudaStream_t st);
+// sketch.cu
+void host_sketch_rows(uint64_t seed, int64_t N, int s, int64_t* out);
+int sketch_draw(fab_ctx* c, int s, uint64_t seed);
+int sketch_batched(fab_ctx* c);              // K5: Theta V_{m+1} after the basis
+int sketch_finalize(fab_ctx* c, int ncols, cudaStream_t st);
+// lsqr.cu / compress
+int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn);
+// dense.cu
+int dense_fe1(fab_ctx* c, int f, double alpha, double sigma, double* c_out, int* iters);
+int dense_qr_sketch(fab_ctx* c, int m, double* R, double* qtb, cudaStream_t st);
+int dense_tri_inverse(fab_ctx* c, const double* R, int m, double* Rinv, cudaStream_t st);
+// apply.cu
+int run_combine(fab_ctx* c, const double* coef_d, double* y_dev);
+
+// the dense pool layout (matrices of m_max^2 doubles)
+constexpr int kDenseMats = 14;
+inline double* dmat(fab_ctx* c, int i) { return c->dense + (size_t)i * c->m_max * c->m_max; }
+// small vector pool layout (each kSmall doubles)
+constexpr int kSmall = kMaxM + 8;
+inline double* svec(fab_ctx* c, int i) { return c->small + (size_t)i * kSmall; }
+constexpr int kSmallVecs = 24;
+
+}  // namespace fab

@@ -1,0 +1,421 @@
+// Compression C_m = V_m^+ A V_m = H_m + h_{m+1,m} y e_m^T (Eq. (6), PAPER.md
+// l.167-171), y = argmin ||V_m z - v_{m+1}|| (Eq. (7), l.174-177):
+//
+//   FAB_BLENDENPIK   QR of the sketch Theta V_m = Q R (Householder, R_ii >= 0)
+//                    and LSQR (Paige & Saunders) on M = V_m R^{-1} (l.183),
+//                    y = R^{-1} z.  One fused streaming pass over V_m per
+//                    iteration (k_lsqr_pass): t <- W p - scal t,
+//                    g = W^T t, ||t||^2, where W holds the unnormalized
+//                    stored columns (V_m = W diag(1/beta)).
+//   FAB_SKETCH_SOLVE y = R^{-1} (Q^T Theta v_{m+1})  (Remark 2, l.249-251)
+//   FAB_NONE         y = 0  (Algorithm 5, l.219-228)
+//
+// The LSQR scalar recurrence runs on the device (k_lsqr_scalar); the host
+// only polls convergence between chunks of iterations.
+#include <math.h>
+
+#include "fab_internal.cuh"
+
+namespace fab {
+
+constexpr int kLsqrThreads = 512;
+constexpr int kLsqrWarps = kLsqrThreads / 32;
+
+// t_new[r] = sum_j W[r,j] p_j - scal * t_old[r];  g_j += W[r,j] t_new[r];
+// tn += t_new[r]^2.  32-row tiles; warp w owns columns j = w + 16 jj.
+// t_old may alias t_new (each row is read before any warp writes it).
+template <int JPW>
+__global__ void __launch_bounds__(kLsqrThreads)
+k_lsqr_pass(const double* __restrict__ W, int64_t ld, int m, int64_t n, const double* __restrict__ p,
+            double scal_unused, const double* t_old, double* t_new, double* __restrict__ part_g,
+            double* __restrict__ part_tn, const DevState* __restrict__ st, int use_state_scal) {
+  if (st->lsqr_done) return;
+  __shared__ double sp[kMaxM];
+  __shared__ double tpart[kLsqrWarps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = threadIdx.x; j < m; j += blockDim.x) sp[j] = p[j];
+  const double scal = use_state_scal ? st->scal : scal_unused;
+  __syncthreads();
+  double acc[JPW];
+#pragma unroll
+  for (int jj = 0; jj < JPW; ++jj) acc[jj] = 0.0;
+  double tn = 0.0;
+  const int64_t ntiles = (n + 31) >> 5;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r = (tile << 5) + lane;
+    const bool valid = r < n;
+    double vr[JPW];
+    double tp = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < JPW; ++jj) {
+      const int j = warp + kLsqrWarps * jj;
+      vr[jj] = (valid && j < m) ? __ldg(W + (int64_t)j * ld + r) : 0.0;
+    }
+    const double told = valid ? t_old[r] : 0.0;
+#pragma unroll
+    for (int jj = 0; jj < JPW; ++jj) {
+      const int j = warp + kLsqrWarps * jj;
+      if (j < m) tp = fma(vr[jj], sp[j], tp);
+    }
+    tpart[warp][lane] = tp;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < kLsqrWarps; ++w) t += tpart[w][lane];
+    t = fma(-scal, told, t);
+    if (!valid) t = 0.0;
+    if (warp == 0 && valid) {
+      t_new[r] = t;
+      tn = fma(t, t, tn);
+    }
+#pragma unroll
+    for (int jj = 0; jj < JPW; ++jj) acc[jj] = fma(vr[jj], t, acc[jj]);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int jj = 0; jj < JPW; ++jj) {
+    const int j = warp + kLsqrWarps * jj;
+    const double a = warp_sum(acc[jj]);
+    if (lane == 0 && j < m) part_g[(int64_t)blockIdx.x * m + j] = a;
+  }
+  if (warp == 0) {
+    const double a = warp_sum(tn);
+    if (lane == 0) part_tn[blockIdx.x] = a;
+  }
+}
+
+typedef void (*LsqrPassFn)(const double*, int64_t, int, int64_t, const double*, double, const double*,
+                           double*, double*, double*, const DevState*, int);
+
+static LsqrPassFn pick_pass(int m, int* jpw) {
+  const int need = (m + kLsqrWarps - 1) / kLsqrWarps;
+#define FAB_PICK(J)              \
+  if (need <= J) {               \
+    *jpw = J;                    \
+    return k_lsqr_pass<J>;       \
+  }
+  FAB_PICK(2) FAB_PICK(4) FAB_PICK(8) FAB_PICK(13) FAB_PICK(16) FAB_PICK(19) FAB_PICK(24)
+  FAB_PICK(32) FAB_PICK(48) FAB_PICK(64)
+#undef FAB_PICK
+  return nullptr;
+}
+
+// ---- small helpers (one CTA of kThreads) ---------------------------------
+// out_i = scale_i * sum_{j>=i} U[i,j] v_j   (U upper triangular, given as UT =
+// U^T column-major: U[i,j] = UT[j + i*m]); warp per output, fixed order.
+__device__ void upper_gemv(const double* UT, int m, const double* v, const double* rscale, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = warp; i < m; i += nw) {
+    double a = 0.0;
+    for (int j = i + lane; j < m; j += 32) a = fma(UT[j + (int64_t)i * m], v[j], a);
+    a = warp_sum(a);
+    if (lane == 0) out[i] = rscale ? a * rscale[i] : a;
+  }
+}
+// out_i = sum_{j<=i} U[j,i] q_j   (U^T q; column i of U is contiguous)
+__device__ void upperT_gemv(const double* U, int m, const double* q, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = warp; i < m; i += nw) {
+    double a = 0.0;
+    for (int j = lane; j <= i; j += 32) a = fma(U[j + (int64_t)i * m], q[j], a);
+    a = warp_sum(a);
+    if (lane == 0) out[i] = a;
+  }
+}
+
+__device__ double block_norm2(const double* v, int m, double* red) {
+  double a = 0.0;
+  for (int j = threadIdx.x; j < m; j += blockDim.x) a = fma(v[j], v[j], a);
+  double v1[1] = {a}, o1[1];
+  block_sum<1>(v1, red, o1);
+  __shared__ double bc;
+  if (threadIdx.x == 0) bc = o1[0];
+  __syncthreads();
+  return bc;
+}
+
+struct LsqrVecs {
+  double *g, *q, *v, *w, *x, *p, *tmp;
+};
+
+// fixed-order reduction of the pass partials -> g (m), returns ||t||^2
+__device__ double reduce_pass(const double* part_g, const double* part_tn, int nparts, int m, double* g,
+                              double* red) {
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    double a = 0.0;
+    for (int b = 0; b < nparts; ++b) a += part_g[(int64_t)b * m + j];
+    g[j] = a;
+  }
+  __shared__ double tn;
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int b = 0; b < nparts; ++b) a += part_tn[b];
+    tn = a;
+  }
+  __syncthreads();
+  return tn;
+}
+
+// LSQR initialisation after the pass t = w_hat_m, g = W^T t:
+//   beta_1 u_1 = v_{m+1} (unit), alpha_1 v_1 = M^T u_1, w_1 = v_1, x_0 = 0
+__global__ void k_lsqr_init(const double* part_g, const double* part_tn, int nparts, int m,
+                            const double* Rinv, const double* RinvT, const double* bcol, LsqrVecs L,
+                            double tol, DevState* st) {
+  __shared__ double red[kWarps];
+  const double tn = reduce_pass(part_g, part_tn, nparts, m, L.g, red);
+  const double bt = sqrt(tn);
+  for (int j = threadIdx.x; j < m; j += blockDim.x) L.q[j] = L.g[j] / bcol[j] / bt;
+  __syncthreads();
+  upperT_gemv(Rinv, m, L.q, L.tmp);                      // M^T u_1 = R^{-T} diag(1/beta) g / bt
+  __syncthreads();
+  const double a2 = block_norm2(L.tmp, m, red);
+  const double alpha = sqrt(a2);
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    const double vj = alpha > 0 ? L.tmp[j] / alpha : 0.0;
+    L.v[j] = vj;
+    L.w[j] = vj;
+    L.x[j] = 0.0;
+  }
+  __syncthreads();
+  upper_gemv(RinvT, m, L.v, nullptr, L.p);               // p = R^{-1} v
+  __syncthreads();
+  for (int j = threadIdx.x; j < m; j += blockDim.x) L.p[j] /= bcol[j];   // diag(1/beta)
+  if (threadIdx.x == 0) {
+    st->alpha = alpha;
+    st->beta = bt;             // scale of u = t / bt
+    st->phibar = 1.0;          // ||b|| = ||v_{m+1}|| = 1
+    st->rhobar = alpha;
+    st->anorm2 = 0.0;
+    st->rnorm = 1.0;
+    st->arnorm = alpha;
+    st->anorm = 0.0;
+    st->scal = alpha / bt;     // next pass: t <- W p - alpha u = W p - (alpha/bt) t
+    st->tol = tol;
+    st->lsqr_iters = 0;
+    st->lsqr_done = (alpha == 0.0) ? 1 : 0;
+  }
+}
+
+// one LSQR iteration's scalar work after the pass t_new = M v - alpha u
+__global__ void k_lsqr_step(const double* part_g, const double* part_tn, int nparts, int m,
+                            const double* Rinv, const double* RinvT, const double* bcol, LsqrVecs L,
+                            int tol_mode, DevState* st) {
+  if (st->lsqr_done) return;
+  __shared__ double red[kWarps];
+  const double tn = reduce_pass(part_g, part_tn, nparts, m, L.g, red);
+  const double beta = sqrt(tn);
+  const double ib = beta > 0 ? 1.0 / beta : 0.0;
+  const double alpha_old = st->alpha;
+  for (int j = threadIdx.x; j < m; j += blockDim.x) L.q[j] = L.g[j] / bcol[j] * ib;
+  __syncthreads();
+  upperT_gemv(Rinv, m, L.q, L.tmp);                      // M^T u_{i+1}
+  __syncthreads();
+  for (int j = threadIdx.x; j < m; j += blockDim.x) L.tmp[j] = fma(-beta, L.v[j], L.tmp[j]);
+  __syncthreads();
+  const double alpha = sqrt(block_norm2(L.tmp, m, red));
+  const double rhobar0 = st->rhobar, phibar0 = st->phibar;
+  const double rho = hypot(rhobar0, beta);
+  const double cs = rhobar0 / rho, sn = beta / rho;
+  const double theta = sn * alpha;
+  const double phi = cs * phibar0;
+  const double phibar = sn * phibar0;
+  const double ia = alpha > 0 ? 1.0 / alpha : 0.0;
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    const double vn = L.tmp[j] * ia;
+    L.x[j] = fma(phi / rho, L.w[j], L.x[j]);
+    L.w[j] = fma(-(theta / rho), L.w[j], vn);
+    L.v[j] = vn;
+  }
+  __syncthreads();
+  upper_gemv(RinvT, m, L.v, nullptr, L.p);
+  __syncthreads();
+  for (int j = threadIdx.x; j < m; j += blockDim.x) L.p[j] /= bcol[j];
+  if (threadIdx.x == 0) {
+    const double anorm2 = st->anorm2 + alpha_old * alpha_old + beta * beta;
+    const double anorm = sqrt(anorm2);
+    const double rnorm = phibar;
+    const double arnorm = phibar * alpha * fabs(cs);
+    st->anorm2 = anorm2;
+    st->anorm = anorm;
+    st->rnorm = rnorm;
+    st->arnorm = arnorm;
+    st->alpha = alpha;
+    st->beta = beta;
+    st->rhobar = -cs * alpha;
+    st->phibar = phibar;
+    st->scal = beta > 0 ? alpha / beta : 0.0;
+    st->lsqr_iters += 1;
+    if (tol_mode) {
+      const double tol = st->tol;
+      if (rnorm <= tol || (rnorm > 0 && arnorm <= tol * anorm * rnorm) || alpha == 0.0 || beta == 0.0)
+        st->lsqr_done = 1;
+    }
+  }
+}
+
+// y = R^{-1} x ;  C = H_m + h_{m+1,m} y e_m^T
+__global__ void k_finish_y(const double* RinvT, const double* x, int m, double* y) {
+  upper_gemv(RinvT, m, x, nullptr, y);
+}
+
+__global__ void k_build_C(const double* H, int ldH, const double* y, int m, int use_y, double* C) {
+  const int64_t total = (int64_t)m * m;
+  const double h = H[m + (int64_t)(m - 1) * ldH];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i % m), col = (int)(i / m);
+    double v = H[r + (int64_t)col * ldH];
+    if (use_y && col == m - 1) v = fma(h, y[r], v);
+    C[i] = v;
+  }
+}
+
+__global__ void k_transpose(const double* A, int m, double* AT) {
+  const int64_t total = (int64_t)m * m;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i % m), col = (int)(i / m);
+    AT[col + (int64_t)r * m] = A[i];
+  }
+}
+
+__global__ void k_reset_lsqr(DevState* st) {
+  st->lsqr_done = 0;
+  st->lsqr_iters = 0;
+}
+
+// R checks: out = {min |R_ii|, max |R_ii|, ||R||_1 ||R^{-1}||_1}
+__global__ void k_r_stats(const double* R, const double* Rinv, int m, double* out) {
+  __shared__ double s1[kThreads], s2[kThreads], s3[kThreads], s4[kThreads];
+  double mn = INFINITY, mx = 0.0, n1 = 0.0, n2 = 0.0;
+  for (int col = threadIdx.x; col < m; col += blockDim.x) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i <= col; ++i) {
+      a += fabs(R[i + (int64_t)col * m]);
+      b += fabs(Rinv[i + (int64_t)col * m]);
+    }
+    const double d = fabs(R[col + (int64_t)col * m]);
+    mn = fmin(mn, d);
+    mx = fmax(mx, d);
+    n1 = fmax(n1, a);
+    n2 = fmax(n2, b);
+  }
+  s1[threadIdx.x] = mn;
+  s2[threadIdx.x] = mx;
+  s3[threadIdx.x] = n1;
+  s4[threadIdx.x] = n2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int t = 1; t < (int)blockDim.x; ++t) {
+      mn = fmin(mn, s1[t]);
+      mx = fmax(mx, s2[t]);
+      n1 = fmax(n1, s3[t]);
+      n2 = fmax(n2, s4[t]);
+    }
+    out[0] = mn;
+    out[1] = mx;
+    out[2] = n1 * n2;
+  }
+}
+
+int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
+  *warn = FAB_OK;
+  const int m = c->m_eff;
+  double* C = dmat(c, 0);
+  double* R = dmat(c, 1);
+  double* Rinv = dmat(c, 2);
+  double* RinvT = dmat(c, 3);
+  double* y = svec(c, 0);
+  double* qtb = svec(c, 1);
+  double* stats = svec(c, 2);
+  LsqrVecs L{svec(c, 3), svec(c, 4), svec(c, 5), svec(c, 6), svec(c, 7), svec(c, 8), svec(c, 9)};
+  cudaStream_t st = c->stream;
+  c->info.lsqr_iters = 0;
+  c->info.lsqr_converged = 0;
+  c->info.cond_R = 0.0;
+  int64_t launches = 0;
+  const bool need_ls = (mode != FAB_NONE) && !c->breakdown;
+  if (mode != FAB_NONE && !c->sketch_in_V) return FAB_EORDER;
+  if (need_ls) {
+    // QR of Theta V_m (s x m) with Theta v_{m+1} as an extra column
+    int rc = dense_qr_sketch(c, m, R, qtb, st);
+    if (rc != FAB_OK) return rc;
+    launches += 2;
+    rc = dense_tri_inverse(c, R, m, Rinv, st);
+    if (rc != FAB_OK) return rc;
+    ++launches;
+    k_r_stats<<<1, kThreads, 0, st>>>(R, Rinv, m, stats);
+    FAB_CHECK_LAUNCH();
+    ++launches;
+    k_transpose<<<(m * m + kThreads - 1) / kThreads, kThreads, 0, st>>>(Rinv, m, RinvT);
+    FAB_CHECK_LAUNCH();
+    ++launches;
+    double hs[3];
+    FAB_CUDA(cudaMemcpyAsync(hs, stats, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    FAB_CUDA(cudaStreamSynchronize(st));
+    c->info.cond_R = hs[2];
+    if (!(hs[0] >= 1e-14 * hs[1])) return FAB_ESINGULAR;
+    if (hs[2] > 1e8) *warn = FAB_ILLCOND;
+    if (mode == FAB_SKETCH_SOLVE) {
+      k_finish_y<<<1, kThreads, 0, st>>>(RinvT, qtb, m, y);
+      FAB_CHECK_LAUNCH();
+      ++launches;
+    } else {
+      int jpw = 0;
+      LsqrPassFn pass = pick_pass(m, &jpw);
+      if (!pass) return FAB_EINVAL;
+      const int fixed = (o && o->iters > 0) ? o->iters : 0;
+      const double tol = (o && o->tol > 0) ? o->tol : 1e-6;
+      const int maxit = fixed ? fixed : ((o && o->maxit > 0) ? o->maxit : 4 * m);
+      const int G = c->grid_lsqr;
+      // init pass: p = 0, t_old = w_hat_m, scal = -1  ->  t = w_hat_m, g = W^T t
+      FAB_CUDA(cudaMemsetAsync(L.p, 0, m * sizeof(double), st));
+      k_reset_lsqr<<<1, 1, 0, st>>>(c->st_d);
+      pass<<<G, kLsqrThreads, 0, st>>>(c->V, c->ld, m, c->n, L.p, -1.0, c->V + (int64_t)m * c->ld,
+                                       c->vec, c->part_g, c->part_tn, c->st_d, 0);
+      FAB_CHECK_LAUNCH();
+      k_lsqr_init<<<1, kThreads, 0, st>>>(c->part_g, c->part_tn, G, m, Rinv, RinvT, c->beta, L, tol,
+                                          c->st_d);
+      FAB_CHECK_LAUNCH();
+      launches += 2;
+      int done_iters = 0;
+      const int chunk = fixed ? maxit : 4;
+      while (done_iters < maxit) {
+        const int nit = (maxit - done_iters) < chunk ? (maxit - done_iters) : chunk;
+        for (int it = 0; it < nit; ++it) {
+          pass<<<G, kLsqrThreads, 0, st>>>(c->V, c->ld, m, c->n, L.p, 0.0, c->vec, c->vec, c->part_g,
+                                           c->part_tn, c->st_d, 1);
+          FAB_CHECK_LAUNCH();
+          k_lsqr_step<<<1, kThreads, 0, st>>>(c->part_g, c->part_tn, G, m, Rinv, RinvT, c->beta, L,
+                                              fixed ? 0 : 1, c->st_d);
+          FAB_CHECK_LAUNCH();
+          launches += 2;
+        }
+        done_iters += nit;
+        if (fixed) break;
+        FAB_CUDA(cudaMemcpyAsync(c->st_h, c->st_d, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+        FAB_CUDA(cudaStreamSynchronize(st));
+        if (c->st_h->lsqr_done) break;
+      }
+      k_finish_y<<<1, kThreads, 0, st>>>(RinvT, L.x, m, y);
+      FAB_CHECK_LAUNCH();
+      ++launches;
+      FAB_CUDA(cudaMemcpyAsync(c->st_h, c->st_d, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+      FAB_CUDA(cudaStreamSynchronize(st));
+      c->info.lsqr_iters = c->st_h->lsqr_iters;
+      c->info.lsqr_converged = c->st_h->lsqr_done;
+      c->info.lsqr_rnorm = c->st_h->rnorm;
+      c->info.lsqr_arnorm = c->st_h->arnorm;
+      c->info.lsqr_anorm = c->st_h->anorm;
+      if (!fixed && !c->st_h->lsqr_done && *warn == FAB_OK) *warn = FAB_NOTCONV;
+    }
+  }
+  k_build_C<<<(m * m + kThreads - 1) / kThreads, kThreads, 0, st>>>(c->H, c->ldH, y, m, need_ls ? 1 : 0, C);
+  FAB_CHECK_LAUNCH();
+  ++launches;
+  if (!need_ls) FAB_CUDA(cudaMemsetAsync(y, 0, m * sizeof(double), st));
+  c->info.launches_compress = launches;
+  return FAB_OK;
+}
+
+}  // namespace fab
