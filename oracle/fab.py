@@ -25,7 +25,7 @@ from .srht import SRHT
 MODES = ("blendenpik", "sketch_solve", "none")
 
 
-def compress(dec, SV, mode, lsqr_tol=1e-6, lsqr_iters=None, lsqr_maxit=None):
+def compress(dec, SV, mode, lsqr_tol=1e-6, lsqr_iters=None, lsqr_maxit=None, rinv="solve"):
     """y and C_m = H_m + h_{m+1,m} y e_m^T from an Alg 2 decomposition."""
     V, H, m = dec["V"], dec["H"], dec["m_eff"]
     Hm = H[:m, :m].copy()
@@ -37,7 +37,7 @@ def compress(dec, SV, mode, lsqr_tol=1e-6, lsqr_iters=None, lsqr_maxit=None):
             R, _ = lsq.householder_qr(SV[:, :m])
     elif mode == "blendenpik":
         y, R, info = lsq.blendenpik(V[:, :m], V[:, m], SV[:, :m], tol=lsqr_tol,
-                                    maxit=lsqr_maxit, iters=lsqr_iters)
+                                    maxit=lsqr_maxit, iters=lsqr_iters, rinv=rinv)
     elif mode == "sketch_solve":
         y, R = lsq.sketch_and_solve(SV[:, :m], SV[:, m])
     else:
@@ -50,7 +50,7 @@ def compress(dec, SV, mode, lsqr_tol=1e-6, lsqr_iters=None, lsqr_maxit=None):
 
 def solve(A, b, m, k, s, seed, mode="blendenpik", f="exp", alpha=1.0,
           sigma=0.0, poly=None, lsqr_tol=1e-6, lsqr_iters=None,
-          lsqr_maxit=None, variant="cgs", keep=True):
+          lsqr_maxit=None, variant="cgs", keep=True, lsqr_rinv="solve"):
     """One f(A)b approximation by Alg 4 / Remark 2 / Alg 5.  Returns a dict
     with f_m and every intermediate (V, H, SV, rows, signs, y, C, c)."""
     dec = krylov.truncated_arnoldi(A, b, m, k, variant=variant)     # Alg 2
@@ -61,7 +61,7 @@ def solve(A, b, m, k, s, seed, mode="blendenpik", f="exp", alpha=1.0,
         if me + 1 > s:
             raise ValueError("InvalidSketchSize: need s >= m+1")
         SV = th.apply(dec["V"])                                     # Theta V_{m+1}
-    y, C, R, info = compress(dec, SV, mode, lsqr_tol, lsqr_iters, lsqr_maxit)
+    y, C, R, info = compress(dec, SV, mode, lsqr_tol, lsqr_iters, lsqr_maxit, lsqr_rinv)
     c = matfun.f_e1(f, C, alpha, sigma, poly)                       # f(C) e_1
     fm = dec["gamma"] * (dec["V"][:, :me] @ c)                      # ||b|| V_m c
     out = dict(f_m=fm, H=dec["H"], gamma=dec["gamma"], m_eff=me,

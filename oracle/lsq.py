@@ -139,13 +139,21 @@ def lsqr(matvec, rmatvec, b: np.ndarray, ncols: int, tol: float = 1e-6,
 
 
 def blendenpik(Vm: np.ndarray, c: np.ndarray, SVm: np.ndarray, tol=1e-6,
-               maxit=None, iters=None):
+               maxit=None, iters=None, rinv="solve"):
     """argmin ||Vm z - c|| by LSQR right-preconditioned with R from the QR
-    of the sketch SVm = Theta Vm.  Returns (y, R, info)."""
+    of the sketch SVm = Theta Vm.  Returns (y, R, info).
+    rinv="inverse" applies R^{-1} as an explicit inverse instead of by
+    substitution: the same method in different rounding, used only to
+    measure the rounding sensitivity of intermediate LSQR iterates."""
     R, _ = householder_qr(SVm)
     m = R.shape[0]
-    mv = lambda p: Vm @ solve_upper(R, p)                       # (Vm R^-1) p
-    rmv = lambda u: solve_upper_transposed(R, Vm.T @ u)         # R^-T Vm^T u
+    if rinv == "inverse":
+        Ri = solve_upper(R, np.eye(m))
+        mv = lambda p: Vm @ (Ri @ p)
+        rmv = lambda u: Ri.T @ (Vm.T @ u)
+    else:
+        mv = lambda p: Vm @ solve_upper(R, p)                   # (Vm R^-1) p
+        rmv = lambda u: solve_upper_transposed(R, Vm.T @ u)     # R^-T Vm^T u
     z, info = lsqr(mv, rmv, c, m, tol=tol, maxit=maxit, iters=iters)
     return solve_upper(R, z), R, info
 

@@ -599,6 +599,8 @@ int run_basis(fab_ctx* c, int m, int k) {
     int rc = FAB_OK;
     k_reset_basis<<<1, 1, 0, c->cap>>>(c->st_d, m);
     ++launches;
+    // underline-H is banded: everything outside the band must read as 0
+    FAB_CUDA(cudaMemsetAsync(c->H, 0, (size_t)c->ldH * m * sizeof(double), c->cap));
     // norm partials of column 0 (= b) for the first lagged norm
     k_norm_partial<<<c->grid_upd, kThreads, 0, c->cap>>>(c->V, c->n, c->row_begin, c->part_norm);
     ++launches;

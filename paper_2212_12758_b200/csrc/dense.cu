@@ -380,7 +380,59 @@ static int read_stats(fab_ctx* c, const double* X, int m, double* h, cudaStream_
     if (rc__ != FAB_OK) return rc__; \
   } while (0)
 
-// exp by [13/13] Pade with scaling and squaring (theta_13 = 5.371920351148152)
+// 1-norms of up to 4 matrices (one CTA each, fixed order)
+struct Mats4 {
+  const double* p[4];
+};
+__global__ void k_norm1_multi(Mats4 M, int m, double scale0, double* out) {
+  __shared__ double smax[kThreads];
+  const double* X = M.p[blockIdx.x];
+  double mx = 0.0;
+  for (int col = threadIdx.x; col < m; col += blockDim.x) {
+    double a = 0.0;
+    for (int r = 0; r < m; ++r) a += fabs(X[r + (int64_t)col * m]);
+    mx = fmax(mx, a);
+  }
+  smax[threadIdx.x] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double M2 = 0.0;
+    for (int t = 0; t < (int)blockDim.x; ++t) M2 = fmax(M2, smax[t]);
+    out[blockIdx.x] = M2;
+  }
+}
+
+// out = || |s X|^p ||_1 computed exactly as max_j (1^T |s X|^p)_j (row-vector
+// powers; all entries are non-negative).  One CTA; warp per column.
+__global__ void k_abs_power_norm(const double* X, int m, double s, int p, double* out) {
+  __shared__ double v[kMaxM], w[kMaxM];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) v[i] = 1.0;
+  __syncthreads();
+  for (int it = 0; it < p; ++it) {
+    for (int j = warp; j < m; j += nw) {
+      double a = 0.0;
+      for (int i = lane; i < m; i += 32) a = fma(v[i], fabs(s * X[i + (int64_t)j * m]), a);
+      a = warp_sum(a);
+      if (lane == 0) w[j] = a;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += blockDim.x) v[i] = w[i];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double mx = 0.0;
+    for (int i = 0; i < m; ++i) mx = fmax(mx, v[i]);
+    out[0] = mx;
+  }
+}
+
+// exp by the scaling and squaring algorithm of Al-Mohy & Higham (2009) --
+// the algorithm of MATLAB's expm that the paper used -- with
+// the [13/13] Pade approximant: s from eta_5 = min(max(d6, d8), max(d8, d10)),
+// d_k = ||X^k||_1^{1/k} (exact norms of the powers, cheap on the device),
+// theta_13 = 4.25, plus the ell(2^-s X, 13) correction that prevents
+// overscaling of nonnormal matrices.
 static int expm_e1(fab_ctx* c, int m, const double* X0, double* c_out, int* iters, cudaStream_t st) {
   static const double b[14] = {64764752532480000.0, 32382376266240000.0, 7771770303897600.0,
                                1187353796428800.0,  129060195264000.0,   10559470521600.0,
@@ -399,10 +451,41 @@ static int expm_e1(fab_ctx* c, int m, const double* X0, double* c_out, int* iter
   double h[3];
   FAB_TRY(read_stats(c, X0, m, h, st));
   if (h[2] != 0.0) return FAB_EDOMAIN;
-  const double theta13 = 5.371920351148152;
+  const double theta13 = 4.25;
+  const double u = ldexp(1.0, -53);
+  const double c27 = 8.829961602018678e-36;   // |c_27| = (13!)^2 / (26! 27!)
   int s = 0;
-  if (h[0] > theta13) s = (int)ceil(log2(h[0] / theta13));
-  if (s < 0) s = 0;
+  if (h[0] > 0.0) {
+    FAB_TRY(gemm(c, m, X0, X0, 1.0, 0.0, nullptr, 0.0, X2, st));
+    FAB_TRY(gemm(c, m, X2, X2, 1.0, 0.0, nullptr, 0.0, X4, st));
+    FAB_TRY(gemm(c, m, X4, X2, 1.0, 0.0, nullptr, 0.0, X6, st));
+    FAB_TRY(gemm(c, m, X4, X4, 1.0, 0.0, nullptr, 0.0, T, st));    // X^8
+    FAB_TRY(gemm(c, m, X4, X6, 1.0, 0.0, nullptr, 0.0, U, st));    // X^10
+    double* nd = svec(c, 17);
+    Mats4 M4{{X4, X6, T, U}};
+    k_norm1_multi<<<4, kThreads, 0, st>>>(M4, m, 1.0, nd);
+    FAB_CHECK_LAUNCH();
+    double hn[4];
+    FAB_CUDA(cudaMemcpyAsync(hn, nd, sizeof(hn), cudaMemcpyDeviceToHost, st));
+    FAB_CUDA(cudaStreamSynchronize(st));
+    const double d6 = pow(hn[1], 1.0 / 6), d8 = pow(hn[2], 1.0 / 8), d10 = pow(hn[3], 1.0 / 10);
+    double eta5 = fmin(fmax(d6, d8), fmax(d8, d10));
+    if (!isfinite(eta5)) eta5 = h[0];            // powers overflowed: fall back to ||X||_1
+    if (eta5 > 0.0) s = (int)ceil(log2(eta5 / theta13));
+    if (s < 0) s = 0;
+    // ell(2^-s X, 13)
+    const double sc = ldexp(1.0, -s);
+    k_abs_power_norm<<<1, kThreads, 0, st>>>(X0, m, sc, 27, nd);
+    FAB_CHECK_LAUNCH();
+    double pn;
+    FAB_CUDA(cudaMemcpyAsync(&pn, nd, sizeof(double), cudaMemcpyDeviceToHost, st));
+    FAB_CUDA(cudaStreamSynchronize(st));
+    if (pn > 0.0 && isfinite(pn)) {
+      const double alpha = c27 * pn / (h[0] * sc);
+      const int ell = (int)ceil(log2(alpha / u) / 26.0);
+      if (ell > 0) s += ell;
+    }
+  }
   const double sc = ldexp(1.0, -s);
   FAB_TRY(lincomb(c, m, sc, X0, 0, nullptr, 0, nullptr, 0.0, X, st));
   FAB_TRY(gemm(c, m, X, X, 1.0, 0.0, nullptr, 0.0, X2, st));
@@ -431,11 +514,11 @@ static int expm_e1(fab_ctx* c, int m, const double* X0, double* c_out, int* iter
   // square s times (the last squaring only needs the first column)
   double* cur = T;
   double* nxt = X2;
+  *iters = s;
   for (int i = 0; i < s; ++i) {
     if (i == s - 1) {
       k_gemv_e<<<(m + 127) / 128, 128, 0, st>>>(cur, m, cur, c_out);   // cur * cur[:,0]
       FAB_CHECK_LAUNCH();
-      *iters = s;
       return FAB_OK;
     }
     FAB_TRY(gemm(c, m, cur, cur, 1.0, 0.0, nullptr, 0.0, nxt, st));
@@ -444,7 +527,6 @@ static int expm_e1(fab_ctx* c, int m, const double* X0, double* c_out, int* iter
     nxt = t;
   }
   FAB_CUDA(cudaMemcpyAsync(c_out, cur, m * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  *iters = s;
   return FAB_OK;
 }
 

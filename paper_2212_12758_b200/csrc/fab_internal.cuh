@@ -193,6 +193,6 @@ inline double* dmat(fab_ctx* c, int i) { return c->dense + (size_t)i * c->m_max 
 // small vector pool layout (each kSmall doubles)
 constexpr int kSmall = kMaxM + 8;
 inline double* svec(fab_ctx* c, int i) { return c->small + (size_t)i * kSmall; }
-constexpr int kSmallVecs = 24;
+constexpr int kSmallVecs = 24;   // svec indices 0..23 (see lsqr.cu, dense.cu, apply.cu)
 
 }  // namespace fab
