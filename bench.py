@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark of the randomized-Krylov f(A)b hot path (arXiv 2212.12758) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fab|reference]
+
+Workload (BASELINE.json metric "Krylov iterations/sec and f(A)b solves/sec at
+n=16M, m=200"; config c3): 3D upwind convection-diffusion 7-point stencil on a
+256^3 grid (n = 2^24), f = sqrt of A + 1e-2 ||A||_inf I, seeded Gaussian b,
+m = 200, k = 4, s = 400.  One STEP = one full Algorithm 4 solve through the C
+ABI: fab_sketch (Theta drawn first, so its application is fused into the basis
+pass) + fab_basis (Algorithm 2) + fab_compress (Blendenpik-LSQR, MATLAB lsqr
+tolerance 1e-6) + fab_apply (gamma_b V_m sqrt(C_m+sigma I) e_1).
+value = solves/s with b and A resident in HBM; e2e = the same through the ABI
+with b read from pinned host memory and f_m written back to it every step.
+
+--impl reference times the fp64 CPU oracle (oracle/) on the host cores on a
+bounded sample of the same workload and reports the same metric (see
+DESIGN.md "Measurement").  Under torchrun (N > 1) only rank 0 runs it.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Krylov iterations/sec and f(A)b solves/sec at n=16M, m=200; HBM GB/s vs peak"
+WORKLOAD = ("c3: 3D 7-point upwind convection-diffusion, 256^3 grid (n=16,777,216), fp64, "
+            "f=sqrt(A + 1e-2||A||_inf I), seeded Gaussian b, m=200, k=4, s=400, "
+            "Algorithm 4 (Blendenpik-LSQR tol 1e-6)")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="fab", choices=["fab", "reference"])
+    ap.add_argument("--g", type=int, default=256, help="grid side (256 = BASELINE c3)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip mode / e2e side measurements")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy bandwidth)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+# ----------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                try:
+                    rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+                except ValueError:
+                    pass
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        loaded = [s for s, _, _ in rows if s > 500] or [s for s, _, _ in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(m for _, m, _ in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------
+# CPU oracle sample (cpu_baseline and --impl reference)
+# ----------------------------------------------------------------------------
+def oracle_sample(p, A, lsqr_iters, small=False):
+    """Time the fp64 oracle on a bounded sample of the c3 solve and scale it to
+    one full solve: m Krylov steps, m+1 SRHT columns, (L+1) LSQR passes over
+    V_m, one dense f(C_m), one combination.  Returns (seconds/solve, desc)."""
+    import numpy as np
+    from oracle import krylov, lsq, matfun, srht
+    n, m, k, s = p.n, p.m, p.k, p.s
+    kb = 3 if small else 6
+    t0 = time.perf_counter()
+    d = krylov.truncated_arnoldi(A, p.b, kb, k, variant="cgs")
+    t_iter = (time.perf_counter() - t0) / kb
+    th = srht.SRHT(n, s, p.sketch_seed)
+    nsk = 1 if small else 2
+    t0 = time.perf_counter()
+    for j in range(nsk):
+        th.apply(d["V"][:, j])
+    t_srht = (time.perf_counter() - t0) / nsk
+    V = d["V"]
+    mm = V.shape[1] - 1
+    # the preconditioner's values do not change the per-iteration cost: use a
+    # cheap s x mm stand-in sketch for R (the timed part is the LSQR passes)
+    SVs = np.random.default_rng(0).standard_normal((s, mm))
+    nl = 1 if small else 2
+    t0 = time.perf_counter()
+    lsq.blendenpik(V[:, :mm], V[:, mm], SVs, iters=nl)
+    t_lsqr = (time.perf_counter() - t0) / nl * (m / mm)
+    rng = np.random.default_rng(1)
+    C = np.diag(np.linspace(1.0, 2.0, m)) + 0.01 * rng.standard_normal((m, m))
+    t0 = time.perf_counter()
+    cvec = matfun.f_e1("sqrt", C, 1.0, 0.0)
+    t_dense = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    _ = V[:, :mm] @ cvec[:mm]
+    t_final = (time.perf_counter() - t0) * (m / mm)
+    T = m * t_iter + (m + 1) * t_srht + (lsqr_iters + 1) * t_lsqr + t_dense + t_final
+    desc = (f"oracle (numpy/scipy fp64) on the full n={n}: {kb} Krylov steps "
+            f"({t_iter:.3f} s/step), {nsk} SRHT column(s) ({t_srht:.3f} s/col), {nl} LSQR "
+            f"iteration(s) on {mm} columns scaled to m={m} ({t_lsqr:.3f} s/iter), dense sqrtm "
+            f"{m}x{m} ({t_dense:.3f} s), combination scaled ({t_final:.3f} s); extrapolated "
+            f"to m={m} steps, m+1 SRHT columns, L+1={lsqr_iters + 1} LSQR passes")
+    return T, desc, dict(t_iter=t_iter, t_srht=t_srht, t_lsqr=t_lsqr, t_dense=t_dense, t_final=t_final)
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    import numpy as np  # noqa: F401
+    import fab_problems as fp
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    p = fp.make("c3", g=args.g)
+    log(f"[reference] building CSR of the c3 operator (n={p.n}) for the oracle ...")
+    A = p.scipy()
+    L = 26   # LSQR iterations of the GPU run at c3 (tol 1e-6); used to scale the sample
+    Ts = []
+    for i in range(args.warmup + args.steps):
+        T, desc, parts = oracle_sample(p, A, L, small=True)
+        if i >= args.warmup:
+            Ts.append(T)
+        log(f"[reference] step {i}: estimated {T:.1f} s/solve {parts}")
+    T = statistics.mean(Ts)
+    val = 1.0 / T
+    cores = cpu_cores()
+    out = {
+        "metric": METRIC, "value": val, "unit": "solves/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": T * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n": p.n, "m": p.m, "k": p.k, "s": p.s},
+        "krylov_iters_per_s": 1.0 / parts["t_iter"],
+        "cpu_baseline": {"value": val, "unit": "solves/s", "cores": cores, "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": val, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import fab_problems as fp
+    import paper_2212_12758_b200 as fab
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    dev = local
+
+    p = fp.make("c3", g=args.g)
+    # independent solves per GPU at N > 1 (distributed single solve: DESIGN.md "Multi-GPU")
+    b_np = p.b if rank == 0 else fp.gaussian_b(p.n, 2003 + 7919 * rank)
+    b = torch.as_tensor(b_np).cuda(dev)
+    op = fab.Operator.from_problem(p)
+    stream = torch.cuda.current_stream(dev)
+    sv = fab.Solver(op, b, m_max=p.m, k_max=p.k, s_max=p.s, device=dev, profile=True)
+    y = torch.empty(p.n, dtype=torch.float64, device=f"cuda:{dev}")
+
+    def step(mode="blendenpik", fused=True):
+        if mode != "none" and fused:
+            sv.sketch(p.s, p.sketch_seed)
+        sv.basis(p.m, p.k)
+        if mode != "none" and not fused:
+            sv.sketch(p.s, p.sketch_seed)
+        sv.compress(mode, tol=1e-6)
+        sv.apply(p.f, p.alpha, p.sigma, out=y)
+        return sv.info()
+
+    for _ in range(args.warmup):
+        step()
+    infos = []
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(dev) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            infos.append(step())
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clocks = clk.summary()
+    ms_step = ms / args.steps
+    value = world * args.steps / (ms / 1e3)
+
+    def avg(key):
+        return statistics.mean(i[key] for i in infos)
+
+    n, m, k, s = p.n, p.m, p.k, p.s
+    launches = sum(i["launches_sketch"] + i["launches_basis"] + i["launches_compress"] + i["launches_apply"]
+                   for i in infos)
+    peak, peak_src = peaks()
+    # dominant kernel: the fused LSQR pass t <- W p - scal t, g = W^T t (8 n (m+2) bytes)
+    passes = sum(i["lsqr_passes"] for i in infos)
+    pass_ms = sum(i["ms_lsqr_pass"] for i in infos) / max(passes, 1)
+    pass_bytes = 8.0 * n * (m + 2)
+    achieved = pass_bytes / (pass_ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "lsqr_pass_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    # basis: algorithmic bytes per Krylov step of this implementation:
+    # K1 reads k window columns and writes z (8n(k+1)); K3 reads z + k columns and
+    # writes one (8n(k+2)) -> 8n(2k+3) = 88 B/row at k = 4
+    b_it = 8.0 * n * (2 * k + 3)
+    basis_ms = avg("ms_basis")
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "solves/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n": n, "m": m, "k": k, "s": s,
+                   "mode": "blendenpik (LSQR tol 1e-6)", "f": "sqrt", "sigma": p.sigma,
+                   "l2": "inputs larger than L2 (V_{m+1} = 27 GB >> 126 MB L2), no flush needed",
+                   "parallelism": "1 GPU" if world == 1 else f"{world} independent solves (one per GPU)"},
+        "krylov_iters_per_s": m / (basis_ms * 1e-3),
+        "phase_ms": {"sketch": avg("ms_sketch"), "basis": basis_ms, "compress": avg("ms_compress"),
+                     "apply": avg("ms_apply")},
+        "lsqr_iters": avg("lsqr_iters"),
+        "basis_effective_gbs": b_it * m / (basis_ms * 1e-3) / 1e9,
+        "roofline": {"kernel": "k_lsqr_pass (Blendenpik-LSQR fused V p / V^T t pass)",
+                     "bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": peak_src,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": pass_bytes, "avg_launch_ms": pass_ms,
+                     "launches_timed": passes},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+
+    # ---- side measurements (not part of value) ----------------------------
+    if not args.no_extras:
+        modes = {}
+        for mode in ("sketch_solve", "none"):
+            step(mode)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step(mode)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            modes[mode] = 1e3 / e0.elapsed_time(e1)
+        modes["blendenpik"] = value / world
+        out["solves_per_s_by_mode"] = modes
+        # API-order variant: sketch after the basis (batched SRHT pass)
+        step("blendenpik", fused=False)
+        inf = step("blendenpik", fused=False)
+        out["api_order_sketch_ms"] = inf["ms_sketch"]
+        # e2e: b from pinned host memory, f_m back to pinned host memory, every step
+        bh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        bh.copy_(torch.as_tensor(b_np))
+        yh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        bh_np, yh_np = bh.numpy(), yh.numpy()
+
+        def e2e_step():
+            sv.set_b(bh_np)
+            sv.sketch(p.s, p.sketch_seed)
+            sv.basis(p.m, p.k)
+            sv.compress("blendenpik", tol=1e-6)
+            sv.apply(p.f, p.alpha, p.sigma, out=yh_np, host=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        ne = max(2, min(args.steps, 3))
+        for _ in range(ne):
+            e2e_step()
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([te], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        out["e2e"] = {"value": world * ne / te, "unit": "solves/s", "h2d_bytes_per_step": 8 * n,
+                      "d2h_bytes_per_step": 8 * n}
+        ok = np.isfinite(yh_np).all()
+        out["e2e"]["output_finite"] = bool(ok)
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only) ---------------------------
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        log("[cpu_baseline] building the c3 CSR for the oracle ...")
+        A = p.scipy()
+        T, desc, parts = oracle_sample(p, A, int(round(out["lsqr_iters"])))
+        out["cpu_baseline"] = {"value": 1.0 / T, "unit": "solves/s", "cores": cpu_cores(),
+                               "kind": "oracle", "sample": desc,
+                               "krylov_iters_per_s": 1.0 / parts["t_iter"]}
+    sv.close()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

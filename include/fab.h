@@ -87,8 +87,13 @@ enum {
   FAB_GET_FC = 8,     /* c = f(alpha C_m + sigma I) e_1, m_eff doubles        */
   FAB_GET_R = 9,      /* R of QR(Theta V_m), m_eff x m_eff doubles            */
   FAB_GET_BETA = 10,  /* norms of the stored columns, m_eff+1 doubles         */
-  FAB_SET_POLY = 100  /* FAB_POLY coefficients p_0..p_d (doubles), d < 64     */
+  FAB_SET_POLY = 100,     /* FAB_POLY coefficients p_0..p_d (doubles), d < 64       */
+  FAB_SET_B_HOST = 101,   /* new b (n_local doubles, HOST): keeps A, drops V/H/C     */
+  FAB_SET_B_DEVICE = 102  /* new b (n_local doubles, DEVICE), same semantics          */
 };
+
+/* fab_opts.flags */
+enum { FAB_FLAG_PROFILE = 1 };  /* time every LSQR pass with CUDA events (fab_info) */
 
 typedef struct fab_ctx fab_ctx;
 
@@ -122,7 +127,7 @@ typedef struct {
   void* workspace;         /* device; NULL => the library allocates (cudaMalloc)    */
   size_t workspace_bytes;  /* size of workspace, >= fab_workspace_size()            */
   int b_location;          /* FAB_DEVICE or FAB_HOST for fab_init's b               */
-  unsigned flags;          /* reserved, 0                                           */
+  unsigned flags;          /* FAB_FLAG_* bits                                       */
   void* comm;              /* reserved for multi-GPU (NCCL); NULL on one GPU        */
 } fab_opts;
 
@@ -148,6 +153,8 @@ typedef struct {
   double lsqr_rnorm, lsqr_arnorm, lsqr_anorm;
   double ms_basis, ms_sketch, ms_compress, ms_apply;  /* device time, CUDA events */
   int64_t launches_basis, launches_sketch, launches_compress, launches_apply;
+  double ms_lsqr_pass;     /* FAB_FLAG_PROFILE: summed device time of the LSQR passes */
+  int64_t lsqr_passes;     /* number of streaming passes over V_m in fab_compress     */
 } fab_info;
 
 /* Library ABI version (FAB_ABI_VERSION). */

@@ -82,7 +82,7 @@ class Operator:
 
 class Solver:
     def __init__(self, op: Operator, b, m_max, k_max=2, s_max=0, stream=None, device=None,
-                 workspace=True):
+                 workspace=True, profile=False):
         torch = _torch()
         self.op = op
         self.torch = torch
@@ -94,6 +94,7 @@ class Solver:
         o.device = dev
         o.m_max, o.k_max, o.s_max = m_max, k_max, s_max
         o.b_location = _lib.FAB_DEVICE
+        o.flags = _lib.FAB_FLAG_PROFILE if profile else 0
         if isinstance(b, np.ndarray):
             b = np.ascontiguousarray(b, dtype=np.float64)
             o.b_location = _lib.FAB_HOST
@@ -131,6 +132,14 @@ class Solver:
         st = check(lib.fab_compress(self.ctx, MODES[mode], C.byref(o)), "fab_compress")
         self.status["compress"] = st
         return st
+
+    def set_b(self, b):
+        """Replace b (numpy host array or CUDA tensor); A and the sketch stay."""
+        if isinstance(b, np.ndarray):
+            check(lib.fab_set(self.ctx, _lib.FAB_SET_B_HOST, C.c_void_p(b.ctypes.data), b.nbytes), "fab_set(b)")
+        else:
+            check(lib.fab_set(self.ctx, _lib.FAB_SET_B_DEVICE, C.c_void_p(b.data_ptr()),
+                              b.numel() * 8), "fab_set(b)")
 
     def set_poly(self, coef):
         a = np.ascontiguousarray(coef, dtype=np.float64)

@@ -17,7 +17,8 @@ FAB_EXP, FAB_SQRT, FAB_INVSQRT, FAB_POLY = 0, 1, 2, 3
 FAB_OP_CSR, FAB_OP_STENCIL = 0, 1
 FAB_DEVICE, FAB_HOST = 0, 1
 GET = dict(info=0, H=1, V=2, SV=3, rows=4, signs=5, y=6, C=7, fc=8, R=9, beta=10)
-FAB_SET_POLY = 100
+FAB_SET_POLY, FAB_SET_B_HOST, FAB_SET_B_DEVICE = 100, 101, 102
+FAB_FLAG_PROFILE = 1
 
 MODES = {"blendenpik": FAB_BLENDENPIK, "sketch_solve": FAB_SKETCH_SOLVE, "none": FAB_NONE}
 FUNCS = {"exp": FAB_EXP, "sqrt": FAB_SQRT, "invsqrt": FAB_INVSQRT, "poly": FAB_POLY}
@@ -56,7 +57,8 @@ class FabInfo(C.Structure):
                 ("ms_basis", C.c_double), ("ms_sketch", C.c_double), ("ms_compress", C.c_double),
                 ("ms_apply", C.c_double), ("launches_basis", C.c_int64),
                 ("launches_sketch", C.c_int64), ("launches_compress", C.c_int64),
-                ("launches_apply", C.c_int64)]
+                ("launches_apply", C.c_int64), ("ms_lsqr_pass", C.c_double),
+                ("lsqr_passes", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad0"}

@@ -147,6 +147,7 @@ static void free_ctx(fab_ctx* c) {
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
   delete c;
 }
 
@@ -218,6 +219,7 @@ int fab_init(fab_ctx** out, const fab_operator* A, const double* b, const fab_op
     return rc;
   }
   c->stream = reinterpret_cast<cudaStream_t>(o->stream);
+  c->flags = o->flags;
   const size_t need = make_layout(c).total;
   if (o->workspace) {
     if (o->workspace_bytes < need || (reinterpret_cast<uintptr_t>(o->workspace) & 255)) {
@@ -316,12 +318,11 @@ int fab_sketch(fab_ctx* c, int s, uint64_t seed) {
   if (s < 1 || s > c->s_max || (int64_t)s > c->N) return FAB_EINVAL;
   if (c->basis_ready && s < (c->breakdown ? c->m_eff : c->m + 1)) return FAB_EINVAL;
   FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
+  const int64_t l0 = c->nlaunch;
   int rc = sketch_draw(c, s, seed);
   if (rc != FAB_OK) return rc;
-  int64_t launches = 1;
   if (c->basis_ready) {
     if ((rc = sketch_batched(c)) != FAB_OK) return rc;
-    launches += 2;
     c->sketch_in_V = true;
     c->compressed = false;
     c->info.sketch_fused = 0;
@@ -332,7 +333,7 @@ int fab_sketch(fab_ctx* c, int s, uint64_t seed) {
   if ((rc = timed_end(c, &ms)) != FAB_OK) return rc;
   c->info.s = s;
   c->info.ms_sketch = ms;
-  c->info.launches_sketch = launches;
+  c->info.launches_sketch = c->nlaunch - l0;
   return FAB_OK;
 }
 
@@ -344,8 +345,10 @@ int fab_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o) {
   if (o && (o->iters < 0 || o->maxit < 0 || o->tol < 0)) return FAB_EINVAL;
   FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
   int warn = FAB_OK;
+  const int64_t l0 = c->nlaunch;
   int rc = run_compress(c, mode, o, &warn);
   if (rc != FAB_OK) return rc;
+  c->info.launches_compress = c->nlaunch - l0;
   double ms = 0;
   if ((rc = timed_end(c, &ms)) != FAB_OK) return rc;
   FAB_CUDA(cudaGetLastError());
@@ -365,6 +368,7 @@ int fab_apply(fab_ctx* c, int f, double alpha, double sigma, double* y, int y_lo
   FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
   double* cvec = svec(c, 16);
   int iters = 0;
+  const int64_t l0 = c->nlaunch;
   int rc = dense_fe1(c, f, alpha, sigma, cvec, &iters);
   if (rc != FAB_OK) return rc;
   const bool direct = (y_location == FAB_DEVICE) && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
@@ -380,6 +384,7 @@ int fab_apply(fab_ctx* c, int f, double alpha, double sigma, double* y, int y_lo
   FAB_CUDA(cudaGetLastError());
   c->info.dense_iters = iters;
   c->info.ms_apply = ms;
+  c->info.launches_apply = c->nlaunch - l0;
   return FAB_OK;
 }
 
@@ -497,6 +502,17 @@ int fab_set(fab_ctx* c, int what, const void* src, size_t bytes) {
     if (n < 1 || n > (size_t)kPolyMax) return FAB_EINVAL;
     memcpy(c->poly, src, n * sizeof(double));
     c->npoly = (int)n;
+    return FAB_OK;
+  }
+  if (what == FAB_SET_B_HOST || what == FAB_SET_B_DEVICE) {
+    if (bytes < (size_t)c->n * sizeof(double)) return FAB_EINVAL;
+    FAB_CUDA(cudaMemcpyAsync(c->V, src, c->n * sizeof(double),
+                             what == FAB_SET_B_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                             c->stream));
+    FAB_CUDA(cudaStreamSynchronize(c->stream));
+    c->basis_ready = false;
+    c->compressed = false;
+    c->sketch_in_V = false;
     return FAB_OK;
   }
   return FAB_EINVAL;

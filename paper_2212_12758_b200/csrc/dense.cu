@@ -117,6 +117,7 @@ int dense_qr_sketch(fab_ctx* c, int m, double* R, double* qtb, cudaStream_t st) 
   void* args[] = {&A, &rows, &nf, &ntot, &diag};
   const int grid = coop_grid(c, (const void*)k_qr_coop, (ntot + kWarps - 1) / kWarps);
   FAB_CUDA(cudaLaunchCooperativeKernel((const void*)k_qr_coop, grid, kThreads, args, 0, st));
+  ++c->nlaunch;
   k_qr_extract<<<(m * m + kThreads - 1) / kThreads, kThreads, 0, st>>>(A, s, m, diag, R, qtb);
   FAB_CHECK_LAUNCH();
   return FAB_OK;
@@ -348,6 +349,7 @@ static int gj_solve(fab_ctx* c, int m, const double* A, double* Awork, double* B
   void* args[] = {&Awork, &B, &mm, &nr, &out};
   const int grid = coop_grid(c, (const void*)k_gj_coop, (m + nrhs + kWarps - 1) / kWarps);
   FAB_CUDA(cudaLaunchCooperativeKernel((const void*)k_gj_coop, grid, kThreads, args, 0, st));
+  ++c->nlaunch;
   return FAB_OK;
 }
 

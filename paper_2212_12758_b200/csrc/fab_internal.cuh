@@ -110,6 +110,9 @@ struct fab_ctx {
   int64_t g_launches = 0;
 
   fab_info info{};
+  unsigned flags = 0;
+  int64_t nlaunch = 0;               // kernels launched outside the basis graph
+  std::vector<cudaEvent_t> prof_ev;   // FAB_FLAG_PROFILE: start/end pairs of LSQR passes
 };
 
 // ------------------------------------------------------------------------
@@ -124,7 +127,12 @@ struct fab_ctx {
     }                                                                    \
   } while (0)
 
-#define FAB_CHECK_LAUNCH() FAB_CUDA(cudaGetLastError())
+// every kernel launch goes through this (counts launches for fab_info)
+#define FAB_CHECK_LAUNCH()            \
+  do {                                \
+    ++c->nlaunch;                     \
+    FAB_CUDA(cudaGetLastError());     \
+  } while (0)
 
 namespace fab {
 

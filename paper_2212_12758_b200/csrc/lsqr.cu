@@ -333,6 +333,8 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
   c->info.lsqr_iters = 0;
   c->info.lsqr_converged = 0;
   c->info.cond_R = 0.0;
+  c->info.lsqr_passes = 0;
+  c->info.ms_lsqr_pass = 0.0;
   int64_t launches = 0;
   const bool need_ls = (mode != FAB_NONE) && !c->breakdown;
   if (mode != FAB_NONE && !c->sketch_in_V) return FAB_EORDER;
@@ -340,7 +342,6 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
     // QR of Theta V_m (s x m) with Theta v_{m+1} as an extra column
     int rc = dense_qr_sketch(c, m, R, qtb, st);
     if (rc != FAB_OK) return rc;
-    launches += 2;
     rc = dense_tri_inverse(c, R, m, Rinv, st);
     if (rc != FAB_OK) return rc;
     ++launches;
@@ -368,12 +369,25 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
       const double tol = (o && o->tol > 0) ? o->tol : 1e-6;
       const int maxit = fixed ? fixed : ((o && o->maxit > 0) ? o->maxit : 4 * m);
       const int G = c->grid_lsqr;
+      const bool prof = (c->flags & FAB_FLAG_PROFILE) != 0;
+      int npass = 0;
+      auto ev_pair = [&](int i) -> cudaEvent_t* {
+        while ((int)c->prof_ev.size() < 2 * (i + 1)) {
+          cudaEvent_t e;
+          cudaEventCreate(&e);
+          c->prof_ev.push_back(e);
+        }
+        return &c->prof_ev[2 * i];
+      };
       // init pass: p = 0, t_old = w_hat_m, scal = -1  ->  t = w_hat_m, g = W^T t
       FAB_CUDA(cudaMemsetAsync(L.p, 0, m * sizeof(double), st));
       k_reset_lsqr<<<1, 1, 0, st>>>(c->st_d);
+      if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[0], st));
       pass<<<G, kLsqrThreads, 0, st>>>(c->V, c->ld, m, c->n, L.p, -1.0, c->V + (int64_t)m * c->ld,
                                        c->vec, c->part_g, c->part_tn, c->st_d, 0);
       FAB_CHECK_LAUNCH();
+      if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[1], st));
+      ++npass;
       k_lsqr_init<<<1, kThreads, 0, st>>>(c->part_g, c->part_tn, G, m, Rinv, RinvT, c->beta, L, tol,
                                           c->st_d);
       FAB_CHECK_LAUNCH();
@@ -383,9 +397,12 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
       while (done_iters < maxit) {
         const int nit = (maxit - done_iters) < chunk ? (maxit - done_iters) : chunk;
         for (int it = 0; it < nit; ++it) {
+          if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[0], st));
           pass<<<G, kLsqrThreads, 0, st>>>(c->V, c->ld, m, c->n, L.p, 0.0, c->vec, c->vec, c->part_g,
                                            c->part_tn, c->st_d, 1);
           FAB_CHECK_LAUNCH();
+          if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[1], st));
+          ++npass;
           k_lsqr_step<<<1, kThreads, 0, st>>>(c->part_g, c->part_tn, G, m, Rinv, RinvT, c->beta, L,
                                               fixed ? 0 : 1, c->st_d);
           FAB_CHECK_LAUNCH();
@@ -403,6 +420,16 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
       FAB_CUDA(cudaMemcpyAsync(c->st_h, c->st_d, sizeof(DevState), cudaMemcpyDeviceToHost, st));
       FAB_CUDA(cudaStreamSynchronize(st));
       c->info.lsqr_iters = c->st_h->lsqr_iters;
+      // passes after convergence exit immediately; count the ones that ran
+      c->info.lsqr_passes = 1 + c->st_h->lsqr_iters;
+      c->info.ms_lsqr_pass = 0.0;
+      if (prof) {
+        for (int i = 0; i < 1 + c->st_h->lsqr_iters && i < npass; ++i) {
+          float t = 0.f;
+          FAB_CUDA(cudaEventElapsedTime(&t, c->prof_ev[2 * i], c->prof_ev[2 * i + 1]));
+          c->info.ms_lsqr_pass += t;
+        }
+      }
       c->info.lsqr_converged = c->st_h->lsqr_done;
       c->info.lsqr_rnorm = c->st_h->rnorm;
       c->info.lsqr_arnorm = c->st_h->arnorm;
@@ -414,7 +441,6 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
   FAB_CHECK_LAUNCH();
   ++launches;
   if (!need_ls) FAB_CUDA(cudaMemsetAsync(y, 0, m * sizeof(double), st));
-  c->info.launches_compress = launches;
   return FAB_OK;
 }
 
