@@ -155,6 +155,7 @@ typedef struct {
   int64_t launches_basis, launches_sketch, launches_compress, launches_apply;
   double ms_lsqr_pass;     /* FAB_FLAG_PROFILE: summed device time of the LSQR passes */
   int64_t lsqr_passes;     /* number of streaming passes over V_m in fab_compress     */
+  double ms_sketch_batched;/* batched Theta V pass run by fab_compress (API order)    */
 } fab_info;
 
 /* Library ABI version (FAB_ABI_VERSION). */
@@ -178,10 +179,12 @@ int fab_init(fab_ctx** ctx, const fab_operator* A, const double* b, const fab_op
 int fab_basis(fab_ctx* ctx, int m, int k);
 
 /* Draw the SRHT Theta (s rows, seed) of l.70: signs from the counter hash of
-   G-10, rows by Floyd sampling without replacement.  Before fab_basis it arms
-   the fused sketch; after it, sketches V_{m+1} in one batched pass.  Results
-   are identical either way.  Requires m+1 <= s <= min(N, s_max).
-   Errors: EINVAL, EORDER, ECUDA. */
+   G-10, rows by Floyd sampling without replacement.  It only draws Theta
+   (O(N/32 + s) work): the next fab_basis applies it fused into the basis
+   pass; if the current basis was built before this call, fab_compress
+   applies it in one batched pass over V_{m+1} (fab_info.ms_sketch_batched).
+   Results are identical either way.  Requires s <= min(N, s_max) and, once
+   a basis exists, s >= m+1.  Errors: EINVAL, ECUDA. */
 int fab_sketch(fab_ctx* ctx, int s, uint64_t seed);
 
 /* Compression (Eq. (6)/(7)).  mode FAB_BLENDENPIK: QR of Theta V_m, LSQR on

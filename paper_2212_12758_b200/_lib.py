@@ -58,7 +58,7 @@ class FabInfo(C.Structure):
                 ("ms_apply", C.c_double), ("launches_basis", C.c_int64),
                 ("launches_sketch", C.c_int64), ("launches_compress", C.c_int64),
                 ("launches_apply", C.c_int64), ("ms_lsqr_pass", C.c_double),
-                ("lsqr_passes", C.c_int64)]
+                ("lsqr_passes", C.c_int64), ("ms_sketch_batched", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad0"}

@@ -111,6 +111,7 @@ static int setup_ctx(fab_ctx* c, const fab_operator* A, const fab_opts* o) {
   c->ldH = o->m_max + 1;
   int rc = basis_setup_grids(c);
   if (rc != FAB_OK) return rc;
+  if ((rc = lsqr_setup(c)) != FAB_OK) return rc;
   c->grid_lsqr = 2 * c->num_sms;
   c->grid_comb = 8 * c->num_sms;
   return FAB_OK;
@@ -321,18 +322,17 @@ int fab_sketch(fab_ctx* c, int s, uint64_t seed) {
   const int64_t l0 = c->nlaunch;
   int rc = sketch_draw(c, s, seed);
   if (rc != FAB_OK) return rc;
-  if (c->basis_ready) {
-    if ((rc = sketch_batched(c)) != FAB_OK) return rc;
-    c->sketch_in_V = true;
-    c->compressed = false;
-    c->info.sketch_fused = 0;
-  } else {
-    c->sketch_ready = true;
-  }
+  // A new Theta invalidates any Theta V of the current basis.  The next
+  // fab_basis fuses the sketch; if the basis already exists, the batched
+  // pass (K5) runs at the start of fab_compress, where Theta V is needed.
+  c->sketch_ready = true;
+  c->sketch_in_V = false;
+  c->compressed = false;
   double ms = 0;
   if ((rc = timed_end(c, &ms)) != FAB_OK) return rc;
   c->info.s = s;
   c->info.ms_sketch = ms;
+  c->info.ms_sketch_batched = 0.0;
   c->info.launches_sketch = c->nlaunch - l0;
   return FAB_OK;
 }
@@ -341,12 +341,24 @@ int fab_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o) {
   if (!c) return FAB_EINVAL;
   if (mode != FAB_BLENDENPIK && mode != FAB_SKETCH_SOLVE && mode != FAB_NONE) return FAB_EINVAL;
   if (!c->basis_ready) return FAB_EORDER;
-  if (mode != FAB_NONE && !c->sketch_in_V) return FAB_EORDER;
+  if (mode != FAB_NONE && !c->sketch_ready) return FAB_EORDER;
   if (o && (o->iters < 0 || o->maxit < 0 || o->tol < 0)) return FAB_EINVAL;
+  int rc;
+  const int64_t l0 = c->nlaunch;
+  if (mode != FAB_NONE && !c->sketch_in_V) {
+    // API order (basis before sketch): one batched SRHT pass over V_{m+1}
+    if (c->s < (c->breakdown ? c->m_eff : c->m + 1)) return FAB_EINVAL;
+    FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
+    if ((rc = sketch_batched(c)) != FAB_OK) return rc;
+    double ms = 0;
+    if ((rc = timed_end(c, &ms)) != FAB_OK) return rc;
+    c->sketch_in_V = true;
+    c->info.sketch_fused = 0;
+    c->info.ms_sketch_batched = ms;
+  }
   FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
   int warn = FAB_OK;
-  const int64_t l0 = c->nlaunch;
-  int rc = run_compress(c, mode, o, &warn);
+  rc = run_compress(c, mode, o, &warn);
   if (rc != FAB_OK) return rc;
   c->info.launches_compress = c->nlaunch - l0;
   double ms = 0;

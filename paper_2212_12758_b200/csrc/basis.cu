@@ -15,6 +15,7 @@
 // result equals the literal algorithm (G-4).  The whole m-step loop is one
 // CUDA graph.
 #include "fab_internal.cuh"
+#include "pipe.cuh"
 
 namespace fab {
 
@@ -24,8 +25,114 @@ struct StencilP {
 };
 
 // ---------------------------------------------------------------------------
-// K1 (stencil): z = A x, dots with the window, fixed-order CTA partials
+// K1 (stencil): z = A x and the window dots in one pass, fixed-order CTA
+// partials.  Vector path (gx even, so a row pair r, r+1 (r even) always lies
+// on one grid line): each thread owns U row pairs of a contiguous block of
+// 2*U*256 rows, issues every load of the block (double2 centre / y / z
+// neighbours, scalar x neighbours, double2 window columns) before any
+// arithmetic, so ~64 KB per SM are in flight at 2 CTAs/SM.  The y and x
+// neighbours of a contiguous block are L1/L2 hits; z neighbours (+-1 plane)
+// are L2 hits.  HBM bytes per row: x (8) + (nw-1) window columns + z (8).
 // ---------------------------------------------------------------------------
+constexpr int kK1U = 2;                       // row pairs per thread per block
+constexpr int kK1Block = kThreads * 2 * kK1U; // rows per CTA per block
+
+__device__ __forceinline__ double2 ld2(const double* p) {
+  return __ldg(reinterpret_cast<const double2*>(p));
+}
+
+template <int DIM, int NWM, int U = (NWM <= 4 ? kK1U : 1)>
+__global__ void __launch_bounds__(kThreads, 2)
+k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP sp, int64_t n,
+                 double* __restrict__ z, double* __restrict__ part, const DevState* __restrict__ st) {
+  if (st->breakdown) return;
+  __shared__ double red[kWarps * NWM];
+  const double* __restrict__ x = V + (int64_t)(c - 1) * ld;
+  const int j0 = c - nw;
+  double d[NWM];
+#pragma unroll
+  for (int t = 0; t < NWM; ++t) d[t] = 0.0;
+  const unsigned gx = (unsigned)sp.gx, gy = (unsigned)sp.gy, gz = (unsigned)sp.gz;
+  const int64_t plane = (int64_t)gx * gy;
+  const double2 zero2 = make_double2(0.0, 0.0);
+  for (int64_t base = (int64_t)blockIdx.x * (kThreads * 2 * U); base < n; base += (int64_t)gridDim.x * (kThreads * 2 * U)) {
+    double2 xc[U], ym[U], yp[U], zm[U], zp[U], w[U][NWM > 1 ? NWM - 1 : 1];
+    double xl[U], xr[U];
+    unsigned ixs[U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = base + 2 * threadIdx.x + 2 * kThreads * u;
+      ok[u] = r < n;                       // n even on this path: r+1 < n too
+      xc[u] = ym[u] = yp[u] = zm[u] = zp[u] = zero2;
+      xl[u] = xr[u] = 0.0;
+      ixs[u] = 0;
+#pragma unroll
+      for (int t = 0; t < NWM - 1; ++t) w[u][t] = zero2;
+      if (ok[u]) {
+        const unsigned ur = (unsigned)r;
+        const unsigned ix = ur % gx;
+        const unsigned rest = ur / gx;
+        const unsigned iy = rest % gy;
+        const unsigned iz = rest / gy;
+        ixs[u] = ix;
+        xc[u] = ld2(x + r);
+        if (ix > 0) xl[u] = __ldg(x + r - 1);
+        if (ix + 2 < gx) xr[u] = __ldg(x + r + 2);
+        if (iy > 0) ym[u] = ld2(x + r - gx);
+        if (iy + 1 < gy) yp[u] = ld2(x + r + gx);
+        if (DIM == 3) {
+          if (iz > 0) zm[u] = ld2(x + r - plane);
+          if (iz + 1 < gz) zp[u] = ld2(x + r + plane);
+        }
+#pragma unroll
+        for (int t = 0; t < NWM - 1; ++t)
+          if (t < nw - 1) w[u][t] = ld2(V + (int64_t)(j0 + t) * ld + r);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!ok[u]) continue;
+      const int64_t r = base + 2 * threadIdx.x + 2 * kThreads * u;
+      // same term order as the scalar kernel: centre, x-, x+, y-, y+, z-, z+
+      double a0 = sp.c0 * xc[u].x, a1 = sp.c0 * xc[u].y;
+      if (ixs[u] > 0) a0 = fma(sp.cxm, xl[u], a0);
+      a1 = fma(sp.cxm, xc[u].x, a1);
+      a0 = fma(sp.cxp, xc[u].y, a0);
+      if (ixs[u] + 2 < gx) a1 = fma(sp.cxp, xr[u], a1);
+      // the y/z neighbour pairs were left at 0 outside the grid; skip them
+      // explicitly so boundary rows sum exactly the in-grid terms
+      const unsigned ur = (unsigned)r;
+      const unsigned rest = ur / gx;
+      const unsigned iy = rest % gy, iz = rest / gy;
+      if (iy > 0) { a0 = fma(sp.cym, ym[u].x, a0); a1 = fma(sp.cym, ym[u].y, a1); }
+      if (iy + 1 < gy) { a0 = fma(sp.cyp, yp[u].x, a0); a1 = fma(sp.cyp, yp[u].y, a1); }
+      if (DIM == 3) {
+        if (iz > 0) { a0 = fma(sp.czm, zm[u].x, a0); a1 = fma(sp.czm, zm[u].y, a1); }
+        if (iz + 1 < gz) { a0 = fma(sp.czp, zp[u].x, a0); a1 = fma(sp.czp, zp[u].y, a1); }
+      }
+      *reinterpret_cast<double2*>(z + r) = make_double2(a0, a1);
+#pragma unroll
+      for (int t = 0; t < NWM - 1; ++t) {
+        if (t < nw - 1) {
+          d[t] = fma(w[u][t].x, a0, d[t]);
+          d[t] = fma(w[u][t].y, a1, d[t]);
+        }
+      }
+      d[NWM - 1] = fma(xc[u].x, a0, d[NWM - 1]);   // j = c-1 (already loaded)
+      d[NWM - 1] = fma(xc[u].y, a1, d[NWM - 1]);
+    }
+  }
+  double out[NWM];
+  block_sum<NWM>(d, red, out);
+  if (threadIdx.x == 0) {
+    double* p = part + (int64_t)blockIdx.x * (kKMax + 1);
+    for (int t = 0; t < nw - 1; ++t) p[t] = out[t];
+    p[nw - 1] = out[NWM - 1];
+  }
+}
+
+// scalar fallback (odd gx): one row per thread, grid-stride
 template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 k_stencil_dots(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP sp, int64_t n,
@@ -237,14 +344,16 @@ __device__ __forceinline__ int sk_addr(int idx) { return idx + (idx >> 4); }
 constexpr int kSkSmem = kSkT + kSkT / 16;
 constexpr int kSkAcc = 3;       // s <= 768
 
-// Transforms the 16 sign-applied values v (layout A) of one tile; the result
-// lands in smem (padded natural order).  Caller syncs before reusing smem.
-__device__ __forceinline__ void tile_fwht(double (&v)[kSkPer], double* sm) {
-  const int tid = threadIdx.x, lane = tid & 31;
+// Transforms the 16 sign-applied values v (layout A, thread t = consumer
+// index 0..255) of one tile; the result lands in sm (padded natural order).
+// Synchronises the 256 consumer threads only (named barrier 1).  The caller
+// syncs again before sm is rewritten.
+__device__ __forceinline__ void tile_fwht(double (&v)[kSkPer], double* sm, int tid) {
+  const int lane = tid & 31;
   reg_fwht16(v);                                      // bits 8..11
 #pragma unroll
   for (int q = 0; q < kSkPer; ++q) sm[sk_addr(tid + kThreads * q)] = v[q];
-  __syncthreads();
+  consumer_sync(1, kThreads);
 #pragma unroll
   for (int q = 0; q < kSkPer; ++q) v[q] = sm[17 * tid + q];
   reg_fwht16(v);                                      // bits 0..3
@@ -256,85 +365,240 @@ __device__ __forceinline__ void tile_fwht(double (&v)[kSkPer], double* sm) {
       v[q] = (lane & h) ? (p - v[q]) : (v[q] + p);
     }
   }
-  __syncthreads();
+  consumer_sync(1, kThreads);
 #pragma unroll
   for (int q = 0; q < kSkPer; ++q) sm[17 * tid + q] = v[q];
-  __syncthreads();
+  consumer_sync(1, kThreads);
 }
 
-__device__ __forceinline__ void tile_gather(const double* sm, const int64_t* __restrict__ rows, int s,
-                                            int64_t tile, double (&acc)[kSkAcc]) {
+// Sampled rows of Theta, held in registers by consumer thread tid for the
+// whole kernel: p = tid + 256 a (a < kSkAcc), loc = r mod T, hi = r / T.
+struct SkRows {
+  int loc[kSkAcc];
+  int64_t hi[kSkAcc];
+};
+
+__device__ __forceinline__ void load_sk_rows(const int64_t* __restrict__ rows, int s, int tid, SkRows& R) {
 #pragma unroll
   for (int a = 0; a < kSkAcc; ++a) {
-    const int p = threadIdx.x + kThreads * a;
+    const int p = tid + kThreads * a;
+    const int64_t r = p < s ? __ldg(rows + p) : 0;
+    R.loc[a] = (int)(r & (kSkT - 1));
+    R.hi[a] = r >> kSkLogT;
+  }
+}
+
+// acc[a] += H_N[r_p, tile part] applied to the transformed tile: the in-tile
+// entry r_p mod T times the cross-tile sign (-1)^popcount((r_p / T) & tile)
+__device__ __forceinline__ void tile_gather(const double* sm, const SkRows& R, int s, int64_t tile, int tid,
+                                            double (&acc)[kSkAcc]) {
+#pragma unroll
+  for (int a = 0; a < kSkAcc; ++a) {
+    const int p = tid + kThreads * a;
     if (p < s) {
-      const int64_t r = __ldg(rows + p);
-      const int loc = (int)(r & (kSkT - 1));
-      const int par = __popcll((unsigned long long)((r >> kSkLogT) & tile)) & 1;
-      const double v = sm[sk_addr(loc)];
+      const int par = __popcll((unsigned long long)(R.hi[a] & tile)) & 1;
+      const double v = sm[sk_addr(R.loc[a])];
       acc[a] += par ? -v : v;
     }
   }
 }
 
-__device__ __forceinline__ bool sign_neg(const uint32_t* __restrict__ signs, int64_t g) {
-  return (__ldg(signs + (g >> 5)) >> (g & 31)) & 1u;
-}
 
-template <bool SKETCH>
-__global__ void __launch_bounds__(kThreads)
-k_update(double* __restrict__ V, int64_t ld, int c, int nw, const double* __restrict__ coef,
-         const double* __restrict__ z, int64_t n, int64_t row_begin, double* __restrict__ part_norm,
-         const uint32_t* __restrict__ signs, const int64_t* __restrict__ rows, int s,
-         double* __restrict__ part_sk, const DevState* __restrict__ st) {
-  if (st->breakdown) return;
-  extern __shared__ double sm[];
+// Streaming pipeline of K3 / K5.  256 consumer threads (8 warps) + 1
+// producer warp; persistent grid (one CTA per SM).  Work order, identical in
+// producer and consumers: for col in [col0, col1): for every tile owned by
+// this CTA (tile = t_first + blockIdx.x + i*gridDim.x): 8 chunks of 512 rows.
+// A ring stage holds nvec vectors x 512 rows:
+//   UPDATE (K3, col1 = col0+1 = c): vector 0 = z, vector 1+t = window column
+//          j0+t; the consumers form w_hat_c, store it, accumulate ||w_hat_c||^2
+//          and (SKETCH) the pruned-FWHT partials of w_hat_c.
+//   !UPDATE (K5 / column 0): vector 0 = column col; sketch partials only.
+constexpr int kChunk = 512;
+constexpr int kChunksPerTile = kSkT / kChunk;   // 8
+constexpr int kPipeThreads = kThreads + 32;
+constexpr int kMaxStages = 16;
+constexpr int kSignPad = 16;   // doubles reserved per stage for the chunk's sign bits
+constexpr int kSmemLimit = 226 * 1024;   // dynamic smem budget per CTA (opt-in max 227 KB)
+
+struct PipeArgs {
+  double* V;
+  int64_t ld;
+  int col0, col1;       // columns produced (UPDATE: output column c) / sketched
+  int nw;               // UPDATE: window size
+  const double* coef;   // UPDATE: coefficients of step c
+  const double* z;      // UPDATE: z = A w_hat_{c-1}
+  int64_t n, row_begin;
+  double* part_norm;    // UPDATE: per-CTA ||w_hat_c||^2
+  const uint32_t* signs;
+  const int64_t* rows;
+  int s;
+  double* part_sk;      // per (col, CTA) sketch partials: [(col*grid + cta)*s + p]
+  const DevState* st;
+  int nstage;
+};
+
+template <bool UPDATE, bool SKETCH>
+__global__ void __launch_bounds__(kPipeThreads, 1) k_stream_tiles(PipeArgs a) {
+  if (a.st->breakdown) return;
+  extern __shared__ __align__(128) double dsm[];
   __shared__ double red[kWarps];
-  const double* cf = coef + (int64_t)c * (kKMax + 1);
-  double cz = cf[0], cw[kKMax];
-#pragma unroll
-  for (int t = 0; t < kKMax; ++t) cw[t] = (t < nw) ? cf[1 + t] : 0.0;
-  const int j0 = c - nw;
-  double* __restrict__ out = V + (int64_t)c * ld;
-  double nrm = 0.0;
-  double acc[kSkAcc] = {0.0, 0.0, 0.0};
-  const int64_t t_first = row_begin >> kSkLogT;
-  const int64_t t_last = (row_begin + n - 1) >> kSkLogT;
-  for (int64_t tile = t_first + blockIdx.x; tile <= t_last; tile += gridDim.x) {
-    const int64_t g0 = tile << kSkLogT;
-    double v[kSkPer];
-#pragma unroll
-    for (int q = 0; q < kSkPer; ++q) {
-      const int64_t g = g0 + threadIdx.x + kThreads * q;
-      const int64_t r = g - row_begin;
-      double val = 0.0;
-      if (r >= 0 && r < n) {
-        val = cz * __ldg(z + r);
-#pragma unroll
-        for (int t = 0; t < kKMax; ++t)
-          if (t < nw) val = fma(cw[t], __ldg(V + (int64_t)(j0 + t) * ld + r), val);
-        out[r] = val;
-        nrm = fma(val, val, nrm);
-        if (SKETCH && sign_neg(signs, g)) val = -val;
+  const int nvec = UPDATE ? 1 + a.nw : 1;
+  const int nstage = a.nstage;
+  // stage: nvec x 512 rows of fp64, then (SKETCH) the 512 sign bits of the
+  // chunk (64 B, padded to 128 B)
+  const int stage_d = nvec * kChunk + (SKETCH ? kSignPad : 0);
+  double* ring = dsm;
+  double* fw = ring + (size_t)nstage * stage_d;
+  uint64_t* full = reinterpret_cast<uint64_t*>(fw + (SKETCH ? kSkSmem : 0));
+  uint64_t* empty = full + nstage;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < nstage; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, kWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t n = a.n, rb = a.row_begin;
+  const int64_t t_first = rb >> kSkLogT;
+  const int64_t t_last = (rb + n - 1) >> kSkLogT;
+  const int j0 = UPDATE ? a.col0 - a.nw : 0;
+
+  if (warp == kWarps) {
+    // ---------------- producer warp ----------------
+    const uint64_t pol = policy_evict_first();
+    RingPos rp;
+    for (int col = a.col0; col < a.col1; ++col) {
+      for (int64_t tile = t_first + blockIdx.x; tile <= t_last; tile += gridDim.x) {
+        for (int ch = 0; ch < kChunksPerTile; ++ch) {
+          const int64_t r0 = (tile << kSkLogT) + ch * kChunk - rb;
+          const int64_t lo = r0 > 0 ? r0 : 0;
+          int64_t hi = r0 + kChunk < n ? r0 + kChunk : n;
+          mbar_wait(empty + rp.stage, rp.phase ^ 1u);
+          if (hi > lo) {
+            hi = (hi + 1) & ~(int64_t)1;   // 16-B multiple; stays inside ld (ld % 32 == 0)
+            const uint32_t bytes = (uint32_t)((hi - lo) * 8);
+            if (lane == 0) mbar_arrive_expect_tx(full + rp.stage, bytes * nvec + (SKETCH ? 64u : 0u));
+            __syncwarp();
+            double* sb = ring + (size_t)rp.stage * stage_d;
+            if (lane < nvec) {
+              const double* src;
+              if (UPDATE)
+                src = lane == 0 ? a.z : a.V + (int64_t)(j0 + lane - 1) * a.ld;
+              else
+                src = a.V + (int64_t)col * a.ld;
+              bulk_g2s(sb + (size_t)lane * kChunk + (lo - r0), src + lo, bytes, full + rp.stage, pol);
+            } else if (SKETCH && lane == nvec) {
+              // sign words of global rows [g, g+512): g is 512-aligned, the
+              // bitmap is padded to 256 B, so the 64 B are always in bounds
+              const int64_t gw = ((tile << kSkLogT) + ch * kChunk) >> 5;
+              bulk_g2s(sb + (size_t)nvec * kChunk, a.signs + gw, 64u, full + rp.stage, pol);
+            }
+          } else if (lane == 0) {
+            mbar_arrive(full + rp.stage);
+          }
+          __syncwarp();
+          rp.advance(nstage);
+        }
       }
-      v[q] = val;
+    }
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  double cz = 1.0, cw[kKMax];
+#pragma unroll
+  for (int t = 0; t < kKMax; ++t) cw[t] = 0.0;
+  if (UPDATE) {
+    const double* cf = a.coef + (int64_t)a.col0 * (kKMax + 1);
+    cz = cf[0];
+#pragma unroll
+    for (int t = 0; t < kKMax; ++t) cw[t] = (t < a.nw) ? cf[1 + t] : 0.0;
+  }
+  double* __restrict__ out = UPDATE ? a.V + (int64_t)a.col0 * a.ld : nullptr;
+  SkRows R;
+  if (SKETCH) load_sk_rows(a.rows, a.s, tid, R);
+  double nrm = 0.0;
+  RingPos rp;
+  for (int col = a.col0; col < a.col1; ++col) {
+    double acc[kSkAcc] = {0.0, 0.0, 0.0};
+    for (int64_t tile = t_first + blockIdx.x; tile <= t_last; tile += gridDim.x) {
+      const int64_t g0 = tile << kSkLogT;
+      double v[kSkPer];
+#pragma unroll
+      for (int ch = 0; ch < kChunksPerTile; ++ch) {
+        mbar_wait(full + rp.stage, rp.phase);
+        const double* sb = ring + (size_t)rp.stage * stage_d;
+        const uint32_t* sgn = reinterpret_cast<const uint32_t*>(sb + nvec * kChunk);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = tid + kThreads * h;
+          const int64_t g = g0 + ch * kChunk + i;
+          const int64_t r = g - rb;
+          double val = 0.0;
+          if (r >= 0 && r < n) {
+            if (UPDATE) {
+              val = cz * sb[i];
+#pragma unroll
+              for (int t = 0; t < kKMax; ++t)
+                if (t < a.nw) val = fma(cw[t], sb[(1 + t) * kChunk + i], val);
+              out[r] = val;
+              nrm = fma(val, val, nrm);
+            } else {
+              val = sb[i];
+            }
+            if (SKETCH && ((sgn[i >> 5] >> (i & 31)) & 1u)) val = -val;
+          }
+          v[2 * ch + h] = val;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + rp.stage);
+        rp.advance(nstage);
+      }
+      if (SKETCH) {
+        tile_fwht(v, fw, tid);
+        tile_gather(fw, R, a.s, tile, tid, acc);
+        consumer_sync(1, kThreads);
+      }
     }
     if (SKETCH) {
-      tile_fwht(v, sm);
-      tile_gather(sm, rows, s, tile, acc);
-      __syncthreads();
-    }
-  }
-  if (SKETCH) {
 #pragma unroll
-    for (int a = 0; a < kSkAcc; ++a) {
-      const int p = threadIdx.x + kThreads * a;
-      if (p < s) part_sk[(int64_t)blockIdx.x * s + p] = acc[a];
+      for (int q = 0; q < kSkAcc; ++q) {
+        const int p = tid + kThreads * q;
+        if (p < a.s) a.part_sk[((int64_t)col * gridDim.x + blockIdx.x) * a.s + p] = acc[q];
+      }
     }
   }
-  double v1[1] = {nrm}, o1[1];
-  block_sum<1>(v1, red, o1);
-  if (threadIdx.x == 0) part_norm[blockIdx.x] = o1[0];
+  if (UPDATE) {
+    const double wsum = warp_sum(nrm);
+    if (lane == 0) red[warp] = wsum;
+    consumer_sync(1, kThreads);
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kWarps; ++w) s += red[w];
+      a.part_norm[blockIdx.x] = s;
+    }
+  }
+}
+
+static int pipe_stages(int nvec, bool sketch, size_t* smem) {
+  const size_t stage = ((size_t)nvec * kChunk + (sketch ? kSignPad : 0)) * sizeof(double);
+  const size_t fixed = (sketch ? kSkSmem * sizeof(double) : 0) + 1024;
+  int ns = (int)((kSmemLimit - fixed) / (stage + 16));
+  if (ns > kMaxStages) ns = kMaxStages;
+  if (ns < 2) ns = 2;
+  *smem = (size_t)ns * stage + (sketch ? kSkSmem * sizeof(double) : 0) + 2 * ns * sizeof(uint64_t);
+  return ns;
+}
+
+template <bool UPDATE, bool SKETCH>
+static int launch_stream(fab_ctx* c, PipeArgs a, int nvec, cudaStream_t st) {
+  size_t smem = 0;
+  a.nstage = pipe_stages(nvec, SKETCH, &smem);
+  k_stream_tiles<UPDATE, SKETCH><<<c->grid_upd, kPipeThreads, smem, st>>>(a);
+  FAB_CHECK_LAUNCH();
+  return FAB_OK;
 }
 
 // partial ||x||^2 with the same grid as k_update (column 0 = b)
@@ -430,22 +694,32 @@ void release_long_rows(fab_ctx* c) {
     }
 }
 
+bool stencil_vec_path(const fab_ctx* c) {
+  // row pairs never straddle a grid line, and double2 accesses stay aligned
+  return c->stencil && (c->op.dims[0] % 2 == 0) && (c->row_begin % 2 == 0);
+}
+
 int basis_setup_grids(fab_ctx* c) {
-  int occ = 0;
-  FAB_CUDA(cudaFuncSetAttribute(k_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                kSkSmem * (int)sizeof(double)));
-  FAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update<true>, kThreads,
-                                                         kSkSmem * sizeof(double)));
-  if (occ < 1) occ = 1;
+  // the ring is sized per launch (pipe_stages); allow the full 227 KB once
+  FAB_CUDA(set_max_dyn_smem((const void*)k_stream_tiles<true, true>, kSmemLimit));
+  FAB_CUDA(set_max_dyn_smem((const void*)k_stream_tiles<true, false>, kSmemLimit));
+  FAB_CUDA(set_max_dyn_smem((const void*)k_stream_tiles<false, true>, kSmemLimit));
+  // K3/K5 pipeline: persistent, one CTA per SM (the ring takes the smem)
   const int64_t ntiles = ((c->row_begin + c->n - 1) >> kSkLogT) - (c->row_begin >> kSkLogT) + 1;
-  int64_t g = (int64_t)c->num_sms * occ;
-  c->grid_upd = (int)(ntiles < g ? ntiles : g);
-  int occ1 = 0;
-  FAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_stencil_dots<3>, kThreads, 0));
-  if (occ1 < 1) occ1 = 1;
-  int64_t g1 = (int64_t)c->num_sms * occ1;
-  const int64_t need = (c->n + kThreads - 1) / kThreads;
-  c->grid_spmv = (int)(need < g1 ? need : g1);
+  c->grid_upd = (int)(ntiles < c->num_sms ? ntiles : c->num_sms);
+  if (stencil_vec_path(c)) {
+    // K1 vector path: 2 CTAs/SM, blocks of kK1Block contiguous rows
+    const int64_t need = (c->n + kK1Block - 1) / kK1Block;
+    const int64_t g1 = 2 * (int64_t)c->num_sms;
+    c->grid_spmv = (int)(need < g1 ? need : g1);
+  } else {
+    int occ1 = 0;
+    FAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_csr_dots<8>, kThreads, 0));
+    if (occ1 < 1) occ1 = 1;
+    const int64_t g1 = (int64_t)c->num_sms * occ1;
+    const int64_t need = (c->n + kThreads - 1) / kThreads;
+    c->grid_spmv = (int)(need < g1 ? need : g1);
+  }
   if (c->grid_spmv < 1) c->grid_spmv = 1;
   return FAB_OK;
 }
@@ -495,12 +769,24 @@ static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st,
   int nparts = c->grid_spmv;
   if (c->stencil) {
     StencilP sp = stencil_params(c);
-    if (c->op.dims[2] > 1)
-      k_stencil_dots<3><<<c->grid_spmv, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, c->vec,
-                                                           c->part_dots, c->st_d);
-    else
-      k_stencil_dots<2><<<c->grid_spmv, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, c->vec,
-                                                           c->part_dots, c->st_d);
+    const bool d3 = c->op.dims[2] > 1;
+    const int G = c->grid_spmv;
+    if (stencil_vec_path(c)) {
+#define FAB_K1V(DIM, NWM) \
+  k_stencil_dots_v<DIM, NWM><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, c->vec, c->part_dots, c->st_d)
+      if (c->k_max <= 2) {
+        if (d3) FAB_K1V(3, 2); else FAB_K1V(2, 2);
+      } else if (c->k_max <= 4) {
+        if (d3) FAB_K1V(3, 4); else FAB_K1V(2, 4);
+      } else {
+        if (d3) FAB_K1V(3, 8); else FAB_K1V(2, 8);
+      }
+#undef FAB_K1V
+    } else if (d3) {
+      k_stencil_dots<3><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, c->vec, c->part_dots, c->st_d);
+    } else {
+      k_stencil_dots<2><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, c->vec, c->part_dots, c->st_d);
+    }
     FAB_CHECK_LAUNCH();
     ++*launches;
   } else {
@@ -523,68 +809,45 @@ static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st,
                                    c->H, c->ldH, c->coef, 0, c->st_d);
   FAB_CHECK_LAUNCH();
   ++*launches;
-  if (fused) {
-    k_update<true><<<c->grid_upd, kThreads, kSkSmem * sizeof(double), st>>>(
-        c->V, c->ld, col, nw, c->coef, c->vec, c->n, c->row_begin, c->part_norm, c->signs_d,
-        c->rows_d, c->s, c->part_sk + (int64_t)col * c->grid_upd * c->s, c->st_d);
-  } else {
-    k_update<false><<<c->grid_upd, kThreads, 0, st>>>(c->V, c->ld, col, nw, c->coef, c->vec, c->n,
-                                                      c->row_begin, c->part_norm, nullptr, nullptr, 0,
-                                                      nullptr, c->st_d);
+  {
+    PipeArgs a{};
+    a.V = c->V;
+    a.ld = c->ld;
+    a.col0 = col;
+    a.col1 = col + 1;
+    a.nw = nw;
+    a.coef = c->coef;
+    a.z = c->vec;
+    a.n = c->n;
+    a.row_begin = c->row_begin;
+    a.part_norm = c->part_norm;
+    a.signs = c->signs_d;
+    a.rows = c->rows_d;
+    a.s = c->s;
+    a.part_sk = c->part_sk;
+    a.st = c->st_d;
+    const int rc = fused ? launch_stream<true, true>(c, a, 1 + nw, st) : launch_stream<true, false>(c, a, 1 + nw, st);
+    if (rc != FAB_OK) return rc;
   }
-  FAB_CHECK_LAUNCH();
   ++*launches;
   return FAB_OK;
 }
 
-// column-0 sketch partials (the fused path sketches w_hat_0 = b here)
-__global__ void __launch_bounds__(kThreads)
-k_sketch_cols(const double* __restrict__ V, int64_t ld, int c0, int c1, int64_t n, int64_t row_begin,
-              const uint32_t* __restrict__ signs, const int64_t* __restrict__ rows, int s,
-              double* __restrict__ part_sk, int grid_parts) {
-  extern __shared__ double sm[];
-  const int64_t t_first = row_begin >> kSkLogT;
-  const int64_t t_last = (row_begin + n - 1) >> kSkLogT;
-  for (int col = c0; col < c1; ++col) {
-    const double* __restrict__ x = V + (int64_t)col * ld;
-    double acc[kSkAcc] = {0.0, 0.0, 0.0};
-    for (int64_t tile = t_first + blockIdx.x; tile <= t_last; tile += gridDim.x) {
-      const int64_t g0 = tile << kSkLogT;
-      double v[kSkPer];
-#pragma unroll
-      for (int q = 0; q < kSkPer; ++q) {
-        const int64_t g = g0 + threadIdx.x + kThreads * q;
-        const int64_t r = g - row_begin;
-        double val = 0.0;
-        if (r >= 0 && r < n) {
-          val = __ldg(x + r);
-          if (sign_neg(signs, g)) val = -val;
-        }
-        v[q] = val;
-      }
-      tile_fwht(v, sm);
-      tile_gather(sm, rows, s, tile, acc);
-      __syncthreads();
-    }
-#pragma unroll
-    for (int a = 0; a < kSkAcc; ++a) {
-      const int p = threadIdx.x + kThreads * a;
-      if (p < s) part_sk[((int64_t)col * grid_parts + blockIdx.x) * s + p] = acc[a];
-    }
-  }
-}
-
+// K5 / column 0: sketch partials of columns [c0, c1) (no writes)
 int launch_sketch_cols(fab_ctx* c, int c0, int c1, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    FAB_CUDA(cudaFuncSetAttribute(k_sketch_cols, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSkSmem * (int)sizeof(double)));
-    attr = true;
-  }
-  k_sketch_cols<<<c->grid_upd, kThreads, kSkSmem * sizeof(double), st>>>(
-      c->V, c->ld, c0, c1, c->n, c->row_begin, c->signs_d, c->rows_d, c->s, c->part_sk, c->grid_upd);
-  FAB_CHECK_LAUNCH();
-  return FAB_OK;
+  PipeArgs a{};
+  a.V = c->V;
+  a.ld = c->ld;
+  a.col0 = c0;
+  a.col1 = c1;
+  a.n = c->n;
+  a.row_begin = c->row_begin;
+  a.signs = c->signs_d;
+  a.rows = c->rows_d;
+  a.s = c->s;
+  a.part_sk = c->part_sk;
+  a.st = c->st_d;
+  return launch_stream<false, true>(c, a, 1, st);
 }
 
 int run_basis(fab_ctx* c, int m, int k) {

@@ -166,6 +166,19 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* smem, double 
   __syncthreads();
 }
 
+// Raise a kernel's dynamic shared-memory cap to min(want, opt-in max - its
+// static shared memory).
+inline cudaError_t set_max_dyn_smem(const void* fn, int want) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return e;
+  int dev = 0, optin = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
+  const int cap = optin - (int)fa.sharedSizeBytes;
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, want < cap ? want : cap);
+}
+
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 inline int64_t next_pow2(int64_t n) {
@@ -187,6 +200,7 @@ int sketch_draw(fab_ctx* c, int s, uint64_t seed);
 int sketch_batched(fab_ctx* c);              // K5: Theta V_{m+1} after the basis
 int sketch_finalize(fab_ctx* c, int ncols, cudaStream_t st);
 // lsqr.cu / compress
+int lsqr_setup(fab_ctx* c);
 int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn);
 // dense.cu
 int dense_fe1(fab_ctx* c, int f, double alpha, double sigma, double* c_out, int* iters);

@@ -15,6 +15,7 @@
 #include <math.h>
 
 #include "fab_internal.cuh"
+#include "pipe.cuh"
 
 namespace fab {
 
@@ -82,6 +83,198 @@ k_lsqr_pass(const double* __restrict__ W, int64_t ld, int m, int64_t n, const do
     const double a = warp_sum(tn);
     if (lane == 0) part_tn[blockIdx.x] = a;
   }
+}
+
+// Pipelined version (m <= 384): one producer warp streams 32-row chunks of
+// the m columns of W and of t_old into a ring of shared-memory stages with
+// cp.async.bulk (m+1 copies of 256 B per chunk); 16 consumer warps do the
+// same arithmetic as k_lsqr_pass from shared memory (warp w owns columns
+// w + 16 jj, lane = row).  One named barrier per chunk (double-buffered
+// cross-warp partials of t).  Persistent grid, one CTA per SM.
+constexpr int kLsR = 32;
+constexpr int kLsConsWarps = 16;
+constexpr int kLsCons = kLsConsWarps * 32;
+constexpr int kLsPipeThreads = kLsCons + 32;
+constexpr int kLsMaxStages = 16;
+constexpr int kLsSmemLimit = 226 * 1024;
+
+template <int JPW, bool KEEP = (JPW <= 13)>
+__global__ void __launch_bounds__(kLsPipeThreads, 1)
+k_lsqr_pipe(const __grid_constant__ CUtensorMap tmW, int boxc, int ncopies, int m, int64_t n,
+            const double* __restrict__ p, double scal_arg, const double* t_old, double* t_new,
+            double* __restrict__ part_g, double* __restrict__ part_tn, const DevState* __restrict__ st,
+            int use_state_scal, int nstage) {
+  if (st->lsqr_done) return;
+  extern __shared__ __align__(128) double ring[];
+  __shared__ double sp[kMaxM];
+  __shared__ double tpart[2][kLsConsWarps][32];
+  const int mpad = boxc * ncopies;      // W columns held per stage (>= m; extra ones zero-filled)
+  const int stage_d = (mpad + 1) * kLsR;   // doubles per stage: W box(es) + the t_old chunk
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)nstage * stage_d);
+  uint64_t* empty = full + nstage;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int j = tid; j < m; j += blockDim.x) sp[j] = p[j];
+  if (tid == 0) {
+    for (int i = 0; i < nstage; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, kLsConsWarps);
+    }
+    fence_barrier_init();
+  }
+  const double scal = use_state_scal ? st->scal : scal_arg;
+  __syncthreads();
+  const int64_t nch = (n + kLsR - 1) / kLsR;
+  if (warp == kLsConsWarps) {
+    // ---------------- producer warp ----------------
+    const uint64_t pol = policy_evict_first();
+    RingPos rp;
+    for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+      const int64_t r0 = ch * kLsR;
+      int64_t rows = n - r0 < kLsR ? n - r0 : kLsR;
+      rows = (rows + 1) & ~(int64_t)1;   // 16-B multiple (inside the padded vector)
+      const uint32_t tbytes = (uint32_t)(rows * 8);
+      mbar_wait(empty + rp.stage, rp.phase ^ 1u);
+      if (lane == 0) {
+        double* sb = ring + (size_t)rp.stage * stage_d;
+        mbar_arrive_expect_tx(full + rp.stage, (uint32_t)(mpad * kLsR * 8) + tbytes);
+        for (int q = 0; q < ncopies; ++q)
+          tma_load_2d(sb + (size_t)q * boxc * kLsR, &tmW, (int)r0, q * boxc, full + rp.stage, pol);
+        bulk_g2s(sb + (size_t)mpad * kLsR, t_old + r0, tbytes, full + rp.stage, pol);
+      }
+      __syncwarp();
+      rp.advance(nstage);
+    }
+    return;
+  }
+  // ---------------- consumer warps ----------------
+  double acc[JPW];
+#pragma unroll
+  for (int jj = 0; jj < JPW; ++jj) acc[jj] = 0.0;
+  double tn = 0.0;
+  int buf = 0;
+  RingPos rp;
+  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+    const int64_t r = ch * kLsR + lane;
+    const bool valid = r < n;
+    mbar_wait(full + rp.stage, rp.phase);
+    const double* sb = ring + (size_t)rp.stage * stage_d;
+    double vr[KEEP ? JPW : 1];
+    double tp = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < JPW; ++jj) {
+      const int j = warp + kLsConsWarps * jj;
+      const double w = (valid && j < m) ? sb[j * kLsR + lane] : 0.0;
+      if (KEEP) vr[jj] = w;
+      if (j < m) tp = fma(w, sp[j], tp);
+    }
+    const double told = valid ? sb[mpad * kLsR + lane] : 0.0;
+    if (KEEP) {   // the chunk's values stay in registers: release the stage now
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + rp.stage);
+      rp.advance(nstage);
+    }
+    tpart[buf][warp][lane] = tp;
+    consumer_sync(1, kLsCons);
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < kLsConsWarps; ++w) t += tpart[buf][w][lane];
+    t = fma(-scal, told, t);
+    if (!valid) t = 0.0;
+    if (warp == 0 && valid) {
+      t_new[r] = t;
+      tn = fma(t, t, tn);
+    }
+    if (KEEP) {
+#pragma unroll
+      for (int jj = 0; jj < JPW; ++jj) acc[jj] = fma(vr[jj], t, acc[jj]);
+    } else {      // large m: re-read the chunk from shared memory, then release it
+#pragma unroll
+      for (int jj = 0; jj < JPW; ++jj) {
+        const int j = warp + kLsConsWarps * jj;
+        const double w = (valid && j < m) ? sb[j * kLsR + lane] : 0.0;
+        acc[jj] = fma(w, t, acc[jj]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + rp.stage);
+      rp.advance(nstage);
+    }
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int jj = 0; jj < JPW; ++jj) {
+    const int j = warp + kLsConsWarps * jj;
+    const double a = warp_sum(acc[jj]);
+    if (lane == 0 && j < m) part_g[(int64_t)blockIdx.x * m + j] = a;
+  }
+  if (warp == 0) {
+    const double a = warp_sum(tn);
+    if (lane == 0) part_tn[blockIdx.x] = a;
+  }
+}
+
+typedef void (*LsqrPipeFn)(const CUtensorMap, int, int, int, int64_t, const double*, double, const double*,
+                           double*, double*, double*, const DevState*, int, int);
+
+static LsqrPipeFn pick_pipe(int m) {
+  const int need = (m + kLsConsWarps - 1) / kLsConsWarps;
+#define FAB_PICK(J) \
+  if (need <= J) return k_lsqr_pipe<J>;
+  FAB_PICK(2) FAB_PICK(4) FAB_PICK(8) FAB_PICK(13) FAB_PICK(16) FAB_PICK(19) FAB_PICK(24)
+#undef FAB_PICK
+  return nullptr;
+}
+
+// W box: 32 rows x boxc columns, ncopies boxes per chunk (TMA box dims <= 256)
+static void lsqr_boxes(int m, int* boxc, int* ncopies) {
+  *ncopies = (m + 255) / 256;
+  *boxc = (m + *ncopies - 1) / *ncopies;
+}
+
+static int lsqr_pipe_stages(int m, size_t* smem) {
+  int boxc, ncopies;
+  lsqr_boxes(m, &boxc, &ncopies);
+  const size_t stage = (size_t)(boxc * ncopies + 1) * kLsR * sizeof(double);
+  const size_t fixed = sizeof(double) * (kMaxM + 2 * kLsConsWarps * 32) + 1024;
+  int ns = (int)((kLsSmemLimit - fixed) / (stage + 16));
+  if (ns > kLsMaxStages) ns = kLsMaxStages;
+  *smem = (size_t)ns * stage + 2 * ns * sizeof(uint64_t);
+  return ns;
+}
+
+// Tensor map over the first ncols columns of a column-major n x ncols fp64
+// matrix with leading dimension ld (doubles): box = box_rows x box_cols,
+// zero fill out of bounds.  cuTensorMapEncodeTiled comes from the driver
+// through the runtime's entry-point query (no -lcuda).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int make_tmap_cols(const double* base, int64_t n, int ncols, int64_t ld, int box_rows, int box_cols,
+                   CUtensorMap* out) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    FAB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) return FAB_ECUDA;
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)ncols};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)box_rows, (cuuint32_t)box_cols};
+  const cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? FAB_OK : FAB_ECUDA;
+}
+
+int lsqr_setup(fab_ctx* c) {
+  static const LsqrPipeFn fns[] = {k_lsqr_pipe<2>, k_lsqr_pipe<4>, k_lsqr_pipe<8>, k_lsqr_pipe<13>,
+                                   k_lsqr_pipe<16>, k_lsqr_pipe<19>, k_lsqr_pipe<24>};
+  const int dyn = kLsSmemLimit - (int)(sizeof(double) * (kMaxM + 2 * kLsConsWarps * 32));
+  for (LsqrPipeFn f : fns) FAB_CUDA(set_max_dyn_smem((const void*)f, dyn));
+  return FAB_OK;
 }
 
 typedef void (*LsqrPassFn)(const double*, int64_t, int, int64_t, const double*, double, const double*,
@@ -364,11 +557,29 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
     } else {
       int jpw = 0;
       LsqrPassFn pass = pick_pass(m, &jpw);
-      if (!pass) return FAB_EINVAL;
+      LsqrPipeFn pipe = pick_pipe(m);
+      size_t pipe_smem = 0;
+      const int pipe_ns = lsqr_pipe_stages(m, &pipe_smem);
+      if (pipe_ns < 2) pipe = nullptr;
+      if (!pass && !pipe) return FAB_EINVAL;
+      CUtensorMap tmW;
+      int boxc = 0, ncopies = 0;
+      lsqr_boxes(m, &boxc, &ncopies);
+      if (pipe && make_tmap_cols(c->V, c->n, m, c->ld, kLsR, boxc, &tmW) != FAB_OK) pipe = nullptr;
+      const int64_t nchunks = (c->n + kLsR - 1) / kLsR;
+      const int G = pipe ? (int)(nchunks < c->num_sms ? nchunks : c->num_sms) : c->grid_lsqr;
+      // one streaming pass over V_m: t_new = W p - scal t_old, g = W^T t_new, ||t_new||^2
+      auto launch_pass = [&](double scal, const double* t_old, int use_state) {
+        if (pipe)
+          pipe<<<G, kLsPipeThreads, pipe_smem, st>>>(tmW, boxc, ncopies, m, c->n, L.p, scal, t_old, c->vec,
+                                                    c->part_g, c->part_tn, c->st_d, use_state, pipe_ns);
+        else
+          pass<<<G, kLsqrThreads, 0, st>>>(c->V, c->ld, m, c->n, L.p, scal, t_old, c->vec, c->part_g,
+                                           c->part_tn, c->st_d, use_state);
+      };
       const int fixed = (o && o->iters > 0) ? o->iters : 0;
       const double tol = (o && o->tol > 0) ? o->tol : 1e-6;
       const int maxit = fixed ? fixed : ((o && o->maxit > 0) ? o->maxit : 4 * m);
-      const int G = c->grid_lsqr;
       const bool prof = (c->flags & FAB_FLAG_PROFILE) != 0;
       int npass = 0;
       auto ev_pair = [&](int i) -> cudaEvent_t* {
@@ -383,8 +594,7 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
       FAB_CUDA(cudaMemsetAsync(L.p, 0, m * sizeof(double), st));
       k_reset_lsqr<<<1, 1, 0, st>>>(c->st_d);
       if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[0], st));
-      pass<<<G, kLsqrThreads, 0, st>>>(c->V, c->ld, m, c->n, L.p, -1.0, c->V + (int64_t)m * c->ld,
-                                       c->vec, c->part_g, c->part_tn, c->st_d, 0);
+      launch_pass(-1.0, c->V + (int64_t)m * c->ld, 0);
       FAB_CHECK_LAUNCH();
       if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[1], st));
       ++npass;
@@ -398,8 +608,7 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
         const int nit = (maxit - done_iters) < chunk ? (maxit - done_iters) : chunk;
         for (int it = 0; it < nit; ++it) {
           if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[0], st));
-          pass<<<G, kLsqrThreads, 0, st>>>(c->V, c->ld, m, c->n, L.p, 0.0, c->vec, c->vec, c->part_g,
-                                           c->part_tn, c->st_d, 1);
+          launch_pass(0.0, c->vec, 1);
           FAB_CHECK_LAUNCH();
           if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[1], st));
           ++npass;
