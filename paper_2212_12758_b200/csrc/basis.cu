@@ -322,10 +322,14 @@ __global__ void k_scalar(int c, int nw, int nparts_dots, int nparts_norm, const 
 // ---------------------------------------------------------------------------
 // K3: update + pruned SRHT partials on aligned tiles of T = 4096 global rows
 // ---------------------------------------------------------------------------
-// In-tile FWHT in natural (Sylvester) order: bits 8..11 in registers (layout
-// A: thread t holds idx = t + 256q), bits 0..3 in registers and bits 4..7 by
-// warp shuffles (layout B: idx = 16t + q).  Smem is padded (+1 double every
-// 16) so both layouts are bank-conflict free.
+// In-tile FWHT in natural (Sylvester) order as three radix-16 rounds, each
+// done in registers (16 values per thread) between conflict-free transposes
+// through padded shared memory (+1 double every 16):
+//   layout A: thread t holds idx = t + 256 q          (q = idx bits 8..11)
+//   layout B: thread t holds idx = 16 t + q           (q = idx bits 0..3)
+//   layout C: idx = (t & 15) + 16 q + 256 (t >> 4)    (q = idx bits 4..7)
+// Butterflies of different bits commute, so the order of the rounds does
+// not change the transform.
 __device__ __forceinline__ void reg_fwht16(double (&v)[kSkPer]) {
 #pragma unroll
   for (int h = 1; h < kSkPer; h <<= 1) {
@@ -346,28 +350,27 @@ constexpr int kSkAcc = 3;       // s <= 768
 
 // Transforms the 16 sign-applied values v (layout A, thread t = consumer
 // index 0..255) of one tile; the result lands in sm (padded natural order).
-// Synchronises the 256 consumer threads only (named barrier 1).  The caller
-// syncs again before sm is rewritten.
+// Synchronises the 256 consumer threads only (named barrier 1).  In layouts
+// B and C each thread rewrites exactly the slots it read, so no barrier is
+// needed between a round's read and its write.  The caller syncs again
+// before sm is rewritten.
 __device__ __forceinline__ void tile_fwht(double (&v)[kSkPer], double* sm, int tid) {
-  const int lane = tid & 31;
-  reg_fwht16(v);                                      // bits 8..11
+  reg_fwht16(v);                                      // bits 8..11 (layout A)
 #pragma unroll
   for (int q = 0; q < kSkPer; ++q) sm[sk_addr(tid + kThreads * q)] = v[q];
   consumer_sync(1, kThreads);
 #pragma unroll
-  for (int q = 0; q < kSkPer; ++q) v[q] = sm[17 * tid + q];
+  for (int q = 0; q < kSkPer; ++q) v[q] = sm[17 * tid + q];             // layout B
   reg_fwht16(v);                                      // bits 0..3
 #pragma unroll
-  for (int h = 1; h < 16; h <<= 1) {                  // bits 4..7
-#pragma unroll
-    for (int q = 0; q < kSkPer; ++q) {
-      const double p = __shfl_xor_sync(0xffffffffu, v[q], h);
-      v[q] = (lane & h) ? (p - v[q]) : (v[q] + p);
-    }
-  }
-  consumer_sync(1, kThreads);
-#pragma unroll
   for (int q = 0; q < kSkPer; ++q) sm[17 * tid + q] = v[q];
+  consumer_sync(1, kThreads);
+  const int cbase = (tid & 15) + 272 * (tid >> 4);                       // layout C
+#pragma unroll
+  for (int q = 0; q < kSkPer; ++q) v[q] = sm[cbase + 17 * q];
+  reg_fwht16(v);                                      // bits 4..7
+#pragma unroll
+  for (int q = 0; q < kSkPer; ++q) sm[cbase + 17 * q] = v[q];
   consumer_sync(1, kThreads);
 }
 
