@@ -218,13 +218,24 @@ def main():
     dev = local
 
     p = fp.make("c3", g=args.g)
-    # independent solves per GPU at N > 1 (distributed single solve: DESIGN.md "Multi-GPU")
-    b_np = p.b if rank == 0 else fp.gaussian_b(p.n, 2003 + 7919 * rank)
+    comm = None
+    if world > 1:
+        # ONE solve over all GPUs: z-slabs of the grid, halo
+        # exchange + one allreduce per Krylov step over NCCL (strong scaling)
+        from paper_2212_12758_b200 import dist as fdist
+        comm = fdist.Comm(device=dev)
+        cuts = fdist.stencil_blocks(p.dims, world)
+        r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+        op = fdist.local_operator(p, r0, r1)
+    else:
+        r0, r1 = 0, p.n
+        op = fab.Operator.from_problem(p)
+    n_loc = r1 - r0
+    b_np = np.ascontiguousarray(p.b[r0:r1])
     b = torch.as_tensor(b_np).cuda(dev)
-    op = fab.Operator.from_problem(p)
     stream = torch.cuda.current_stream(dev)
-    sv = fab.Solver(op, b, m_max=p.m, k_max=p.k, s_max=p.s, device=dev, profile=True)
-    y = torch.empty(p.n, dtype=torch.float64, device=f"cuda:{dev}")
+    sv = fab.Solver(op, b, m_max=p.m, k_max=p.k, s_max=p.s, device=dev, profile=True, comm=comm)
+    y = torch.empty(n_loc, dtype=torch.float64, device=f"cuda:{dev}")
 
     def step(mode="blendenpik", fused=True):
         if mode != "none" and fused:
@@ -259,7 +270,7 @@ def main():
         ms = float(t.item())
     clocks = clk.summary()
     ms_step = ms / args.steps
-    value = world * args.steps / (ms / 1e3)
+    value = args.steps / (ms / 1e3)          # solves of the whole job per second
 
     def avg(key):
         return statistics.mean(i[key] for i in infos)
@@ -271,7 +282,7 @@ def main():
     # dominant kernel: the fused LSQR pass t <- W p - scal t, g = W^T t (8 n (m+2) bytes)
     passes = sum(i["lsqr_passes"] for i in infos)
     pass_ms = sum(i["ms_lsqr_pass"] for i in infos) / max(passes, 1)
-    pass_bytes = 8.0 * n * (m + 2)
+    pass_bytes = 8.0 * n_loc * (m + 2)       # this GPU's rows
     achieved = pass_bytes / (pass_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "lsqr_pass_traffic.json")
@@ -294,14 +305,15 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": ms_step,
         "higher_is_better": True,
-        "scaling": "weak" if world > 1 else "strong",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": WORKLOAD, "n": n, "m": m, "k": k, "s": s,
                    "mode": "blendenpik (LSQR tol 1e-6)", "f": "sqrt", "sigma": p.sigma,
                    "l2": "inputs larger than L2 (V_{m+1} = 27 GB >> 126 MB L2), no flush needed",
-                   "parallelism": "1 GPU" if world == 1 else f"{world} independent solves (one per GPU)"},
+                   "parallelism": "1 GPU" if world == 1 else
+                   f"{world} GPUs: one solve, z-slab row blocks, NCCL halo + allreduce"},
         "krylov_iters_per_s": m / (basis_ms * 1e-3),
         "phase_ms": {"sketch": avg("ms_sketch"), "basis": basis_ms, "compress": avg("ms_compress"),
                      "apply": avg("ms_apply")},
@@ -329,16 +341,16 @@ def main():
             e1.record(stream)
             torch.cuda.synchronize()
             modes[mode] = 1e3 / e0.elapsed_time(e1)
-        modes["blendenpik"] = value / world
+        modes["blendenpik"] = value
         out["solves_per_s_by_mode"] = modes
         # API-order variant: sketch after the basis (batched SRHT pass)
         step("blendenpik", fused=False)
         inf = step("blendenpik", fused=False)
         out["api_order_sketch_ms"] = inf["ms_sketch_batched"]
         # e2e: b from pinned host memory, f_m back to pinned host memory, every step
-        bh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        bh = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
         bh.copy_(torch.as_tensor(b_np))
-        yh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        yh = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
         bh_np, yh_np = bh.numpy(), yh.numpy()
 
         def e2e_step():
@@ -362,7 +374,7 @@ def main():
             t = torch.tensor([te], device=f"cuda:{dev}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
-        out["e2e"] = {"value": world * ne / te, "unit": "solves/s", "h2d_bytes_per_step": 8 * n,
+        out["e2e"] = {"value": ne / te, "unit": "solves/s", "h2d_bytes_per_step": 8 * n,
                       "d2h_bytes_per_step": 8 * n}
         ok = np.isfinite(yh_np).all()
         out["e2e"]["output_finite"] = bool(ok)
@@ -376,6 +388,8 @@ def main():
                                "kind": "oracle", "sample": desc,
                                "krylov_iters_per_s": 1.0 / parts["t_iter"]}
     sv.close()
+    if comm is not None:
+        comm.close()
     if rank == 0:
         print(json.dumps(out), flush=True)
     if dist:

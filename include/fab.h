@@ -102,12 +102,12 @@ typedef struct {
   int kind;                /* FAB_OP_CSR or FAB_OP_STENCIL                          */
   int row_ptr_64;          /* reserved (row_ptr is always int64)                    */
   int64_t n;               /* global dimension                                      */
-  int64_t row_begin;       /* first owned row (multi-GPU block rows); 0 on 1 GPU    */
+  int64_t row_begin;       /* first owned (global) row: 0 on 1 GPU; a multiple of 32 */
   int64_t row_end;         /* one past the last owned row; n on 1 GPU               */
   /* CSR (kind == FAB_OP_CSR): device pointers, local rows, GLOBAL column ids  */
   int64_t nnz;
-  const int64_t* row_ptr;  /* row_end-row_begin+1 entries, row_ptr[0] == 0         */
-  const int32_t* col_idx;  /* nnz, sorted ascending within each row                */
+  const int64_t* row_ptr;  /* row_end-row_begin+1 entries (local rows), row_ptr[0]==0 */
+  const int32_t* col_idx;  /* nnz GLOBAL column ids, sorted ascending within a row  */
   const double* values;    /* nnz; NULL => every stored entry equals value_scale    */
   double value_scale;      /* multiplies every value (1.0 = unscaled)               */
   /* constant-coefficient stencil (kind == FAB_OP_STENCIL), Dirichlet BC:
@@ -128,7 +128,11 @@ typedef struct {
   size_t workspace_bytes;  /* size of workspace, >= fab_workspace_size()            */
   int b_location;          /* FAB_DEVICE or FAB_HOST for fab_init's b               */
   unsigned flags;          /* FAB_FLAG_* bits                                       */
-  void* comm;              /* reserved for multi-GPU (NCCL); NULL on one GPU        */
+  void* comm;              /* NULL: one GPU owns every row.  Else a communicator from
+                              fab_comm_init: this rank owns rows [row_begin, row_end)
+                              of A (row_begin % 32 == 0); the ranks' blocks must tile
+                              [0, n) in rank order (checked by fab_init, collectively)
+                              and, for a stencil, each hold >= one halo (a plane in 3D) */
 } fab_opts;
 
 typedef struct {
@@ -157,6 +161,28 @@ typedef struct {
   int64_t lsqr_passes;     /* number of streaming passes over V_m in fab_compress     */
   double ms_sketch_batched;/* batched Theta V pass run by fab_compress (API order)    */
 } fab_info;
+
+/* ---- multi-GPU (one process per GPU, NCCL over NVLink) ----
+   The path is row-partitioned: contiguous row blocks of A, V, b
+   and f_m.  Per Krylov step: a halo exchange of w_hat_{i-1} (stencil: hal rows
+   to / from each neighbour; CSR: all-gather-v of x) and ONE allreduce of k+1
+   doubles (window dots + lagged norm).  Per solve: one allreduce of the
+   s x (m+1) sketch partials (the SRHT of a row block needs no all-to-all:
+   reading R-1), one allreduce of m+1 doubles per LSQR iteration.  QR, LSQR
+   scalars and f(C_m) are replicated; y_out stays distributed (n_local rows).
+   Every rank calls every fab_* function in the same order (as for NCCL
+   collectives).  NCCL (libnccl.so.2) is loaded at run time; FAB_ENCCL if it
+   cannot be loaded.  The caller owns the communicator. */
+
+/* 128-byte NCCL unique id (rank 0 creates it; broadcast it to the others). */
+int fab_comm_unique_id(unsigned char id[128]);
+
+/* Communicator for rank `rank` of `nranks` on CUDA device `device` (collective
+   over the ranks).  *comm is passed as fab_opts.comm.  Errors: EINVAL, ENCCL. */
+int fab_comm_init(void** comm, const unsigned char id[128], int rank, int nranks, int device);
+
+/* Destroy a communicator (after every context using it is destroyed). */
+int fab_comm_destroy(void* comm);
 
 /* Library ABI version (FAB_ABI_VERSION). */
 int fab_version(void);

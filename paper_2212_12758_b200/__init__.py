@@ -40,19 +40,23 @@ class Operator:
         return int(self.st.n)
 
     @staticmethod
-    def stencil(dims, coeffs):
+    def stencil(dims, coeffs, rows=None):
+        """Constant-coefficient stencil; rows = (row_begin, row_end) of this
+        rank on several GPUs (dist.stencil_blocks), None = all rows."""
         st = FabOperator()
         st.kind = _lib.FAB_OP_STENCIL
         gx, gy, gz = (list(dims) + [1, 1])[:3]
         st.n = gx * gy * gz
-        st.row_begin, st.row_end = 0, st.n
+        st.row_begin, st.row_end = (0, st.n) if rows is None else rows
         st.dims[:] = [gx, gy, gz]
         st.coeffs[:] = list(coeffs)
         st.value_scale = 1.0
         return Operator(st)
 
     @staticmethod
-    def csr(indptr, indices, data=None, n=None, value_scale=1.0, device="cuda"):
+    def csr(indptr, indices, data=None, n=None, value_scale=1.0, device="cuda", rows=None):
+        """CSR rows of A with GLOBAL column ids; rows = (row_begin, row_end)
+        when these are one rank's block (dist.local_csr), n = global size."""
         torch = _torch()
         ip = torch.as_tensor(np.ascontiguousarray(indptr, dtype=np.int64)).to(device)
         ix = torch.as_tensor(np.ascontiguousarray(indices, dtype=np.int32)).to(device)
@@ -63,7 +67,8 @@ class Operator:
         st.kind = _lib.FAB_OP_CSR
         nrows = len(indptr) - 1
         st.n = nrows if n is None else n
-        st.row_begin, st.row_end = 0, nrows
+        st.row_begin, st.row_end = (0, nrows) if rows is None else rows
+        assert st.row_end - st.row_begin == nrows
         st.nnz = int(indptr[-1])
         st.row_ptr = ip.data_ptr()
         st.col_idx = ix.data_ptr() if st.nnz else None
@@ -82,7 +87,10 @@ class Operator:
 
 class Solver:
     def __init__(self, op: Operator, b, m_max, k_max=2, s_max=0, stream=None, device=None,
-                 workspace=True, profile=False):
+                 workspace=True, profile=False, comm=None):
+        """b: this rank's rows (numpy host array or CUDA float64 tensor).
+        comm: dist.Comm for a row-partitioned multi-GPU solve (every rank
+        makes the same calls in the same order), None on one GPU."""
         torch = _torch()
         self.op = op
         self.torch = torch
@@ -95,6 +103,8 @@ class Solver:
         o.m_max, o.k_max, o.s_max = m_max, k_max, s_max
         o.b_location = _lib.FAB_DEVICE
         o.flags = _lib.FAB_FLAG_PROFILE if profile else 0
+        self.comm = comm
+        o.comm = comm.handle.value if comm is not None else None
         if isinstance(b, np.ndarray):
             b = np.ascontiguousarray(b, dtype=np.float64)
             o.b_location = _lib.FAB_HOST

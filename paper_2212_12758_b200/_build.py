@@ -19,8 +19,24 @@ INC = os.path.join(os.path.dirname(HERE), "include")
 OUT = os.path.join(HERE, "libfab.so")
 OBJ = os.path.join(HERE, "build")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+def nccl_include():
+    """nccl.h of the NCCL that torch ships (libnccl.so.2 is dlopen'ed at run time)."""
+    try:
+        import nvidia.nccl
+        for base in list(getattr(nvidia.nccl, "__path__", [])):
+            inc = os.path.join(base, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except ImportError:
+        pass
+    for inc in ("/usr/include", "/usr/local/include"):
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc
+    raise RuntimeError("nccl.h not found (nvidia-nccl wheel or system NCCL headers)")
+
+
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-                "--expt-relaxed-constexpr", "-I", INC]
+                "--expt-relaxed-constexpr", "-I", INC, "-I", nccl_include()]
 
 
 def nvcc():
@@ -74,7 +90,7 @@ def build(force=False, ptxas_verbose=False, quiet=False):
         msg = "\n".join(" ".join(c) + "\n" + e for c, e in failed)
         raise RuntimeError("nvcc failed:\n" + msg)
     if force or jobs or _stale(OUT, objs):
-        cmd = [nv] + ARCH + ["-shared", "-o", OUT] + objs
+        cmd = [nv] + ARCH + ["-shared", "-o", OUT] + objs + ["-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stderr)

@@ -26,7 +26,8 @@ FUNCS = {"exp": FAB_EXP, "sqrt": FAB_SQRT, "invsqrt": FAB_INVSQRT, "poly": FAB_P
 # every function declared in include/fab.h
 EXPORTS = ("fab_version", "fab_strerror", "fab_workspace_size", "fab_init", "fab_basis",
            "fab_sketch", "fab_compress", "fab_apply", "fab_get", "fab_get_column", "fab_get_vrows",
-           "fab_set", "fab_last_error", "fab_destroy")
+           "fab_set", "fab_last_error", "fab_destroy", "fab_comm_unique_id", "fab_comm_init",
+           "fab_comm_destroy")
 
 
 class FabOperator(C.Structure):
@@ -85,6 +86,9 @@ def load():
         "fab_get_column": (I, [P, I, P]),
         "fab_get_vrows": (I, [P, P, I, P]),
         "fab_destroy": (I, [P]),
+        "fab_comm_unique_id": (I, [P]),
+        "fab_comm_init": (I, [C.POINTER(P), P, I, I, I]),
+        "fab_comm_destroy": (I, [P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

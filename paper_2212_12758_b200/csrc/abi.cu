@@ -18,7 +18,7 @@ void set_last_cuda_error(cudaError_t e, const char* what, const char* file, int 
 }
 
 struct Layout {
-  size_t V, vec, H, beta, coef, part_norm, part_sk, SV, rows, signs, part_g, part_tn, small, dense, qr, st;
+  size_t V, vec, H, beta, coef, part_norm, part_sk, SV, rows, signs, part_g, part_tn, small, dense, qr, red, xg, st;
   size_t total;
 };
 
@@ -47,6 +47,8 @@ static Layout make_layout(const fab_ctx* c) {
   L.small = carve(cur, (size_t)kSmallVecs * kSmall * 8);
   L.dense = carve(cur, (size_t)kDenseMats * c->m_max * c->m_max * 8);
   L.qr = carve(cur, (size_t)(c->s_max > 0 ? c->s_max : 1) * m1 * 8);
+  L.red = carve(cur, (size_t)kSmall * 8);
+  L.xg = carve(cur, (c->comm && !c->stencil) ? (size_t)c->n_global * 8 : 8);
   L.st = carve(cur, sizeof(DevState));
   L.total = cur;
   return L;
@@ -66,7 +68,6 @@ static int validate_operator(const fab_operator* A) {
   } else if (A->kind == FAB_OP_STENCIL) {
     if (A->dims[0] < 1 || A->dims[1] < 1 || A->dims[2] < 1) return FAB_EINVAL;
     if (A->dims[0] * A->dims[1] * A->dims[2] != A->n) return FAB_EINVAL;
-    if (A->row_begin != 0 || A->row_end != A->n) return FAB_EINVAL;   // one GPU only (this round)
     for (int i = 0; i < 7; ++i)
       if (!isfinite(A->coeffs[i])) return FAB_EINVAL;
   } else {
@@ -81,7 +82,14 @@ static int validate_opts(const fab_operator* A, const fab_opts* o) {
   if (o->k_max < 1 || o->k_max > kKMax) return FAB_EINVAL;
   if (o->s_max < 0 || o->s_max > kThreads * 3) return FAB_EINVAL;
   if (o->b_location != FAB_DEVICE && o->b_location != FAB_HOST) return FAB_EINVAL;
-  if (o->comm) return FAB_EINVAL;   // multi-GPU: not in this build
+  if (!o->comm) {
+    // one GPU owns every row
+    if (A->row_begin != 0 || A->row_end != A->n) return FAB_EINVAL;
+  } else {
+    // row blocks start on a 32-row boundary (256-B aligned bulk copies and
+    // double2 stencil pairs); fab_init checks that the blocks tile [0, n)
+    if (A->row_begin % 32 != 0) return FAB_EINVAL;
+  }
   return FAB_OK;
 }
 
@@ -103,7 +111,14 @@ static int setup_ctx(fab_ctx* c, const fab_operator* A, const fab_opts* o) {
   c->n_global = A->n;
   c->row_begin = A->row_begin;
   c->n = A->row_end - A->row_begin;
-  c->ld = round_up(c->n, 32);
+  c->comm = static_cast<Comm*>(o->comm);
+  c->hal = 0;
+  if (c->stencil && comm_size(c) > 1) {
+    // widest stencil offset: one plane (3D), one line (2D), one row (1D)
+    c->hal = A->dims[2] > 1 ? A->dims[0] * A->dims[1] : (A->dims[1] > 1 ? A->dims[0] : 1);
+  }
+  c->hpad = round_up(c->hal, 32);
+  c->ld = round_up(c->n + 2 * c->hpad, 32);
   c->N = next_pow2(c->n_global);
   c->m_max = o->m_max;
   c->k_max = o->k_max;
@@ -120,7 +135,7 @@ static int setup_ctx(fab_ctx* c, const fab_operator* A, const fab_opts* o) {
 static void assign_buffers(fab_ctx* c) {
   Layout L = make_layout(c);
   char* w = c->ws;
-  c->V = reinterpret_cast<double*>(w + L.V);
+  c->V = reinterpret_cast<double*>(w + L.V) + c->hpad;   // local row 0 of column 0 (after its halo pad)
   c->vec = reinterpret_cast<double*>(w + L.vec);
   c->H = reinterpret_cast<double*>(w + L.H);
   c->beta = reinterpret_cast<double*>(w + L.beta);
@@ -134,6 +149,8 @@ static void assign_buffers(fab_ctx* c) {
   c->part_tn = reinterpret_cast<double*>(w + L.part_tn);
   c->small = reinterpret_cast<double*>(w + L.small);
   c->dense = reinterpret_cast<double*>(w + L.dense);
+  c->red = reinterpret_cast<double*>(w + L.red);
+  c->xg = (c->comm && !c->stencil) ? reinterpret_cast<double*>(w + L.xg) : nullptr;
   c->st_d = reinterpret_cast<DevState*>(w + L.st);
 }
 
@@ -188,7 +205,7 @@ const char* fab_strerror(int s) {
     case FAB_ENOCONV: return "matrix function iteration did not converge";
     case FAB_ENOMEM: return "out of memory / workspace too small";
     case FAB_ECUDA: return g_err[0] ? g_err : "CUDA error";
-    case FAB_ENCCL: return "NCCL error";
+    case FAB_ENCCL: return nccl_last_error()[0] ? nccl_last_error() : "NCCL error (or libnccl.so.2 not loadable)";
     case FAB_ENODEV: return "no sm_100 CUDA device";
     default: return "unknown status";
   }
@@ -262,7 +279,17 @@ int fab_init(fab_ctx** out, const fab_operator* A, const double* b, const fab_op
     for (int i = 0; i < 7; ++i) s += fabs(c->op.coeffs[i]);
     c->norm_inf = s;
   }
-  rc = init_vector_norm(c);   // CSR: ||A||_inf, long-row list, dot partial buffer
+  rc = comm_setup_partition(c);   // row blocks tile [0, n) in rank order, each >= halo
+  if (rc == FAB_OK) rc = init_vector_norm(c);   // CSR: ||A||_inf, long-row list, dot partial buffer
+  if (rc == FAB_OK && c->comm && !c->stencil) {
+    // ||A||_inf = max over the ranks' row blocks
+    rc = cudaMemcpy(c->red, &c->norm_inf, sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess ? FAB_OK
+                                                                                                 : FAB_ECUDA;
+    if (rc == FAB_OK) rc = comm_allreduce(c, c->red, 1, true, c->stream);
+    if (rc == FAB_OK && cudaStreamSynchronize(c->stream) != cudaSuccess) rc = FAB_ECUDA;
+    if (rc == FAB_OK && cudaMemcpy(&c->norm_inf, c->red, sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+      rc = FAB_ECUDA;
+  }
   if (rc != FAB_OK) {
     free_ctx(c);
     return rc;

@@ -43,7 +43,7 @@ __device__ __forceinline__ double2 ld2(const double* p) {
 
 template <int DIM, int NWM, int U = (NWM <= 4 ? kK1U : 1)>
 __global__ void __launch_bounds__(kThreads, 2)
-k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP sp, int64_t n,
+k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP sp, int64_t n, int64_t gbase,
                  double* __restrict__ z, double* __restrict__ part, const DevState* __restrict__ st) {
   if (st->breakdown) return;
   __shared__ double red[kWarps * NWM];
@@ -70,7 +70,7 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
 #pragma unroll
       for (int t = 0; t < NWM - 1; ++t) w[u][t] = zero2;
       if (ok[u]) {
-        const unsigned ur = (unsigned)r;
+        const unsigned ur = (unsigned)(r + gbase);   // global grid index (row blocks: halo slots hold x[r -+ offsets])
         const unsigned ix = ur % gx;
         const unsigned rest = ur / gx;
         const unsigned iy = rest % gy;
@@ -102,7 +102,7 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
       if (ixs[u] + 2 < gx) a1 = fma(sp.cxp, xr[u], a1);
       // the y/z neighbour pairs were left at 0 outside the grid; skip them
       // explicitly so boundary rows sum exactly the in-grid terms
-      const unsigned ur = (unsigned)r;
+      const unsigned ur = (unsigned)(r + gbase);
       const unsigned rest = ur / gx;
       const unsigned iy = rest % gy, iz = rest / gy;
       if (iy > 0) { a0 = fma(sp.cym, ym[u].x, a0); a1 = fma(sp.cym, ym[u].y, a1); }
@@ -135,7 +135,7 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
 // scalar fallback (odd gx): one row per thread, grid-stride
 template <int DIM>
 __global__ void __launch_bounds__(kThreads)
-k_stencil_dots(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP sp, int64_t n,
+k_stencil_dots(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP sp, int64_t n, int64_t gbase,
                double* __restrict__ z, double* __restrict__ part, const DevState* __restrict__ st) {
   if (st->breakdown) return;
   __shared__ double red[kWarps * kKMax];
@@ -147,7 +147,7 @@ k_stencil_dots(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t plane = (int64_t)sp.gx * sp.gy;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
-    const unsigned ur = (unsigned)r;
+    const unsigned ur = (unsigned)(r + gbase);
     const unsigned ix = ur % (unsigned)sp.gx;
     const unsigned rest = ur / (unsigned)sp.gx;
     const unsigned iy = rest % (unsigned)sp.gy;
@@ -189,11 +189,12 @@ template <int G>
 __global__ void __launch_bounds__(kThreads)
 k_csr_dots(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
            const double* __restrict__ vals, double vscale, const double* __restrict__ V,
-           int64_t ld, int c, int nw, int64_t n, double* __restrict__ z,
+           int64_t ld, int c, int nw, int64_t n, const double* __restrict__ xg, double* __restrict__ z,
            double* __restrict__ part, const DevState* __restrict__ st) {
   if (st->breakdown) return;
   __shared__ double red[kWarps * kKMax];
-  const double* __restrict__ x = V + (int64_t)(c - 1) * ld;
+  const double* __restrict__ x = V + (int64_t)(c - 1) * ld;   // local rows of w_hat_{c-1}
+  // xg: w_hat_{c-1} indexed by GLOBAL column id (== x on one GPU)
   const int j0 = c - nw;
   const int lane = threadIdx.x & 31;
   const int sub = lane % G;
@@ -215,9 +216,9 @@ k_csr_dots(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
     }
     if (valid) {
       if (vals) {
-        for (int64_t q = s0 + sub; q < s1; q += G) acc = fma(__ldg(vals + q), __ldg(x + __ldg(ci + q)), acc);
+        for (int64_t q = s0 + sub; q < s1; q += G) acc = fma(__ldg(vals + q), __ldg(xg + __ldg(ci + q)), acc);
       } else {
-        for (int64_t q = s0 + sub; q < s1; q += G) acc += __ldg(x + __ldg(ci + q));
+        for (int64_t q = s0 + sub; q < s1; q += G) acc += __ldg(xg + __ldg(ci + q));
       }
     }
 #pragma unroll
@@ -244,16 +245,15 @@ k_csr_dots(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
 __global__ void __launch_bounds__(kThreads)
 k_csr_long(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
            const double* __restrict__ vals, double vscale, const int64_t* __restrict__ long_rows,
-           const double* __restrict__ V, int64_t ld, int c, int nw, double* __restrict__ z,
-           double* __restrict__ part, const DevState* __restrict__ st) {
+           const double* __restrict__ V, int64_t ld, int c, int nw, const double* __restrict__ xg,
+           double* __restrict__ z, double* __restrict__ part, const DevState* __restrict__ st) {
   if (st->breakdown) return;
   __shared__ double red[kWarps];
-  const double* __restrict__ x = V + (int64_t)(c - 1) * ld;
   const int64_t row = long_rows[blockIdx.x];
   const int64_t s0 = rp[row], s1 = rp[row + 1];
   double acc = 0.0;
   for (int64_t q = s0 + threadIdx.x; q < s1; q += blockDim.x)
-    acc = fma(vals ? __ldg(vals + q) : 1.0, __ldg(x + __ldg(ci + q)), acc);
+    acc = fma(vals ? __ldg(vals + q) : 1.0, __ldg(xg + __ldg(ci + q)), acc);
   double v1[1] = {acc}, o1[1];
   block_sum<1>(v1, red, o1);
   if (threadIdx.x == 0) {
@@ -278,17 +278,40 @@ __device__ double det_sum(const double* p, int count, int stride, int off, doubl
   return o1[0];   // valid in thread 0
 }
 
+// Multi-GPU: this rank's step scalars (window dots, then the lagged norm) in
+// the same fixed order as k_scalar, into sums[0..nw] for the allreduce (C2).
+__global__ void k_step_reduce(int nw, int nparts_dots, int nparts_norm, const double* part_dots,
+                              const double* part_norm, double* sums, const DevState* st) {
+  __shared__ double red[kWarps];
+  if (st->breakdown) return;
+  const double nu = det_sum(part_norm, nparts_norm, 1, 0, red);
+  if (threadIdx.x == 0) sums[nw] = nu;
+  for (int t = 0; t < nw; ++t) {
+    const double dv = det_sum(part_dots, nparts_dots, kKMax + 1, t, red);
+    if (threadIdx.x == 0) sums[t] = dv;
+  }
+}
+
+// sums != nullptr: take the (allreduced) scalars from sums[0..nw] instead of
+// reducing this CTA's partials
 __global__ void k_scalar(int c, int nw, int nparts_dots, int nparts_norm, const double* part_dots,
-                         const double* part_norm, double* beta, double* H, int ldH, double* coef,
-                         int final_step, DevState* st) {
+                         const double* part_norm, const double* sums, double* beta, double* H, int ldH,
+                         double* coef, int final_step, DevState* st) {
   __shared__ double red[kWarps];
   __shared__ double dj[kKMax];
   __shared__ int bd;
   if (st->breakdown) return;
-  const double nu = det_sum(part_norm, nparts_norm, 1, 0, red);
-  for (int t = 0; t < nw; ++t) {
-    double dv = det_sum(part_dots, nparts_dots, kKMax + 1, t, red);
-    if (threadIdx.x == 0) dj[t] = dv;
+  double nu;
+  if (sums) {
+    nu = sums[nw];
+    if (threadIdx.x < nw) dj[threadIdx.x] = sums[threadIdx.x];
+    __syncthreads();
+  } else {
+    nu = det_sum(part_norm, nparts_norm, 1, 0, red);
+    for (int t = 0; t < nw; ++t) {
+      double dv = det_sum(part_dots, nparts_dots, kKMax + 1, t, red);
+      if (threadIdx.x == 0) dj[t] = dv;
+    }
   }
   if (threadIdx.x == 0) {
     const double b = sqrt(nu);
@@ -767,16 +790,40 @@ int init_vector_norm(fab_ctx* c) {
 
 
 // Enqueue one Krylov step c (1..m) on stream st.
+// K2 (+ C2 on several GPUs): the step scalars of column col-1
+static int enqueue_scalar(fab_ctx* c, int col, int nw, int nparts, int final_step, cudaStream_t st,
+                          int64_t* launches) {
+  const double* sums = nullptr;
+  if (c->comm) {
+    k_step_reduce<<<1, kThreads, 0, st>>>(nw, nparts, c->grid_upd, c->part_dots, c->part_norm, c->red, c->st_d);
+    FAB_CHECK_LAUNCH();
+    ++*launches;
+    const int rc = comm_allreduce(c, c->red, (size_t)nw + 1, false, st);
+    if (rc != FAB_OK) return rc;
+    sums = c->red;
+  }
+  k_scalar<<<1, kThreads, 0, st>>>(col, nw, nparts, c->grid_upd, c->part_dots, c->part_norm, sums, c->beta,
+                                   c->H, c->ldH, c->coef, final_step, c->st_d);
+  FAB_CHECK_LAUNCH();
+  ++*launches;
+  return FAB_OK;
+}
+
+// Enqueue one Krylov step c (1..m) on stream st.
 static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st, int64_t* launches) {
   const int nw = col < k ? col : k;
   int nparts = c->grid_spmv;
+  double* x = c->V + (int64_t)(col - 1) * c->ld;
   if (c->stencil) {
+    int rc = comm_halo(c, x, st);   // C1: neighbour rows of w_hat_{col-1}
+    if (rc != FAB_OK) return rc;
     StencilP sp = stencil_params(c);
     const bool d3 = c->op.dims[2] > 1;
     const int G = c->grid_spmv;
+    const int64_t gb = c->row_begin;
     if (stencil_vec_path(c)) {
 #define FAB_K1V(DIM, NWM) \
-  k_stencil_dots_v<DIM, NWM><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, c->vec, c->part_dots, c->st_d)
+  k_stencil_dots_v<DIM, NWM><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, c->vec, c->part_dots, c->st_d)
       if (c->k_max <= 2) {
         if (d3) FAB_K1V(3, 2); else FAB_K1V(2, 2);
       } else if (c->k_max <= 4) {
@@ -786,32 +833,36 @@ static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st,
       }
 #undef FAB_K1V
     } else if (d3) {
-      k_stencil_dots<3><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, c->vec, c->part_dots, c->st_d);
+      k_stencil_dots<3><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, c->vec, c->part_dots, c->st_d);
     } else {
-      k_stencil_dots<2><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, c->vec, c->part_dots, c->st_d);
+      k_stencil_dots<2><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, c->vec, c->part_dots, c->st_d);
     }
     FAB_CHECK_LAUNCH();
     ++*launches;
   } else {
+    const double* xg = x;
+    if (c->comm) {
+      int rc = comm_gather_x(c, x, st);   // C1: x by global column id
+      if (rc != FAB_OK) return rc;
+      xg = c->xg;
+    }
     k_csr_dots<8><<<c->grid_spmv, kThreads, 0, st>>>(c->op.row_ptr, c->op.col_idx, c->op.values,
-                                                      c->op.value_scale, c->V, c->ld, col, nw, c->n,
+                                                      c->op.value_scale, c->V, c->ld, col, nw, c->n, xg,
                                                       c->vec, c->part_dots, c->st_d);
     FAB_CHECK_LAUNCH();
     ++*launches;
     LongRows* L = long_rows(c);
     if (L && L->count) {
       k_csr_long<<<(unsigned)L->count, kThreads, 0, st>>>(
-          c->op.row_ptr, c->op.col_idx, c->op.values, c->op.value_scale, L->d, c->V, c->ld, col, nw,
+          c->op.row_ptr, c->op.col_idx, c->op.values, c->op.value_scale, L->d, c->V, c->ld, col, nw, xg,
           c->vec, c->part_dots + (int64_t)c->grid_spmv * (kKMax + 1), c->st_d);
       FAB_CHECK_LAUNCH();
       ++*launches;
       nparts += (int)L->count;
     }
   }
-  k_scalar<<<1, kThreads, 0, st>>>(col, nw, nparts, c->grid_upd, c->part_dots, c->part_norm, c->beta,
-                                   c->H, c->ldH, c->coef, 0, c->st_d);
-  FAB_CHECK_LAUNCH();
-  ++*launches;
+  int rc = enqueue_scalar(c, col, nw, nparts, 0, st, launches);
+  if (rc != FAB_OK) return rc;
   {
     PipeArgs a{};
     a.V = c->V;
@@ -829,7 +880,7 @@ static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st,
     a.s = c->s;
     a.part_sk = c->part_sk;
     a.st = c->st_d;
-    const int rc = fused ? launch_stream<true, true>(c, a, 1 + nw, st) : launch_stream<true, false>(c, a, 1 + nw, st);
+    rc = fused ? launch_stream<true, true>(c, a, 1 + nw, st) : launch_stream<true, false>(c, a, 1 + nw, st);
     if (rc != FAB_OK) return rc;
   }
   ++*launches;
@@ -877,10 +928,8 @@ int run_basis(fab_ctx* c, int m, int k) {
     for (int col = 1; col <= m && rc == FAB_OK; ++col) rc = enqueue_step(c, col, k, fused, c->cap, &launches);
     if (rc == FAB_OK) {
       // final lagged norm: beta_m = h_{m+1,m}; breakdown test of the last step
-      k_scalar<<<1, kThreads, 0, c->cap>>>(m + 1, 0, 0, c->grid_upd, c->part_dots, c->part_norm,
-                                           c->beta, c->H, c->ldH, c->coef, 1, c->st_d);
-      ++launches;
-      if (fused) {
+      rc = enqueue_scalar(c, m + 1, 0, 0, 1, c->cap, &launches);
+      if (rc == FAB_OK && fused) {
         rc = sketch_finalize(c, m + 1, c->cap);
         ++launches;
       }

@@ -376,12 +376,6 @@ static int read_stats(fab_ctx* c, const double* X, int m, double* h, cudaStream_
   return FAB_OK;
 }
 
-#define FAB_TRY(x)          \
-  do {                      \
-    int rc__ = (x);         \
-    if (rc__ != FAB_OK) return rc__; \
-  } while (0)
-
 // 1-norms of up to 4 matrices (one CTA each, fixed order)
 struct Mats4 {
   const double* p[4];

@@ -43,6 +43,8 @@ struct DevState {
   double scratch[8];
 };
 
+struct Comm;   // comm.cu: NCCL communicator of the row-partitioned path
+
 }  // namespace fab
 
 // The opaque context of the ABI.
@@ -60,6 +62,9 @@ struct fab_ctx {
   int64_t n_global = 0;
   int64_t row_begin = 0;
   int64_t ld = 0;         // column stride of V (doubles)
+  int64_t hal = 0;        // stencil halo rows per side (multi-GPU row blocks; 0 on one GPU)
+  int64_t hpad = 0;       // hal rounded up to 32: column j's local row 0 is at V + j*ld,
+                          // its halo slots at V + j*ld - hal .. and V + j*ld + n ..
   int64_t N = 0;          // SRHT length, next pow2 of n_global
   double norm_inf = 0.0;
 
@@ -87,6 +92,8 @@ struct fab_ctx {
   double* part_tn = nullptr;     // grid_lsqr
   double* small = nullptr;       // small vectors (LSQR, dense)
   double* dense = nullptr;       // dense pool: kDenseMats * m_max^2
+  double* red = nullptr;         // kSmall: this rank's step / pass scalars (allreduced in place)
+  double* xg = nullptr;          // CSR on several GPUs: w_hat_{i-1} gathered to global length
   fab::DevState* st_d = nullptr;
   fab::DevState* st_h = nullptr; // pinned mirror
 
@@ -108,6 +115,9 @@ struct fab_ctx {
   int g_m = -1, g_k = -1, g_s = -1;
   bool g_fused = false;
   int64_t g_launches = 0;
+
+  fab::Comm* comm = nullptr;          // NULL: one GPU
+  std::vector<int64_t> rank_rows;     // row_begin of every rank, plus n_global
 
   fab_info info{};
   unsigned flags = 0;
@@ -187,7 +197,21 @@ inline int64_t next_pow2(int64_t n) {
   return p;
 }
 
+#define FAB_TRY(x)          \
+  do {                      \
+    int rc__ = (x);         \
+    if (rc__ != FAB_OK) return rc__; \
+  } while (0)
+
 // ---- sub-module entry points (host side) ---------------------------------
+// comm.cu (every call is a no-op when c->comm == NULL)
+int comm_rank(const fab_ctx* c);
+int comm_size(const fab_ctx* c);
+int comm_allreduce(fab_ctx* c, double* buf, size_t count, bool use_max, cudaStream_t st);
+int comm_halo(fab_ctx* c, double* x, cudaStream_t st);
+int comm_gather_x(fab_ctx* c, const double* x, cudaStream_t st);
+int comm_setup_partition(fab_ctx* c);
+const char* nccl_last_error();
 // basis.cu
 int basis_setup_grids(fab_ctx* c);
 int init_vector_norm(fab_ctx* c);            // partial norms of column 0, norm_inf

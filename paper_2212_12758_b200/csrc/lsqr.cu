@@ -331,9 +331,17 @@ struct LsqrVecs {
   double *g, *q, *v, *w, *x, *p, *tmp;
 };
 
-// fixed-order reduction of the pass partials -> g (m), returns ||t||^2
+// fixed-order reduction of the pass partials -> g (m), returns ||t||^2.
+// nparts < 0: part_g already holds the (allreduced) g[0..m-1], ||t||^2 = part_g[m].
 __device__ double reduce_pass(const double* part_g, const double* part_tn, int nparts, int m, double* g,
                               double* red) {
+  if (nparts < 0) {
+    for (int j = threadIdx.x; j < m; j += blockDim.x) g[j] = part_g[j];
+    __shared__ double tn0;
+    if (threadIdx.x == 0) tn0 = part_g[m];
+    __syncthreads();
+    return tn0;
+  }
   for (int j = threadIdx.x; j < m; j += blockDim.x) {
     double a = 0.0;
     for (int b = 0; b < nparts; ++b) a += part_g[(int64_t)b * m + j];
@@ -347,6 +355,16 @@ __device__ double reduce_pass(const double* part_g, const double* part_tn, int n
   }
   __syncthreads();
   return tn;
+}
+
+// Multi-GPU: this rank's pass scalars (g = W^T t over its rows, ||t||^2) in
+// the fixed order of reduce_pass, into out[0..m] for the allreduce (C4).
+__global__ void k_pass_reduce(const double* part_g, const double* part_tn, int nparts, int m, double* out,
+                              const DevState* st) {
+  if (st->lsqr_done) return;
+  __shared__ double red[kWarps];
+  const double tn = reduce_pass(part_g, part_tn, nparts, m, out, red);
+  if (threadIdx.x == 0) out[m] = tn;
 }
 
 // LSQR initialisation after the pass t = w_hat_m, g = W^T t:
@@ -598,8 +616,22 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
       FAB_CHECK_LAUNCH();
       if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[1], st));
       ++npass;
-      k_lsqr_init<<<1, kThreads, 0, st>>>(c->part_g, c->part_tn, G, m, Rinv, RinvT, c->beta, L, tol,
-                                          c->st_d);
+      // C4 on several GPUs: reduce this rank's partials, allreduce m+1 scalars
+      auto pass_scalars = [&](const double** pg, int* np) -> int {
+        *pg = c->part_g;
+        *np = G;
+        if (!c->comm) return FAB_OK;
+        k_pass_reduce<<<1, kThreads, 0, st>>>(c->part_g, c->part_tn, G, m, c->red, c->st_d);
+        FAB_CHECK_LAUNCH();
+        ++launches;
+        *pg = c->red;
+        *np = -1;
+        return comm_allreduce(c, c->red, (size_t)m + 1, false, st);
+      };
+      const double* pg = nullptr;
+      int np = 0;
+      FAB_TRY(pass_scalars(&pg, &np));
+      k_lsqr_init<<<1, kThreads, 0, st>>>(pg, c->part_tn, np, m, Rinv, RinvT, c->beta, L, tol, c->st_d);
       FAB_CHECK_LAUNCH();
       launches += 2;
       int done_iters = 0;
@@ -612,8 +644,9 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
           FAB_CHECK_LAUNCH();
           if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[1], st));
           ++npass;
-          k_lsqr_step<<<1, kThreads, 0, st>>>(c->part_g, c->part_tn, G, m, Rinv, RinvT, c->beta, L,
-                                              fixed ? 0 : 1, c->st_d);
+          FAB_TRY(pass_scalars(&pg, &np));
+          k_lsqr_step<<<1, kThreads, 0, st>>>(pg, c->part_tn, np, m, Rinv, RinvT, c->beta, L, fixed ? 0 : 1,
+                                              c->st_d);
           FAB_CHECK_LAUNCH();
           launches += 2;
         }

@@ -109,7 +109,9 @@ int sketch_finalize(fab_ctx* c, int ncols, cudaStream_t st) {
   k_sketch_finalize<<<grid, kThreads, 0, st>>>(c->part_sk, c->grid_upd, c->s, ncols, c->beta, c->SV,
                                                c->st_d);
   FAB_CHECK_LAUNCH();
-  return FAB_OK;
+  // C3: every rank sketched its own rows on globally aligned tiles (R-1);
+  // the sum over ranks is Theta V (nothing else crosses GPUs for the SRHT)
+  return comm_allreduce(c, c->SV, (size_t)c->s * ncols, false, st);
 }
 
 // K5: the sketch drawn after the basis -- one batched streaming pass over
