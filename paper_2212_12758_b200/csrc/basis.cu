@@ -19,10 +19,54 @@
 
 namespace fab {
 
+// n / d for 0 <= n < 2^31 by multiply-shift (Granlund-Montgomery round-up
+// method with a 33-bit magic; exact on that range, checked exhaustively at
+// the boundaries): the grid coordinates of a row without integer division.
+struct FastDiv {
+  uint64_t M = 1;
+  int sh = 0;
+  __host__ void init(uint32_t d) {
+    int l = 0;
+    while ((1ull << l) < d) ++l;   // ceil(log2 d)
+    M = ((1ull << (32 + l)) / d) + 1;
+    sh = 32 + l;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (uint32_t)(((uint64_t)n * M) >> sh); }
+};
+
 struct StencilP {
   int gx, gy, gz;
   double c0, cxm, cxp, cym, cyp, czm, czp;
+  FastDiv dx, dy;   // division by gx, gy
 };
+
+__device__ __forceinline__ void grid_coords(const StencilP& sp, uint32_t g, uint32_t& ix, uint32_t& iy,
+                                            uint32_t& iz) {
+  const uint32_t q = sp.dx.div(g);
+  ix = g - q * (uint32_t)sp.gx;
+  iz = sp.dy.div(q);
+  iy = q - iz * (uint32_t)sp.gy;
+}
+
+// (A x)_r of the constant-coefficient stencil at grid point (ix, iy, iz),
+// Dirichlet: neighbours outside the grid are skipped.  ONE definition of the
+// term order (centre, x-, x+, y-, y+, z-, z+; fma) for every kernel, so z
+// recomputed in K3 is bitwise the z of K1's dots.
+template <int DIM>
+__device__ __forceinline__ double stencil_row(const StencilP& sp, uint32_t ix, uint32_t iy, uint32_t iz,
+                                              double xc, double xm, double xp, double ym, double yp,
+                                              double zm, double zp) {
+  double acc = sp.c0 * xc;
+  if (ix > 0) acc = fma(sp.cxm, xm, acc);
+  if (ix + 1 < (uint32_t)sp.gx) acc = fma(sp.cxp, xp, acc);
+  if (iy > 0) acc = fma(sp.cym, ym, acc);
+  if (iy + 1 < (uint32_t)sp.gy) acc = fma(sp.cyp, yp, acc);
+  if (DIM == 3) {
+    if (iz > 0) acc = fma(sp.czm, zm, acc);
+    if (iz + 1 < (uint32_t)sp.gz) acc = fma(sp.czp, zp, acc);
+  }
+  return acc;
+}
 
 // ---------------------------------------------------------------------------
 // K1 (stencil): z = A x and the window dots in one pass, fixed-order CTA
@@ -32,7 +76,9 @@ struct StencilP {
 // neighbours, scalar x neighbours, double2 window columns) before any
 // arithmetic, so ~64 KB per SM are in flight at 2 CTAs/SM.  The y and x
 // neighbours of a contiguous block are L1/L2 hits; z neighbours (+-1 plane)
-// are L2 hits.  HBM bytes per row: x (8) + (nw-1) window columns + z (8).
+// are L2 hits.  STORE_Z: write z for K3 (HBM bytes per row x + (nw-1)
+// window columns + z); !STORE_Z (matrix-free): K3 recomputes z, so z never
+// reaches HBM.
 // ---------------------------------------------------------------------------
 constexpr int kK1U = 2;                       // row pairs per thread per block
 constexpr int kK1Block = kThreads * 2 * kK1U; // rows per CTA per block
@@ -41,7 +87,7 @@ __device__ __forceinline__ double2 ld2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
 
-template <int DIM, int NWM, int U = (NWM <= 4 ? kK1U : 1)>
+template <int DIM, int NWM, bool STORE_Z, int U = (NWM <= 4 ? kK1U : 1)>
 __global__ void __launch_bounds__(kThreads, 2)
 k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP sp, int64_t n, int64_t gbase,
                  double* __restrict__ z, double* __restrict__ part, const DevState* __restrict__ st) {
@@ -52,13 +98,13 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
   double d[NWM];
 #pragma unroll
   for (int t = 0; t < NWM; ++t) d[t] = 0.0;
-  const unsigned gx = (unsigned)sp.gx, gy = (unsigned)sp.gy, gz = (unsigned)sp.gz;
-  const int64_t plane = (int64_t)gx * gy;
+  const int64_t gx = sp.gx, plane = (int64_t)sp.gx * sp.gy;
   const double2 zero2 = make_double2(0.0, 0.0);
-  for (int64_t base = (int64_t)blockIdx.x * (kThreads * 2 * U); base < n; base += (int64_t)gridDim.x * (kThreads * 2 * U)) {
+  for (int64_t base = (int64_t)blockIdx.x * (kThreads * 2 * U); base < n;
+       base += (int64_t)gridDim.x * (kThreads * 2 * U)) {
     double2 xc[U], ym[U], yp[U], zm[U], zp[U], w[U][NWM > 1 ? NWM - 1 : 1];
     double xl[U], xr[U];
-    unsigned ixs[U];
+    uint32_t ixs[U], iys[U], izs[U];
     bool ok[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -66,24 +112,24 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
       ok[u] = r < n;                       // n even on this path: r+1 < n too
       xc[u] = ym[u] = yp[u] = zm[u] = zp[u] = zero2;
       xl[u] = xr[u] = 0.0;
-      ixs[u] = 0;
+      ixs[u] = iys[u] = izs[u] = 0;
 #pragma unroll
       for (int t = 0; t < NWM - 1; ++t) w[u][t] = zero2;
       if (ok[u]) {
-        const unsigned ur = (unsigned)(r + gbase);   // global grid index (row blocks: halo slots hold x[r -+ offsets])
-        const unsigned ix = ur % gx;
-        const unsigned rest = ur / gx;
-        const unsigned iy = rest % gy;
-        const unsigned iz = rest / gy;
+        // global grid coordinates (row blocks: the halo slots hold x[r -+ offsets])
+        uint32_t ix, iy, iz;
+        grid_coords(sp, (uint32_t)(r + gbase), ix, iy, iz);
         ixs[u] = ix;
+        iys[u] = iy;
+        izs[u] = iz;
         xc[u] = ld2(x + r);
         if (ix > 0) xl[u] = __ldg(x + r - 1);
-        if (ix + 2 < gx) xr[u] = __ldg(x + r + 2);
+        if (ix + 2 < (uint32_t)sp.gx) xr[u] = __ldg(x + r + 2);
         if (iy > 0) ym[u] = ld2(x + r - gx);
-        if (iy + 1 < gy) yp[u] = ld2(x + r + gx);
+        if (iy + 1 < (uint32_t)sp.gy) yp[u] = ld2(x + r + gx);
         if (DIM == 3) {
           if (iz > 0) zm[u] = ld2(x + r - plane);
-          if (iz + 1 < gz) zp[u] = ld2(x + r + plane);
+          if (iz + 1 < (uint32_t)sp.gz) zp[u] = ld2(x + r + plane);
         }
 #pragma unroll
         for (int t = 0; t < NWM - 1; ++t)
@@ -94,24 +140,11 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
     for (int u = 0; u < U; ++u) {
       if (!ok[u]) continue;
       const int64_t r = base + 2 * threadIdx.x + 2 * kThreads * u;
-      // same term order as the scalar kernel: centre, x-, x+, y-, y+, z-, z+
-      double a0 = sp.c0 * xc[u].x, a1 = sp.c0 * xc[u].y;
-      if (ixs[u] > 0) a0 = fma(sp.cxm, xl[u], a0);
-      a1 = fma(sp.cxm, xc[u].x, a1);
-      a0 = fma(sp.cxp, xc[u].y, a0);
-      if (ixs[u] + 2 < gx) a1 = fma(sp.cxp, xr[u], a1);
-      // the y/z neighbour pairs were left at 0 outside the grid; skip them
-      // explicitly so boundary rows sum exactly the in-grid terms
-      const unsigned ur = (unsigned)(r + gbase);
-      const unsigned rest = ur / gx;
-      const unsigned iy = rest % gy, iz = rest / gy;
-      if (iy > 0) { a0 = fma(sp.cym, ym[u].x, a0); a1 = fma(sp.cym, ym[u].y, a1); }
-      if (iy + 1 < gy) { a0 = fma(sp.cyp, yp[u].x, a0); a1 = fma(sp.cyp, yp[u].y, a1); }
-      if (DIM == 3) {
-        if (iz > 0) { a0 = fma(sp.czm, zm[u].x, a0); a1 = fma(sp.czm, zm[u].y, a1); }
-        if (iz + 1 < gz) { a0 = fma(sp.czp, zp[u].x, a0); a1 = fma(sp.czp, zp[u].y, a1); }
-      }
-      *reinterpret_cast<double2*>(z + r) = make_double2(a0, a1);
+      const double a0 = stencil_row<DIM>(sp, ixs[u], iys[u], izs[u], xc[u].x, xl[u], xc[u].y, ym[u].x, yp[u].x,
+                                         zm[u].x, zp[u].x);
+      const double a1 = stencil_row<DIM>(sp, ixs[u] + 1, iys[u], izs[u], xc[u].y, xc[u].x, xr[u], ym[u].y,
+                                         yp[u].y, zm[u].y, zp[u].y);
+      if (STORE_Z) *reinterpret_cast<double2*>(z + r) = make_double2(a0, a1);
 #pragma unroll
       for (int t = 0; t < NWM - 1; ++t) {
         if (t < nw - 1) {
@@ -147,21 +180,14 @@ k_stencil_dots(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t plane = (int64_t)sp.gx * sp.gy;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
-    const unsigned ur = (unsigned)(r + gbase);
-    const unsigned ix = ur % (unsigned)sp.gx;
-    const unsigned rest = ur / (unsigned)sp.gx;
-    const unsigned iy = rest % (unsigned)sp.gy;
-    const unsigned iz = rest / (unsigned)sp.gy;
+    uint32_t ix, iy, iz;
+    grid_coords(sp, (uint32_t)(r + gbase), ix, iy, iz);
     const double xc = __ldg(x + r);
-    double acc = sp.c0 * xc;
-    if (ix > 0) acc = fma(sp.cxm, __ldg(x + r - 1), acc);
-    if (ix + 1 < (unsigned)sp.gx) acc = fma(sp.cxp, __ldg(x + r + 1), acc);
-    if (iy > 0) acc = fma(sp.cym, __ldg(x + r - sp.gx), acc);
-    if (iy + 1 < (unsigned)sp.gy) acc = fma(sp.cyp, __ldg(x + r + sp.gx), acc);
-    if (DIM == 3) {
-      if (iz > 0) acc = fma(sp.czm, __ldg(x + r - plane), acc);
-      if (iz + 1 < (unsigned)sp.gz) acc = fma(sp.czp, __ldg(x + r + plane), acc);
-    }
+    const double acc = stencil_row<DIM>(
+        sp, ix, iy, iz, xc, ix > 0 ? __ldg(x + r - 1) : 0.0, ix + 1 < (uint32_t)sp.gx ? __ldg(x + r + 1) : 0.0,
+        iy > 0 ? __ldg(x + r - sp.gx) : 0.0, iy + 1 < (uint32_t)sp.gy ? __ldg(x + r + sp.gx) : 0.0,
+        (DIM == 3 && iz > 0) ? __ldg(x + r - plane) : 0.0,
+        (DIM == 3 && iz + 1 < (uint32_t)sp.gz) ? __ldg(x + r + plane) : 0.0);
     z[r] = acc;
 #pragma unroll
     for (int t = 0; t < kKMax; ++t) {
@@ -452,7 +478,7 @@ struct PipeArgs {
   int col0, col1;       // columns produced (UPDATE: output column c) / sketched
   int nw;               // UPDATE: window size
   const double* coef;   // UPDATE: coefficients of step c
-  const double* z;      // UPDATE: z = A w_hat_{c-1}
+  const double* z;      // UPDATE (SDIM == 0): z = A w_hat_{c-1} from K1
   int64_t n, row_begin;
   double* part_norm;    // UPDATE: per-CTA ||w_hat_c||^2
   const uint32_t* signs;
@@ -461,18 +487,99 @@ struct PipeArgs {
   double* part_sk;      // per (col, CTA) sketch partials: [(col*grid + cta)*s + p]
   const DevState* st;
   int nstage;
+  // SDIM > 0 (matrix-free stencil): z is recomputed from w_hat_{c-1}
+  StencilP sp;
+  int64_t hal;          // halo rows held in each column's padding (0 on one GPU)
 };
 
-template <bool UPDATE, bool SKETCH>
+// Ring-stage slots (doubles) of one 512-row chunk [r0, r0+512):
+//   SDIM == 0, UPDATE : z | window columns j0 .. c-1                (512 each)
+//   SDIM  > 0, UPDATE : w_hat_{c-1} rows [r0-16, r0+528) (544) | window
+//                       columns j0 .. c-2 | w_hat_{c-1} at r0 -+ gx (and
+//                       r0 -+ gx*gy in 3D): the stencil neighbours, L2 hits
+//   !UPDATE           : column col
+//   + (SKETCH) the chunk's 512 sign bits (64 B, padded to 128 B)
+constexpr int kXExt = 544;   // rows [r0-16, r0+528): 128-B aligned copy with a 16-row apron
+struct SlotGeom {
+  int nslot;      // data slots
+  int stage_d;    // doubles per stage
+};
+
+template <bool UPDATE, bool SKETCH, int SDIM>
+__host__ __device__ __forceinline__ SlotGeom slot_geom(int nw) {
+  SlotGeom g;
+  if (!UPDATE) {
+    g.nslot = 1;
+    g.stage_d = kChunk;
+  } else if (SDIM == 0) {
+    g.nslot = 1 + nw;
+    g.stage_d = (1 + nw) * kChunk;
+  } else {
+    const int nnb = SDIM == 3 ? 4 : 2;
+    g.nslot = 1 + (nw - 1) + nnb;
+    g.stage_d = kXExt + (nw - 1 + nnb) * kChunk;
+  }
+  g.stage_d += SKETCH ? kSignPad : 0;
+  return g;
+}
+
+// Source, destination offset and clamped row range of slot v.
+template <bool UPDATE, int SDIM>
+__device__ __forceinline__ void slot_copy(const PipeArgs& a, int v, int col, int64_t r0, const double** src,
+                                          int* dst_off, int64_t* lo, int64_t* hi) {
+  const int j0 = a.col0 - a.nw;
+  int64_t base = r0, len = kChunk, clo = 0, chi = a.n;
+  int off = v * kChunk;
+  if (!UPDATE) {
+    *src = a.V + (int64_t)col * a.ld;
+  } else if (SDIM == 0) {
+    *src = v == 0 ? a.z : a.V + (int64_t)(j0 + v - 1) * a.ld;
+  } else {
+    const double* x = a.V + (int64_t)(a.col0 - 1) * a.ld;
+    const int64_t hale = (a.hal + 15) & ~(int64_t)15;   // <= the column's padding
+    if (v == 0) {                               // w_hat_{c-1} with an apron either side
+      *src = x;
+      base = r0 - 16;
+      len = kXExt;
+      off = 0;
+      clo = -hale;
+      chi = a.n + a.hal;
+    } else if (v < a.nw) {                      // window column j0 + v - 1
+      *src = a.V + (int64_t)(j0 + v - 1) * a.ld;
+      off = kXExt + (v - 1) * kChunk;
+    } else {                                    // neighbour chunk q of w_hat_{c-1}
+      const int q = v - a.nw;
+      const int64_t gx = a.sp.gx, pl = (int64_t)a.sp.gx * a.sp.gy;
+      const int64_t shift = q == 0 ? -gx : q == 1 ? gx : q == 2 ? -pl : pl;
+      *src = x;
+      base = r0 + shift;
+      off = kXExt + (a.nw - 1 + q) * kChunk;
+      clo = -hale;
+      chi = a.n + a.hal;
+    }
+  }
+  int64_t l = base > clo ? base : clo;
+  int64_t h = base + len < chi ? base + len : chi;
+  if (h > l) {
+    // round the end up to 128 B (inside the column's padding / ld), but never
+    // past the slot; both bounds are even, so the size stays a 16-B multiple
+    h = (h + 15) & ~(int64_t)15;
+    if (h > base + len) h = base + len;
+  }
+  *lo = l;
+  *hi = h;
+  *dst_off = off + (int)(l - base);
+}
+
+template <bool UPDATE, bool SKETCH, int SDIM>
 __global__ void __launch_bounds__(kPipeThreads, 1) k_stream_tiles(PipeArgs a) {
   if (a.st->breakdown) return;
   extern __shared__ __align__(128) double dsm[];
   __shared__ double red[kWarps];
-  const int nvec = UPDATE ? 1 + a.nw : 1;
+  const SlotGeom geo = slot_geom<UPDATE, SKETCH, SDIM>(a.nw);
   const int nstage = a.nstage;
-  // stage: nvec x 512 rows of fp64, then (SKETCH) the 512 sign bits of the
-  // chunk (64 B, padded to 128 B)
-  const int stage_d = nvec * kChunk + (SKETCH ? kSignPad : 0);
+  const int stage_d = geo.stage_d;
+  const int sign_off = stage_d - (SKETCH ? kSignPad : 0);
   double* ring = dsm;
   double* fw = ring + (size_t)nstage * stage_d;
   uint64_t* full = reinterpret_cast<uint64_t*>(fw + (SKETCH ? kSkSmem : 0));
@@ -489,37 +596,44 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_stream_tiles(PipeArgs a) {
   const int64_t n = a.n, rb = a.row_begin;
   const int64_t t_first = rb >> kSkLogT;
   const int64_t t_last = (rb + n - 1) >> kSkLogT;
-  const int j0 = UPDATE ? a.col0 - a.nw : 0;
 
   if (warp == kWarps) {
     // ---------------- producer warp ----------------
     const uint64_t pol = policy_evict_first();
+    // w_hat_{c-1} (slot 0 and the neighbour slots) is re-read by the CTAs of
+    // the neighbouring tiles within microseconds: keep it in L2
+    const uint64_t pol_x = policy_evict_last();
     RingPos rp;
     for (int col = a.col0; col < a.col1; ++col) {
       for (int64_t tile = t_first + blockIdx.x; tile <= t_last; tile += gridDim.x) {
         for (int ch = 0; ch < kChunksPerTile; ++ch) {
           const int64_t r0 = (tile << kSkLogT) + ch * kChunk - rb;
-          const int64_t lo = r0 > 0 ? r0 : 0;
-          int64_t hi = r0 + kChunk < n ? r0 + kChunk : n;
+          const bool any = (r0 + kChunk > 0) && (r0 < n);   // the chunk holds local rows
           mbar_wait(empty + rp.stage, rp.phase ^ 1u);
-          if (hi > lo) {
-            hi = (hi + 1) & ~(int64_t)1;   // 16-B multiple; stays inside ld (ld % 32 == 0)
-            const uint32_t bytes = (uint32_t)((hi - lo) * 8);
-            if (lane == 0) mbar_arrive_expect_tx(full + rp.stage, bytes * nvec + (SKETCH ? 64u : 0u));
-            __syncwarp();
+          if (any) {
             double* sb = ring + (size_t)rp.stage * stage_d;
-            if (lane < nvec) {
-              const double* src;
-              if (UPDATE)
-                src = lane == 0 ? a.z : a.V + (int64_t)(j0 + lane - 1) * a.ld;
-              else
-                src = a.V + (int64_t)col * a.ld;
-              bulk_g2s(sb + (size_t)lane * kChunk + (lo - r0), src + lo, bytes, full + rp.stage, pol);
-            } else if (SKETCH && lane == nvec) {
+            const double* src = nullptr;
+            int doff = 0;
+            int64_t lo = 0, hi = 0;
+            if (lane == 0) {
+              uint32_t total = SKETCH ? 64u : 0u;
+              for (int v = 0; v < geo.nslot; ++v) {
+                slot_copy<UPDATE, SDIM>(a, v, col, r0, &src, &doff, &lo, &hi);
+                if (hi > lo) total += (uint32_t)((hi - lo) * 8);
+              }
+              mbar_arrive_expect_tx(full + rp.stage, total);
+            }
+            __syncwarp();
+            if (lane < geo.nslot) {
+              slot_copy<UPDATE, SDIM>(a, lane, col, r0, &src, &doff, &lo, &hi);
+              const bool xslot = UPDATE && SDIM > 0 && (lane == 0 || lane >= a.nw);
+              if (hi > lo)
+                bulk_g2s(sb + doff, src + lo, (uint32_t)((hi - lo) * 8), full + rp.stage, xslot ? pol_x : pol);
+            } else if (SKETCH && lane == geo.nslot) {
               // sign words of global rows [g, g+512): g is 512-aligned, the
               // bitmap is padded to 256 B, so the 64 B are always in bounds
               const int64_t gw = ((tile << kSkLogT) + ch * kChunk) >> 5;
-              bulk_g2s(sb + (size_t)nvec * kChunk, a.signs + gw, 64u, full + rp.stage, pol);
+              bulk_g2s(sb + sign_off, a.signs + gw, 64u, full + rp.stage, pol);
             }
           } else if (lane == 0) {
             mbar_arrive(full + rp.stage);
@@ -556,7 +670,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_stream_tiles(PipeArgs a) {
       for (int ch = 0; ch < kChunksPerTile; ++ch) {
         mbar_wait(full + rp.stage, rp.phase);
         const double* sb = ring + (size_t)rp.stage * stage_d;
-        const uint32_t* sgn = reinterpret_cast<const uint32_t*>(sb + nvec * kChunk);
+        const uint32_t* sgn = reinterpret_cast<const uint32_t*>(sb + sign_off);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int i = tid + kThreads * h;
@@ -564,15 +678,34 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_stream_tiles(PipeArgs a) {
           const int64_t r = g - rb;
           double val = 0.0;
           if (r >= 0 && r < n) {
-            if (UPDATE) {
+            if (UPDATE && SDIM == 0) {
               val = cz * sb[i];
 #pragma unroll
               for (int t = 0; t < kKMax; ++t)
                 if (t < a.nw) val = fma(cw[t], sb[(1 + t) * kChunk + i], val);
-              out[r] = val;
-              nrm = fma(val, val, nrm);
+            } else if (UPDATE) {
+              // z_r = (A w_hat_{c-1})_r recomputed exactly as K1 did (stencil_row)
+              uint32_t ix, iy, iz;
+              grid_coords(a.sp, (uint32_t)g, ix, iy, iz);
+              const double* xs = sb + 16;                         // row i at xs[i]
+              const double* nb = sb + kXExt + (a.nw - 1) * kChunk;  // y-, y+, z-, z+
+              const double xc = xs[i];
+              const double zr = stencil_row<SDIM>(a.sp, ix, iy, iz, xc, xs[i - 1], xs[i + 1], nb[i],
+                                                  nb[kChunk + i], SDIM == 3 ? nb[2 * kChunk + i] : 0.0,
+                                                  SDIM == 3 ? nb[3 * kChunk + i] : 0.0);
+              val = cz * zr;
+#pragma unroll
+              for (int t = 0; t < kKMax - 1; ++t)
+                if (t < a.nw - 1) val = fma(cw[t], sb[kXExt + t * kChunk + i], val);
+#pragma unroll
+              for (int t = 0; t < kKMax; ++t)                     // j = c-1 is the last window term
+                if (t == a.nw - 1) val = fma(cw[t], xc, val);
             } else {
               val = sb[i];
+            }
+            if (UPDATE) {
+              out[r] = val;
+              nrm = fma(val, val, nrm);
             }
             if (SKETCH && ((sgn[i >> 5] >> (i & 31)) & 1u)) val = -val;
           }
@@ -608,8 +741,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_stream_tiles(PipeArgs a) {
   }
 }
 
-static int pipe_stages(int nvec, bool sketch, size_t* smem) {
-  const size_t stage = ((size_t)nvec * kChunk + (sketch ? kSignPad : 0)) * sizeof(double);
+static int pipe_stages(int stage_d, bool sketch, size_t* smem) {
+  const size_t stage = (size_t)stage_d * sizeof(double);
   const size_t fixed = (sketch ? kSkSmem * sizeof(double) : 0) + 1024;
   int ns = (int)((kSmemLimit - fixed) / (stage + 16));
   if (ns > kMaxStages) ns = kMaxStages;
@@ -618,14 +751,15 @@ static int pipe_stages(int nvec, bool sketch, size_t* smem) {
   return ns;
 }
 
-template <bool UPDATE, bool SKETCH>
-static int launch_stream(fab_ctx* c, PipeArgs a, int nvec, cudaStream_t st) {
+template <bool UPDATE, bool SKETCH, int SDIM>
+static int launch_stream(fab_ctx* c, PipeArgs a, cudaStream_t st) {
   size_t smem = 0;
-  a.nstage = pipe_stages(nvec, SKETCH, &smem);
-  k_stream_tiles<UPDATE, SKETCH><<<c->grid_upd, kPipeThreads, smem, st>>>(a);
+  a.nstage = pipe_stages(slot_geom<UPDATE, SKETCH, SDIM>(a.nw).stage_d, SKETCH, &smem);
+  k_stream_tiles<UPDATE, SKETCH, SDIM><<<c->grid_upd, kPipeThreads, smem, st>>>(a);
   FAB_CHECK_LAUNCH();
   return FAB_OK;
 }
+
 
 // partial ||x||^2 with the same grid as k_update (column 0 = b)
 __global__ void __launch_bounds__(kThreads)
@@ -690,6 +824,8 @@ static StencilP stencil_params(const fab_ctx* c) {
   p.cyp = c->op.coeffs[4];
   p.czm = c->op.coeffs[5];
   p.czp = c->op.coeffs[6];
+  p.dx.init((uint32_t)p.gx);
+  p.dy.init((uint32_t)p.gy);
   return p;
 }
 
@@ -727,9 +863,21 @@ bool stencil_vec_path(const fab_ctx* c) {
 
 int basis_setup_grids(fab_ctx* c) {
   // the ring is sized per launch (pipe_stages); allow the full 227 KB once
-  FAB_CUDA(set_max_dyn_smem((const void*)k_stream_tiles<true, true>, kSmemLimit));
-  FAB_CUDA(set_max_dyn_smem((const void*)k_stream_tiles<true, false>, kSmemLimit));
-  FAB_CUDA(set_max_dyn_smem((const void*)k_stream_tiles<false, true>, kSmemLimit));
+  FAB_CUDA(set_max_dyn_smem((const void*)k_stream_tiles<true, true, 0>, kSmemLimit));
+  FAB_CUDA(set_max_dyn_smem((const void*)k_stream_tiles<true, false, 0>, kSmemLimit));
+  FAB_CUDA(set_max_dyn_smem((const void*)k_stream_tiles<false, true, 0>, kSmemLimit));
+  FAB_CUDA(set_max_dyn_smem((const void*)k_stream_tiles<true, true, 2>, kSmemLimit));
+  FAB_CUDA(set_max_dyn_smem((const void*)k_stream_tiles<true, false, 2>, kSmemLimit));
+  FAB_CUDA(set_max_dyn_smem((const void*)k_stream_tiles<true, true, 3>, kSmemLimit));
+  FAB_CUDA(set_max_dyn_smem((const void*)k_stream_tiles<true, false, 3>, kSmemLimit));
+  // matrix-free stencil (FAB_MATRIX_FREE=1): z = A w_hat_{c-1} is recomputed
+  // in K3 from w_hat_{c-1} and its neighbour chunks instead of round-tripping
+  // through HBM (72 instead of 88 B/row at k = 4).  Correct and tested, but
+  // not the default: with the tile order of the persistent grid the +-plane
+  // neighbour chunks are first-touch misses that stall the ring (K3 347 us vs
+  // 120 us, profiles/r01_v2); needs a z-marching tile order.
+  const char* mfe = getenv("FAB_MATRIX_FREE");
+  c->mf = stencil_vec_path(c) && (mfe && mfe[0] == '1');
   // K3/K5 pipeline: persistent, one CTA per SM (the ring takes the smem)
   const int64_t ntiles = ((c->row_begin + c->n - 1) >> kSkLogT) - (c->row_begin >> kSkLogT) + 1;
   c->grid_upd = (int)(ntiles < c->num_sms ? ntiles : c->num_sms);
@@ -822,8 +970,15 @@ static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st,
     const int G = c->grid_spmv;
     const int64_t gb = c->row_begin;
     if (stencil_vec_path(c)) {
-#define FAB_K1V(DIM, NWM) \
-  k_stencil_dots_v<DIM, NWM><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, c->vec, c->part_dots, c->st_d)
+#define FAB_K1V(DIM, NWM)                                                                                    \
+  do {                                                                                                       \
+    if (c->mf)                                                                                               \
+      k_stencil_dots_v<DIM, NWM, false><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, c->vec,  \
+                                                                c->part_dots, c->st_d);                      \
+    else                                                                                                     \
+      k_stencil_dots_v<DIM, NWM, true><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, c->vec,   \
+                                                               c->part_dots, c->st_d);                       \
+  } while (0)
       if (c->k_max <= 2) {
         if (d3) FAB_K1V(3, 2); else FAB_K1V(2, 2);
       } else if (c->k_max <= 4) {
@@ -880,7 +1035,16 @@ static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st,
     a.s = c->s;
     a.part_sk = c->part_sk;
     a.st = c->st_d;
-    rc = fused ? launch_stream<true, true>(c, a, 1 + nw, st) : launch_stream<true, false>(c, a, 1 + nw, st);
+    if (c->mf) {
+      a.sp = stencil_params(c);
+      a.hal = c->hal;
+      if (c->op.dims[2] > 1)
+        rc = fused ? launch_stream<true, true, 3>(c, a, st) : launch_stream<true, false, 3>(c, a, st);
+      else
+        rc = fused ? launch_stream<true, true, 2>(c, a, st) : launch_stream<true, false, 2>(c, a, st);
+    } else {
+      rc = fused ? launch_stream<true, true, 0>(c, a, st) : launch_stream<true, false, 0>(c, a, st);
+    }
     if (rc != FAB_OK) return rc;
   }
   ++*launches;
@@ -901,7 +1065,7 @@ int launch_sketch_cols(fab_ctx* c, int c0, int c1, cudaStream_t st) {
   a.s = c->s;
   a.part_sk = c->part_sk;
   a.st = c->st_d;
-  return launch_stream<false, true>(c, a, 1, st);
+  return launch_stream<false, true, 0>(c, a, st);
 }
 
 int run_basis(fab_ctx* c, int m, int k) {

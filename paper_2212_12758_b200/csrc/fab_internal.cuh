@@ -58,6 +58,7 @@ struct fab_ctx {
   // operator
   fab_operator op{};
   bool stencil = false;
+  bool mf = false;        // matrix-free stencil basis: z recomputed in K3, never stored
   int64_t n = 0;          // local rows
   int64_t n_global = 0;
   int64_t row_begin = 0;
