@@ -32,7 +32,7 @@ from typing import Optional
 
 import numpy as np
 
-__all__ = ["Problem", "make", "CONFIGS", "stencil_coeffs", "stencil_csr",
+__all__ = ["Problem", "make", "CONFIGS", "stencil_coeffs", "stencil_csr", "stencil_row",
            "chung_lu", "random_sparse", "gaussian_b"]
 
 # (center, x-, x+, y-, y+, z-, z+)
@@ -132,6 +132,20 @@ def stencil_csr(dims, coeffs):
     indices = cols[mask].astype(np.int32)
     data = vals[mask].astype(np.float64)
     return indptr, indices, data
+
+
+def stencil_row(dims, coeffs, r):
+    """(columns, values) of row r of the stencil operator (ascending
+    columns, Dirichlet boundary): the same operator as stencil_csr, one row
+    at a time for full-size spot checks."""
+    gx, gy, gz = dims
+    x, y, z = r % gx, (r // gx) % gy, r // (gx * gy)
+    c0, cxm, cxp, cym, cyp, czm, czp = coeffs
+    ent = [(-gx * gy, czm, z > 0), (-gx, cym, y > 0), (-1, cxm, x > 0), (0, c0, True),
+           (1, cxp, x < gx - 1), (gx, cyp, y < gy - 1), (gx * gy, czp, z < gz - 1)]
+    cols = [r + off for off, _, ok in ent if ok]
+    vals = [v for _, v, ok in ent if ok]
+    return np.asarray(cols, dtype=np.int64), np.asarray(vals, dtype=np.float64)
 
 
 # ----------------------------------------------------------------------------

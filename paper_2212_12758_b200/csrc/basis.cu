@@ -490,23 +490,24 @@ struct PipeArgs {
   // SDIM > 0 (matrix-free stencil): z is recomputed from w_hat_{c-1}
   StencilP sp;
   int64_t hal;          // halo rows held in each column's padding (0 on one GPU)
+  int apron;            // rows of w_hat_{c-1} staged either side of a chunk (16)
 };
 
 // Ring-stage slots (doubles) of one 512-row chunk [r0, r0+512):
 //   SDIM == 0, UPDATE : z | window columns j0 .. c-1                (512 each)
-//   SDIM  > 0, UPDATE : w_hat_{c-1} rows [r0-16, r0+528) (544) | window
-//                       columns j0 .. c-2 | w_hat_{c-1} at r0 -+ gx (and
-//                       r0 -+ gx*gy in 3D): the stencil neighbours, L2 hits
+//   SDIM  > 0, UPDATE : w_hat_{c-1} rows [r0-16, r0+528) (the x neighbours,
+//                       one 128-B aligned copy) | window columns j0 .. c-2;
+//                       the y / z neighbours (+-gx, +-gx*gy rows: L2 hits)
+//                       are loaded by the consumers one chunk ahead
 //   !UPDATE           : column col
 //   + (SKETCH) the chunk's 512 sign bits (64 B, padded to 128 B)
-constexpr int kXExt = 544;   // rows [r0-16, r0+528): 128-B aligned copy with a 16-row apron
 struct SlotGeom {
   int nslot;      // data slots
   int stage_d;    // doubles per stage
 };
 
 template <bool UPDATE, bool SKETCH, int SDIM>
-__host__ __device__ __forceinline__ SlotGeom slot_geom(int nw) {
+__host__ __device__ __forceinline__ SlotGeom slot_geom(int nw, int apron) {
   SlotGeom g;
   if (!UPDATE) {
     g.nslot = 1;
@@ -515,9 +516,8 @@ __host__ __device__ __forceinline__ SlotGeom slot_geom(int nw) {
     g.nslot = 1 + nw;
     g.stage_d = (1 + nw) * kChunk;
   } else {
-    const int nnb = SDIM == 3 ? 4 : 2;
-    g.nslot = 1 + (nw - 1) + nnb;
-    g.stage_d = kXExt + (nw - 1 + nnb) * kChunk;
+    g.nslot = 1 + (nw - 1);
+    g.stage_d = (kChunk + 2 * apron) + (nw - 1) * kChunk;
   }
   g.stage_d += SKETCH ? kSignPad : 0;
   return g;
@@ -537,25 +537,17 @@ __device__ __forceinline__ void slot_copy(const PipeArgs& a, int v, int col, int
   } else {
     const double* x = a.V + (int64_t)(a.col0 - 1) * a.ld;
     const int64_t hale = (a.hal + 15) & ~(int64_t)15;   // <= the column's padding
-    if (v == 0) {                               // w_hat_{c-1} with an apron either side
+    const int xw = kChunk + 2 * a.apron;
+    if (v == 0) {                               // w_hat_{c-1} with the x / y neighbour apron
       *src = x;
-      base = r0 - 16;
-      len = kXExt;
+      base = r0 - a.apron;
+      len = xw;
       off = 0;
       clo = -hale;
       chi = a.n + a.hal;
-    } else if (v < a.nw) {                      // window column j0 + v - 1
+    } else {                                    // window column j0 + v - 1
       *src = a.V + (int64_t)(j0 + v - 1) * a.ld;
-      off = kXExt + (v - 1) * kChunk;
-    } else {                                    // neighbour chunk q of w_hat_{c-1}
-      const int q = v - a.nw;
-      const int64_t gx = a.sp.gx, pl = (int64_t)a.sp.gx * a.sp.gy;
-      const int64_t shift = q == 0 ? -gx : q == 1 ? gx : q == 2 ? -pl : pl;
-      *src = x;
-      base = r0 + shift;
-      off = kXExt + (a.nw - 1 + q) * kChunk;
-      clo = -hale;
-      chi = a.n + a.hal;
+      off = xw + (v - 1) * kChunk;
     }
   }
   int64_t l = base > clo ? base : clo;
@@ -576,7 +568,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_stream_tiles(PipeArgs a) {
   if (a.st->breakdown) return;
   extern __shared__ __align__(128) double dsm[];
   __shared__ double red[kWarps];
-  const SlotGeom geo = slot_geom<UPDATE, SKETCH, SDIM>(a.nw);
+  const SlotGeom geo = slot_geom<UPDATE, SKETCH, SDIM>(a.nw, a.apron);
   const int nstage = a.nstage;
   const int stage_d = geo.stage_d;
   const int sign_off = stage_d - (SKETCH ? kSignPad : 0);
@@ -661,6 +653,28 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_stream_tiles(PipeArgs a) {
   if (SKETCH) load_sk_rows(a.rows, a.s, tid, R);
   double nrm = 0.0;
   RingPos rp;
+  // SDIM > 0: y / z neighbours of the rows (tid, tid+256) of the next chunk,
+  // loaded from global (L2) one chunk ahead: nbr[h][0..3] = x[r-gx], x[r+gx],
+  // x[r-plane], x[r+plane] (0 outside the grid)
+  double nbr[2][4];
+  const double* xcol = (UPDATE && SDIM > 0) ? a.V + (int64_t)(a.col0 - 1) * a.ld : nullptr;
+  auto load_nbr = [&](int64_t g0c) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t g = g0c + tid + kThreads * h, r = g - rb;
+      nbr[h][0] = nbr[h][1] = nbr[h][2] = nbr[h][3] = 0.0;
+      if (r >= 0 && r < n) {
+        uint32_t ix, iy, iz;
+        grid_coords(a.sp, (uint32_t)g, ix, iy, iz);
+        const int64_t gx = a.sp.gx, pl = (int64_t)a.sp.gx * a.sp.gy;
+        if (iy > 0) nbr[h][0] = __ldg(xcol + r - gx);
+        if (iy + 1 < (uint32_t)a.sp.gy) nbr[h][1] = __ldg(xcol + r + gx);
+        if (SDIM == 3 && iz > 0) nbr[h][2] = __ldg(xcol + r - pl);
+        if (SDIM == 3 && iz + 1 < (uint32_t)a.sp.gz) nbr[h][3] = __ldg(xcol + r + pl);
+      }
+    }
+  };
+  if (UPDATE && SDIM > 0 && t_first + blockIdx.x <= t_last) load_nbr((t_first + blockIdx.x) << kSkLogT);
   for (int col = a.col0; col < a.col1; ++col) {
     double acc[kSkAcc] = {0.0, 0.0, 0.0};
     for (int64_t tile = t_first + blockIdx.x; tile <= t_last; tile += gridDim.x) {
@@ -668,6 +682,17 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_stream_tiles(PipeArgs a) {
       double v[kSkPer];
 #pragma unroll
       for (int ch = 0; ch < kChunksPerTile; ++ch) {
+        double cur[2][4];
+        if (UPDATE && SDIM > 0) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cur[h][q] = nbr[h][q];
+          // issue the next chunk's neighbour loads before waiting on this one
+          const int64_t gn = ch + 1 < kChunksPerTile ? g0 + (ch + 1) * kChunk
+                                                     : ((tile + gridDim.x) << kSkLogT);
+          if (ch + 1 < kChunksPerTile || tile + gridDim.x <= t_last) load_nbr(gn);
+        }
         mbar_wait(full + rp.stage, rp.phase);
         const double* sb = ring + (size_t)rp.stage * stage_d;
         const uint32_t* sgn = reinterpret_cast<const uint32_t*>(sb + sign_off);
@@ -687,16 +712,15 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_stream_tiles(PipeArgs a) {
               // z_r = (A w_hat_{c-1})_r recomputed exactly as K1 did (stencil_row)
               uint32_t ix, iy, iz;
               grid_coords(a.sp, (uint32_t)g, ix, iy, iz);
-              const double* xs = sb + 16;                         // row i at xs[i]
-              const double* nb = sb + kXExt + (a.nw - 1) * kChunk;  // y-, y+, z-, z+
+              const int xw = kChunk + 2 * a.apron;
+              const double* xs = sb + a.apron;                    // row i at xs[i]
               const double xc = xs[i];
-              const double zr = stencil_row<SDIM>(a.sp, ix, iy, iz, xc, xs[i - 1], xs[i + 1], nb[i],
-                                                  nb[kChunk + i], SDIM == 3 ? nb[2 * kChunk + i] : 0.0,
-                                                  SDIM == 3 ? nb[3 * kChunk + i] : 0.0);
+              const double zr = stencil_row<SDIM>(a.sp, ix, iy, iz, xc, xs[i - 1], xs[i + 1], cur[h][0],
+                                                  cur[h][1], cur[h][2], cur[h][3]);
               val = cz * zr;
 #pragma unroll
               for (int t = 0; t < kKMax - 1; ++t)
-                if (t < a.nw - 1) val = fma(cw[t], sb[kXExt + t * kChunk + i], val);
+                if (t < a.nw - 1) val = fma(cw[t], sb[xw + t * kChunk + i], val);
 #pragma unroll
               for (int t = 0; t < kKMax; ++t)                     // j = c-1 is the last window term
                 if (t == a.nw - 1) val = fma(cw[t], xc, val);
@@ -754,7 +778,7 @@ static int pipe_stages(int stage_d, bool sketch, size_t* smem) {
 template <bool UPDATE, bool SKETCH, int SDIM>
 static int launch_stream(fab_ctx* c, PipeArgs a, cudaStream_t st) {
   size_t smem = 0;
-  a.nstage = pipe_stages(slot_geom<UPDATE, SKETCH, SDIM>(a.nw).stage_d, SKETCH, &smem);
+  a.nstage = pipe_stages(slot_geom<UPDATE, SKETCH, SDIM>(a.nw, a.apron).stage_d, SKETCH, &smem);
   k_stream_tiles<UPDATE, SKETCH, SDIM><<<c->grid_upd, kPipeThreads, smem, st>>>(a);
   FAB_CHECK_LAUNCH();
   return FAB_OK;
@@ -1038,6 +1062,7 @@ static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st,
     if (c->mf) {
       a.sp = stencil_params(c);
       a.hal = c->hal;
+      a.apron = 16;
       if (c->op.dims[2] > 1)
         rc = fused ? launch_stream<true, true, 3>(c, a, st) : launch_stream<true, false, 3>(c, a, st);
       else
