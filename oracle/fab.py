@@ -2,6 +2,8 @@
 
   alg4   Algorithm 4 (l.199-209): Alg 2 basis, y by Blendenpik, return
          ||b|| V_m f(H_m + h_{m+1,m} y e_m^T) e_1
+  alg3   Algorithm 3 (l.187-197): Alg 1 basis, y by (plain) LSQR, return
+         r_11 V_m f(H_m + h_{m+1,m} y e_m^T) e_1
   ss     Remark 2 (l.249-251): as Alg 4 with y from sketch-and-solve
          (mathematically sFOM, Eq. (9))
   alg5   Algorithm 5 (l.219-228): ||b|| V_m f(H_m) e_1, no least squares
@@ -104,3 +106,30 @@ def fom(A, b, m, f="exp", alpha=1.0, sigma=0.0, poly=None):
 def dense(A, b, f="exp", alpha=1.0, sigma=0.0, poly=None):
     Ad = A.toarray() if hasattr(A, "toarray") else np.asarray(A)
     return matfun.f_dense_apply(f, Ad, b, alpha, sigma, poly)
+
+
+def alg3(A, b, m, s, seed, f="exp", alpha=1.0, sigma=0.0, poly=None, lsqr_tol=1e-6,
+         lsqr_iters=None, mode="lsqr"):
+    """Algorithm 3: basis by Algorithm 1 with the SRHT
+    Theta (l.70; the same Theta as fab_sketch(s, seed)), y = argmin ||V_m z
+    - v_{m+1}|| by LSQR (l.182: "a few iterations of LSQR ... is sufficient"
+    for the well-conditioned BG basis), f_m = r_11 V_m f(C_m) e_1 (l.195).
+    mode "none" skips the least squares (y = 0).  Returns a dict like solve."""
+    th = SRHT(b.shape[0], s, seed)
+    dec = krylov.sketched_gs(A, b, m, th)
+    me = dec["m_eff"]
+    V, H = dec["V"], dec["H"]
+    y = np.zeros(me)
+    info = {}
+    if not dec["breakdown"] and mode == "lsqr":
+        Vm, c = V[:, :me], V[:, me]
+        y, info = lsq.lsqr(lambda z: Vm @ z, lambda u: Vm.T @ u, c, me, tol=lsqr_tol,
+                           iters=lsqr_iters)                               # l.194
+    C = H[:me, :me].copy()
+    if not dec["breakdown"]:
+        C[:, me - 1] += H[me, me - 1] * y                                   # Eq. (6)
+    cvec = matfun.f_e1(f, C, alpha, sigma, poly)
+    fm = dec["gamma"] * (V[:, :me] @ cvec)                                  # l.195
+    return dict(f_m=fm, V=V, H=H, S=dec["S"], R=dec["R"], gamma=dec["gamma"], m_eff=me,
+                breakdown=dec["breakdown"], y=y, C=C, c=cvec, lsqr=info, rows=th.rows,
+                signs=th.signs)

@@ -1,5 +1,6 @@
-"""Krylov bases: Algorithm 2 (truncated orthogonalization, PAPER.md
-l.102-130, §2.1.2) and the Arnoldi decomposition (Eq. (2), l.38-48).
+"""Krylov bases: Algorithm 1 (sketched Gram-Schmidt, PAPER.md l.61-100,
+§2.1.1), Algorithm 2 (truncated orthogonalization, l.102-130, §2.1.2) and
+the Arnoldi decomposition (Eq. (2), l.38-48).
 
 Algorithm 2 as printed (l.118-127):
     v_1 <- b / ||b||_2
@@ -93,3 +94,52 @@ def arnoldi(A, b, m: int, breakdown_tol: float = 1e-14):
                         m_eff=c, breakdown=True)
         U[:, c] = w / hn
     return dict(V=U, H=K, gamma=gamma, m_eff=m, breakdown=False)
+
+
+def sketched_gs(A, b, m: int, theta, breakdown_tol: float = 1e-14):
+    """Algorithm 1 (after Balabanov & Grigori), literally:
+
+        w_1 <- b;  p_1 <- Theta w_1;  r_11 <- ||p_1||;  s_1 <- p_1 / r_11;
+        v_1 <- w_1 / r_11
+        for i = 2 .. m+1:
+            w_i <- A v_{i-1}                          (l.89)
+            p_i <- Theta w_i                          (l.90)
+            r_i <- S_{i-1}^T p_i;  R(1:i-1, i) <- r_i  (l.91)
+            s_i <- p_i - S_{i-1} r_i                  (l.92)
+            r_ii <- ||s_i||                           (l.93)
+            s_i <- s_i / r_ii;  S_i <- [S_{i-1} s_i]  (l.94)
+            v_i <- (w_i - V_{i-1} r_i) / r_ii         (l.95)
+        underline-H_m <- R(:, 2:m+1)                  (l.97)
+
+    theta: an object with .apply(x) = Theta x (oracle.srht.SRHT).
+    Breakdown (reading G-5 applied to r_ii, the sketched norm of the new
+    direction): stop when r_ii <= 1e-14 ||A||_inf ||Theta v_{i-1}||-scale,
+    i.e. r_ii <= 1e-14 ||A||_inf (S is orthonormal, so ||Theta v_j|| = 1).
+    Returns dict(V, H, S, R, gamma=r_11, m_eff, breakdown)."""
+    n = b.shape[0]
+    V = np.zeros((n, m + 1))
+    R = np.zeros((m + 1, m + 1))
+    p1 = theta.apply(b)
+    s = p1.shape[0]
+    S = np.zeros((s, m + 1))
+    r11 = float(np.linalg.norm(p1))                      # l.86
+    R[0, 0] = r11
+    S[:, 0] = p1 / r11                                    # l.87
+    V[:, 0] = b / r11                                     # l.88
+    thresh = breakdown_tol * _norm_inf(A)
+    for i in range(2, m + 2):                             # l.89 (paper index)
+        c = i - 1
+        w = A @ V[:, c - 1]
+        p = theta.apply(w)
+        r = S[:, :c].T @ p                                # l.91
+        R[:c, c] = r
+        sv = p - S[:, :c] @ r                             # l.92
+        rii = float(np.linalg.norm(sv))                   # l.93
+        R[c, c] = rii
+        if rii <= thresh:
+            m_eff = c
+            return dict(V=V[:, :m_eff], H=R[: m_eff + 1, 1: m_eff + 1], S=S[:, :m_eff],
+                        R=R[: m_eff + 1, : m_eff + 1], gamma=r11, m_eff=m_eff, breakdown=True)
+        S[:, c] = sv / rii                                # l.94
+        V[:, c] = (w - V[:, :c] @ r) / rii                # l.95
+    return dict(V=V, H=R[:, 1:], S=S, R=R, gamma=r11, m_eff=m, breakdown=False)

@@ -170,3 +170,33 @@ def test_modes_agree_when_converged_c2_small():
     ref = fab.dense(A, b, "exp", alpha=-1e-3) if p.n <= 4000 else None
     for o in outs:
         assert rel(o["f_m"], ref) <= 1e-10
+
+
+# ---- Algorithm 3 (Alg 1 basis + LSQR) -----------------
+def test_alg3_exact_ls_equals_fom_lemma1():
+    # Lemma 1 (l.151-166): with the exact least-squares y, Alg 3 = FOM Eq. (4)
+    for name, kw in [("c1", dict(g=30, m=20, s=50)), ("c5", dict(n=2000, m=25, s=60))]:
+        p = fp.make(name, **kw)
+        A = p.scipy()
+        r = fab.alg3(A, p.b, p.m, p.s, p.sketch_seed, f=p.f, alpha=p.alpha, sigma=p.sigma, lsqr_tol=1e-14)
+        fo = fab.fom(A, p.b, p.m, f=p.f, alpha=p.alpha, sigma=p.sigma)
+        assert np.linalg.norm(r["f_m"] - fo) <= 1e-9 * np.linalg.norm(fo), name
+
+
+def test_alg3_polynomial_exactness():
+    # l.329-330: polynomials of degree <= m-1 are reproduced exactly
+    p = fp.make("c3", g=10, m=8, s=30)
+    A = p.scipy()
+    coef = np.random.default_rng(9).standard_normal(8)
+    alpha = 1.0 / p.norm_inf
+    r = fab.alg3(A, p.b, p.m, p.s, 5, f="poly", alpha=alpha, poly=coef, lsqr_tol=1e-14)
+    ref = fab.dense(A, p.b, "poly", alpha=alpha, poly=coef)
+    assert np.linalg.norm(r["f_m"] - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+def test_alg3_converges_to_dense_exp():
+    p = fp.make("c4", n=1 << 10, m=30, s=70)
+    A = p.scipy()
+    r = fab.alg3(A, p.b, p.m, p.s, p.sketch_seed, f=p.f, alpha=p.alpha, lsqr_tol=1e-14)
+    ref = fab.dense(A, p.b, p.f, alpha=p.alpha)
+    assert np.linalg.norm(r["f_m"] - ref) <= 1e-10 * np.linalg.norm(ref)

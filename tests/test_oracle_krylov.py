@@ -96,3 +96,50 @@ def test_breakdown_distinct_eigenvalues():
     b = np.random.default_rng(1).standard_normal(40)
     d = krylov.truncated_arnoldi(A, b, 10, 10)
     assert d["breakdown"] and d["m_eff"] == 4
+
+
+# ---- Algorithm 1 (sketched Gram-Schmidt) ---------------
+def _srht(n, s, seed=1):
+    from oracle.srht import SRHT
+    return SRHT(n, s, seed)
+
+
+def test_sketched_gs_sketch_orthonormal_and_arnoldi_like():
+    # l.94: S_i stays orthonormal by construction; l.97 / Eq. (3): A V_m = V_{m+1} H_m
+    # (a problem whose Krylov space is not yet saturated at m: with r_ii << ||p_i||
+    # one CGS pass loses sketch orthogonality, as for any single-pass GS)
+    p = fp.make("c1", g=40, m=30, k=2, s=70)
+    A = p.scipy()
+    d = krylov.sketched_gs(A, p.b, p.m, _srht(p.n, p.s, 7))
+    S, V, H = d["S"], d["V"], d["H"]
+    # one CGS pass per step: orthogonality holds to ~eps ||p_i|| / r_ii (here
+    # r_ii / ||p_i|| ~ 1e-3 late in the run), so 1e-10, not machine precision
+    assert np.abs(S.T @ S - np.eye(p.m + 1)).max() <= 1e-10
+    assert _arnoldi_like_residual(A, V, H) <= 1e-13
+    assert np.allclose(H, np.triu(H, -1))                     # upper Hessenberg
+    th = _srht(p.n, p.s, 7)
+    assert np.abs(th.apply(V) - S).max() <= 1e-12             # S = Theta V (the sketch is exact)
+    assert abs(d["gamma"] - np.linalg.norm(th.apply(p.b))) <= 1e-14 * d["gamma"]
+    assert np.linalg.cond(V) <= 10.0                          # well-conditioned (Balabanov-Grigori Prop 4.1)
+
+
+def test_sketched_gs_with_orthogonal_sketch_is_arnoldi():
+    # s = N = n: Theta = (1/sqrt N) H_N D is orthogonal, so sketched GS is exact
+    # Gram-Schmidt: V orthonormal and underline-H = Arnoldi's (up to rounding)
+    n = 256
+    A = sp.diags([np.full(n - 1, -1.0), 2 + np.linspace(0, 3, n), np.full(n - 1, -0.5)], [-1, 0, 1]).tocsr()
+    b = np.random.default_rng(3).standard_normal(n)
+    d = krylov.sketched_gs(A, b, 12, _srht(n, n, 11))
+    ref = krylov.arnoldi(A, b, 12)
+    assert np.abs(d["V"].T @ d["V"] - np.eye(13)).max() <= 1e-12
+    assert np.abs(d["H"] - ref["H"]).max() <= 1e-12 * np.abs(ref["H"]).max()
+    assert np.abs(d["V"] - ref["V"]).max() <= 1e-12
+    assert abs(d["gamma"] - np.linalg.norm(b)) <= 1e-13 * np.linalg.norm(b)
+
+
+def test_sketched_gs_breakdown_distinct_eigenvalues():
+    vals = np.repeat([1.0, 2.0, 3.5, 5.0], 64)
+    A = sp.diags(vals).tocsr()
+    b = np.random.default_rng(4).standard_normal(len(vals))
+    d = krylov.sketched_gs(A, b, 10, _srht(len(vals), 24, 2))
+    assert d["breakdown"] and d["m_eff"] == 4
