@@ -69,7 +69,7 @@ enum {
 };
 
 /* ---- enums ------------------------------------------------------------ */
-enum { FAB_BLENDENPIK = 0, FAB_SKETCH_SOLVE = 1, FAB_NONE = 2 };       /* fab_compress */
+enum { FAB_BLENDENPIK = 0, FAB_SKETCH_SOLVE = 1, FAB_NONE = 2, FAB_LSQR = 3 };  /* fab_compress */
 enum { FAB_EXP = 0, FAB_SQRT = 1, FAB_INVSQRT = 2, FAB_POLY = 3 };     /* fab_apply    */
 enum { FAB_OP_CSR = 0, FAB_OP_STENCIL = 1 };                          /* operator kind */
 enum { FAB_DEVICE = 0, FAB_HOST = 1 };                                /* pointer space */
@@ -149,7 +149,7 @@ typedef struct {
   int mode;                /* last fab_compress mode                                 */
   int lsqr_iters, lsqr_converged;
   int dense_iters;         /* DB iterations / Pade squarings of the last fab_apply   */
-  int pad0;
+  int basis_alg;           /* 2: fab_basis (Algorithm 2); 1: fab_basis_sgs (Alg 1)    */
   double gamma_b;          /* ||b||_2                                                */
   double h_last;           /* h_{m+1,m}                                              */
   double norm_inf;         /* ||A||_inf                                              */
@@ -204,6 +204,17 @@ int fab_init(fab_ctx** ctx, const fab_operator* A, const double* b, const fab_op
    breakdown.  Errors: EORDER, EINVAL, ECUDA. */
 int fab_basis(fab_ctx* ctx, int m, int k);
 
+/* Algorithm 1 (l.76-100, sketched Gram-Schmidt after Balabanov & Grigori):
+   the basis V_{m+1} whose sketch S = Theta V_{m+1} is orthonormal, with the
+   Theta of the preceding fab_sketch (required: FAB_EORDER otherwise;
+   s >= m+1).  Per step: w_i = A v_{i-1}, p_i = Theta w_i, one Gram-Schmidt
+   step on the s x i sketch (r_i, r_ii), v_i = (w_i - V_{i-1} r_i) / r_ii --
+   O(n i) bytes per step (Table 1, l.265).  gamma_b = r_11 = ||Theta b||
+   (l.195).  Algorithm 3 = this basis + fab_compress(FAB_LSQR).  Returns
+   FAB_BREAKDOWN (m_eff in fab_info) when r_ii <= 1e-14 ||A||_inf (G-5).
+   Errors: EORDER, EINVAL, ECUDA, ENCCL. */
+int fab_basis_sgs(fab_ctx* ctx, int m);
+
 /* Draw the SRHT Theta (s rows, seed) of l.70: signs from the counter hash of
    G-10, rows by Floyd sampling without replacement.  It only draws Theta
    (O(N/32 + s) work): the next fab_basis applies it fused into the basis
@@ -215,8 +226,9 @@ int fab_sketch(fab_ctx* ctx, int s, uint64_t seed);
 
 /* Compression (Eq. (6)/(7)).  mode FAB_BLENDENPIK: QR of Theta V_m, LSQR on
    V_m R^{-1} (opts NULL => tol 1e-6, maxit 4m); FAB_SKETCH_SOLVE:
-   y = R^{-1} Q^T Theta v_{m+1}; FAB_NONE: y = 0 (Alg 5).  Warnings: ILLCOND,
-   NOTCONV.  Errors: EORDER, ESINGULAR, ECUDA. */
+   y = R^{-1} Q^T Theta v_{m+1}; FAB_NONE: y = 0 (Alg 5); FAB_LSQR: plain LSQR
+   on V_m (Alg 3, l.194; needs no sketch).  Warnings: ILLCOND, NOTCONV.
+   Errors: EORDER, ESINGULAR, ECUDA. */
 int fab_compress(fab_ctx* ctx, int mode, const fab_lsqr_opts* opts);
 
 /* y_out (n_local doubles, device or host per y_location) =

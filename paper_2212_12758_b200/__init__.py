@@ -132,6 +132,12 @@ class Solver:
         self.status["basis"] = st
         return st
 
+    def basis_sgs(self, m):
+        """Algorithm 1 (sketched Gram-Schmidt) with the Theta of sketch()."""
+        st = check(lib.fab_basis_sgs(self.ctx, m), "fab_basis_sgs")
+        self.status["basis"] = st
+        return st
+
     def sketch(self, s, seed):
         st = check(lib.fab_sketch(self.ctx, s, C.c_uint64(seed)), "fab_sketch")
         self.status["sketch"] = st

@@ -12,7 +12,7 @@ LIB_PATH = os.path.join(HERE, "libfab.so")
 FAB_OK, FAB_BREAKDOWN, FAB_ILLCOND, FAB_NOTCONV = 0, 1, 2, 3
 FAB_EINVAL, FAB_EORDER, FAB_ESINGULAR, FAB_EDOMAIN = -1, -2, -3, -4
 FAB_ENOCONV, FAB_ENOMEM, FAB_ECUDA, FAB_ENCCL, FAB_ENODEV = -5, -6, -7, -8, -9
-FAB_BLENDENPIK, FAB_SKETCH_SOLVE, FAB_NONE = 0, 1, 2
+FAB_BLENDENPIK, FAB_SKETCH_SOLVE, FAB_NONE, FAB_LSQR = 0, 1, 2, 3
 FAB_EXP, FAB_SQRT, FAB_INVSQRT, FAB_POLY = 0, 1, 2, 3
 FAB_OP_CSR, FAB_OP_STENCIL = 0, 1
 FAB_DEVICE, FAB_HOST = 0, 1
@@ -20,11 +20,11 @@ GET = dict(info=0, H=1, V=2, SV=3, rows=4, signs=5, y=6, C=7, fc=8, R=9, beta=10
 FAB_SET_POLY, FAB_SET_B_HOST, FAB_SET_B_DEVICE = 100, 101, 102
 FAB_FLAG_PROFILE = 1
 
-MODES = {"blendenpik": FAB_BLENDENPIK, "sketch_solve": FAB_SKETCH_SOLVE, "none": FAB_NONE}
+MODES = {"blendenpik": FAB_BLENDENPIK, "sketch_solve": FAB_SKETCH_SOLVE, "none": FAB_NONE, "lsqr": FAB_LSQR}
 FUNCS = {"exp": FAB_EXP, "sqrt": FAB_SQRT, "invsqrt": FAB_INVSQRT, "poly": FAB_POLY}
 
 # every function declared in include/fab.h
-EXPORTS = ("fab_version", "fab_strerror", "fab_workspace_size", "fab_init", "fab_basis",
+EXPORTS = ("fab_version", "fab_strerror", "fab_workspace_size", "fab_init", "fab_basis", "fab_basis_sgs",
            "fab_sketch", "fab_compress", "fab_apply", "fab_get", "fab_get_column", "fab_get_vrows",
            "fab_set", "fab_last_error", "fab_destroy", "fab_comm_unique_id", "fab_comm_init",
            "fab_comm_destroy")
@@ -52,7 +52,7 @@ class FabInfo(C.Structure):
     _fields_ = [("n", C.c_int64), ("N", C.c_int64), ("m", C.c_int), ("k", C.c_int), ("s", C.c_int),
                 ("m_eff", C.c_int), ("breakdown", C.c_int), ("sketch_fused", C.c_int),
                 ("mode", C.c_int), ("lsqr_iters", C.c_int), ("lsqr_converged", C.c_int),
-                ("dense_iters", C.c_int), ("pad0", C.c_int), ("gamma_b", C.c_double),
+                ("dense_iters", C.c_int), ("basis_alg", C.c_int), ("gamma_b", C.c_double),
                 ("h_last", C.c_double), ("norm_inf", C.c_double), ("cond_R", C.c_double),
                 ("lsqr_rnorm", C.c_double), ("lsqr_arnorm", C.c_double), ("lsqr_anorm", C.c_double),
                 ("ms_basis", C.c_double), ("ms_sketch", C.c_double), ("ms_compress", C.c_double),
@@ -62,7 +62,7 @@ class FabInfo(C.Structure):
                 ("lsqr_passes", C.c_int64), ("ms_sketch_batched", C.c_double)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad0"}
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 def load():
@@ -78,6 +78,7 @@ def load():
         "fab_workspace_size": (I, [C.POINTER(FabOperator), C.POINTER(FabOpts), C.POINTER(C.c_size_t)]),
         "fab_init": (I, [C.POINTER(P), C.POINTER(FabOperator), P, C.POINTER(FabOpts)]),
         "fab_basis": (I, [P, I, I]),
+        "fab_basis_sgs": (I, [P, I]),
         "fab_sketch": (I, [P, I, C.c_uint64]),
         "fab_compress": (I, [P, I, C.POINTER(FabLsqrOpts)]),
         "fab_apply": (I, [P, I, D, D, P, I]),

@@ -158,6 +158,7 @@ static void free_ctx(fab_ctx* c) {
   if (!c) return;
   release_long_rows(c);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->gexec_sgs) cudaGraphExecDestroy(c->gexec_sgs);
   if (c->part_dots) cudaFree(c->part_dots);
   if (c->own_ws && c->ws) cudaFree(c->ws);
   if (c->st_h) cudaFreeHost(c->st_h);
@@ -338,6 +339,39 @@ int fab_basis(fab_ctx* c, int m, int k) {
     FAB_CUDA(cudaMemcpy(&hl, c->H + m + (int64_t)(m - 1) * c->ldH, sizeof(double), cudaMemcpyDeviceToHost));
   }
   c->info.h_last = hl;
+  c->info.basis_alg = 2;
+  return c->breakdown ? FAB_BREAKDOWN : FAB_OK;
+}
+
+int fab_basis_sgs(fab_ctx* c, int m) {
+  if (!c) return FAB_EINVAL;
+  if (!c->sketch_ready) return FAB_EORDER;   // Algorithm 1 sketches every new vector
+  if (m < 1 || m > c->m_max || m >= c->n_global || c->s < m + 1) return FAB_EINVAL;
+  FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
+  int rc = run_basis_sgs(c, m);
+  if (rc != FAB_OK) return rc;
+  double ms = 0;
+  if ((rc = timed_end(c, &ms)) != FAB_OK) return rc;
+  if ((rc = pull_state(c)) != FAB_OK) return rc;
+  c->m = m;
+  c->k = 0;
+  c->breakdown = c->st_h->breakdown != 0;
+  c->m_eff = c->st_h->m_eff;
+  c->basis_ready = true;
+  c->compressed = false;
+  c->sketch_in_V = true;   // S = Theta V_{m+1} is built with the basis
+  c->info.m = m;
+  c->info.k = 0;
+  c->info.m_eff = c->m_eff;
+  c->info.breakdown = c->breakdown;
+  c->info.sketch_fused = 1;
+  c->info.gamma_b = c->st_h->gamma;
+  c->info.ms_basis = ms;
+  c->info.basis_alg = 1;
+  double hl = 0;
+  if (!c->breakdown)
+    FAB_CUDA(cudaMemcpy(&hl, c->H + m + (int64_t)(m - 1) * c->ldH, sizeof(double), cudaMemcpyDeviceToHost));
+  c->info.h_last = hl;
   return c->breakdown ? FAB_BREAKDOWN : FAB_OK;
 }
 
@@ -366,13 +400,15 @@ int fab_sketch(fab_ctx* c, int s, uint64_t seed) {
 
 int fab_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o) {
   if (!c) return FAB_EINVAL;
-  if (mode != FAB_BLENDENPIK && mode != FAB_SKETCH_SOLVE && mode != FAB_NONE) return FAB_EINVAL;
+  if (mode != FAB_BLENDENPIK && mode != FAB_SKETCH_SOLVE && mode != FAB_NONE && mode != FAB_LSQR)
+    return FAB_EINVAL;
   if (!c->basis_ready) return FAB_EORDER;
-  if (mode != FAB_NONE && !c->sketch_ready) return FAB_EORDER;
+  const bool needs_sketch = (mode == FAB_BLENDENPIK || mode == FAB_SKETCH_SOLVE);
+  if (needs_sketch && !c->sketch_ready) return FAB_EORDER;
   if (o && (o->iters < 0 || o->maxit < 0 || o->tol < 0)) return FAB_EINVAL;
   int rc;
   const int64_t l0 = c->nlaunch;
-  if (mode != FAB_NONE && !c->sketch_in_V) {
+  if (needs_sketch && !c->sketch_in_V) {
     // API order (basis before sketch): one batched SRHT pass over V_{m+1}
     if (c->s < (c->breakdown ? c->m_eff : c->m + 1)) return FAB_EINVAL;
     FAB_CUDA(cudaEventRecord(c->ev0, c->stream));

@@ -961,7 +961,6 @@ int init_vector_norm(fab_ctx* c) {
 }
 
 
-// Enqueue one Krylov step c (1..m) on stream st.
 // K2 (+ C2 on several GPUs): the step scalars of column col-1
 static int enqueue_scalar(fab_ctx* c, int col, int nw, int nparts, int final_step, cudaStream_t st,
                           int64_t* launches) {
@@ -981,10 +980,12 @@ static int enqueue_scalar(fab_ctx* c, int col, int nw, int nparts, int final_ste
   return FAB_OK;
 }
 
-// Enqueue one Krylov step c (1..m) on stream st.
-static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st, int64_t* launches) {
-  const int nw = col < k ? col : k;
-  int nparts = c->grid_spmv;
+// K1 of step col: z = A w_hat_{col-1} (stored in z unless matrix-free and
+// !need_z) and the partial window dots (nw columns ending at col-1); C1 first
+// on several GPUs.  *nparts = partial slots written.
+int enqueue_k1(fab_ctx* c, int col, int nw, double* z, bool need_z, cudaStream_t st, int64_t* launches,
+               int* nparts) {
+  *nparts = c->grid_spmv;
   double* x = c->V + (int64_t)(col - 1) * c->ld;
   if (c->stencil) {
     int rc = comm_halo(c, x, st);   // C1: neighbour rows of w_hat_{col-1}
@@ -993,14 +994,15 @@ static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st,
     const bool d3 = c->op.dims[2] > 1;
     const int G = c->grid_spmv;
     const int64_t gb = c->row_begin;
+    const bool store = need_z || !c->mf;
     if (stencil_vec_path(c)) {
 #define FAB_K1V(DIM, NWM)                                                                                    \
   do {                                                                                                       \
-    if (c->mf)                                                                                               \
-      k_stencil_dots_v<DIM, NWM, false><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, c->vec,  \
+    if (!store)                                                                                              \
+      k_stencil_dots_v<DIM, NWM, false><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, z,       \
                                                                 c->part_dots, c->st_d);                      \
     else                                                                                                     \
-      k_stencil_dots_v<DIM, NWM, true><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, c->vec,   \
+      k_stencil_dots_v<DIM, NWM, true><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, z,        \
                                                                c->part_dots, c->st_d);                       \
   } while (0)
       if (c->k_max <= 2) {
@@ -1012,9 +1014,9 @@ static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st,
       }
 #undef FAB_K1V
     } else if (d3) {
-      k_stencil_dots<3><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, c->vec, c->part_dots, c->st_d);
+      k_stencil_dots<3><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, z, c->part_dots, c->st_d);
     } else {
-      k_stencil_dots<2><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, c->vec, c->part_dots, c->st_d);
+      k_stencil_dots<2><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, z, c->part_dots, c->st_d);
     }
     FAB_CHECK_LAUNCH();
     ++*launches;
@@ -1026,20 +1028,28 @@ static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st,
       xg = c->xg;
     }
     k_csr_dots<8><<<c->grid_spmv, kThreads, 0, st>>>(c->op.row_ptr, c->op.col_idx, c->op.values,
-                                                      c->op.value_scale, c->V, c->ld, col, nw, c->n, xg,
-                                                      c->vec, c->part_dots, c->st_d);
+                                                      c->op.value_scale, c->V, c->ld, col, nw, c->n, xg, z,
+                                                      c->part_dots, c->st_d);
     FAB_CHECK_LAUNCH();
     ++*launches;
     LongRows* L = long_rows(c);
     if (L && L->count) {
       k_csr_long<<<(unsigned)L->count, kThreads, 0, st>>>(
-          c->op.row_ptr, c->op.col_idx, c->op.values, c->op.value_scale, L->d, c->V, c->ld, col, nw, xg,
-          c->vec, c->part_dots + (int64_t)c->grid_spmv * (kKMax + 1), c->st_d);
+          c->op.row_ptr, c->op.col_idx, c->op.values, c->op.value_scale, L->d, c->V, c->ld, col, nw, xg, z,
+          c->part_dots + (int64_t)c->grid_spmv * (kKMax + 1), c->st_d);
       FAB_CHECK_LAUNCH();
       ++*launches;
-      nparts += (int)L->count;
+      *nparts += (int)L->count;
     }
   }
+  return FAB_OK;
+}
+
+// Enqueue one Krylov step c (1..m) on stream st.
+static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st, int64_t* launches) {
+  const int nw = col < k ? col : k;
+  int nparts = 0;
+  FAB_TRY(enqueue_k1(c, col, nw, c->vec, false, st, launches, &nparts));
   int rc = enqueue_scalar(c, col, nw, nparts, 0, st, launches);
   if (rc != FAB_OK) return rc;
   {

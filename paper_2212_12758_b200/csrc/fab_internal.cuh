@@ -120,6 +120,11 @@ struct fab_ctx {
   fab::Comm* comm = nullptr;          // NULL: one GPU
   std::vector<int64_t> rank_rows;     // row_begin of every rank, plus n_global
 
+  // cached Algorithm 1 graph
+  cudaGraphExec_t gexec_sgs = nullptr;
+  int g_sgs_m = -1, g_sgs_s = -1;
+  int64_t g_sgs_launches = 0;
+
   fab_info info{};
   unsigned flags = 0;
   int64_t nlaunch = 0;               // kernels launched outside the basis graph
@@ -217,6 +222,8 @@ const char* nccl_last_error();
 int basis_setup_grids(fab_ctx* c);
 int init_vector_norm(fab_ctx* c);            // partial norms of column 0, norm_inf
 int run_basis(fab_ctx* c, int m, int k);
+// sgs.cu (Algorithm 1)
+int run_basis_sgs(fab_ctx* c, int m);
 void release_long_rows(fab_ctx* c);
 int launch_sketch_cols(fab_ctx* c, int c0, int c1, cudaStream_t st);
 // sketch.cu

@@ -9,6 +9,8 @@
 //                    stored columns (V_m = W diag(1/beta)).
 //   FAB_SKETCH_SOLVE y = R^{-1} (Q^T Theta v_{m+1})  (Remark 2, l.249-251)
 //   FAB_NONE         y = 0  (Algorithm 5, l.219-228)
+//   FAB_LSQR         plain LSQR on V_m (Algorithm 3, l.194: the basis of
+//                    Algorithm 1 is well conditioned), i.e. R = I
 //
 // The LSQR scalar recurrence runs on the device (k_lsqr_scalar); the host
 // only polls convergence between chunks of iterations.
@@ -293,6 +295,38 @@ static LsqrPassFn pick_pass(int m, int* jpw) {
   return nullptr;
 }
 
+// One streaming pass over the first ncols stored columns W of V (K6):
+// t_new = W p - scal t_old (scal from st->scal if use_state_scal), with the
+// g = W^T t_new, ||t_new||^2 partials into part_g / part_tn.  Used by LSQR
+// and, with ncols = i-1, by Algorithm 1's update v_i = (w_i - V_{i-1} r_i)/r_ii.
+// t_old may alias t_new.  Tensor maps and ring depth are built on the host
+// (graph-capture safe: the map is a by-value kernel parameter).
+int launch_tall_gemv(fab_ctx* c, int ncols, const double* p, double scal, int use_state_scal,
+                     const double* t_old, double* t_new, cudaStream_t st) {
+  LsqrPipeFn pipe = pick_pipe(ncols);
+  size_t smem = 0;
+  const int ns = lsqr_pipe_stages(ncols, &smem);
+  if (ns < 2) pipe = nullptr;
+  CUtensorMap tm;
+  int boxc = 0, ncopies = 0;
+  lsqr_boxes(ncols, &boxc, &ncopies);
+  if (pipe && make_tmap_cols(c->V, c->n, ncols, c->ld, kLsR, boxc, &tm) != FAB_OK) pipe = nullptr;
+  if (pipe) {
+    const int64_t nch = (c->n + kLsR - 1) / kLsR;
+    const int G = (int)(nch < c->num_sms ? nch : c->num_sms);
+    pipe<<<G, kLsPipeThreads, smem, st>>>(tm, boxc, ncopies, ncols, c->n, p, scal, t_old, t_new, c->part_g,
+                                         c->part_tn, c->st_d, use_state_scal, ns);
+  } else {
+    int jpw = 0;
+    LsqrPassFn pass = pick_pass(ncols, &jpw);
+    if (!pass) return FAB_EINVAL;
+    pass<<<c->grid_lsqr, kLsqrThreads, 0, st>>>(c->V, c->ld, ncols, c->n, p, scal, t_old, t_new, c->part_g,
+                                                c->part_tn, c->st_d, use_state_scal);
+  }
+  FAB_CHECK_LAUNCH();
+  return FAB_OK;
+}
+
 // ---- small helpers (one CTA of kThreads) ---------------------------------
 // out_i = scale_i * sum_{j>=i} U[i,j] v_j   (U upper triangular, given as UT =
 // U^T column-major: U[i,j] = UT[j + i*m]); warp per output, fixed order.
@@ -394,10 +428,14 @@ __global__ void k_lsqr_init(const double* part_g, const double* part_tn, int npa
   if (threadIdx.x == 0) {
     st->alpha = alpha;
     st->beta = bt;             // scale of u = t / bt
-    st->phibar = 1.0;          // ||b|| = ||v_{m+1}|| = 1
+    // ||b|| = ||v_{m+1}|| = ||w_hat_m|| / beta_m: 1 for Algorithm 2's
+    // normalised columns, not for Algorithm 1's (unit sketch, not unit norm)
+    const double bnorm = bt / bcol[m];
+    st->phibar = bnorm;
     st->rhobar = alpha;
     st->anorm2 = 0.0;
-    st->rnorm = 1.0;
+    st->rnorm = bnorm;
+    st->scratch[0] = bnorm;
     st->arnorm = alpha;
     st->anorm = 0.0;
     st->scal = alpha / bt;     // next pass: t <- W p - alpha u = W p - (alpha/bt) t
@@ -458,7 +496,8 @@ __global__ void k_lsqr_step(const double* part_g, const double* part_tn, int npa
     st->lsqr_iters += 1;
     if (tol_mode) {
       const double tol = st->tol;
-      if (rnorm <= tol || (rnorm > 0 && arnorm <= tol * anorm * rnorm) || alpha == 0.0 || beta == 0.0)
+      if (rnorm <= tol * st->scratch[0] || (rnorm > 0 && arnorm <= tol * anorm * rnorm) || alpha == 0.0 ||
+          beta == 0.0)
         st->lsqr_done = 1;
     }
   }
@@ -488,6 +527,12 @@ __global__ void k_transpose(const double* A, int m, double* AT) {
     const int r = (int)(i % m), col = (int)(i / m);
     AT[col + (int64_t)r * m] = A[i];
   }
+}
+
+__global__ void k_eye(int m, double* X) {
+  const int64_t total = (int64_t)m * m;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+    X[i] = (i % m == i / m) ? 1.0 : 0.0;
 }
 
 __global__ void k_reset_lsqr(DevState* st) {
@@ -548,8 +593,16 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
   c->info.ms_lsqr_pass = 0.0;
   int64_t launches = 0;
   const bool need_ls = (mode != FAB_NONE) && !c->breakdown;
-  if (mode != FAB_NONE && !c->sketch_in_V) return FAB_EORDER;
-  if (need_ls) {
+  if (mode != FAB_NONE && mode != FAB_LSQR && !c->sketch_in_V) return FAB_EORDER;
+  if (need_ls && mode == FAB_LSQR) {
+    // Algorithm 3 (l.194): plain LSQR on V_m -- the Blendenpik iteration with R = I
+    k_eye<<<(m * m + kThreads - 1) / kThreads, kThreads, 0, st>>>(m, R);
+    k_eye<<<(m * m + kThreads - 1) / kThreads, kThreads, 0, st>>>(m, Rinv);
+    k_eye<<<(m * m + kThreads - 1) / kThreads, kThreads, 0, st>>>(m, RinvT);
+    FAB_CHECK_LAUNCH();
+    launches += 3;
+    c->info.cond_R = 1.0;
+  } else if (need_ls) {
     // QR of Theta V_m (s x m) with Theta v_{m+1} as an extra column
     int rc = dense_qr_sketch(c, m, R, qtb, st);
     if (rc != FAB_OK) return rc;
@@ -568,6 +621,8 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
     c->info.cond_R = hs[2];
     if (!(hs[0] >= 1e-14 * hs[1])) return FAB_ESINGULAR;
     if (hs[2] > 1e8) *warn = FAB_ILLCOND;
+  }
+  if (need_ls) {
     if (mode == FAB_SKETCH_SOLVE) {
       k_finish_y<<<1, kThreads, 0, st>>>(RinvT, qtb, m, y);
       FAB_CHECK_LAUNCH();

@@ -252,3 +252,80 @@ def test_edge_cases():
     sv.compress("none")
     y = sv.apply("exp", -1.0, 0.0)
     assert np.isfinite(y.cpu().numpy()).all()
+
+
+# ---- Algorithm 1 basis + Algorithm 3 -------
+@pytest.mark.parametrize("name,kw,csr", [
+    ("c1", {}, False),
+    ("c3", dict(g=24, m=40, s=90), False),
+    ("c3", dict(g=16, m=30, s=70), True),
+    ("c5", dict(n=5000, m=12, s=40), True),
+    ("c4", dict(n=1 << 14, m=20, s=50), True),
+])
+def test_alg3_sketched_gs_parity(name, kw, csr):
+    """H and V of Algorithm 1 are rounding-sensitive (each v_i carries the
+    error of w_i - V r_i amplified by 1/r_ii): they are compared at 10x the
+    oracle's own noise floor -- its change under a 1e-15 relative perturbation
+    of b (c1: 2.3e-10 for H) -- and f_m at BASELINE's 1e-10."""
+    import torch
+    import paper_2212_12758_b200 as fab
+    p = fp.make(name, **kw)
+    sv = fab.Solver(fab.Operator.from_problem(p, csr=csr), torch.as_tensor(p.b).cuda(), p.m, p.k, p.s)
+    sv.sketch(p.s, p.sketch_seed)
+    sv.basis_sgs(p.m)
+    # plain LSQR contracts by ~(k-1)/(k+1) ~ 0.7 per iteration on this basis
+    # (cond(V) ~ 5): 150 iterations reach the unique LS solution, so y and f_m
+    # are compared where they are determined (an intermediate iterate is
+    # rounding-sensitive, reading R-3)
+    L = 150
+    ref = ofab.alg3(p.scipy(), p.b, p.m, p.s, p.sketch_seed, f=p.f, alpha=p.alpha, sigma=p.sigma,
+                    lsqr_iters=L)
+    inf = sv.info()
+    assert inf["basis_alg"] == 1 and inf["m_eff"] == ref["m_eff"] == p.m
+    assert abs(inf["gamma_b"] - ref["gamma"]) <= 1e-13 * ref["gamma"]
+    b2 = p.b * (1 + 1e-15 * np.random.default_rng(1).standard_normal(p.n))
+    from oracle import krylov as ok
+    from oracle.srht import SRHT
+    d2 = ok.sketched_gs(p.scipy(), b2, p.m, SRHT(p.n, p.s, p.sketch_seed))
+    nH = max(1e-13, np.abs(d2["H"] - ref["H"]).max() / np.abs(ref["H"]).max())
+    nV = max(1e-13, np.abs(d2["V"] - ref["V"]).max())
+    nS = max(1e-13, np.abs(d2["S"] - ref["S"]).max())
+    H = sv.get("H")
+    assert np.abs(H - ref["H"]).max() <= 10 * nH * np.abs(ref["H"]).max()
+    assert np.abs(sv.get("SV") - ref["S"]).max() <= 10 * nS
+    V = sv.get("V")                                   # v_j = stored / beta (beta_0 = r_11)
+    assert np.abs(V - ref["V"]).max() <= 10 * nV
+    sv.compress("lsqr", iters=L)
+    y = sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()
+    assert rel(y, ref["f_m"]) <= 1e-10, rel(y, ref["f_m"])
+    r2 = ofab.alg3(p.scipy(), b2, p.m, p.s, p.sketch_seed, f=p.f, alpha=p.alpha, sigma=p.sigma, lsqr_iters=L)
+    ny = rel(r2["y"], ref["y"])                      # y is determined only to the oracle's noise (G-24)
+    assert rel(sv.get("y"), ref["y"]) <= max(1e-9, 10 * ny), (rel(sv.get("y"), ref["y"]), ny)
+    ref5 = ofab.alg3(p.scipy(), p.b, p.m, p.s, p.sketch_seed, f=p.f, alpha=p.alpha, sigma=p.sigma,
+                     mode="none")
+    # without the LS correction f(H_m) inherits H's rounding sensitivity on an
+    # Alg 1 basis: compare at 10x the oracle's own noise floor (c1: 1e-9;
+    # DESIGN.md reading R-4)
+    r5b = ofab.alg3(p.scipy(), b2, p.m, p.s, p.sketch_seed, f=p.f, alpha=p.alpha, sigma=p.sigma, mode="none")
+    n5 = rel(r5b["f_m"], ref5["f_m"])
+    sv.compress("none")
+    y5 = sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()
+    assert rel(y5, ref5["f_m"]) <= max(1e-10, 10 * n5), (rel(y5, ref5["f_m"]), n5)
+    sv.compress("blendenpik", iters=L)               # R = qr(S_m) ~ I: the same LSQR
+    yb = sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()
+    assert rel(yb, ref["f_m"]) <= 1e-9
+
+
+def test_alg3_breakdown_diagonal_exact():
+    import scipy.sparse as sp
+    import torch
+    import paper_2212_12758_b200 as fab
+    vals = np.repeat([-0.5, -1.0, -2.0, -3.0, -4.0], 40)
+    A = sp.diags(vals).tocsr()
+    b = np.random.default_rng(0).standard_normal(len(vals))
+    sv = fab.Solver(fab.Operator.csr(A.indptr, A.indices, A.data), torch.as_tensor(b).cuda(), 10, 2, 20)
+    sv.sketch(20, 1)
+    assert sv.basis_sgs(10) == 1 and sv.info()["m_eff"] == 5
+    sv.compress("lsqr", iters=10)
+    y = sv.apply("exp", 1.0, 0.0).cpu().numpy()
+    assert rel(y, np.exp(vals) * b) <= 1e-12
