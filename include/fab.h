@@ -149,7 +149,7 @@ typedef struct {
   int mode;                /* last fab_compress mode                                 */
   int lsqr_iters, lsqr_converged;
   int dense_iters;         /* DB iterations / Pade squarings of the last fab_apply   */
-  int basis_alg;           /* 2: fab_basis (Algorithm 2); 1: fab_basis_sgs (Alg 1)    */
+  int basis_alg;           /* 2: fab_basis (Alg 2); 1: fab_basis_sgs (Alg 1); 0: Arnoldi */
   double gamma_b;          /* ||b||_2                                                */
   double h_last;           /* h_{m+1,m}                                              */
   double norm_inf;         /* ||A||_inf                                              */
@@ -214,6 +214,13 @@ int fab_basis(fab_ctx* ctx, int m, int k);
    FAB_BREAKDOWN (m_eff in fab_info) when r_ii <= 1e-14 ||A||_inf (G-5).
    Errors: EORDER, EINVAL, ECUDA, ENCCL. */
 int fab_basis_sgs(fab_ctx* ctx, int m);
+
+/* Full Arnoldi (Eq. (2), l.38-48), the paper's baseline: an orthonormal
+   basis by classical Gram-Schmidt with one reorthogonalisation (three
+   streaming passes over V_i per step, O(n m^2) bytes; Table 1).
+   fab_compress(FAB_NONE) afterwards gives FOM, Eq. (4) (l.139-141).
+   Returns FAB_BREAKDOWN as fab_basis.  Errors: EINVAL, ECUDA, ENCCL. */
+int fab_basis_arnoldi(fab_ctx* ctx, int m);
 
 /* Draw the SRHT Theta (s rows, seed) of l.70: signs from the counter hash of
    G-10, rows by Floyd sampling without replacement.  It only draws Theta

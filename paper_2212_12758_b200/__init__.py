@@ -138,6 +138,12 @@ class Solver:
         self.status["basis"] = st
         return st
 
+    def basis_arnoldi(self, m):
+        """Full Arnoldi (CGS2), the paper's baseline; compress("none") = FOM."""
+        st = check(lib.fab_basis_arnoldi(self.ctx, m), "fab_basis_arnoldi")
+        self.status["basis"] = st
+        return st
+
     def sketch(self, s, seed):
         st = check(lib.fab_sketch(self.ctx, s, C.c_uint64(seed)), "fab_sketch")
         self.status["sketch"] = st

@@ -24,7 +24,7 @@ MODES = {"blendenpik": FAB_BLENDENPIK, "sketch_solve": FAB_SKETCH_SOLVE, "none":
 FUNCS = {"exp": FAB_EXP, "sqrt": FAB_SQRT, "invsqrt": FAB_INVSQRT, "poly": FAB_POLY}
 
 # every function declared in include/fab.h
-EXPORTS = ("fab_version", "fab_strerror", "fab_workspace_size", "fab_init", "fab_basis", "fab_basis_sgs",
+EXPORTS = ("fab_version", "fab_strerror", "fab_workspace_size", "fab_init", "fab_basis", "fab_basis_sgs", "fab_basis_arnoldi",
            "fab_sketch", "fab_compress", "fab_apply", "fab_get", "fab_get_column", "fab_get_vrows",
            "fab_set", "fab_last_error", "fab_destroy", "fab_comm_unique_id", "fab_comm_init",
            "fab_comm_destroy")
@@ -79,6 +79,7 @@ def load():
         "fab_init": (I, [C.POINTER(P), C.POINTER(FabOperator), P, C.POINTER(FabOpts)]),
         "fab_basis": (I, [P, I, I]),
         "fab_basis_sgs": (I, [P, I]),
+        "fab_basis_arnoldi": (I, [P, I]),
         "fab_sketch": (I, [P, I, C.c_uint64]),
         "fab_compress": (I, [P, I, C.POINTER(FabLsqrOpts)]),
         "fab_apply": (I, [P, I, D, D, P, I]),

@@ -159,6 +159,7 @@ static void free_ctx(fab_ctx* c) {
   release_long_rows(c);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->gexec_sgs) cudaGraphExecDestroy(c->gexec_sgs);
+  if (c->gexec_arn) cudaGraphExecDestroy(c->gexec_arn);
   if (c->part_dots) cudaFree(c->part_dots);
   if (c->own_ws && c->ws) cudaFree(c->ws);
   if (c->st_h) cudaFreeHost(c->st_h);
@@ -340,6 +341,37 @@ int fab_basis(fab_ctx* c, int m, int k) {
   }
   c->info.h_last = hl;
   c->info.basis_alg = 2;
+  return c->breakdown ? FAB_BREAKDOWN : FAB_OK;
+}
+
+int fab_basis_arnoldi(fab_ctx* c, int m) {
+  if (!c) return FAB_EINVAL;
+  if (m < 1 || m > c->m_max || m >= c->n_global) return FAB_EINVAL;
+  FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
+  int rc = run_basis_arnoldi(c, m);
+  if (rc != FAB_OK) return rc;
+  double ms = 0;
+  if ((rc = timed_end(c, &ms)) != FAB_OK) return rc;
+  if ((rc = pull_state(c)) != FAB_OK) return rc;
+  c->m = m;
+  c->k = m;
+  c->breakdown = c->st_h->breakdown != 0;
+  c->m_eff = c->st_h->m_eff;
+  c->basis_ready = true;
+  c->compressed = false;
+  c->sketch_in_V = false;   // a sketch, if wanted, is applied in one batched pass
+  c->info.m = m;
+  c->info.k = m;
+  c->info.m_eff = c->m_eff;
+  c->info.breakdown = c->breakdown;
+  c->info.sketch_fused = 0;
+  c->info.gamma_b = c->st_h->gamma;
+  c->info.ms_basis = ms;
+  c->info.basis_alg = 0;
+  double hl = 0;
+  if (!c->breakdown)
+    FAB_CUDA(cudaMemcpy(&hl, c->H + m + (int64_t)(m - 1) * c->ldH, sizeof(double), cudaMemcpyDeviceToHost));
+  c->info.h_last = hl;
   return c->breakdown ? FAB_BREAKDOWN : FAB_OK;
 }
 

@@ -125,6 +125,11 @@ struct fab_ctx {
   int g_sgs_m = -1, g_sgs_s = -1;
   int64_t g_sgs_launches = 0;
 
+  // cached Arnoldi (CGS2) graph
+  cudaGraphExec_t gexec_arn = nullptr;
+  int g_arn_m = -1;
+  int64_t g_arn_launches = 0;
+
   fab_info info{};
   unsigned flags = 0;
   int64_t nlaunch = 0;               // kernels launched outside the basis graph
@@ -224,6 +229,8 @@ int init_vector_norm(fab_ctx* c);            // partial norms of column 0, norm_
 int run_basis(fab_ctx* c, int m, int k);
 // sgs.cu (Algorithm 1)
 int run_basis_sgs(fab_ctx* c, int m);
+// arnoldi.cu (the paper's baseline, Eq. (2))
+int run_basis_arnoldi(fab_ctx* c, int m);
 void release_long_rows(fab_ctx* c);
 int launch_sketch_cols(fab_ctx* c, int c0, int c1, cudaStream_t st);
 // sketch.cu

@@ -302,7 +302,7 @@ static LsqrPassFn pick_pass(int m, int* jpw) {
 // t_old may alias t_new.  Tensor maps and ring depth are built on the host
 // (graph-capture safe: the map is a by-value kernel parameter).
 int launch_tall_gemv(fab_ctx* c, int ncols, const double* p, double scal, int use_state_scal,
-                     const double* t_old, double* t_new, cudaStream_t st) {
+                     const double* t_old, double* t_new, cudaStream_t st, int* nparts_out) {
   LsqrPipeFn pipe = pick_pipe(ncols);
   size_t smem = 0;
   const int ns = lsqr_pipe_stages(ncols, &smem);
@@ -316,12 +316,14 @@ int launch_tall_gemv(fab_ctx* c, int ncols, const double* p, double scal, int us
     const int G = (int)(nch < c->num_sms ? nch : c->num_sms);
     pipe<<<G, kLsPipeThreads, smem, st>>>(tm, boxc, ncopies, ncols, c->n, p, scal, t_old, t_new, c->part_g,
                                          c->part_tn, c->st_d, use_state_scal, ns);
+    if (nparts_out) *nparts_out = G;
   } else {
     int jpw = 0;
     LsqrPassFn pass = pick_pass(ncols, &jpw);
     if (!pass) return FAB_EINVAL;
     pass<<<c->grid_lsqr, kLsqrThreads, 0, st>>>(c->V, c->ld, ncols, c->n, p, scal, t_old, t_new, c->part_g,
                                                 c->part_tn, c->st_d, use_state_scal);
+    if (nparts_out) *nparts_out = c->grid_lsqr;
   }
   FAB_CHECK_LAUNCH();
   return FAB_OK;
@@ -399,6 +401,13 @@ __global__ void k_pass_reduce(const double* part_g, const double* part_tn, int n
   __shared__ double red[kWarps];
   const double tn = reduce_pass(part_g, part_tn, nparts, m, out, red);
   if (threadIdx.x == 0) out[m] = tn;
+}
+
+// host wrapper: out[0..ncols-1] = sum of the g partials, out[ncols] = ||t||^2
+int launch_pass_reduce(fab_ctx* c, int nparts, int ncols, double* out, cudaStream_t st) {
+  k_pass_reduce<<<1, kThreads, 0, st>>>(c->part_g, c->part_tn, nparts, ncols, out, c->st_d);
+  FAB_CHECK_LAUNCH();
+  return comm_allreduce(c, out, (size_t)ncols + 1, false, st);
 }
 
 // LSQR initialisation after the pass t = w_hat_m, g = W^T t:

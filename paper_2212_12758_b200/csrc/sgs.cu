@@ -116,7 +116,7 @@ __global__ void k_sgs_reset(DevState* st, int m) {
 }
 
 int launch_tall_gemv(fab_ctx* c, int ncols, const double* p, double scal, int use_state_scal,
-                     const double* t_old, double* t_new, cudaStream_t st);
+                     const double* t_old, double* t_new, cudaStream_t st, int* nparts_out);
 int enqueue_k1(fab_ctx* c, int col, int nw, double* z, bool need_z, cudaStream_t st, int64_t* launches,
                int* nparts);
 
@@ -160,7 +160,7 @@ int run_basis_sgs(fab_ctx* c, int m) {
       k_sgs_step<<<1, kThreads, 0, st>>>(col, c->s, praw, c->SV, c->H, c->ldH, c->beta, pvec, sbuf,
                                          col == m ? 1 : 0, c->st_d);                 // l.91-94
       ++launches;
-      rc = launch_tall_gemv(c, col, pvec, 0.0, 1, wcol, wcol, st);                  // l.95
+      rc = launch_tall_gemv(c, col, pvec, 0.0, 1, wcol, wcol, st, nullptr);         // l.95
       ++launches;
     }
     cudaGraph_t graph = nullptr;

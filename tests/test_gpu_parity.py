@@ -329,3 +329,33 @@ def test_alg3_breakdown_diagonal_exact():
     sv.compress("lsqr", iters=10)
     y = sv.apply("exp", 1.0, 0.0).cpu().numpy()
     assert rel(y, np.exp(vals) * b) <= 1e-12
+
+
+# ---- the paper's baseline: full Arnoldi + FOM (Eq. (2), Eq. (4)) ------------
+@pytest.mark.parametrize("name,kw,csr", [
+    ("c1", dict(m=30), False),
+    ("c3", dict(g=20, m=40, s=90), False),
+    ("c5", dict(n=4000, m=12, s=30), True),
+])
+def test_arnoldi_fom_parity(name, kw, csr):
+    import torch
+    import paper_2212_12758_b200 as fab
+    p = fp.make(name, **kw)
+    sv = fab.Solver(fab.Operator.from_problem(p, csr=csr), torch.as_tensor(p.b).cuda(), p.m, p.k, p.s)
+    sv.basis_arnoldi(p.m)
+    ref = okrylov.arnoldi(p.scipy(), p.b, p.m)
+    inf = sv.info()
+    assert inf["basis_alg"] == 0 and inf["m_eff"] == ref["m_eff"] == p.m
+    H, V = sv.get("H"), sv.get("V")
+    assert np.abs(H - ref["H"]).max() <= 1e-11 * np.abs(ref["H"]).max()
+    assert np.abs(V - ref["V"]).max() <= 1e-10
+    assert np.abs(V.T @ V - np.eye(p.m + 1)).max() <= 1e-12          # orthonormal (CGS2)
+    sv.compress("none")
+    y = sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()
+    fom = ofab.fom(p.scipy(), p.b, p.m, f=p.f, alpha=p.alpha, sigma=p.sigma)
+    assert rel(y, fom) <= 1e-10, rel(y, fom)
+    # Lemma 1 (l.151-166): Algorithm 4 with an exact LS solve equals FOM
+    sv.sketch(p.s, p.sketch_seed)
+    sv.compress("blendenpik", iters=60)
+    y4 = sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()
+    assert rel(y4, fom) <= 1e-10
