@@ -347,6 +347,21 @@ def main():
         step("blendenpik", fused=False)
         inf = step("blendenpik", fused=False)
         out["api_order_sketch_ms"] = inf["ms_sketch_batched"]
+        # the paper's basis comparison (Table 1) on
+        # the same operator: Alg 2 (the step above), Alg 1 (sketched GS, O(n m^2)
+        # bytes, one pass over V_i per step) and full Arnoldi (CGS2, three passes)
+        algs = {"alg2_truncated_k%d" % k: avg("ms_basis")}
+        sv.sketch(p.s, p.sketch_seed)
+        sv.basis_sgs(p.m)
+        algs["alg1_sketched_gs"] = sv.info()["ms_basis"]
+        sv.compress("lsqr", tol=1e-6)
+        sv.apply(p.f, p.alpha, p.sigma, out=y)
+        a3 = sv.info()
+        sv.basis_arnoldi(p.m)
+        algs["arnoldi_cgs2"] = sv.info()["ms_basis"]
+        out["basis_ms_by_algorithm"] = algs
+        out["alg3_solve_ms"] = a3["ms_basis"] + a3["ms_compress"] + a3["ms_apply"]
+        out["alg3_lsqr_iters"] = a3["lsqr_iters"]
         # e2e: b from pinned host memory, f_m back to pinned host memory, every step
         bh = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
         bh.copy_(torch.as_tensor(b_np))
