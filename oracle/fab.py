@@ -133,3 +133,19 @@ def alg3(A, b, m, s, seed, f="exp", alpha=1.0, sigma=0.0, poly=None, lsqr_tol=1e
     return dict(f_m=fm, V=V, H=H, S=dec["S"], R=dec["R"], gamma=dec["gamma"], m_eff=me,
                 breakdown=dec["breakdown"], y=y, C=C, c=cvec, lsqr=info, rows=th.rows,
                 signs=th.signs)
+
+
+def solve_whitened(A, b, m, k, s, seed, mode="blendenpik", f="exp", alpha=1.0, sigma=0.0, poly=None,
+                   cond_max=1000.0, lsqr_tol=1e-6, lsqr_iters=None):
+    """Algorithm 4 / Remark 2 / Algorithm 5 on the whitened basis (Algorithm 2
+    with whitening at cond > cond_max, then Algorithm 1; PAPER.md l.106,
+    l.395, l.457-458), f_m = gamma V_m f(C_m) e_1."""
+    th = SRHT(b.shape[0], s, seed)
+    dec = krylov.whitened_basis(A, b, m, k, th, cond_max=cond_max)
+    me = dec["m_eff"]
+    SV = th.apply(dec["V"]) if mode != "none" else None
+    y, C, R, info = compress(dec, SV, mode, lsqr_tol, lsqr_iters, None)
+    c = matfun.f_e1(f, C, alpha, sigma, poly)
+    fm = dec["gamma"] * (dec["V"][:, :me] @ c)
+    return dict(f_m=fm, V=dec["V"], H=dec["H"], SV=SV, gamma=dec["gamma"], m_eff=me,
+                breakdown=dec["breakdown"], whitened_at=dec["whitened_at"], y=y, C=C, c=c, lsqr=info)

@@ -143,3 +143,79 @@ def sketched_gs(A, b, m: int, theta, breakdown_tol: float = 1e-14):
         S[:, c] = sv / rii                                # l.94
         V[:, c] = (w - V[:, :c] @ r) / rii                # l.95
     return dict(V=V, H=R[:, 1:], S=S, R=R, gamma=r11, m_eff=m, breakdown=False)
+
+
+def cond1_upper(R):
+    """||R||_1 ||R^{-1}||_1 of an upper-triangular R (exact, by triangular
+    solves): the conditioning measure of the sketched basis (reading R-5)."""
+    from .lsq import solve_upper
+    m = R.shape[0]
+    Ri = solve_upper(R, np.eye(m))
+    return float(np.abs(R).sum(axis=0).max() * np.abs(Ri).sum(axis=0).max())
+
+
+def whitened_basis(A, b, m: int, k: int, theta, cond_max: float = 1000.0,
+                   breakdown_tol: float = 1e-14):
+    """Algorithm 2 with whitening (§5.1.3 l.395), literally:
+
+    run Algorithm 2 (truncated orthogonalisation, MGS window as printed); after
+    each new basis vector (V_i, i = 2, 3, ...) form the sketch Theta V_i and
+    its QR factor R_i (Householder, R_jj >= 0); the first time the
+    conditioning of Theta V_i exceeds cond_max (l.395: 1000; measured as
+    ||R_i||_1 ||R_i^{-1}||_1, reading R-5), whiten:
+        V_i <- V_i R_i^{-1},   underline-H_{i-1} <- R_i underline-H_{i-1} R_{i-1}^{-1}
+    and "continue the construction of the basis as in Algorithm 1, using the
+    same sketch matrix Theta" (l.106) up to V_{m+1}; then V_{m+1} satisfies
+    the Arnoldi-like relation Eq. (3) with the sketch S = Theta V orthonormal
+    from column i on.  gamma = ||b||_2 R_11 (V^+ b = gamma e_1).
+    Returns dict(V, H, gamma, m_eff, breakdown, whitened_at (i or 0))."""
+    from .lsq import householder_qr, solve_upper
+    n = b.shape[0]
+    thresh = breakdown_tol * _norm_inf(A)
+    gamma = float(np.linalg.norm(b))
+    V = np.zeros((n, m + 1))
+    H = np.zeros((m + 1, m))
+    V[:, 0] = b / gamma
+    i_w = 0
+    for i in range(2, m + 2):                                    # Algorithm 2 steps
+        c = i - 1
+        w = A @ V[:, c - 1]
+        for j in range(max(1, i - k), i):
+            H[j - 1, c - 1] = V[:, j - 1] @ w
+            w = w - H[j - 1, c - 1] * V[:, j - 1]
+        hn = float(np.linalg.norm(w))
+        H[c, c - 1] = hn
+        if hn <= thresh:
+            return dict(V=V[:, :c], H=H[: c + 1, :c], gamma=gamma, m_eff=c, breakdown=True,
+                        whitened_at=0)
+        V[:, c] = w / hn
+        if c + 1 == m + 1:
+            break                                                # V_{m+1} complete without whitening
+        R, _ = householder_qr(theta.apply(V[:, : c + 1]))       # Theta V_i = Q_i R_i, i = c+1
+        if cond1_upper(R) > cond_max:
+            i_w = c + 1
+            V[:, :i_w] = V[:, :i_w] @ solve_upper(R, np.eye(i_w))
+            Hs = H[:i_w, : i_w - 1]
+            H[:i_w, : i_w - 1] = R @ Hs @ solve_upper(R[: i_w - 1, : i_w - 1], np.eye(i_w - 1))
+            gamma = gamma * float(R[0, 0])
+            break
+    if i_w == 0:
+        return dict(V=V, H=H, gamma=gamma, m_eff=m, breakdown=False, whitened_at=0)
+    # Algorithm 1 from column i_w on (l.89-95), S = Theta V (orthonormal)
+    S = np.zeros((theta.s, m + 1))
+    S[:, :i_w] = theta.apply(V[:, :i_w])
+    for i in range(i_w + 1, m + 2):
+        c = i - 1
+        w = A @ V[:, c - 1]
+        p = theta.apply(w)
+        r = S[:, :c].T @ p
+        sv = p - S[:, :c] @ r
+        rii = float(np.linalg.norm(sv))
+        H[:c, c - 1] = r
+        H[c, c - 1] = rii
+        if rii <= thresh:
+            return dict(V=V[:, :c], H=H[: c + 1, :c], gamma=gamma, m_eff=c, breakdown=True,
+                        whitened_at=i_w)
+        S[:, c] = sv / rii
+        V[:, c] = (w - V[:, :c] @ r) / rii
+    return dict(V=V, H=H, gamma=gamma, m_eff=m, breakdown=False, whitened_at=i_w)

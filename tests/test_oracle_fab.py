@@ -200,3 +200,16 @@ def test_alg3_converges_to_dense_exp():
     r = fab.alg3(A, p.b, p.m, p.s, p.sketch_seed, f=p.f, alpha=p.alpha, lsqr_tol=1e-14)
     ref = fab.dense(A, p.b, p.f, alpha=p.alpha)
     assert np.linalg.norm(r["f_m"] - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+def test_whitened_alg4_on_graph_matches_dense_exp():
+    # whitening makes the least-squares modes well posed on a Lanczos-like
+    # problem (l.457-458); exp of the scaled graph is converged at m = 60
+    p = fp.make("c4", n=1 << 12, m=60, s=130)
+    A = p.scipy()
+    ref = fab.dense(A, p.b, p.f, alpha=p.alpha)
+    for mode in ("blendenpik", "sketch_solve", "none"):
+        r = fab.solve_whitened(A, p.b, p.m, p.k, p.s, p.sketch_seed, mode=mode, f=p.f, alpha=p.alpha,
+                               lsqr_iters=60)
+        assert r["whitened_at"] > 0
+        assert np.linalg.norm(r["f_m"] - ref) <= 1e-10 * np.linalg.norm(ref), mode

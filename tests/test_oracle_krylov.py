@@ -143,3 +143,54 @@ def test_sketched_gs_breakdown_distinct_eigenvalues():
     b = np.random.default_rng(4).standard_normal(len(vals))
     d = krylov.sketched_gs(A, b, 10, _srht(len(vals), 24, 2))
     assert d["breakdown"] and d["m_eff"] == 4
+
+
+# ---- Algorithm 2 with whitening ----------------
+def test_whitening_restores_a_well_conditioned_basis():
+    # c4 (power-law graph): the truncated basis goes numerically rank-deficient
+    # (cond ~1e15 by m = 50); whitening at cond > 1000 keeps it
+    # well-conditioned and the Arnoldi-like relation / V^+ b = gamma e_1 hold
+    p = fp.make("c4", n=1 << 13, m=60, k=2, s=130)
+    A = p.scipy()
+    th = _srht(p.n, p.s, p.sketch_seed)
+    plain = krylov.truncated_arnoldi(A, p.b, p.m, p.k, variant="mgs")
+    assert np.linalg.cond(plain["V"]) > 1e8
+    d = krylov.whitened_basis(A, p.b, p.m, p.k, th)
+    V, H = d["V"], d["H"]
+    assert 2 < d["whitened_at"] <= p.m
+    assert np.linalg.cond(V) <= 20
+    assert _arnoldi_like_residual(A, V, H) <= 1e-13
+    S = th.apply(V)
+    assert np.abs(S.T @ S - np.eye(p.m + 1)).max() <= 1e-10      # orthonormal sketch after whitening
+    coef = np.linalg.lstsq(V[:, : p.m], p.b, rcond=None)[0]
+    assert np.abs(coef - d["gamma"] * np.eye(p.m)[0]).max() <= 1e-12 * d["gamma"]
+
+
+def test_whitening_never_triggered_is_algorithm2():
+    p = fp.make("c3", g=16, m=30, k=4, s=70)
+    A = p.scipy()
+    d = krylov.whitened_basis(A, p.b, p.m, p.k, _srht(p.n, p.s, 1), cond_max=np.inf)
+    ref = krylov.truncated_arnoldi(A, p.b, p.m, p.k, variant="mgs")
+    assert d["whitened_at"] == 0
+    assert np.array_equal(d["V"], ref["V"]) and np.array_equal(d["H"], ref["H"])
+
+
+def test_whitening_at_first_check_is_algorithm1_remark():
+    # Remark after Alg 2 (l.109): Alg 1 = Alg 2 followed by whitening.  Whitening
+    # at the first check (V_2) and continuing with Alg 1 reproduces Alg 1 (the
+    # QR factor with positive diagonal is unique)
+    p = fp.make("c1", g=30, m=20, k=2, s=50)
+    A = p.scipy()
+    th = _srht(p.n, p.s, 4)
+    d = krylov.whitened_basis(A, p.b, p.m, p.k, th, cond_max=0.0)
+    ref = krylov.sketched_gs(A, p.b, p.m, th)
+    assert d["whitened_at"] == 2
+    assert np.abs(d["V"] - ref["V"]).max() <= 1e-10 * np.abs(ref["V"]).max()
+    assert np.abs(d["H"] - ref["H"]).max() <= 1e-10 * np.abs(ref["H"]).max()
+    assert abs(d["gamma"] - ref["gamma"]) <= 1e-12 * ref["gamma"]
+
+
+def test_cond1_upper_closed_form():
+    R = np.array([[2.0, 1.0], [0.0, 0.5]])
+    # ||R||_1 = 2.0 (col 0: 2, col 1: 1.5); R^-1 = [[0.5, -1], [0, 2]] -> ||.||_1 = 3
+    assert krylov.cond1_upper(R) == 6.0
