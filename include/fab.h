@@ -149,7 +149,7 @@ typedef struct {
   int mode;                /* last fab_compress mode                                 */
   int lsqr_iters, lsqr_converged;
   int dense_iters;         /* DB iterations / Pade squarings of the last fab_apply   */
-  int basis_alg;           /* 2: fab_basis (Alg 2); 1: fab_basis_sgs (Alg 1); 0: Arnoldi */
+  int basis_alg;           /* 2: Alg 2; 1: Alg 1; 0: Arnoldi; 12: Alg 2 whitened -> Alg 1 */
   double gamma_b;          /* ||b||_2                                                */
   double h_last;           /* h_{m+1,m}                                              */
   double norm_inf;         /* ||A||_inf                                              */
@@ -160,6 +160,9 @@ typedef struct {
   double ms_lsqr_pass;     /* FAB_FLAG_PROFILE: summed device time of the LSQR passes */
   int64_t lsqr_passes;     /* number of streaming passes over V_m in fab_compress     */
   double ms_sketch_batched;/* batched Theta V pass run by fab_compress (API order)    */
+  int whitened_at;         /* fab_basis_whiten: i of the whitening (0: not triggered) */
+  int pad1;
+  double whiten_cond;      /* cond_1(R_i) that triggered it                           */
 } fab_info;
 
 /* ---- multi-GPU (one process per GPU, NCCL over NVLink) ----
@@ -203,6 +206,18 @@ int fab_init(fab_ctx** ctx, const fab_operator* A, const double* b, const fab_op
    m < n).  Returns FAB_BREAKDOWN (with m_eff in fab_info) on a lucky
    breakdown.  Errors: EORDER, EINVAL, ECUDA. */
 int fab_basis(fab_ctx* ctx, int m, int k);
+
+/* Algorithm 2 with whitening (l.106-108, l.395, l.457-458): Algorithm 2
+   (truncation k, fused sketch) while monitoring Theta V_i = Q_i R_i; the
+   first time ||R_i||_1 ||R_i^{-1}||_1 > cond_max (the paper: 1000), V_i <-
+   V_i R_i^{-1}, underline-H_{i-1} <- R_i underline-H_{i-1} R_{i-1}^{-1}, and
+   the basis continues as Algorithm 1 with the same Theta.  Requires a
+   preceding fab_sketch (EORDER) with s >= m+1.  fab_info.whitened_at = i (0
+   if never triggered: then the result is fab_basis's).  One host round trip
+   per Algorithm 2 step (the switch is data dependent); the whitening is one
+   in-place pass over V_i.  Column 0 keeps b.  Errors: EORDER, EINVAL,
+   ENOMEM (scratch), ECUDA, ENCCL. */
+int fab_basis_whiten(fab_ctx* ctx, int m, int k, double cond_max);
 
 /* Algorithm 1 (l.76-100, sketched Gram-Schmidt after Balabanov & Grigori):
    the basis V_{m+1} whose sketch S = Theta V_{m+1} is orthonormal, with the

@@ -138,6 +138,12 @@ class Solver:
         self.status["basis"] = st
         return st
 
+    def basis_whiten(self, m, k, cond_max=1000.0):
+        """Algorithm 2 with whitening at cond > cond_max, then Algorithm 1."""
+        st = check(lib.fab_basis_whiten(self.ctx, m, k, float(cond_max)), "fab_basis_whiten")
+        self.status["basis"] = st
+        return st
+
     def basis_arnoldi(self, m):
         """Full Arnoldi (CGS2), the paper's baseline; compress("none") = FOM."""
         st = check(lib.fab_basis_arnoldi(self.ctx, m), "fab_basis_arnoldi")

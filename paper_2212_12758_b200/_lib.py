@@ -24,7 +24,7 @@ MODES = {"blendenpik": FAB_BLENDENPIK, "sketch_solve": FAB_SKETCH_SOLVE, "none":
 FUNCS = {"exp": FAB_EXP, "sqrt": FAB_SQRT, "invsqrt": FAB_INVSQRT, "poly": FAB_POLY}
 
 # every function declared in include/fab.h
-EXPORTS = ("fab_version", "fab_strerror", "fab_workspace_size", "fab_init", "fab_basis", "fab_basis_sgs", "fab_basis_arnoldi",
+EXPORTS = ("fab_version", "fab_strerror", "fab_workspace_size", "fab_init", "fab_basis", "fab_basis_sgs", "fab_basis_arnoldi", "fab_basis_whiten",
            "fab_sketch", "fab_compress", "fab_apply", "fab_get", "fab_get_column", "fab_get_vrows",
            "fab_set", "fab_last_error", "fab_destroy", "fab_comm_unique_id", "fab_comm_init",
            "fab_comm_destroy")
@@ -59,10 +59,11 @@ class FabInfo(C.Structure):
                 ("ms_apply", C.c_double), ("launches_basis", C.c_int64),
                 ("launches_sketch", C.c_int64), ("launches_compress", C.c_int64),
                 ("launches_apply", C.c_int64), ("ms_lsqr_pass", C.c_double),
-                ("lsqr_passes", C.c_int64), ("ms_sketch_batched", C.c_double)]
+                ("lsqr_passes", C.c_int64), ("ms_sketch_batched", C.c_double),
+                ("whitened_at", C.c_int), ("pad1", C.c_int), ("whiten_cond", C.c_double)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad1"}
 
 
 def load():
@@ -80,6 +81,7 @@ def load():
         "fab_basis": (I, [P, I, I]),
         "fab_basis_sgs": (I, [P, I]),
         "fab_basis_arnoldi": (I, [P, I]),
+        "fab_basis_whiten": (I, [P, I, I, D]),
         "fab_sketch": (I, [P, I, C.c_uint64]),
         "fab_compress": (I, [P, I, C.POINTER(FabLsqrOpts)]),
         "fab_apply": (I, [P, I, D, D, P, I]),

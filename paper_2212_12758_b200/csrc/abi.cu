@@ -160,6 +160,7 @@ static void free_ctx(fab_ctx* c) {
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->gexec_sgs) cudaGraphExecDestroy(c->gexec_sgs);
   if (c->gexec_arn) cudaGraphExecDestroy(c->gexec_arn);
+  if (c->wbuf) cudaFree(c->wbuf);
   if (c->part_dots) cudaFree(c->part_dots);
   if (c->own_ws && c->ws) cudaFree(c->ws);
   if (c->st_h) cudaFreeHost(c->st_h);
@@ -368,6 +369,43 @@ int fab_basis_arnoldi(fab_ctx* c, int m) {
   c->info.gamma_b = c->st_h->gamma;
   c->info.ms_basis = ms;
   c->info.basis_alg = 0;
+  double hl = 0;
+  if (!c->breakdown)
+    FAB_CUDA(cudaMemcpy(&hl, c->H + m + (int64_t)(m - 1) * c->ldH, sizeof(double), cudaMemcpyDeviceToHost));
+  c->info.h_last = hl;
+  return c->breakdown ? FAB_BREAKDOWN : FAB_OK;
+}
+
+int fab_basis_whiten(fab_ctx* c, int m, int k, double cond_max) {
+  if (!c) return FAB_EINVAL;
+  if (!c->sketch_ready) return FAB_EORDER;   // the monitor and Algorithm 1 need Theta
+  if (k < 1 || k > c->k_max || m < 1 || m > c->m_max || m >= c->n_global || c->s < m + 1) return FAB_EINVAL;
+  if (!(cond_max >= 0.0)) return FAB_EINVAL;
+  FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
+  int iw = 0;
+  double cond = 0.0;
+  int rc = run_basis_whiten(c, m, k, cond_max, &iw, &cond);
+  if (rc != FAB_OK) return rc;
+  double ms = 0;
+  if ((rc = timed_end(c, &ms)) != FAB_OK) return rc;
+  if ((rc = pull_state(c)) != FAB_OK) return rc;
+  c->m = m;
+  c->k = k;
+  c->breakdown = c->st_h->breakdown != 0;
+  c->m_eff = c->st_h->m_eff;
+  c->basis_ready = true;
+  c->compressed = false;
+  c->sketch_in_V = true;
+  c->info.m = m;
+  c->info.k = k;
+  c->info.m_eff = c->m_eff;
+  c->info.breakdown = c->breakdown;
+  c->info.sketch_fused = 1;
+  c->info.gamma_b = c->st_h->gamma;
+  c->info.ms_basis = ms;
+  c->info.basis_alg = iw ? 12 : 2;
+  c->info.whitened_at = iw;
+  c->info.whiten_cond = cond;
   double hl = 0;
   if (!c->breakdown)
     FAB_CUDA(cudaMemcpy(&hl, c->H + m + (int64_t)(m - 1) * c->ldH, sizeof(double), cudaMemcpyDeviceToHost));

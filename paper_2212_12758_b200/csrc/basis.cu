@@ -962,8 +962,8 @@ int init_vector_norm(fab_ctx* c) {
 
 
 // K2 (+ C2 on several GPUs): the step scalars of column col-1
-static int enqueue_scalar(fab_ctx* c, int col, int nw, int nparts, int final_step, cudaStream_t st,
-                          int64_t* launches) {
+int enqueue_scalar(fab_ctx* c, int col, int nw, int nparts, int final_step, cudaStream_t st,
+                   int64_t* launches) {
   const double* sums = nullptr;
   if (c->comm) {
     k_step_reduce<<<1, kThreads, 0, st>>>(nw, nparts, c->grid_upd, c->part_dots, c->part_norm, c->red, c->st_d);
@@ -1045,45 +1045,48 @@ int enqueue_k1(fab_ctx* c, int col, int nw, double* z, bool need_z, cudaStream_t
   return FAB_OK;
 }
 
+// K3 of step col: w_hat_col from z and the window, its norm partials and
+// (fused) its sketch partials
+int enqueue_k3(fab_ctx* c, int col, int nw, bool fused, cudaStream_t st, int64_t* launches) {
+  PipeArgs a{};
+  a.V = c->V;
+  a.ld = c->ld;
+  a.col0 = col;
+  a.col1 = col + 1;
+  a.nw = nw;
+  a.coef = c->coef;
+  a.z = c->vec;
+  a.n = c->n;
+  a.row_begin = c->row_begin;
+  a.part_norm = c->part_norm;
+  a.signs = c->signs_d;
+  a.rows = c->rows_d;
+  a.s = c->s;
+  a.part_sk = c->part_sk;
+  a.st = c->st_d;
+  int rc;
+  if (c->mf) {
+    a.sp = stencil_params(c);
+    a.hal = c->hal;
+    a.apron = 16;
+    if (c->op.dims[2] > 1)
+      rc = fused ? launch_stream<true, true, 3>(c, a, st) : launch_stream<true, false, 3>(c, a, st);
+    else
+      rc = fused ? launch_stream<true, true, 2>(c, a, st) : launch_stream<true, false, 2>(c, a, st);
+  } else {
+    rc = fused ? launch_stream<true, true, 0>(c, a, st) : launch_stream<true, false, 0>(c, a, st);
+  }
+  ++*launches;
+  return rc;
+}
+
 // Enqueue one Krylov step c (1..m) on stream st.
 static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st, int64_t* launches) {
   const int nw = col < k ? col : k;
   int nparts = 0;
   FAB_TRY(enqueue_k1(c, col, nw, c->vec, false, st, launches, &nparts));
-  int rc = enqueue_scalar(c, col, nw, nparts, 0, st, launches);
-  if (rc != FAB_OK) return rc;
-  {
-    PipeArgs a{};
-    a.V = c->V;
-    a.ld = c->ld;
-    a.col0 = col;
-    a.col1 = col + 1;
-    a.nw = nw;
-    a.coef = c->coef;
-    a.z = c->vec;
-    a.n = c->n;
-    a.row_begin = c->row_begin;
-    a.part_norm = c->part_norm;
-    a.signs = c->signs_d;
-    a.rows = c->rows_d;
-    a.s = c->s;
-    a.part_sk = c->part_sk;
-    a.st = c->st_d;
-    if (c->mf) {
-      a.sp = stencil_params(c);
-      a.hal = c->hal;
-      a.apron = 16;
-      if (c->op.dims[2] > 1)
-        rc = fused ? launch_stream<true, true, 3>(c, a, st) : launch_stream<true, false, 3>(c, a, st);
-      else
-        rc = fused ? launch_stream<true, true, 2>(c, a, st) : launch_stream<true, false, 2>(c, a, st);
-    } else {
-      rc = fused ? launch_stream<true, true, 0>(c, a, st) : launch_stream<true, false, 0>(c, a, st);
-    }
-    if (rc != FAB_OK) return rc;
-  }
-  ++*launches;
-  return FAB_OK;
+  FAB_TRY(enqueue_scalar(c, col, nw, nparts, 0, st, launches));
+  return enqueue_k3(c, col, nw, fused, st, launches);
 }
 
 // K5 / column 0: sketch partials of columns [c0, c1) (no writes)
@@ -1103,6 +1106,23 @@ int launch_sketch_cols(fab_ctx* c, int c0, int c1, cudaStream_t st) {
   return launch_stream<false, true, 0>(c, a, st);
 }
 
+// Before step 1 of Algorithm 2: reset the device state, zero underline-H
+// (banded: everything outside the band must read as 0), norm partials of
+// column 0 (= b) for the first lagged norm, and (fused) its sketch partials.
+int enqueue_basis_prologue(fab_ctx* c, int m, bool fused, cudaStream_t st, int64_t* launches) {
+  k_reset_basis<<<1, 1, 0, st>>>(c->st_d, m);
+  ++*launches;
+  FAB_CUDA(cudaMemsetAsync(c->H, 0, (size_t)c->ldH * m * sizeof(double), st));
+  k_norm_partial<<<c->grid_upd, kThreads, 0, st>>>(c->V, c->n, c->row_begin, c->part_norm);
+  FAB_CHECK_LAUNCH();
+  ++*launches;
+  if (fused) {
+    FAB_TRY(launch_sketch_cols(c, 0, 1, st));
+    ++*launches;
+  }
+  return FAB_OK;
+}
+
 int run_basis(fab_ctx* c, int m, int k) {
   const bool fused = c->sketch_ready;
   if (!(c->gexec && c->g_m == m && c->g_k == k && c->g_fused == fused && (!fused || c->g_s == c->s))) {
@@ -1112,18 +1132,7 @@ int run_basis(fab_ctx* c, int m, int k) {
     }
     int64_t launches = 0;
     FAB_CUDA(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
-    int rc = FAB_OK;
-    k_reset_basis<<<1, 1, 0, c->cap>>>(c->st_d, m);
-    ++launches;
-    // underline-H is banded: everything outside the band must read as 0
-    FAB_CUDA(cudaMemsetAsync(c->H, 0, (size_t)c->ldH * m * sizeof(double), c->cap));
-    // norm partials of column 0 (= b) for the first lagged norm
-    k_norm_partial<<<c->grid_upd, kThreads, 0, c->cap>>>(c->V, c->n, c->row_begin, c->part_norm);
-    ++launches;
-    if (fused) {
-      rc = launch_sketch_cols(c, 0, 1, c->cap);
-      ++launches;
-    }
+    int rc = enqueue_basis_prologue(c, m, fused, c->cap, &launches);
     for (int col = 1; col <= m && rc == FAB_OK; ++col) rc = enqueue_step(c, col, k, fused, c->cap, &launches);
     if (rc == FAB_OK) {
       // final lagged norm: beta_m = h_{m+1,m}; breakdown test of the last step

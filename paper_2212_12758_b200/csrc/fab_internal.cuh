@@ -117,6 +117,7 @@ struct fab_ctx {
   bool g_fused = false;
   int64_t g_launches = 0;
 
+  double* wbuf = nullptr;             // whitening scratch (Q, R, R^-1), allocated on first use
   fab::Comm* comm = nullptr;          // NULL: one GPU
   std::vector<int64_t> rank_rows;     // row_begin of every rank, plus n_global
 
@@ -231,6 +232,8 @@ int run_basis(fab_ctx* c, int m, int k);
 int run_basis_sgs(fab_ctx* c, int m);
 // arnoldi.cu (the paper's baseline, Eq. (2))
 int run_basis_arnoldi(fab_ctx* c, int m);
+// whiten.cu (Algorithm 2 + whitening -> Algorithm 1)
+int run_basis_whiten(fab_ctx* c, int m, int k, double cond_max, int* whitened_at, double* cond_at);
 void release_long_rows(fab_ctx* c);
 int launch_sketch_cols(fab_ctx* c, int c0, int c1, cudaStream_t st);
 // sketch.cu

@@ -120,14 +120,37 @@ int launch_tall_gemv(fab_ctx* c, int ncols, const double* p, double scal, int us
 int enqueue_k1(fab_ctx* c, int col, int nw, double* z, bool need_z, cudaStream_t st, int64_t* launches,
                int* nparts);
 
-static int enqueue_col_sketch(fab_ctx* c, int col, double* p, cudaStream_t st, int64_t* launches) {
-  FAB_TRY(launch_sketch_cols(c, col, col + 1, st));
-  ++*launches;
+// p = Theta w_hat_col from its sketch partials (already in part_sk), C3 on several GPUs
+int enqueue_col_sketch_reduce(fab_ctx* c, int col, double* p, cudaStream_t st, int64_t* launches) {
   k_sketch_col_raw<<<(c->s + kThreads - 1) / kThreads, kThreads, 0, st>>>(c->part_sk, c->grid_upd, c->s, col,
                                                                           p, c->st_d);
   FAB_CHECK_LAUNCH();
   ++*launches;
-  return comm_allreduce(c, p, (size_t)c->s, false, st);   // C3 for one column
+  return comm_allreduce(c, p, (size_t)c->s, false, st);
+}
+
+int enqueue_col_sketch(fab_ctx* c, int col, double* p, cudaStream_t st, int64_t* launches) {
+  FAB_TRY(launch_sketch_cols(c, col, col + 1, st));
+  ++*launches;
+  return enqueue_col_sketch_reduce(c, col, p, st, launches);
+}
+
+// One step of Algorithm 1 producing column col (l.89-95)
+int enqueue_sgs_column(fab_ctx* c, int col, int m, cudaStream_t st, int64_t* launches) {
+  double* praw = svec(c, 20);   // p = Theta w (s <= 768 < kSmall)
+  double* sbuf = svec(c, 21);
+  double* pvec = svec(c, 22);
+  double* wcol = c->V + (int64_t)col * c->ld;
+  int nparts = 0;
+  FAB_TRY(enqueue_k1(c, col, 1, wcol, true, st, launches, &nparts));                 // l.89
+  FAB_TRY(enqueue_col_sketch(c, col, praw, st, launches));                          // l.90
+  k_sgs_step<<<1, kThreads, 0, st>>>(col, c->s, praw, c->SV, c->H, c->ldH, c->beta, pvec, sbuf,
+                                     col == m ? 1 : 0, c->st_d);                     // l.91-94
+  FAB_CHECK_LAUNCH();
+  ++*launches;
+  FAB_TRY(launch_tall_gemv(c, col, pvec, 0.0, 1, wcol, wcol, st, nullptr));          // l.95
+  ++*launches;
+  return FAB_OK;
 }
 
 int run_basis_sgs(fab_ctx* c, int m) {
@@ -136,9 +159,7 @@ int run_basis_sgs(fab_ctx* c, int m) {
       cudaGraphExecDestroy(c->gexec_sgs);
       c->gexec_sgs = nullptr;
     }
-    double* praw = svec(c, 20);   // p = Theta w (s <= 768 < kSmall)
-    double* sbuf = svec(c, 21);
-    double* pvec = svec(c, 22);
+    double* praw = svec(c, 20);
     int64_t launches = 0;
     cudaStream_t st = c->cap;
     FAB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
@@ -151,18 +172,7 @@ int run_basis_sgs(fab_ctx* c, int m) {
       k_sgs_first<<<1, kThreads, 0, st>>>(praw, c->s, c->m_max, c->SV, c->beta, c->st_d);
       ++launches;
     }
-    for (int col = 1; col <= m && rc == FAB_OK; ++col) {
-      double* wcol = c->V + (int64_t)col * c->ld;
-      int nparts = 0;
-      rc = enqueue_k1(c, col, 1, wcol, true, st, &launches, &nparts);                 // l.89
-      if (rc == FAB_OK) rc = enqueue_col_sketch(c, col, praw, st, &launches);       // l.90
-      if (rc != FAB_OK) break;
-      k_sgs_step<<<1, kThreads, 0, st>>>(col, c->s, praw, c->SV, c->H, c->ldH, c->beta, pvec, sbuf,
-                                         col == m ? 1 : 0, c->st_d);                 // l.91-94
-      ++launches;
-      rc = launch_tall_gemv(c, col, pvec, 0.0, 1, wcol, wcol, st, nullptr);         // l.95
-      ++launches;
-    }
+    for (int col = 1; col <= m && rc == FAB_OK; ++col) rc = enqueue_sgs_column(c, col, m, st, &launches);
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(st, &graph);
     if (rc != FAB_OK) {
