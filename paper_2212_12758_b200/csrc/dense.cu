@@ -341,9 +341,161 @@ k_gj_coop(double* A, double* B, int m, int nrhs, double* out) {
   }
 }
 
+// Gauss-Jordan with partial pivoting on ONE thread-block cluster of kGjCl
+// CTAs: the columns of [A | B] are dealt round-robin to the CTAs and live in
+// their shared memory for the whole elimination (m <= ~330: 2m/8 columns of
+// m doubles per CTA).  Pivot step k: the owner of column k searches the
+// pivot and publishes the column in a double-buffered broadcast slot; ONE
+// cluster barrier; every CTA reads it through distributed shared memory and
+// updates its own columns.  No global-memory traffic and no grid-wide
+// barrier inside the elimination (the cooperative k_gj_coop pays one grid
+// sync and a global round trip per pivot).  Same arithmetic per element as
+// k_gj_coop (swap rows k, p and eliminate), same tie rule for the pivot.
+constexpr int kGjCl = 8;
+constexpr int kGjClMaxM = 330;
+
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_gj_cluster(const double* __restrict__ A, double* B, int m,
+                                                            int nrhs, double* out) {
+  namespace cgx = cooperative_groups;
+  cgx::cluster_group cl = cgx::this_cluster();
+  extern __shared__ double sm[];
+  const int q = (int)cl.block_rank();
+  const int ntot = m + nrhs;
+  const int nloc = (ntot - q + kGjCl - 1) / kGjCl;   // columns j = q + kGjCl * l
+  const int nmax = (ntot + kGjCl - 1) / kGjCl;       // same layout in every CTA (DSMEM offsets)
+  double* cols = sm;                                 // [nmax][m]
+  double* bc = cols + (size_t)nmax * m;              // [2][m + 2]: column, then pivot index
+  double* pc = bc + 2 * (m + 2);                     // local copy of the broadcast column
+  __shared__ double red_log[kWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int l = 0; l < nloc; ++l) {
+    const int j = q + kGjCl * l;
+    const double* src = j < m ? A + (int64_t)j * m : B + (int64_t)(j - m) * m;
+    for (int i = tid; i < m; i += blockDim.x) cols[(size_t)l * m + i] = src[i];
+  }
+  double logdet = 0.0;
+  int singular = 0;
+  __syncthreads();
+  cluster_barrier();
+  for (int k = 0; k < m; ++k) {
+    const int owner = k % kGjCl, lk = k / kGjCl;
+    double* slot = bc + (size_t)(k & 1) * (m + 2);
+    if (q == owner && warp == 0) {
+      const double* ck = cols + (size_t)lk * m;
+      double best = -1.0;
+      int bi = m;
+      for (int i = k + lane; i < m; i += 32) {
+        const double a = fabs(ck[i]);
+        if (a > best) {
+          best = a;
+          bi = i;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      for (int i = lane; i < m; i += 32) slot[i] = ck[i];
+      if (lane == 0) slot[m] = (double)bi;
+    }
+    cluster_barrier();
+    const double* rs = cl.map_shared_rank(slot, owner);
+    for (int i = tid; i <= m; i += blockDim.x) pc[i] = rs[i];
+    __syncthreads();
+    const int p = (int)pc[m];
+    const double piv = pc[p], ckk = pc[k];
+    if (!(fabs(piv) > 0.0)) singular = 1;
+    if (q == owner && tid == 0) logdet += log(fabs(piv));
+    const double ipiv = 1.0 / piv;
+    // columns j > k of A and every column of B (j >= m)
+    for (int l = warp; l < nloc; l += kWarps) {
+      const int j = q + kGjCl * l;
+      if (j <= k) continue;
+      double* col = cols + (size_t)l * m;
+      const double ap = col[p], ak = col[k];
+      const double rr = ap * ipiv;
+      __syncwarp();
+      for (int i = lane; i < m; i += 32) {
+        double nv;
+        if (i == k)
+          nv = rr;
+        else if (i == p)
+          nv = fma(-ckk, rr, ak);
+        else
+          nv = fma(-pc[i], rr, col[i]);
+        col[i] = nv;
+      }
+    }
+    __syncthreads();
+  }
+  for (int l = 0; l < nloc; ++l) {
+    const int j = q + kGjCl * l;
+    if (j < m) continue;
+    double* dst = B + (int64_t)(j - m) * m;
+    for (int i = tid; i < m; i += blockDim.x) dst[i] = cols[(size_t)l * m + i];
+  }
+  // log|det| and the singular flag: per-CTA (owner) sums, reduced on rank 0
+  if (tid == 0) {
+    pc[0] = logdet;
+    pc[1] = singular ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  cluster_barrier();
+  if (q == 0 && tid == 0) {
+    double lsum = 0.0, sg = 0.0;
+    for (int r = 0; r < kGjCl; ++r) {
+      const double* o = cl.map_shared_rank(pc, r);
+      lsum += o[0];
+      sg = fmax(sg, o[1]);
+    }
+    out[0] = lsum;
+    out[1] = sg;
+  }
+  cluster_barrier();   // keep every CTA's shared memory alive until rank 0 has read it
+  (void)red_log;
+}
+
+static size_t gj_cluster_smem(int m, int nrhs) {
+  const int nloc = (m + nrhs + kGjCl - 1) / kGjCl;
+  return ((size_t)nloc * m + 3 * ((size_t)m + 2)) * sizeof(double);
+}
+
 // solve A X = B; A is copied to a scratch so the input survives
 static int gj_solve(fab_ctx* c, int m, const double* A, double* Awork, double* B, int nrhs, double* out,
                     cudaStream_t st) {
+  const size_t smem = gj_cluster_smem(m, nrhs);
+  if (m <= kGjClMaxM && smem <= 226 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      FAB_CUDA(set_max_dyn_smem((const void*)k_gj_cluster, 226 * 1024));
+      attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kGjCl, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kGjCl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    FAB_CUDA(cudaLaunchKernelEx(&cfg, k_gj_cluster, A, B, m, nrhs, out));
+    ++c->nlaunch;
+    return FAB_OK;
+  }
   FAB_CUDA(cudaMemcpyAsync(Awork, A, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
   int mm = m, nr = nrhs;
   void* args[] = {&Awork, &B, &mm, &nr, &out};
