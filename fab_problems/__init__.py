@@ -23,6 +23,21 @@ G-23, G-25, G-26, G-27):
 * c5: nonsymmetric random sparse, 16 distinct uniform columns per row,
   values N(0,1)/4, diagonal shifted by -5.  Stand-in for the nonnormal
   examples.
+
+The paper's own experiments that need no dataset:
+
+* e1: the variable-coefficient convection-diffusion operator of PAPER.md
+  l.366-374 (Pe = 200, D1 = 1000 on [1/4,3/4]^2 else 1, D2 = D1/2,
+  v = (x+y, x-y), skew-symmetric convection form) on a 352 x 352 grid,
+  b = sin(pi x) sin(pi y) normalized, f = exp(-t A) with t = 1e3/||A||_inf
+  (reading G-30).  CSR (variable coefficients).
+* e4: stand-in for the sign-function example (bfw782a, not
+  available): nonsymmetric random sparse as c5 but with the diagonal shift
+  +-5 by a seeded Rademacher sign per row (spectrum in both half planes),
+  b a random unit vector, f = sign via (A^2)^{-1/2} (A b).
+* e5: the 3D Laplacian of PAPER.md l.417-421, T_N (x) I (x) I + I (x) T_N (x) I
+  + I (x) I (x) T_N, T_N = tridiag(-1, 2, -1) (G-28), N = 80, f = invsqrt,
+  b a random unit vector, sketch s = floor(1.05 m) (l.421).
 """
 from __future__ import annotations
 
@@ -45,7 +60,7 @@ class Problem:
     n: int
     kind: str                      # "stencil" | "csr"
     b: np.ndarray
-    f: str                         # "exp" | "sqrt" | "invsqrt"
+    f: str                         # "exp" | "sqrt" | "invsqrt" | "sign"
     alpha: float
     sigma: float
     m: int
@@ -210,11 +225,12 @@ def lanczos_lambda_max(indptr, indices, data, n, steps=64):
     return float(ev[-1])
 
 
-def random_sparse(n: int, seed: int, per_row: int = 16, shift: float = -5.0,
+def random_sparse(n: int, seed: int, per_row: int = 16, shift=-5.0,
                   scale: float = 0.25):
     """Nonsymmetric random sparse matrix (G-26): per row `per_row` distinct
     uniform columns with N(0,1)*scale values, plus `shift` on the diagonal
-    (merged into an existing diagonal entry when one was drawn)."""
+    (merged into an existing diagonal entry when one was drawn).  `shift`
+    is a scalar or a per-row array (e4)."""
     rng = np.random.default_rng(seed)
     per_row = min(per_row, n)
     cols = rng.integers(0, n, size=(n, per_row), dtype=np.int64)
@@ -230,9 +246,10 @@ def random_sparse(n: int, seed: int, per_row: int = 16, shift: float = -5.0,
     r = np.arange(n, dtype=np.int64)
     is_diag = cols == r[:, None]
     has_diag = is_diag.any(axis=1)
-    vals[is_diag] += shift
+    shift_r = np.broadcast_to(np.asarray(shift, dtype=np.float64), (n,))
+    vals[is_diag] += np.broadcast_to(shift_r[:, None], vals.shape)[is_diag]
     extra_col = np.where(has_diag, n, r)            # n = sentinel (dropped)
-    extra_val = np.where(has_diag, 0.0, shift)
+    extra_val = np.where(has_diag, 0.0, shift_r)
     cols = np.concatenate([cols, extra_col[:, None]], axis=1)
     vals = np.concatenate([vals, extra_val[:, None]], axis=1)
     order = np.argsort(cols, axis=1, kind="stable")
@@ -242,6 +259,49 @@ def random_sparse(n: int, seed: int, per_row: int = 16, shift: float = -5.0,
     counts = mask.sum(axis=1)
     indptr = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(counts, out=indptr[1:])
+    return indptr, cols[mask].astype(np.int32), vals[mask].astype(np.float64)
+
+
+def convdiff_var(g: int, pe: float = 200.0):
+    """CSR of the variable-coefficient convection-diffusion operator of
+    PAPER.md l.366-374 on the unit square, g x g interior points, h = 1/(g+1),
+    homogeneous Dirichlet, x fastest:
+      L[u] = -(D1 u_x)_x - (D2 u_y)_y + Pe (1/2 (v1 u_x + v2 u_y)
+             + 1/2 ((v1 u)_x + (v2 u)_y)),
+      D1 = 1000 on [1/4, 3/4]^2 else 1, D2 = D1/2, v1 = x+y, v2 = x-y.
+    Second-order finite differences (reading G-31): the diffusion flux with
+    D at the cell faces (x +- h/2), both convection terms by central
+    differences."""
+    h = 1.0 / (g + 1)
+    n = g * g
+    r = np.arange(n, dtype=np.int64)
+    ix = r % g
+    iy = r // g
+    x = (ix + 1) * h
+    y = (iy + 1) * h
+
+    def d1(px, py):
+        inside = (px >= 0.25) & (px <= 0.75) & (py >= 0.25) & (py <= 0.75)
+        return np.where(inside, 1000.0, 1.0)
+
+    dxm, dxp = d1(x - h / 2, y), d1(x + h / 2, y)
+    dym, dyp = 0.5 * d1(x, y - h / 2), 0.5 * d1(x, y + h / 2)
+    v1 = lambda px, py: px + py          # noqa: E731
+    v2 = lambda px, py: px - py          # noqa: E731
+    h2, c2 = h * h, pe / (4.0 * h)
+    # u_x ~ (u_{i+1} - u_{i-1}) / 2h;  (v1 u)_x ~ (v1_{i+1} u_{i+1} - v1_{i-1} u_{i-1}) / 2h
+    cxm = -dxm / h2 - c2 * (v1(x, y) + v1(x - h, y))
+    cxp = -dxp / h2 + c2 * (v1(x, y) + v1(x + h, y))
+    cym = -dym / h2 - c2 * (v2(x, y) + v2(x, y - h))
+    cyp = -dyp / h2 + c2 * (v2(x, y) + v2(x, y + h))
+    cc = (dxm + dxp + dym + dyp) / h2
+    slots = [(-g, cym, iy > 0), (-1, cxm, ix > 0), (0, cc, np.ones(n, dtype=bool)),
+             (1, cxp, ix < g - 1), (g, cyp, iy < g - 1)]
+    cols = np.stack([r + off for off, _, _ in slots], axis=1)
+    vals = np.stack([v for _, v, _ in slots], axis=1)
+    mask = np.stack([mk for _, _, mk in slots], axis=1)
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(mask.sum(axis=1), out=indptr[1:])
     return indptr, cols[mask].astype(np.int32), vals[mask].astype(np.float64)
 
 
@@ -269,6 +329,10 @@ CONFIGS = {
     "c3": dict(g=256, m=200, k=4, s=400),
     "c4": dict(n=1 << 22, m=150, k=2, s=300),
     "c5": dict(n=1 << 25, m=300, k=2, s=600),
+    # the paper's dataset-free experiments (defaults: one point of the m sweep)
+    "e1": dict(g=352, m=60, k=2, s=120),
+    "e4": dict(n=1 << 20, m=40, k=2, s=80),
+    "e5": dict(g=80, m=100, k=2, s=None),
 }
 
 
@@ -280,9 +344,36 @@ def make(name: str, **over) -> Problem:
         raise KeyError(name)
     p = dict(CONFIGS[name])
     p.update(over)
-    idx = int(name[1])
+    idx = int(name[1]) + (10 if name[0] == "e" else 0)
     mseed, bseed, sseed = 1000 + idx, 2000 + idx, 3000 + idx
     m, k, s = p["m"], p["k"], p["s"]
+    if name == "e5" and s is None:
+        s = int(math.floor(1.05 * m))               # l.421
+    if name == "e1":
+        g = p["g"]
+        ip, ix, dv = convdiff_var(g)
+        ninf = csr_norm_inf(ip, dv)
+        t = 1e3 / ninf                               # G-30
+        hh = 1.0 / (g + 1)
+        xs = np.sin(np.pi * hh * np.arange(1, g + 1))
+        b = np.outer(xs, xs).ravel()                 # sin(pi x) sin(pi y), x fastest (symmetric)
+        b /= np.linalg.norm(b)
+        return Problem(name, g * g, "csr", b, "exp", -t, 0.0, m, k, s, sseed, ninf, _csr=(ip, ix, dv),
+                       meta=dict(g=g, t=t, nnz=int(ip[-1])))
+    if name == "e4":
+        n = p["n"]
+        sg = np.where(np.random.default_rng(mseed + 500).random(n) < 0.5, -5.0, 5.0)
+        ip, ix, dv = random_sparse(n, mseed, shift=sg)
+        b = gaussian_b(n, bseed, normalize=True)
+        return Problem(name, n, "csr", b, "sign", 1.0, 0.0, m, k, s, sseed, csr_norm_inf(ip, dv),
+                       _csr=(ip, ix, dv), meta=dict(nnz=int(ip[-1])))
+    if name == "e5":
+        g = p["g"]
+        c = (6.0, -1.0, -1.0, -1.0, -1.0, -1.0, -1.0)
+        n = g ** 3
+        b = gaussian_b(n, bseed, normalize=True)
+        return Problem(name, n, "stencil", b, "invsqrt", 1.0, 0.0, m, k, s, sseed, 12.0,
+                       dims=(g, g, g), coeffs=c, meta=dict(g=g, dim=3))
     if name in ("c1", "c2"):
         g = p["g"]
         scale_to = None if p.get("unscaled") else 1e3

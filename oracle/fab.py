@@ -10,6 +10,8 @@
   sfom   the literal Eq. (9) formula (cross-check of `ss`)
   fom    Eq. (4) with a full Arnoldi basis (the paper's baseline 'Arnoldi')
   dense  f(A) b formed densely (small n only)
+  sign   sign(A) b by the formula of l.406, (A^2)^{-1/2} (A b): any of the
+         above on the operator A^2 with the start vector A b, f = invsqrt
 
 Compression (Eq. (6), l.167-171): V_m^+ A V_m = H_m + h_{m+1,m} (V_m^+ v_{m+1})
 e_m^T, gamma_b = ||b||_2 for Alg 2 (l.172).  f is applied as
@@ -149,3 +151,22 @@ def solve_whitened(A, b, m, k, s, seed, mode="blendenpik", f="exp", alpha=1.0, s
     fm = dec["gamma"] * (dec["V"][:, :me] @ c)
     return dict(f_m=fm, V=dec["V"], H=dec["H"], SV=SV, gamma=dec["gamma"], m_eff=me,
                 breakdown=dec["breakdown"], whitened_at=dec["whitened_at"], y=y, C=C, c=c, lsqr=info)
+
+
+def sign(A, b, m, k, s, seed, mode="blendenpik", whiten=False, cond_max=1000.0, lsqr_tol=1e-6,
+         lsqr_iters=None, keep=True):
+    """sign(A) b ("to apply the sign function to a vector we
+    use the formula f(A)b = (A^2)^{-1/2} (Ab)", Higham 2008 Ch. 5): the
+    method -- Algorithm 4 / Remark 2 / Algorithm 5 on the Algorithm 2 basis,
+    or on the whitened basis (l.395-406: the paper's sign example needs
+    whitening) -- applied to the operator A^2 (formed as a sparse product)
+    and the vector A b, with f = invsqrt (alpha = 1, sigma = 0)."""
+    A2 = A @ A
+    if hasattr(A2, "tocsr"):
+        A2 = A2.tocsr()
+    Ab = A @ b
+    if whiten:
+        return solve_whitened(A2, Ab, m, k, s, seed, mode=mode, f="invsqrt", cond_max=cond_max,
+                              lsqr_tol=lsqr_tol, lsqr_iters=lsqr_iters)
+    return solve(A2, Ab, m, k, s, seed, mode=mode, f="invsqrt", lsqr_tol=lsqr_tol, lsqr_iters=lsqr_iters,
+                 keep=keep)
