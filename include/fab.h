@@ -70,7 +70,8 @@ enum {
 
 /* ---- enums ------------------------------------------------------------ */
 enum { FAB_BLENDENPIK = 0, FAB_SKETCH_SOLVE = 1, FAB_NONE = 2, FAB_LSQR = 3 };  /* fab_compress */
-enum { FAB_EXP = 0, FAB_SQRT = 1, FAB_INVSQRT = 2, FAB_POLY = 3 };     /* fab_apply    */
+enum { FAB_EXP = 0, FAB_SQRT = 1, FAB_INVSQRT = 2, FAB_POLY = 3,     /* fab_apply    */
+       FAB_SIGN = 4 };  /* sign(A) b = (A^2)^{-1/2} (A b); needs FAB_FLAG_SQUARE */
 enum { FAB_OP_CSR = 0, FAB_OP_STENCIL = 1 };                          /* operator kind */
 enum { FAB_DEVICE = 0, FAB_HOST = 1 };                                /* pointer space */
 
@@ -93,7 +94,17 @@ enum {
 };
 
 /* fab_opts.flags */
-enum { FAB_FLAG_PROFILE = 1 };  /* time every LSQR pass with CUDA events (fab_info) */
+enum {
+  FAB_FLAG_PROFILE = 1,  /* time every LSQR pass with CUDA events (fab_info)            */
+  /* Squared operator ("to apply the sign function to a vector we
+     use the formula f(A)b = (A^2)^{-1/2} (Ab)"): every basis algorithm builds
+     the Krylov space of A^2, each product applied as A (A w) (two SpMV passes,
+     the first writes t = A w to an extra padded scratch vector of the
+     workspace, the second fuses the window dots); fab_init (and fab_set of a
+     new b) replaces b by A b, so gamma_b = ||A b||.  fab_apply(FAB_SIGN, 1, 0)
+     then returns sign(A) b.  The breakdown threshold is 1e-14 ||A||_inf^2. */
+  FAB_FLAG_SQUARE = 2
+};
 
 typedef struct fab_ctx fab_ctx;
 
@@ -255,6 +266,9 @@ int fab_compress(fab_ctx* ctx, int mode, const fab_lsqr_opts* opts);
 
 /* y_out (n_local doubles, device or host per y_location) =
    gamma_b V_m f(alpha C_m + sigma I) e_1, f in {EXP, SQRT, INVSQRT, POLY}.
+   FAB_SIGN (contexts created with FAB_FLAG_SQUARE only, else EINVAL) is
+   INVSQRT on the compression of A^2 with the start vector A b: with alpha = 1,
+   sigma = 0 the result approximates sign(A) b (l.406).
    Errors: EORDER, EINVAL, EDOMAIN, ENOCONV, ESINGULAR, ECUDA. */
 int fab_apply(fab_ctx* ctx, int f, double alpha, double sigma, double* y_out, int y_location);
 

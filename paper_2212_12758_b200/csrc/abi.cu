@@ -18,7 +18,7 @@ void set_last_cuda_error(cudaError_t e, const char* what, const char* file, int 
 }
 
 struct Layout {
-  size_t V, vec, H, beta, coef, part_norm, part_sk, SV, rows, signs, part_g, part_tn, small, dense, qr, red, xg, st;
+  size_t V, vec, H, beta, coef, part_norm, part_sk, SV, rows, signs, part_g, part_tn, small, dense, qr, red, xg, sq, st;
   size_t total;
 };
 
@@ -49,6 +49,7 @@ static Layout make_layout(const fab_ctx* c) {
   L.qr = carve(cur, (size_t)(c->s_max > 0 ? c->s_max : 1) * m1 * 8);
   L.red = carve(cur, (size_t)kSmall * 8);
   L.xg = carve(cur, (c->comm && !c->stencil) ? (size_t)c->n_global * 8 : 8);
+  L.sq = carve(cur, (c->flags & FAB_FLAG_SQUARE) ? (size_t)c->ld * 8 : 8);
   L.st = carve(cur, sizeof(DevState));
   L.total = cur;
   return L;
@@ -112,6 +113,7 @@ static int setup_ctx(fab_ctx* c, const fab_operator* A, const fab_opts* o) {
   c->row_begin = A->row_begin;
   c->n = A->row_end - A->row_begin;
   c->comm = static_cast<Comm*>(o->comm);
+  c->flags = o->flags;
   c->hal = 0;
   if (c->stencil && comm_size(c) > 1) {
     // widest stencil offset: one plane (3D), one line (2D), one row (1D)
@@ -151,6 +153,7 @@ static void assign_buffers(fab_ctx* c) {
   c->dense = reinterpret_cast<double*>(w + L.dense);
   c->red = reinterpret_cast<double*>(w + L.red);
   c->xg = (c->comm && !c->stencil) ? reinterpret_cast<double*>(w + L.xg) : nullptr;
+  c->sq = (c->flags & FAB_FLAG_SQUARE) ? reinterpret_cast<double*>(w + L.sq) + c->hpad : nullptr;
   c->st_d = reinterpret_cast<DevState*>(w + L.st);
 }
 
@@ -300,9 +303,16 @@ int fab_init(fab_ctx** out, const fab_operator* A, const double* b, const fab_op
   DevState h;
   memset(&h, 0, sizeof(h));
   h.norm_inf = c->norm_inf;
-  h.thresh = 1e-14 * c->norm_inf;
+  // breakdown threshold (G-5) relative to ||Op||_inf; Op = A^2 when squared
+  // (bounded by ||A||_inf^2)
+  h.thresh = 1e-14 * ((c->flags & FAB_FLAG_SQUARE) ? c->norm_inf * c->norm_inf : c->norm_inf);
   *c->st_h = h;
   INIT_CUDA(cudaMemcpyAsync(c->st_d, c->st_h, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
+  INIT_CUDA(cudaStreamSynchronize(c->stream));
+  if ((rc = square_rhs(c)) != FAB_OK) {   // squared operator: start from A b (l.406)
+    free_ctx(c);
+    return rc;
+  }
   INIT_CUDA(cudaStreamSynchronize(c->stream));
 #undef INIT_CUDA
   c->info.n = c->n;
@@ -506,7 +516,11 @@ int fab_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o) {
 
 int fab_apply(fab_ctx* c, int f, double alpha, double sigma, double* y, int y_location) {
   if (!c || !y) return FAB_EINVAL;
-  if (f < FAB_EXP || f > FAB_POLY) return FAB_EINVAL;
+  if (f < FAB_EXP || f > FAB_SIGN) return FAB_EINVAL;
+  if (f == FAB_SIGN) {   // (A^2)^{-1/2} (A b) (l.406): invsqrt on the squared operator's compression
+    if (!(c->flags & FAB_FLAG_SQUARE)) return FAB_EINVAL;
+    f = FAB_INVSQRT;
+  }
   if (y_location != FAB_DEVICE && y_location != FAB_HOST) return FAB_EINVAL;
   if (!isfinite(alpha) || !isfinite(sigma)) return FAB_EINVAL;
   if (!c->compressed) return FAB_EORDER;
@@ -654,6 +668,7 @@ int fab_set(fab_ctx* c, int what, const void* src, size_t bytes) {
     FAB_CUDA(cudaMemcpyAsync(c->V, src, c->n * sizeof(double),
                              what == FAB_SET_B_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
                              c->stream));
+    FAB_TRY(square_rhs(c));
     FAB_CUDA(cudaStreamSynchronize(c->stream));
     c->basis_ready = false;
     c->compressed = false;

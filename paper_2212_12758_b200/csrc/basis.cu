@@ -87,13 +87,18 @@ __device__ __forceinline__ double2 ld2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
 
-template <int DIM, int NWM, bool STORE_Z, int U = (NWM <= 4 ? kK1U : 1)>
+// SQ (squared operator, FAB_FLAG_SQUARE): the SpMV input is xin = A w_hat_{c-1}
+// (written by a K0 = this kernel with nw = 0), so z = A^2 w_hat_{c-1}; the
+// j = c-1 window dot then reads w_hat_{c-1} itself (one more column load).
+template <int DIM, int NWM, bool STORE_Z, bool SQ = false, int U = (NWM <= 4 ? kK1U : 1)>
 __global__ void __launch_bounds__(kThreads, 2)
 k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP sp, int64_t n, int64_t gbase,
-                 double* __restrict__ z, double* __restrict__ part, const DevState* __restrict__ st) {
+                 const double* __restrict__ xin, double* __restrict__ z, double* __restrict__ part,
+                 const DevState* __restrict__ st) {
   if (st->breakdown) return;
   __shared__ double red[kWarps * NWM];
-  const double* __restrict__ x = V + (int64_t)(c - 1) * ld;
+  const double* __restrict__ xw = V + (int64_t)(c - 1) * ld;   // w_hat_{c-1} (window dot)
+  const double* __restrict__ x = SQ ? xin : xw;                // SpMV input
   const int j0 = c - nw;
   double d[NWM];
 #pragma unroll
@@ -102,7 +107,7 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
   const double2 zero2 = make_double2(0.0, 0.0);
   for (int64_t base = (int64_t)blockIdx.x * (kThreads * 2 * U); base < n;
        base += (int64_t)gridDim.x * (kThreads * 2 * U)) {
-    double2 xc[U], ym[U], yp[U], zm[U], zp[U], w[U][NWM > 1 ? NWM - 1 : 1];
+    double2 xc[U], ym[U], yp[U], zm[U], zp[U], w[U][NWM > 1 ? NWM - 1 : 1], xd[U];
     double xl[U], xr[U];
     uint32_t ixs[U], iys[U], izs[U];
     bool ok[U];
@@ -110,7 +115,7 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
     for (int u = 0; u < U; ++u) {
       const int64_t r = base + 2 * threadIdx.x + 2 * kThreads * u;
       ok[u] = r < n;                       // n even on this path: r+1 < n too
-      xc[u] = ym[u] = yp[u] = zm[u] = zp[u] = zero2;
+      xc[u] = ym[u] = yp[u] = zm[u] = zp[u] = xd[u] = zero2;
       xl[u] = xr[u] = 0.0;
       ixs[u] = iys[u] = izs[u] = 0;
 #pragma unroll
@@ -134,6 +139,7 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
 #pragma unroll
         for (int t = 0; t < NWM - 1; ++t)
           if (t < nw - 1) w[u][t] = ld2(V + (int64_t)(j0 + t) * ld + r);
+        if (SQ) xd[u] = ld2(xw + r);
       }
     }
 #pragma unroll
@@ -152,13 +158,14 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
           d[t] = fma(w[u][t].y, a1, d[t]);
         }
       }
-      d[NWM - 1] = fma(xc[u].x, a0, d[NWM - 1]);   // j = c-1 (already loaded)
-      d[NWM - 1] = fma(xc[u].y, a1, d[NWM - 1]);
+      const double2 xl2 = SQ ? xd[u] : xc[u];       // j = c-1 (already loaded unless SQ)
+      d[NWM - 1] = fma(xl2.x, a0, d[NWM - 1]);
+      d[NWM - 1] = fma(xl2.y, a1, d[NWM - 1]);
     }
   }
   double out[NWM];
   block_sum<NWM>(d, red, out);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && nw > 0) {
     double* p = part + (int64_t)blockIdx.x * (kKMax + 1);
     for (int t = 0; t < nw - 1; ++t) p[t] = out[t];
     p[nw - 1] = out[NWM - 1];
@@ -169,10 +176,13 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
 template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 k_stencil_dots(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP sp, int64_t n, int64_t gbase,
-               double* __restrict__ z, double* __restrict__ part, const DevState* __restrict__ st) {
+               const double* __restrict__ xin, double* __restrict__ z, double* __restrict__ part,
+               const DevState* __restrict__ st) {
   if (st->breakdown) return;
   __shared__ double red[kWarps * kKMax];
-  const double* __restrict__ x = V + (int64_t)(c - 1) * ld;
+  const double* __restrict__ xw = V + (int64_t)(c - 1) * ld;   // w_hat_{c-1} (window dot)
+  const double* __restrict__ x = xin;                          // SpMV input (== xw unless squared)
+  const bool sq = xin != xw;
   const int j0 = c - nw;
   double d[kKMax];
 #pragma unroll
@@ -193,11 +203,11 @@ k_stencil_dots(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP
     for (int t = 0; t < kKMax; ++t) {
       if (t < nw - 1) d[t] = fma(__ldg(V + (int64_t)(j0 + t) * ld + r), acc, d[t]);
     }
-    if (nw >= 1) d[kKMax - 1] = fma(xc, acc, d[kKMax - 1]);   // j = c-1 (already loaded)
+    if (nw >= 1) d[kKMax - 1] = fma(sq ? __ldg(xw + r) : xc, acc, d[kKMax - 1]);   // j = c-1
   }
   double out[kKMax];
   block_sum<kKMax>(d, red, out);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && nw > 0) {
     double* p = part + (int64_t)blockIdx.x * (kKMax + 1);
     for (int t = 0; t < nw - 1; ++t) p[t] = out[t];
     p[nw - 1] = out[kKMax - 1];
@@ -205,90 +215,132 @@ k_stencil_dots(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP
 }
 
 // ---------------------------------------------------------------------------
-// K1 (CSR): G lanes per row; rows longer than kLongRow are skipped here and
-// handled by one CTA each in k_csr_long (so hub rows of power-law graphs do
-// not serialize a lane group).
+// K1 (CSR): nnz-balanced row blocks ("CSR-stream").  At fab_init the local
+// rows are cut into blocks of consecutive rows holding <= kCsrNB stored
+// entries (a row with more entries is a block of its own).  A persistent CTA
+// takes blocks b = blockIdx.x + i * gridDim.x (static, so every reduction
+// order is fixed):
+//   stream : the block's entries are read as one contiguous range -- col ids
+//            and values coalesced, kCsrU gathers of x per thread issued back to
+//            back -- and the products land in shared memory;
+//   reduce : G lanes per row (G = the power of two nearest the block's mean
+//            row length / 4, 1..32) sum each row's products in fixed order,
+//            then z_r and the window dots of row r;
+//   long   : a row with > kCsrNB entries is summed by the whole CTA.
+// Power-law rows (c4) and short random rows (c5) both keep every lane busy
+// and ~kCsrNB independent gathers in flight per CTA.
 // ---------------------------------------------------------------------------
-constexpr int kLongRow = 256;
+constexpr int kCsrNB = 4096;                 // entries per block (32 KB of products)
+constexpr int kCsrU = kCsrNB / kThreads;     // 16 gathers per thread per block
 
-template <int G>
 __global__ void __launch_bounds__(kThreads)
-k_csr_dots(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-           const double* __restrict__ vals, double vscale, const double* __restrict__ V,
-           int64_t ld, int c, int nw, int64_t n, const double* __restrict__ xg, double* __restrict__ z,
-           double* __restrict__ part, const DevState* __restrict__ st) {
+k_csr_stream(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, const double* __restrict__ vals,
+             double vscale, const int64_t* __restrict__ blk, int64_t nblk, const double* __restrict__ V,
+             int64_t ld, int c, int nw, const double* __restrict__ xg, double* __restrict__ z,
+             double* __restrict__ part, const DevState* __restrict__ st) {
   if (st->breakdown) return;
+  __shared__ double prod[kCsrNB];
   __shared__ double red[kWarps * kKMax];
+  // xg: the SpMV input indexed by GLOBAL column id: w_hat_{c-1} (== x on one
+  // GPU), or A w_hat_{c-1} gathered (squared operator, FAB_FLAG_SQUARE)
   const double* __restrict__ x = V + (int64_t)(c - 1) * ld;   // local rows of w_hat_{c-1}
-  // xg: w_hat_{c-1} indexed by GLOBAL column id (== x on one GPU)
   const int j0 = c - nw;
-  const int lane = threadIdx.x & 31;
-  const int sub = lane % G;
+  const int tid = threadIdx.x, lane = tid & 31;
   double d[kKMax];
 #pragma unroll
   for (int t = 0; t < kKMax; ++t) d[t] = 0.0;
-  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  constexpr int RPW = 32 / G;   // rows per warp per step
-  for (int64_t base = wid * RPW; base < n; base += warps_total * RPW) {
-    const int64_t row = base + lane / G;
-    double acc = 0.0;
-    bool valid = row < n;
-    int64_t s0 = 0, s1 = 0;
-    if (valid) {
-      s0 = __ldg(rp + row);
-      s1 = __ldg(rp + row + 1);
-      if (s1 - s0 > kLongRow) valid = false;
+  auto row_dots = [&](int64_t row, double zr) {
+#pragma unroll
+    for (int t = 0; t < kKMax; ++t)
+      if (t < nw - 1) d[t] = fma(__ldg(V + (int64_t)(j0 + t) * ld + row), zr, d[t]);
+    if (nw >= 1) d[kKMax - 1] = fma(__ldg(x + row), zr, d[kKMax - 1]);
+  };
+  for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
+    const int64_t r0 = blk[b], r1 = blk[b + 1];
+    const int64_t q0 = __ldg(rp + r0), q1 = __ldg(rp + r1);
+    const int64_t cnt = q1 - q0;
+    if (cnt > kCsrNB) {
+      // long row (r1 == r0 + 1): the whole CTA, products summed in registers
+      double acc = 0.0;
+      for (int64_t base = 0; base < cnt; base += kThreads * kCsrU) {
+        int col[kCsrU];
+        double v[kCsrU];
+#pragma unroll
+        for (int u = 0; u < kCsrU; ++u) {
+          const int64_t i = base + tid + kThreads * u;
+          col[u] = i < cnt ? __ldg(ci + q0 + i) : -1;
+          v[u] = (vals && i < cnt) ? __ldg(vals + q0 + i) : 1.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kCsrU; ++u)
+          if (col[u] >= 0) acc = fma(v[u], __ldg(xg + col[u]), acc);
+      }
+      double a1[1] = {acc}, o1[1];
+      block_sum<1>(a1, red, o1);
+      if (tid == 0) {
+        const double zr = o1[0] * vscale;
+        z[r0] = zr;
+        row_dots(r0, zr);
+      }
+      continue;
     }
-    if (valid) {
-      if (vals) {
-        for (int64_t q = s0 + sub; q < s1; q += G) acc = fma(__ldg(vals + q), __ldg(xg + __ldg(ci + q)), acc);
-      } else {
-        for (int64_t q = s0 + sub; q < s1; q += G) acc += __ldg(xg + __ldg(ci + q));
+    // stream: products of the block's entries into shared memory
+    {
+      int col[kCsrU];
+      double v[kCsrU], xv[kCsrU];
+#pragma unroll
+      for (int u = 0; u < kCsrU; ++u) {
+        const int i = tid + kThreads * u;
+        col[u] = i < cnt ? __ldg(ci + q0 + i) : -1;
+        v[u] = (vals && i < cnt) ? __ldg(vals + q0 + i) : 1.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kCsrU; ++u) xv[u] = col[u] >= 0 ? __ldg(xg + col[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kCsrU; ++u) {
+        const int i = tid + kThreads * u;
+        if (i < cnt) prod[i] = v[u] * xv[u];
       }
     }
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (valid && sub == 0) {
-      acc *= vscale;
-      z[row] = acc;
-#pragma unroll
-      for (int t = 0; t < kKMax; ++t)
-        if (t < nw - 1) d[t] = fma(__ldg(V + (int64_t)(j0 + t) * ld + row), acc, d[t]);
-      if (nw >= 1) d[kKMax - 1] = fma(__ldg(x + row), acc, d[kKMax - 1]);
+    __syncthreads();
+    // reduce: G lanes per row, fixed order
+    const int nrows = (int)(r1 - r0);
+    const int64_t avg = nrows > 0 ? cnt / nrows : 0;
+    int G = 1;
+    while (G < 32 && 4 * G < avg) G <<= 1;
+    const int P = kThreads / G;
+    for (int rb = 0; rb < nrows; rb += P) {
+      const int rl = rb + tid / G, sub = tid & (G - 1);
+      double acc = 0.0;
+      if (rl < nrows) {
+        const int a = (int)(__ldg(rp + r0 + rl) - q0), e = (int)(__ldg(rp + r0 + rl + 1) - q0);
+        for (int i = a + sub; i < e; i += G) acc += prod[i];
+      }
+      for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (rl < nrows && sub == 0) {
+        const double zr = acc * vscale;
+        z[r0 + rl] = zr;
+        row_dots(r0 + rl, zr);
+      }
     }
+    __syncthreads();
   }
+  (void)lane;
   double out[kKMax];
   block_sum<kKMax>(d, red, out);
-  if (threadIdx.x == 0) {
+  if (tid == 0 && nw > 0) {
     double* p = part + (int64_t)blockIdx.x * (kKMax + 1);
     for (int t = 0; t < nw - 1; ++t) p[t] = out[t];
     p[nw - 1] = out[kKMax - 1];
   }
 }
 
-// one CTA per long row (list built deterministically at init)
-__global__ void __launch_bounds__(kThreads)
-k_csr_long(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-           const double* __restrict__ vals, double vscale, const int64_t* __restrict__ long_rows,
-           const double* __restrict__ V, int64_t ld, int c, int nw, const double* __restrict__ xg,
-           double* __restrict__ z, double* __restrict__ part, const DevState* __restrict__ st) {
-  if (st->breakdown) return;
-  __shared__ double red[kWarps];
-  const int64_t row = long_rows[blockIdx.x];
-  const int64_t s0 = rp[row], s1 = rp[row + 1];
-  double acc = 0.0;
-  for (int64_t q = s0 + threadIdx.x; q < s1; q += blockDim.x)
-    acc = fma(vals ? __ldg(vals + q) : 1.0, __ldg(xg + __ldg(ci + q)), acc);
-  double v1[1] = {acc}, o1[1];
-  block_sum<1>(v1, red, o1);
-  if (threadIdx.x == 0) {
-    const double zr = o1[0] * vscale;
-    z[row] = zr;
-    double* p = part + (int64_t)blockIdx.x * (kKMax + 1);
-    const int j0 = c - nw;
-    for (int t = 0; t < nw; ++t) p[t] = V[(int64_t)(j0 + t) * ld + row] * zr;
-  }
+// uniform values: 1 in every CTA partial iff every value in its range equals v0
+__global__ void k_csr_uniform(const double* __restrict__ vals, int64_t nnz, double v0, int* flag) {
+  bool same = true;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz; q += (int64_t)gridDim.x * blockDim.x)
+    same &= (vals[q] == v0);
+  if (!__syncthreads_and(same) && threadIdx.x == 0) atomicExch(flag, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -853,29 +905,24 @@ static StencilP stencil_params(const fab_ctx* c) {
   return p;
 }
 
-// per-context CSR long-row list (host-built, deterministic)
-struct LongRows {
+// per-context CSR row-block list of k_csr_stream (host-built, deterministic)
+struct CsrBlocks {
   int64_t* d = nullptr;
   int64_t count = 0;
 };
-static std::vector<std::pair<fab_ctx*, LongRows>> g_long;
+static std::vector<std::pair<fab_ctx*, CsrBlocks>> g_blk;
 
-static LongRows* long_rows(fab_ctx* c) {
-  for (auto& p : g_long)
+static CsrBlocks* csr_blocks(fab_ctx* c) {
+  for (auto& p : g_blk)
     if (p.first == c) return &p.second;
   return nullptr;
 }
 
-int64_t csr_long_count(fab_ctx* c) {
-  LongRows* L = long_rows(c);
-  return L ? L->count : 0;
-}
-
 void release_long_rows(fab_ctx* c) {
-  for (size_t i = 0; i < g_long.size(); ++i)
-    if (g_long[i].first == c) {
-      if (g_long[i].second.d) cudaFree(g_long[i].second.d);
-      g_long.erase(g_long.begin() + i);
+  for (size_t i = 0; i < g_blk.size(); ++i)
+    if (g_blk[i].first == c) {
+      if (g_blk[i].second.d) cudaFree(g_blk[i].second.d);
+      g_blk.erase(g_blk.begin() + i);
       return;
     }
 }
@@ -901,7 +948,7 @@ int basis_setup_grids(fab_ctx* c) {
   // neighbour chunks are first-touch misses that stall the ring (K3 347 us vs
   // 120 us, profiles/r01_v2); needs a z-marching tile order.
   const char* mfe = getenv("FAB_MATRIX_FREE");
-  c->mf = stencil_vec_path(c) && (mfe && mfe[0] == '1');
+  c->mf = stencil_vec_path(c) && (mfe && mfe[0] == '1') && !(c->flags & FAB_FLAG_SQUARE);
   // K3/K5 pipeline: persistent, one CTA per SM (the ring takes the smem)
   const int64_t ntiles = ((c->row_begin + c->n - 1) >> kSkLogT) - (c->row_begin >> kSkLogT) + 1;
   c->grid_upd = (int)(ntiles < c->num_sms ? ntiles : c->num_sms);
@@ -911,12 +958,12 @@ int basis_setup_grids(fab_ctx* c) {
     const int64_t g1 = 2 * (int64_t)c->num_sms;
     c->grid_spmv = (int)(need < g1 ? need : g1);
   } else {
+    // persistent k_csr_stream: every resident CTA (the block count is known
+    // only at fab_init; init_vector_norm trims the grid to it)
     int occ1 = 0;
-    FAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_csr_dots<8>, kThreads, 0));
+    FAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_csr_stream, kThreads, 0));
     if (occ1 < 1) occ1 = 1;
-    const int64_t g1 = (int64_t)c->num_sms * occ1;
-    const int64_t need = (c->n + kThreads - 1) / kThreads;
-    c->grid_spmv = (int)(need < g1 ? need : g1);
+    c->grid_spmv = c->num_sms * occ1;
   }
   if (c->grid_spmv < 1) c->grid_spmv = 1;
   return FAB_OK;
@@ -938,23 +985,51 @@ int init_vector_norm(fab_ctx* c) {
     double mx = 0.0;
     for (double v : h) mx = v > mx ? v : mx;
     c->norm_inf = mx;
-    // long rows, in ascending row order
+    // uniform values (e.g. a scaled 0/1 adjacency, c4): drop the value array
+    // (8 B per entry per SpMV) and fold the value into value_scale
+    if (c->op.values && c->op.nnz > 0) {
+      double v0 = 0.0;
+      FAB_CUDA(cudaMemcpy(&v0, c->op.values, sizeof(double), cudaMemcpyDeviceToHost));
+      int* flag = reinterpret_cast<int*>(c->vec);
+      const int one = 1;
+      FAB_CUDA(cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+      k_csr_uniform<<<4 * c->num_sms, kThreads, 0, c->stream>>>(c->op.values, c->op.nnz, v0, flag);
+      FAB_CHECK_LAUNCH();
+      int same = 0;
+      FAB_CUDA(cudaMemcpyAsync(&same, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      FAB_CUDA(cudaStreamSynchronize(c->stream));
+      if (same && isfinite(v0)) {
+        c->op.values = nullptr;
+        c->op.value_scale *= v0;
+      }
+    }
+    // row blocks of k_csr_stream: consecutive rows with <= kCsrNB entries, a
+    // longer row alone
     std::vector<int64_t> rp(c->n + 1);
     FAB_CUDA(cudaMemcpy(rp.data(), c->op.row_ptr, (c->n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
-    std::vector<int64_t> lr;
-    for (int64_t r = 0; r < c->n; ++r)
-      if (rp[r + 1] - rp[r] > kLongRow) lr.push_back(r);
-    LongRows L;
-    L.count = (int64_t)lr.size();
-    if (L.count) {
-      FAB_CUDA(cudaMalloc(&L.d, L.count * sizeof(int64_t)));
-      FAB_CUDA(cudaMemcpy(L.d, lr.data(), L.count * sizeof(int64_t), cudaMemcpyHostToDevice));
+    std::vector<int64_t> bl;
+    bl.reserve(c->op.nnz / kCsrNB + c->n / kThreads + 2);
+    bl.push_back(0);
+    int64_t r = 0;
+    while (r < c->n) {
+      if (rp[r + 1] - rp[r] > kCsrNB) {
+        bl.push_back(++r);
+        continue;
+      }
+      const int64_t q0 = rp[r];
+      while (r < c->n && rp[r + 1] - q0 <= kCsrNB) ++r;
+      bl.push_back(r);
     }
+    CsrBlocks B;
+    B.count = (int64_t)bl.size() - 1;
+    FAB_CUDA(cudaMalloc(&B.d, bl.size() * sizeof(int64_t)));
+    FAB_CUDA(cudaMemcpy(B.d, bl.data(), bl.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     release_long_rows(c);
-    g_long.push_back({c, L});
+    g_blk.push_back({c, B});
+    if (B.count < c->grid_spmv) c->grid_spmv = (int)(B.count > 0 ? B.count : 1);
   }
-  // per-step dot partials: one slot per CTA of K1 plus one per long CSR row
-  const int64_t slots = (int64_t)c->grid_spmv + csr_long_count(c);
+  // per-step dot partials: one slot per CTA of K1
+  const int64_t slots = (int64_t)c->grid_spmv;
   if (c->part_dots) cudaFree(c->part_dots);
   FAB_CUDA(cudaMalloc(&c->part_dots, slots * (kKMax + 1) * sizeof(double)));
   return FAB_OK;
@@ -980,29 +1055,31 @@ int enqueue_scalar(fab_ctx* c, int col, int nw, int nparts, int final_step, cuda
   return FAB_OK;
 }
 
-// K1 of step col: z = A w_hat_{col-1} (stored in z unless matrix-free and
-// !need_z) and the partial window dots (nw columns ending at col-1); C1 first
-// on several GPUs.  *nparts = partial slots written.
-int enqueue_k1(fab_ctx* c, int col, int nw, double* z, bool need_z, cudaStream_t st, int64_t* launches,
-               int* nparts) {
+// One SpMV pass: z = A xin and, if nw > 0, the partial window dots of z
+// against the nw columns ending at col-1 (the j = col-1 dot reads w_hat_{col-1}
+// = V[:, col-1], which is xin unless the operator is squared).  xin: stencil --
+// local rows with their halo slots filled; CSR -- indexed by global column id.
+static int launch_k1(fab_ctx* c, int col, int nw, const double* xin, double* z, bool store, cudaStream_t st,
+                     int64_t* launches, int* nparts) {
   *nparts = c->grid_spmv;
-  double* x = c->V + (int64_t)(col - 1) * c->ld;
+  const double* x = c->V + (int64_t)(col - 1) * c->ld;
   if (c->stencil) {
-    int rc = comm_halo(c, x, st);   // C1: neighbour rows of w_hat_{col-1}
-    if (rc != FAB_OK) return rc;
     StencilP sp = stencil_params(c);
     const bool d3 = c->op.dims[2] > 1;
     const int G = c->grid_spmv;
     const int64_t gb = c->row_begin;
-    const bool store = need_z || !c->mf;
+    const bool sq = xin != x;
     if (stencil_vec_path(c)) {
 #define FAB_K1V(DIM, NWM)                                                                                    \
   do {                                                                                                       \
-    if (!store)                                                                                              \
-      k_stencil_dots_v<DIM, NWM, false><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, z,       \
+    if (sq)                                                                                                  \
+      k_stencil_dots_v<DIM, NWM, true, true><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, xin, \
+                                                                     z, c->part_dots, c->st_d);              \
+    else if (!store)                                                                                         \
+      k_stencil_dots_v<DIM, NWM, false><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, xin, z,  \
                                                                 c->part_dots, c->st_d);                      \
     else                                                                                                     \
-      k_stencil_dots_v<DIM, NWM, true><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, z,        \
+      k_stencil_dots_v<DIM, NWM, true><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, xin, z,   \
                                                                c->part_dots, c->st_d);                       \
   } while (0)
       if (c->k_max <= 2) {
@@ -1014,34 +1091,71 @@ int enqueue_k1(fab_ctx* c, int col, int nw, double* z, bool need_z, cudaStream_t
       }
 #undef FAB_K1V
     } else if (d3) {
-      k_stencil_dots<3><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, z, c->part_dots, c->st_d);
+      k_stencil_dots<3><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, xin, z, c->part_dots,
+                                                c->st_d);
     } else {
-      k_stencil_dots<2><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, z, c->part_dots, c->st_d);
+      k_stencil_dots<2><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, xin, z, c->part_dots,
+                                                c->st_d);
     }
     FAB_CHECK_LAUNCH();
     ++*launches;
-  } else {
-    const double* xg = x;
-    if (c->comm) {
-      int rc = comm_gather_x(c, x, st);   // C1: x by global column id
-      if (rc != FAB_OK) return rc;
-      xg = c->xg;
-    }
-    k_csr_dots<8><<<c->grid_spmv, kThreads, 0, st>>>(c->op.row_ptr, c->op.col_idx, c->op.values,
-                                                      c->op.value_scale, c->V, c->ld, col, nw, c->n, xg, z,
-                                                      c->part_dots, c->st_d);
-    FAB_CHECK_LAUNCH();
-    ++*launches;
-    LongRows* L = long_rows(c);
-    if (L && L->count) {
-      k_csr_long<<<(unsigned)L->count, kThreads, 0, st>>>(
-          c->op.row_ptr, c->op.col_idx, c->op.values, c->op.value_scale, L->d, c->V, c->ld, col, nw, xg, z,
-          c->part_dots + (int64_t)c->grid_spmv * (kKMax + 1), c->st_d);
-      FAB_CHECK_LAUNCH();
-      ++*launches;
-      *nparts += (int)L->count;
-    }
+    return FAB_OK;
   }
+  CsrBlocks* B = csr_blocks(c);
+  if (!B) return FAB_EORDER;
+  k_csr_stream<<<c->grid_spmv, kThreads, 0, st>>>(c->op.row_ptr, c->op.col_idx, c->op.values, c->op.value_scale,
+                                                  B->d, B->count, c->V, c->ld, col, nw, xin, z, c->part_dots,
+                                                  c->st_d);
+  FAB_CHECK_LAUNCH();
+  ++*launches;
+  return FAB_OK;
+}
+
+// The SpMV input for a product with the local vector x (local rows): C1 on
+// several GPUs (stencil: fill x's halo slots; CSR: all-gather-v into xg).
+static int spmv_input(fab_ctx* c, double* x, cudaStream_t st, const double** xin) {
+  if (c->stencil) {
+    FAB_TRY(comm_halo(c, x, st));
+    *xin = x;
+    return FAB_OK;
+  }
+  *xin = x;
+  if (c->comm) {
+    FAB_TRY(comm_gather_x(c, x, st));
+    *xin = c->xg;
+  }
+  return FAB_OK;
+}
+
+// K1 of step col: z = Op w_hat_{col-1} (stored in z unless matrix-free and
+// !need_z) and the partial window dots (nw columns ending at col-1); C1 first
+// on several GPUs.  Op = A, or A^2 applied as A (A w) when the context was
+// created with FAB_FLAG_SQUARE (sign(A) b = (A^2)^{-1/2} (A b)):
+// then a K0 pass (the same kernel, no dots) writes t = A w_hat_{col-1} to the
+// padded scratch c->sq first.  *nparts = partial slots written.
+int enqueue_k1(fab_ctx* c, int col, int nw, double* z, bool need_z, cudaStream_t st, int64_t* launches,
+               int* nparts) {
+  double* x = c->V + (int64_t)(col - 1) * c->ld;
+  const double* xin = nullptr;
+  FAB_TRY(spmv_input(c, x, st, &xin));
+  if (c->flags & FAB_FLAG_SQUARE) {
+    int np0 = 0;
+    FAB_TRY(launch_k1(c, col, 0, xin, c->sq, true, st, launches, &np0));   // K0: t = A w_hat_{col-1}
+    FAB_TRY(spmv_input(c, c->sq, st, &xin));
+  }
+  return launch_k1(c, col, nw, xin, z, need_z || !c->mf, st, launches, nparts);
+}
+
+// FAB_FLAG_SQUARE: the starting vector of the Krylov space of A^2 is A b
+// (l.406).  V[:, 0] = b on entry; V[:, 0] <- A b on exit (c->stream, async).
+int square_rhs(fab_ctx* c) {
+  if (!(c->flags & FAB_FLAG_SQUARE)) return FAB_OK;
+  int64_t launches = 0;
+  int np = 0;
+  const double* xin = nullptr;
+  FAB_TRY(spmv_input(c, c->V, c->stream, &xin));
+  FAB_TRY(launch_k1(c, 1, 0, xin, c->sq, true, c->stream, &launches, &np));
+  FAB_CUDA(cudaMemcpyAsync(c->V, c->sq, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   return FAB_OK;
 }
 

@@ -95,6 +95,7 @@ struct fab_ctx {
   double* dense = nullptr;       // dense pool: kDenseMats * m_max^2
   double* red = nullptr;         // kSmall: this rank's step / pass scalars (allreduced in place)
   double* xg = nullptr;          // CSR on several GPUs: w_hat_{i-1} gathered to global length
+  double* sq = nullptr;          // FAB_FLAG_SQUARE: t = A w_hat_{i-1} (local rows, halo-padded like V)
   fab::DevState* st_d = nullptr;
   fab::DevState* st_h = nullptr; // pinned mirror
 
@@ -228,6 +229,7 @@ const char* nccl_last_error();
 int basis_setup_grids(fab_ctx* c);
 int init_vector_norm(fab_ctx* c);            // partial norms of column 0, norm_inf
 int run_basis(fab_ctx* c, int m, int k);
+int square_rhs(fab_ctx* c);                  // FAB_FLAG_SQUARE: V[:, 0] <- A V[:, 0]
 // sgs.cu (Algorithm 1)
 int run_basis_sgs(fab_ctx* c, int m);
 // arnoldi.cu (the paper's baseline, Eq. (2))
