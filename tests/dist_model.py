@@ -82,10 +82,12 @@ def local_sketch_partial(x_loc, r0, th):
     return out
 
 
-def rank_solve(rank, P, A, b, cuts, hal, m, k, s, seed, f, alpha, sigma, lsqr_iters):
+def rank_solve(rank, P, A, b, cuts, hal, m, k, s, seed, f, alpha, sigma, lsqr_iters, square=False):
     """One rank of the row-partitioned Algorithm 4 (Blendenpik, fixed L).
-    hal = halo rows (stencil) or None (CSR: gathered x).  Returns (f_m rows,
-    H, SV, y) of this rank (H, SV, y replicated)."""
+    hal = halo rows (stencil) or None (CSR: gathered x).  square: the
+    operator is A^2 applied as A (A w) with a C1 exchange before each of the
+    two products, and the start vector is A b (FAB_FLAG_SQUARE, sign(A) b by
+    l.406).  Returns (f_m rows, H, SV, y) of this rank (H, SV, y replicated)."""
     r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
     n_loc = r1 - r0
     n = A.shape[0]
@@ -100,18 +102,21 @@ def rank_solve(rank, P, A, b, cuts, hal, m, k, s, seed, f, alpha, sigma, lsqr_it
         assert A_loc.col.min() >= lo_col and A_loc.col.max() < r1 + hal, "halo too narrow"
         A_ext = sp.csr_matrix((A_loc.data, (A_loc.row, A_loc.col - lo_col)), shape=(n_loc, n_loc + 2 * hal))
 
+    def spmv(x):                                                  # C1 + one local product
+        if hal is None:
+            xe = gather_x(x, cuts, rank, P)
+        else:
+            xe = halo_exchange(x, hal, rank, P) if P > 1 else np.concatenate([np.zeros(hal), x, np.zeros(hal)])
+        return A_ext @ xe
+
     W = np.zeros((n_loc, m + 1))
-    W[:, 0] = b[r0:r1]
+    W[:, 0] = spmv(b[r0:r1]) if square else b[r0:r1]
     H = np.zeros((m + 1, m))
     beta = np.zeros(m + 1)
     nu_loc = W[:, 0] @ W[:, 0]
     for c in range(1, m + 1):
         x = W[:, c - 1]
-        if hal is None:
-            xe = gather_x(x, cuts, rank, P)
-        else:
-            xe = halo_exchange(x, hal, rank, P) if P > 1 else np.concatenate([np.zeros(hal), x, np.zeros(hal)])
-        z = A_ext @ xe                                             # K1
+        z = spmv(spmv(x)) if square else spmv(x)                   # (K0 +) K1
         js = list(range(max(0, c - k), c))
         red = allreduce(np.array([W[:, j] @ z for j in js] + [nu_loc]))   # C2: k+1 scalars
         beta[c - 1] = math.sqrt(red[-1])

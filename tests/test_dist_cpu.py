@@ -68,7 +68,8 @@ def _worker(rank, P, port, case, q):
         import sys
         sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
         import dist_model
-        name, kw = case
+        name, kw = case[:2]
+        square = len(case) > 2 and case[2] == "square"
         p = fp.make(name, **kw)
         A = p.scipy()
         if p.kind == "stencil":
@@ -77,8 +78,9 @@ def _worker(rank, P, port, case, q):
         else:
             cuts = fdist.csr_blocks(p.csr()[0], P)
             hal = None                                        # CSR: x gathered (all-gather-v)
+        f = "invsqrt" if square else p.f
         fm, H, SV, y = dist_model.rank_solve(rank, P, A, p.b, cuts, hal, p.m, p.k, p.s, p.sketch_seed,
-                                             p.f, p.alpha, p.sigma, 40)
+                                             f, p.alpha, p.sigma, 40, square=square)
         q.put((rank, cuts[rank], fm, H, SV, y))
     except BaseException as e:  # report instead of leaving the parent waiting
         q.put((rank, None, repr(e), None, None, None))
@@ -91,6 +93,9 @@ def _worker(rank, P, port, case, q):
     ("c3", dict(g=16, m=30, k=4, s=60)),       # 3D stencil, 4096-row slabs of 16 planes -> halo = 1 plane
     ("c1", dict(g=64, m=24, k=2, s=48)),       # 2D, 64-row lines; blocks not tile aligned
     ("c5", dict(n=6000, m=20, k=2, s=40)),     # CSR, ragged n, row blocks cut mid-tile
+    # squared operator (sign(A) b = (A^2)^{-1/2} (A b), l.406): two C1 exchanges per step
+    ("e4", dict(n=6000, m=20, k=2, s=40), "square"),     # CSR: x and A x gathered
+    ("e5", dict(g=16, m=20, k=2, s=40), "square"),       # stencil: halo of x and of A x
 ])
 def test_row_partitioned_solve_matches_oracle_gloo(case):
     from oracle import fab as ofab
@@ -107,12 +112,15 @@ def test_row_partitioned_solve_matches_oracle_gloo(case):
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
-    name, kw = case
+    name, kw = case[:2]
     p = fp.make(name, **kw)
-    ref = ofab.solve(p.scipy(), p.b, p.m, p.k, p.s, p.sketch_seed, mode="blendenpik", f=p.f,
-                     alpha=p.alpha, sigma=p.sigma, lsqr_iters=40, variant="cgs")
+    if len(case) > 2:
+        ref = ofab.sign(p.scipy(), p.b, p.m, p.k, p.s, p.sketch_seed, mode="blendenpik", lsqr_iters=40)
+    else:
+        ref = ofab.solve(p.scipy(), p.b, p.m, p.k, p.s, p.sketch_seed, mode="blendenpik", f=p.f,
+                         alpha=p.alpha, sigma=p.sigma, lsqr_iters=40, variant="cgs")
     fm = np.concatenate([r[2] for r in res])
-    assert res[1][1] % 4096 != 0 or name == "c3"               # a block boundary inside a sketch tile
+    assert res[1][1] % 4096 != 0 or name in ("c3", "e5")      # a block boundary inside a sketch tile
     for r in res:                                             # replicated quantities agree
         assert np.array_equal(r[3], res[0][3]) and np.array_equal(r[4], res[0][4])
     H, SV = res[0][3], res[0][4]
