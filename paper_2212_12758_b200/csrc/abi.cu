@@ -37,7 +37,7 @@ static Layout make_layout(const fab_ctx* c) {
   L.H = carve(cur, m1 * c->m_max * 8);
   L.beta = carve(cur, ((size_t)c->m_max + 2) * 8);
   L.coef = carve(cur, ((size_t)c->m_max + 2) * (kKMax + 1) * 8);
-  L.part_norm = carve(cur, (size_t)c->grid_upd * 8);
+  L.part_norm = carve(cur, (size_t)2 * c->grid_upd * 8);   // double buffered (norm_parts)
   L.part_sk = carve(cur, c->s_max > 0 ? m1 * c->grid_upd * c->s_max * 8 : 8);
   L.SV = carve(cur, (size_t)(c->s_max > 0 ? c->s_max : 1) * m1 * 8);
   L.rows = carve(cur, (size_t)(c->s_max > 0 ? c->s_max : 1) * 8);
@@ -159,7 +159,7 @@ static void assign_buffers(fab_ctx* c) {
 
 static void free_ctx(fab_ctx* c) {
   if (!c) return;
-  release_long_rows(c);
+  csr_release(c);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->gexec_sgs) cudaGraphExecDestroy(c->gexec_sgs);
   if (c->gexec_arn) cudaGraphExecDestroy(c->gexec_arn);

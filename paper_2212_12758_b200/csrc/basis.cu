@@ -215,135 +215,6 @@ k_stencil_dots(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP
 }
 
 // ---------------------------------------------------------------------------
-// K1 (CSR): nnz-balanced row blocks ("CSR-stream").  At fab_init the local
-// rows are cut into blocks of consecutive rows holding <= kCsrNB stored
-// entries (a row with more entries is a block of its own).  A persistent CTA
-// takes blocks b = blockIdx.x + i * gridDim.x (static, so every reduction
-// order is fixed):
-//   stream : the block's entries are read as one contiguous range -- col ids
-//            and values coalesced, kCsrU gathers of x per thread issued back to
-//            back -- and the products land in shared memory;
-//   reduce : G lanes per row (G = the power of two nearest the block's mean
-//            row length / 4, 1..32) sum each row's products in fixed order,
-//            then z_r and the window dots of row r;
-//   long   : a row with > kCsrNB entries is summed by the whole CTA.
-// Power-law rows (c4) and short random rows (c5) both keep every lane busy
-// and ~kCsrNB independent gathers in flight per CTA.
-// ---------------------------------------------------------------------------
-constexpr int kCsrNB = 4096;                 // entries per block (32 KB of products)
-constexpr int kCsrU = kCsrNB / kThreads;     // 16 gathers per thread per block
-
-__global__ void __launch_bounds__(kThreads)
-k_csr_stream(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, const double* __restrict__ vals,
-             double vscale, const int64_t* __restrict__ blk, int64_t nblk, const double* __restrict__ V,
-             int64_t ld, int c, int nw, const double* __restrict__ xg, double* __restrict__ z,
-             double* __restrict__ part, const DevState* __restrict__ st) {
-  if (st->breakdown) return;
-  __shared__ double prod[kCsrNB];
-  __shared__ double red[kWarps * kKMax];
-  // xg: the SpMV input indexed by GLOBAL column id: w_hat_{c-1} (== x on one
-  // GPU), or A w_hat_{c-1} gathered (squared operator, FAB_FLAG_SQUARE)
-  const double* __restrict__ x = V + (int64_t)(c - 1) * ld;   // local rows of w_hat_{c-1}
-  const int j0 = c - nw;
-  const int tid = threadIdx.x, lane = tid & 31;
-  double d[kKMax];
-#pragma unroll
-  for (int t = 0; t < kKMax; ++t) d[t] = 0.0;
-  auto row_dots = [&](int64_t row, double zr) {
-#pragma unroll
-    for (int t = 0; t < kKMax; ++t)
-      if (t < nw - 1) d[t] = fma(__ldg(V + (int64_t)(j0 + t) * ld + row), zr, d[t]);
-    if (nw >= 1) d[kKMax - 1] = fma(__ldg(x + row), zr, d[kKMax - 1]);
-  };
-  for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
-    const int64_t r0 = blk[b], r1 = blk[b + 1];
-    const int64_t q0 = __ldg(rp + r0), q1 = __ldg(rp + r1);
-    const int64_t cnt = q1 - q0;
-    if (cnt > kCsrNB) {
-      // long row (r1 == r0 + 1): the whole CTA, products summed in registers
-      double acc = 0.0;
-      for (int64_t base = 0; base < cnt; base += kThreads * kCsrU) {
-        int col[kCsrU];
-        double v[kCsrU];
-#pragma unroll
-        for (int u = 0; u < kCsrU; ++u) {
-          const int64_t i = base + tid + kThreads * u;
-          col[u] = i < cnt ? __ldg(ci + q0 + i) : -1;
-          v[u] = (vals && i < cnt) ? __ldg(vals + q0 + i) : 1.0;
-        }
-#pragma unroll
-        for (int u = 0; u < kCsrU; ++u)
-          if (col[u] >= 0) acc = fma(v[u], __ldg(xg + col[u]), acc);
-      }
-      double a1[1] = {acc}, o1[1];
-      block_sum<1>(a1, red, o1);
-      if (tid == 0) {
-        const double zr = o1[0] * vscale;
-        z[r0] = zr;
-        row_dots(r0, zr);
-      }
-      continue;
-    }
-    // stream: products of the block's entries into shared memory
-    {
-      int col[kCsrU];
-      double v[kCsrU], xv[kCsrU];
-#pragma unroll
-      for (int u = 0; u < kCsrU; ++u) {
-        const int i = tid + kThreads * u;
-        col[u] = i < cnt ? __ldg(ci + q0 + i) : -1;
-        v[u] = (vals && i < cnt) ? __ldg(vals + q0 + i) : 1.0;
-      }
-#pragma unroll
-      for (int u = 0; u < kCsrU; ++u) xv[u] = col[u] >= 0 ? __ldg(xg + col[u]) : 0.0;
-#pragma unroll
-      for (int u = 0; u < kCsrU; ++u) {
-        const int i = tid + kThreads * u;
-        if (i < cnt) prod[i] = v[u] * xv[u];
-      }
-    }
-    __syncthreads();
-    // reduce: G lanes per row, fixed order
-    const int nrows = (int)(r1 - r0);
-    const int64_t avg = nrows > 0 ? cnt / nrows : 0;
-    int G = 1;
-    while (G < 32 && 4 * G < avg) G <<= 1;
-    const int P = kThreads / G;
-    for (int rb = 0; rb < nrows; rb += P) {
-      const int rl = rb + tid / G, sub = tid & (G - 1);
-      double acc = 0.0;
-      if (rl < nrows) {
-        const int a = (int)(__ldg(rp + r0 + rl) - q0), e = (int)(__ldg(rp + r0 + rl + 1) - q0);
-        for (int i = a + sub; i < e; i += G) acc += prod[i];
-      }
-      for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (rl < nrows && sub == 0) {
-        const double zr = acc * vscale;
-        z[r0 + rl] = zr;
-        row_dots(r0 + rl, zr);
-      }
-    }
-    __syncthreads();
-  }
-  (void)lane;
-  double out[kKMax];
-  block_sum<kKMax>(d, red, out);
-  if (tid == 0 && nw > 0) {
-    double* p = part + (int64_t)blockIdx.x * (kKMax + 1);
-    for (int t = 0; t < nw - 1; ++t) p[t] = out[t];
-    p[nw - 1] = out[kKMax - 1];
-  }
-}
-
-// uniform values: 1 in every CTA partial iff every value in its range equals v0
-__global__ void k_csr_uniform(const double* __restrict__ vals, int64_t nnz, double v0, int* flag) {
-  bool same = true;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz; q += (int64_t)gridDim.x * blockDim.x)
-    same &= (vals[q] == v0);
-  if (!__syncthreads_and(same) && threadIdx.x == 0) atomicExch(flag, 0);
-}
-
-// ---------------------------------------------------------------------------
 // K2: scalar step (one CTA).  Fixed-order sums of the partials.
 // ---------------------------------------------------------------------------
 __device__ double det_sum(const double* p, int count, int stride, int off, double* red) {
@@ -539,6 +410,17 @@ struct PipeArgs {
   double* part_sk;      // per (col, CTA) sketch partials: [(col*grid + cta)*s + p]
   const DevState* st;
   int nstage;
+  // fused K2 (one GPU): the step scalars of k_scalar are formed in this
+  // kernel's prologue -- every CTA reduces the K1 / norm partials in
+  // k_scalar's order (bitwise the same), CTA 0 stores beta, H and the state
+  int fuse_k2;
+  int nparts_dots;
+  const double* part_dots;
+  const double* part_norm_prev;
+  double* beta;
+  double* H;
+  int ldH;
+  DevState* stw;
   // SDIM > 0 (matrix-free stencil): z is recomputed from w_hat_{c-1}
   StencilP sp;
   int64_t hal;          // halo rows held in each column's padding (0 on one GPU)
@@ -615,11 +497,30 @@ __device__ __forceinline__ void slot_copy(const PipeArgs& a, int v, int col, int
   *dst_off = off + (int)(l - base);
 }
 
+// k_scalar's det_sum inside the pipeline CTA: the 256 consumer threads sum
+// p[b*stride+off], b = t, t+256, ..., then the 8 warp sums in order -- the
+// same operations in the same order as det_sum in a 256-thread CTA.  Called
+// by the consumer warps only (named barrier 2), so the producer warp starts
+// streaming while the scalars are formed.
+__device__ __forceinline__ double cta_det_sum(const double* p, int count, int stride, int off, double* red) {
+  double a = 0.0;
+  for (int b = threadIdx.x; b < count; b += kThreads) a += p[(int64_t)b * stride + off];
+  a = warp_sum(a);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  consumer_sync(2, kThreads);
+  double r = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kWarps; ++w) r += red[w];
+  consumer_sync(2, kThreads);
+  return r;   // valid in thread 0
+}
+
 template <bool UPDATE, bool SKETCH, int SDIM>
 __global__ void __launch_bounds__(kPipeThreads, 1) k_stream_tiles(PipeArgs a) {
   if (a.st->breakdown) return;
   extern __shared__ __align__(128) double dsm[];
   __shared__ double red[kWarps];
+  __shared__ double scal[kKMax + 2];   // fused K2: 1/beta, -h_j/beta_j, breakdown flag
   const SlotGeom geo = slot_geom<UPDATE, SKETCH, SDIM>(a.nw, a.apron);
   const int nstage = a.nstage;
   const int stage_d = geo.stage_d;
@@ -637,6 +538,46 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_stream_tiles(PipeArgs a) {
     fence_barrier_init();
   }
   __syncthreads();
+  if (UPDATE && a.fuse_k2 && threadIdx.x < kThreads) {
+    // K2 of step c = col0: k_scalar (sums == nullptr, final_step = 0) in every
+    // CTA's consumer warps; only CTA 0 stores.  beta_{c-1} is this step's b
+    // (CTA 0 is writing beta[c-1] concurrently), older beta_j come from memory.
+    const int c = a.col0, nw = a.nw, j0 = c - nw;
+    const double nu = cta_det_sum(a.part_norm_prev, gridDim.x, 1, 0, red);
+    double dj[kKMax];
+#pragma unroll
+    for (int t = 0; t < kKMax; ++t) dj[t] = t < nw ? cta_det_sum(a.part_dots, a.nparts_dots, kKMax + 1, t, red) : 0.0;
+    if (threadIdx.x == 0) {
+      const double b = sqrt(nu);
+      const bool st0 = blockIdx.x == 0;
+      int bd = 0;
+      if (st0) a.beta[c - 1] = b;
+      if (c - 1 == 0) {
+        if (st0) a.stw->gamma = b;
+      } else {
+        if (st0) a.H[(c - 1) + (int64_t)(c - 2) * a.ldH] = b;       // h_{c, c-1} (paper index)
+        if (!(b > a.st->thresh)) {                                  // G-5 (also NaN)
+          bd = 1;
+          if (st0) {
+            a.stw->breakdown = 1;
+            a.stw->m_eff = c - 1;
+          }
+        }
+      }
+      scal[kKMax + 1] = bd;
+      if (!bd) {
+        scal[0] = 1.0 / b;
+        for (int t = 0; t < nw; ++t) {
+          const int j = j0 + t;
+          const double bj = (j == c - 1) ? b : a.beta[j];
+          const double h = dj[t] / (bj * b);
+          if (st0) a.H[j + (int64_t)(c - 1) * a.ldH] = h;
+          scal[1 + t] = -h / bj;
+        }
+      }
+    }
+    consumer_sync(2, kThreads);
+  }
   const int64_t n = a.n, rb = a.row_begin;
   const int64_t t_first = rb >> kSkLogT;
   const int64_t t_last = (rb + n - 1) >> kSkLogT;
@@ -694,8 +635,10 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_stream_tiles(PipeArgs a) {
   double cz = 1.0, cw[kKMax];
 #pragma unroll
   for (int t = 0; t < kKMax; ++t) cw[t] = 0.0;
+  bool skip = false;   // fused K2 found a breakdown: consume the ring, write nothing
   if (UPDATE) {
-    const double* cf = a.coef + (int64_t)a.col0 * (kKMax + 1);
+    const double* cf = a.fuse_k2 ? scal : a.coef + (int64_t)a.col0 * (kKMax + 1);
+    skip = a.fuse_k2 && scal[kKMax + 1] != 0.0;
     cz = cf[0];
 #pragma unroll
     for (int t = 0; t < kKMax; ++t) cw[t] = (t < a.nw) ? cf[1 + t] : 0.0;
@@ -779,7 +722,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_stream_tiles(PipeArgs a) {
             } else {
               val = sb[i];
             }
-            if (UPDATE) {
+            if (UPDATE && !skip) {
               out[r] = val;
               nrm = fma(val, val, nrm);
             }
@@ -791,13 +734,13 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_stream_tiles(PipeArgs a) {
         if (lane == 0) mbar_arrive(empty + rp.stage);
         rp.advance(nstage);
       }
-      if (SKETCH) {
+      if (SKETCH && !skip) {
         tile_fwht(v, fw, tid);
         tile_gather(fw, R, a.s, tile, tid, acc);
         consumer_sync(1, kThreads);
       }
     }
-    if (SKETCH) {
+    if (SKETCH && !skip) {
 #pragma unroll
       for (int q = 0; q < kSkAcc; ++q) {
         const int p = tid + kThreads * q;
@@ -905,28 +848,6 @@ static StencilP stencil_params(const fab_ctx* c) {
   return p;
 }
 
-// per-context CSR row-block list of k_csr_stream (host-built, deterministic)
-struct CsrBlocks {
-  int64_t* d = nullptr;
-  int64_t count = 0;
-};
-static std::vector<std::pair<fab_ctx*, CsrBlocks>> g_blk;
-
-static CsrBlocks* csr_blocks(fab_ctx* c) {
-  for (auto& p : g_blk)
-    if (p.first == c) return &p.second;
-  return nullptr;
-}
-
-void release_long_rows(fab_ctx* c) {
-  for (size_t i = 0; i < g_blk.size(); ++i)
-    if (g_blk[i].first == c) {
-      if (g_blk[i].second.d) cudaFree(g_blk[i].second.d);
-      g_blk.erase(g_blk.begin() + i);
-      return;
-    }
-}
-
 bool stencil_vec_path(const fab_ctx* c) {
   // row pairs never straddle a grid line, and double2 accesses stay aligned
   return c->stencil && (c->op.dims[0] % 2 == 0) && (c->row_begin % 2 == 0);
@@ -960,10 +881,7 @@ int basis_setup_grids(fab_ctx* c) {
   } else {
     // persistent k_csr_stream: every resident CTA (the block count is known
     // only at fab_init; init_vector_norm trims the grid to it)
-    int occ1 = 0;
-    FAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k_csr_stream, kThreads, 0));
-    if (occ1 < 1) occ1 = 1;
-    c->grid_spmv = c->num_sms * occ1;
+    FAB_TRY(csr_grid(c, &c->grid_spmv));
   }
   if (c->grid_spmv < 1) c->grid_spmv = 1;
   return FAB_OK;
@@ -985,48 +903,10 @@ int init_vector_norm(fab_ctx* c) {
     double mx = 0.0;
     for (double v : h) mx = v > mx ? v : mx;
     c->norm_inf = mx;
-    // uniform values (e.g. a scaled 0/1 adjacency, c4): drop the value array
-    // (8 B per entry per SpMV) and fold the value into value_scale
-    if (c->op.values && c->op.nnz > 0) {
-      double v0 = 0.0;
-      FAB_CUDA(cudaMemcpy(&v0, c->op.values, sizeof(double), cudaMemcpyDeviceToHost));
-      int* flag = reinterpret_cast<int*>(c->vec);
-      const int one = 1;
-      FAB_CUDA(cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, c->stream));
-      k_csr_uniform<<<4 * c->num_sms, kThreads, 0, c->stream>>>(c->op.values, c->op.nnz, v0, flag);
-      FAB_CHECK_LAUNCH();
-      int same = 0;
-      FAB_CUDA(cudaMemcpyAsync(&same, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-      FAB_CUDA(cudaStreamSynchronize(c->stream));
-      if (same && isfinite(v0)) {
-        c->op.values = nullptr;
-        c->op.value_scale *= v0;
-      }
-    }
-    // row blocks of k_csr_stream: consecutive rows with <= kCsrNB entries, a
-    // longer row alone
-    std::vector<int64_t> rp(c->n + 1);
-    FAB_CUDA(cudaMemcpy(rp.data(), c->op.row_ptr, (c->n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
-    std::vector<int64_t> bl;
-    bl.reserve(c->op.nnz / kCsrNB + c->n / kThreads + 2);
-    bl.push_back(0);
-    int64_t r = 0;
-    while (r < c->n) {
-      if (rp[r + 1] - rp[r] > kCsrNB) {
-        bl.push_back(++r);
-        continue;
-      }
-      const int64_t q0 = rp[r];
-      while (r < c->n && rp[r + 1] - q0 <= kCsrNB) ++r;
-      bl.push_back(r);
-    }
-    CsrBlocks B;
-    B.count = (int64_t)bl.size() - 1;
-    FAB_CUDA(cudaMalloc(&B.d, bl.size() * sizeof(int64_t)));
-    FAB_CUDA(cudaMemcpy(B.d, bl.data(), bl.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
-    release_long_rows(c);
-    g_blk.push_back({c, B});
-    if (B.count < c->grid_spmv) c->grid_spmv = (int)(B.count > 0 ? B.count : 1);
+    // K1 plan: uniform values, nnz-balanced row blocks, column blocking (csr.cu)
+    FAB_TRY(csr_setup(c));
+    const int64_t nb = csr_max_blocks(c);
+    if (nb < c->grid_spmv) c->grid_spmv = (int)(nb > 0 ? nb : 1);
   }
   // per-step dot partials: one slot per CTA of K1
   const int64_t slots = (int64_t)c->grid_spmv;
@@ -1036,19 +916,24 @@ int init_vector_norm(fab_ctx* c) {
 }
 
 
+// Norm partials of stored column j (double buffered by parity: K3 of step c
+// writes column c's while the fused K2 in the same kernel reads column c-1's)
+double* norm_parts(fab_ctx* c, int j) { return c->part_norm + (int64_t)(j & 1) * c->grid_upd; }
+
 // K2 (+ C2 on several GPUs): the step scalars of column col-1
 int enqueue_scalar(fab_ctx* c, int col, int nw, int nparts, int final_step, cudaStream_t st,
                    int64_t* launches) {
   const double* sums = nullptr;
+  const double* pn = norm_parts(c, col - 1);
   if (c->comm) {
-    k_step_reduce<<<1, kThreads, 0, st>>>(nw, nparts, c->grid_upd, c->part_dots, c->part_norm, c->red, c->st_d);
+    k_step_reduce<<<1, kThreads, 0, st>>>(nw, nparts, c->grid_upd, c->part_dots, pn, c->red, c->st_d);
     FAB_CHECK_LAUNCH();
     ++*launches;
     const int rc = comm_allreduce(c, c->red, (size_t)nw + 1, false, st);
     if (rc != FAB_OK) return rc;
     sums = c->red;
   }
-  k_scalar<<<1, kThreads, 0, st>>>(col, nw, nparts, c->grid_upd, c->part_dots, c->part_norm, sums, c->beta,
+  k_scalar<<<1, kThreads, 0, st>>>(col, nw, nparts, c->grid_upd, c->part_dots, pn, sums, c->beta,
                                    c->H, c->ldH, c->coef, final_step, c->st_d);
   FAB_CHECK_LAUNCH();
   ++*launches;
@@ -1101,14 +986,7 @@ static int launch_k1(fab_ctx* c, int col, int nw, const double* xin, double* z, 
     ++*launches;
     return FAB_OK;
   }
-  CsrBlocks* B = csr_blocks(c);
-  if (!B) return FAB_EORDER;
-  k_csr_stream<<<c->grid_spmv, kThreads, 0, st>>>(c->op.row_ptr, c->op.col_idx, c->op.values, c->op.value_scale,
-                                                  B->d, B->count, c->V, c->ld, col, nw, xin, z, c->part_dots,
-                                                  c->st_d);
-  FAB_CHECK_LAUNCH();
-  ++*launches;
-  return FAB_OK;
+  return csr_spmv(c, col, nw, xin, z, st, launches, nparts);
 }
 
 // The SpMV input for a product with the local vector x (local rows): C1 on
@@ -1160,8 +1038,9 @@ int square_rhs(fab_ctx* c) {
 }
 
 // K3 of step col: w_hat_col from z and the window, its norm partials and
-// (fused) its sketch partials
-int enqueue_k3(fab_ctx* c, int col, int nw, bool fused, cudaStream_t st, int64_t* launches) {
+// (fused) its sketch partials.  nparts_k2 > 0: K2 of the step (k_scalar) is
+// done in K3's prologue from nparts_k2 K1 dot partials (one GPU only).
+int enqueue_k3(fab_ctx* c, int col, int nw, bool fused, cudaStream_t st, int64_t* launches, int nparts_k2 = 0) {
   PipeArgs a{};
   a.V = c->V;
   a.ld = c->ld;
@@ -1172,12 +1051,22 @@ int enqueue_k3(fab_ctx* c, int col, int nw, bool fused, cudaStream_t st, int64_t
   a.z = c->vec;
   a.n = c->n;
   a.row_begin = c->row_begin;
-  a.part_norm = c->part_norm;
+  a.part_norm = norm_parts(c, col);
   a.signs = c->signs_d;
   a.rows = c->rows_d;
   a.s = c->s;
   a.part_sk = c->part_sk;
   a.st = c->st_d;
+  if (nparts_k2 > 0) {
+    a.fuse_k2 = 1;
+    a.nparts_dots = nparts_k2;
+    a.part_dots = c->part_dots;
+    a.part_norm_prev = norm_parts(c, col - 1);
+    a.beta = c->beta;
+    a.H = c->H;
+    a.ldH = c->ldH;
+    a.stw = c->st_d;
+  }
   int rc;
   if (c->mf) {
     a.sp = stencil_params(c);
@@ -1199,8 +1088,11 @@ static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st,
   const int nw = col < k ? col : k;
   int nparts = 0;
   FAB_TRY(enqueue_k1(c, col, nw, c->vec, false, st, launches, &nparts));
-  FAB_TRY(enqueue_scalar(c, col, nw, nparts, 0, st, launches));
-  return enqueue_k3(c, col, nw, fused, st, launches);
+  if (c->comm) {   // C2: the scalars come from the allreduce
+    FAB_TRY(enqueue_scalar(c, col, nw, nparts, 0, st, launches));
+    return enqueue_k3(c, col, nw, fused, st, launches);
+  }
+  return enqueue_k3(c, col, nw, fused, st, launches, nparts);   // K2 fused into K3
 }
 
 // K5 / column 0: sketch partials of columns [c0, c1) (no writes)

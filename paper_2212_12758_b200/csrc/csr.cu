@@ -1,0 +1,448 @@
+// K1 for a CSR operator (A1 + A2 of SURVEY §8a: z = A x and the window dots,
+// PAPER.md l.120-122) -- nnz-balanced row blocks, optionally column-blocked.
+//
+// Row blocks ("CSR-stream"): at fab_init the local rows are cut into blocks
+// of consecutive rows holding <= kCsrNB stored entries and <= kCsrRows rows (a
+// row with more entries is a block of its own).  A persistent CTA takes
+// blocks b = blockIdx.x + i * gridDim.x (static, so every reduction order is
+// fixed and results are bitwise reproducible):
+//   stream : the block's entries are one contiguous range -- col ids and
+//            values coalesced, kCsrU gathers of x per thread issued back to
+//            back -- products to shared memory, row pointers to shared memory;
+//   reduce : G lanes per row (G = pow2 ~ mean row length / 4, 1..32) sum each
+//            row's products in fixed order; the row's window-column loads are
+//            issued before the sum so they overlap it;
+//   long   : a row with > kCsrNB entries is summed by the whole CTA.
+//
+// Column blocking: when x (global length) does not fit in ~40 % of L2, a
+// random gather from HBM moves a 64-B burst per 8-B entry (measured: 69 B of
+// DRAM traffic per entry at n = 2^24, c5).  The entries are then regrouped
+// at fab_init into P column blocks whose slice of x fits in L2; K1 becomes P
+// passes (z = A_0 x_0, z += A_j x_j, the last pass forms the dots), so every
+// gather is an L2 hit and HBM sees the entries once plus 2(P-1) z passes.
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "fab_internal.cuh"
+
+namespace fab {
+
+// entries per block: NB = 1024 (8 KB of products, 4 gathers per thread in
+// flight, 6 CTAs/SM; the default) or 2048 (16 KB, 8 gathers, 4 CTAs/SM;
+// FAB_CSR_NB=2048).  Measured per Krylov step (K1 + K3): c4 339 vs 340 us,
+// c5 4.24 vs 4.37 ms; NB = 4096 (3 CTAs/SM) was slower (420 us, 5.26 ms).
+constexpr int kCsrNBDefault = 1024;
+constexpr int kCsrRows = 2048;               // rows per block (cap)
+
+struct CsrArgs {
+  const int64_t* rp64;     // row pointers (absolute offsets), or
+  const int32_t* rp32;     // row pointers relative to this pass's entries (column-blocked)
+  const int32_t* ci;       // global column ids of this pass
+  const double* vals;      // NULL: every entry is 1 (times vscale)
+  double vscale;
+  const int64_t* blk;      // row blocks: rows [blk[b], blk[b+1])
+  int64_t nblk;
+  const double* V;
+  int64_t ld;
+  int c, nw;               // step column c; window of nw columns ending at c-1
+  const double* xg;        // SpMV input by global column id
+  double* z;
+  double* part;            // per-CTA dot partials (DOTS)
+  const DevState* st;
+};
+
+// Cache policy: the entries, row pointers and z stream through once per pass
+// (L1 no-allocate, L2 evict-first); the gathered slice of x is what L2 must
+// keep (evict-last), so the streams do not push it out.
+__device__ __forceinline__ uint64_t pol_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int ld_s32(const int32_t* p, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int64_t ld_s64(const int64_t* p, uint64_t pol) {
+  int64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_sf(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_keep(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ int64_t rowq(const CsrArgs& a, int64_t r, uint64_t pol) {
+  return a.rp64 ? ld_s64(a.rp64 + r, pol) : (int64_t)ld_s32(a.rp32 + r, pol);
+}
+
+// ACC: z += this pass (else z =); DOTS: form the window dots of the final z
+template <int NWM, bool ACC, bool DOTS, int kCsrNB>
+__global__ void __launch_bounds__(kThreads, kCsrNB == 1024 ? 6 : 4) k_csr_stream(CsrArgs a) {
+  constexpr int kCsrU = kCsrNB / kThreads;
+  if (a.st->breakdown) return;
+  __shared__ double prod[kCsrNB];
+  __shared__ int rps[kCsrRows + 1];
+  __shared__ double red[kWarps * NWM];
+  const double* __restrict__ x = a.V + (int64_t)(a.c - 1) * a.ld;   // local rows of w_hat_{c-1}
+  const int j0 = a.c - a.nw;
+  const int tid = threadIdx.x;
+  double d[NWM];
+#pragma unroll
+  for (int t = 0; t < NWM; ++t) d[t] = 0.0;
+  const uint64_t pf = pol_first(), pl = pol_last();
+
+  for (int64_t b = blockIdx.x; b < a.nblk; b += gridDim.x) {
+    const int64_t r0 = a.blk[b], r1 = a.blk[b + 1];
+    const int64_t q0 = rowq(a, r0, pf), q1 = rowq(a, r1, pf);
+    const int64_t cnt = q1 - q0;
+    if (cnt > kCsrNB) {
+      // long row (r1 == r0 + 1): the whole CTA, products summed in registers
+      double acc = 0.0;
+      for (int64_t base = 0; base < cnt; base += kThreads * kCsrU) {
+        int col[kCsrU];
+        double v[kCsrU];
+#pragma unroll
+        for (int u = 0; u < kCsrU; ++u) {
+          const int64_t i = base + tid + kThreads * u;
+          col[u] = i < cnt ? ld_s32(a.ci + q0 + i, pf) : -1;
+          v[u] = (a.vals && i < cnt) ? ld_sf(a.vals + q0 + i, pf) : 1.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kCsrU; ++u)
+          if (col[u] >= 0) acc = fma(v[u], ld_keep(a.xg + col[u], pl), acc);
+      }
+      double a1[1] = {acc}, o1[1];
+      block_sum<1>(a1, red, o1);
+      if (tid == 0) {
+        double zr = o1[0] * a.vscale;
+        if (ACC) zr += a.z[r0];
+        a.z[r0] = zr;
+        if (DOTS) {
+#pragma unroll
+          for (int t = 0; t < NWM - 1; ++t)
+            if (t < a.nw - 1) d[t] = fma(a.V[(int64_t)(j0 + t) * a.ld + r0], zr, d[t]);
+          d[NWM - 1] = fma(x[r0], zr, d[NWM - 1]);
+        }
+      }
+      continue;
+    }
+    const int nrows = (int)(r1 - r0);
+    // stream: row pointers and products of the block's entries to shared memory
+    for (int i = tid; i <= nrows; i += kThreads) rps[i] = (int)(rowq(a, r0 + i, pf) - q0);
+    {
+      int col[kCsrU];
+      double v[kCsrU], xv[kCsrU];
+#pragma unroll
+      for (int u = 0; u < kCsrU; ++u) {
+        const int i = tid + kThreads * u;
+        col[u] = i < cnt ? ld_s32(a.ci + q0 + i, pf) : -1;
+        v[u] = (a.vals && i < cnt) ? ld_sf(a.vals + q0 + i, pf) : 1.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kCsrU; ++u) xv[u] = col[u] >= 0 ? ld_keep(a.xg + col[u], pl) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kCsrU; ++u) {
+        const int i = tid + kThreads * u;
+        if (i < cnt) prod[i] = v[u] * xv[u];
+      }
+    }
+    __syncthreads();
+    // reduce: G lanes per row, fixed order
+    const int64_t avg = cnt / nrows;
+    int G = 1;
+    while (G < 32 && 4 * G < avg) G <<= 1;
+    const int P = kThreads / G;
+    for (int rb = 0; rb < nrows; rb += P) {
+      const int rl = rb + tid / G, sub = tid & (G - 1);
+      const bool own = rl < nrows && sub == 0;
+      const int64_t row = r0 + rl;
+      double wv[NWM], zold = 0.0;
+      if (own) {   // issue the row's other loads before summing
+        if (ACC) zold = ld_sf(a.z + row, pf);
+        if (DOTS) {
+#pragma unroll
+          for (int t = 0; t < NWM - 1; ++t) wv[t] = (t < a.nw - 1) ? __ldg(a.V + (int64_t)(j0 + t) * a.ld + row) : 0.0;
+          wv[NWM - 1] = __ldg(x + row);
+        }
+      }
+      double acc = 0.0;
+      if (rl < nrows) {
+        const int e = rps[rl + 1];
+        for (int i = rps[rl] + sub; i < e; i += G) acc += prod[i];
+      }
+      for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (own) {
+        double zr = acc * a.vscale;
+        if (ACC) zr += zold;
+        a.z[row] = zr;
+        if (DOTS) {
+#pragma unroll
+          for (int t = 0; t < NWM; ++t) d[t] = fma(wv[t], zr, d[t]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (DOTS) {
+    double out[NWM];
+    block_sum<NWM>(d, red, out);
+    if (tid == 0) {
+      double* p = a.part + (int64_t)blockIdx.x * (kKMax + 1);
+      for (int t = 0; t < a.nw - 1; ++t) p[t] = out[t];
+      p[a.nw - 1] = out[NWM - 1];
+    }
+  }
+}
+
+// uniform values: flag stays 1 iff every value equals v0
+__global__ void k_csr_uniform(const double* __restrict__ vals, int64_t nnz, double v0, int* flag) {
+  bool same = true;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz; q += (int64_t)gridDim.x * blockDim.x)
+    same &= (vals[q] == v0);
+  if (!__syncthreads_and(same) && threadIdx.x == 0) atomicExch(flag, 0);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+struct CsrPass {
+  const int64_t* rp64 = nullptr;
+  const int32_t* rp32 = nullptr;
+  const int32_t* ci = nullptr;
+  const double* vals = nullptr;
+  int64_t* blk = nullptr;   // owned
+  int64_t nblk = 0;
+};
+
+struct CsrPlan {
+  std::vector<CsrPass> pass;
+  std::vector<void*> owned;   // device buffers of the column-blocked copy
+  int64_t width = 0;          // columns per block (0: not column-blocked)
+  int nb = kCsrNBDefault;     // entries per row block
+  ~CsrPlan() {
+    for (auto& p : pass)
+      if (p.blk) cudaFree(p.blk);
+    for (void* q : owned) cudaFree(q);
+  }
+};
+
+// row blocks over row pointers q(r), r in [0, n]
+template <typename Q>
+static std::vector<int64_t> build_blocks(int64_t n, int64_t kCsrNB, Q q) {
+  std::vector<int64_t> bl;
+  bl.push_back(0);
+  int64_t r = 0;
+  while (r < n) {
+    if (q(r + 1) - q(r) > kCsrNB) {
+      bl.push_back(++r);
+      continue;
+    }
+    const int64_t q0 = q(r), rs = r;
+    while (r < n && q(r + 1) - q0 <= kCsrNB && r - rs < kCsrRows) ++r;
+    bl.push_back(r);
+  }
+  return bl;
+}
+
+static int upload_blocks(const std::vector<int64_t>& bl, CsrPass* p) {
+  p->nblk = (int64_t)bl.size() - 1;
+  FAB_CUDA(cudaMalloc(&p->blk, bl.size() * sizeof(int64_t)));
+  FAB_CUDA(cudaMemcpy(p->blk, bl.data(), bl.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  return FAB_OK;
+}
+
+void csr_release(fab_ctx* c) {
+  delete c->csr;
+  c->csr = nullptr;
+}
+
+static int csr_nb_choice() {
+  const char* e = getenv("FAB_CSR_NB");
+  return (e && atoi(e) == 2048) ? 2048 : kCsrNBDefault;
+}
+
+int csr_grid(fab_ctx* c, int* grid) {
+  int occ = 0;
+  if (csr_nb_choice() == 2048)
+    FAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_stream<4, false, true, 2048>, kThreads, 0));
+  else
+    FAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_stream<4, false, true, 1024>, kThreads, 0));
+  if (occ < 1) occ = 1;
+  *grid = c->num_sms * occ;
+  return FAB_OK;
+}
+
+// At fab_init: uniform-value detection, the row blocks, and (if x is larger
+// than the L2 budget) the column-blocked copy of the entries.
+int csr_setup(fab_ctx* c) {
+  csr_release(c);
+  CsrPlan* plan = new CsrPlan();
+  c->csr = plan;
+  plan->nb = csr_nb_choice();
+  // uniform values (e.g. a scaled 0/1 adjacency, c4): drop the value array
+  // (8 B per entry per SpMV) and fold the value into value_scale
+  if (c->op.values && c->op.nnz > 0) {
+    double v0 = 0.0;
+    FAB_CUDA(cudaMemcpy(&v0, c->op.values, sizeof(double), cudaMemcpyDeviceToHost));
+    int* flag = reinterpret_cast<int*>(c->vec);
+    const int one = 1;
+    FAB_CUDA(cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    k_csr_uniform<<<4 * c->num_sms, kThreads, 0, c->stream>>>(c->op.values, c->op.nnz, v0, flag);
+    FAB_CHECK_LAUNCH();
+    int same = 0;
+    FAB_CUDA(cudaMemcpyAsync(&same, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    FAB_CUDA(cudaStreamSynchronize(c->stream));
+    if (same && isfinite(v0)) {
+      c->op.values = nullptr;
+      c->op.value_scale *= v0;
+    }
+  }
+  const int64_t n = c->n, nnz = c->op.nnz;
+  std::vector<int64_t> rp(n + 1);
+  FAB_CUDA(cudaMemcpy(rp.data(), c->op.row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  // column-block width: the slice of x a pass gathers from stays in ~40 % of L2
+  int l2 = 0;
+  FAB_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device));
+  int64_t width = (int64_t)(0.4 * (double)l2) / 8;
+  if (width < 1024) width = 1024;
+  const char* env = getenv("FAB_CSR_COLBLOCK");   // tests: force a width (columns)
+  if (env && atoll(env) > 0) width = atoll(env);
+  const int64_t P = (c->n_global + width - 1) / width;
+  if (P <= 1 || nnz == 0) {
+    CsrPass p;
+    p.rp64 = c->op.row_ptr;
+    p.ci = c->op.col_idx;
+    p.vals = c->op.values;
+    FAB_TRY(upload_blocks(build_blocks(n, plan->nb, [&](int64_t r) { return rp[r]; }), &p));
+    plan->pass.push_back(p);
+    return FAB_OK;
+  }
+  // column-blocked copy: entries of block j (columns [j w, (j+1) w)) of every
+  // local row, rows in order, in-row order kept
+  std::vector<int32_t> ci(nnz);
+  FAB_CUDA(cudaMemcpy(ci.data(), c->op.col_idx, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  std::vector<double> va;
+  if (c->op.values) {
+    va.resize(nnz);
+    FAB_CUDA(cudaMemcpy(va.data(), c->op.values, nnz * sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  std::vector<int64_t> cntb(P, 0);
+  for (int64_t q = 0; q < nnz; ++q) ++cntb[ci[q] / width];
+  std::vector<int64_t> base(P + 1, 0);
+  for (int64_t j = 0; j < P; ++j) {
+    if (cntb[j] >= ((int64_t)1 << 31)) return FAB_EINVAL;   // int32 relative row pointers
+    base[j + 1] = base[j] + cntb[j];
+  }
+  std::vector<int32_t> ci2(nnz), rp2((size_t)P * (n + 1));
+  std::vector<double> va2(va.empty() ? 0 : nnz);
+  std::vector<int64_t> fill(P, 0);
+  for (int64_t r = 0; r < n; ++r) {
+    for (int64_t j = 0; j < P; ++j) rp2[(size_t)j * (n + 1) + r] = (int32_t)fill[j];
+    for (int64_t q = rp[r]; q < rp[r + 1]; ++q) {
+      const int64_t j = ci[q] / width;
+      const int64_t dst = base[j] + fill[j]++;
+      ci2[dst] = ci[q];
+      if (!va.empty()) va2[dst] = va[q];
+    }
+  }
+  for (int64_t j = 0; j < P; ++j) rp2[(size_t)j * (n + 1) + n] = (int32_t)fill[j];
+  int32_t *dci = nullptr, *drp = nullptr;
+  double* dva = nullptr;
+  FAB_CUDA(cudaMalloc(&dci, nnz * sizeof(int32_t)));
+  plan->owned.push_back(dci);
+  FAB_CUDA(cudaMalloc(&drp, rp2.size() * sizeof(int32_t)));
+  plan->owned.push_back(drp);
+  FAB_CUDA(cudaMemcpy(dci, ci2.data(), nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
+  FAB_CUDA(cudaMemcpy(drp, rp2.data(), rp2.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  if (!va2.empty()) {
+    FAB_CUDA(cudaMalloc(&dva, nnz * sizeof(double)));
+    plan->owned.push_back(dva);
+    FAB_CUDA(cudaMemcpy(dva, va2.data(), nnz * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  plan->width = width;
+  for (int64_t j = 0; j < P; ++j) {
+    CsrPass p;
+    const int32_t* rj = rp2.data() + (size_t)j * (n + 1);
+    p.rp32 = drp + (size_t)j * (n + 1);
+    p.ci = dci + base[j];
+    p.vals = dva ? dva + base[j] : nullptr;
+    FAB_TRY(upload_blocks(build_blocks(n, plan->nb, [&](int64_t r) { return (int64_t)rj[r]; }), &p));
+    plan->pass.push_back(p);
+  }
+  return FAB_OK;
+}
+
+int csr_passes(const fab_ctx* c) { return c->csr ? (int)c->csr->pass.size() : 0; }
+
+int64_t csr_max_blocks(const fab_ctx* c) {
+  int64_t m = 0;
+  if (c->csr)
+    for (const auto& p : c->csr->pass) m = p.nblk > m ? p.nblk : m;
+  return m;
+}
+
+template <int NWM, int NB>
+static void launch_pass_nb(const CsrArgs& a, int grid, bool acc, bool dots, cudaStream_t st) {
+  if (!acc && dots) k_csr_stream<NWM, false, true, NB><<<grid, kThreads, 0, st>>>(a);
+  else if (!acc) k_csr_stream<NWM, false, false, NB><<<grid, kThreads, 0, st>>>(a);
+  else if (dots) k_csr_stream<NWM, true, true, NB><<<grid, kThreads, 0, st>>>(a);
+  else k_csr_stream<NWM, true, false, NB><<<grid, kThreads, 0, st>>>(a);
+}
+
+template <int NWM>
+static void launch_pass(const CsrArgs& a, int grid, int nb, bool acc, bool dots, cudaStream_t st) {
+  if (nb == 2048) launch_pass_nb<NWM, 2048>(a, grid, acc, dots, st);
+  else launch_pass_nb<NWM, 1024>(a, grid, acc, dots, st);
+}
+
+// z = A xin (+ the window dots when nw > 0), one launch per column block.
+int csr_spmv(fab_ctx* c, int col, int nw, const double* xin, double* z, cudaStream_t st, int64_t* launches,
+             int* nparts) {
+  CsrPlan* plan = c->csr;
+  if (!plan || plan->pass.empty()) return FAB_EORDER;
+  *nparts = c->grid_spmv;
+  const int np = (int)plan->pass.size();
+  for (int j = 0; j < np; ++j) {
+    const CsrPass& p = plan->pass[j];
+    CsrArgs a;
+    a.rp64 = p.rp64;
+    a.rp32 = p.rp32;
+    a.ci = p.ci;
+    a.vals = p.vals;
+    a.vscale = c->op.value_scale;
+    a.blk = p.blk;
+    a.nblk = p.nblk;
+    a.V = c->V;
+    a.ld = c->ld;
+    a.c = col;
+    a.nw = nw;
+    a.xg = xin;
+    a.z = z;
+    a.part = c->part_dots;
+    a.st = c->st_d;
+    const bool acc = j > 0, dots = (j == np - 1) && nw > 0;
+    if (c->k_max <= 2) launch_pass<2>(a, c->grid_spmv, plan->nb, acc, dots, st);
+    else if (c->k_max <= 4) launch_pass<4>(a, c->grid_spmv, plan->nb, acc, dots, st);
+    else launch_pass<8>(a, c->grid_spmv, plan->nb, acc, dots, st);
+    FAB_CHECK_LAUNCH();
+    ++*launches;
+  }
+  return FAB_OK;
+}
+
+}  // namespace fab

@@ -44,6 +44,7 @@ struct DevState {
 };
 
 struct Comm;   // comm.cu: NCCL communicator of the row-partitioned path
+struct CsrPlan;   // csr.cu: row blocks / column-blocked copy of a CSR operator
 
 }  // namespace fab
 
@@ -120,6 +121,7 @@ struct fab_ctx {
 
   double* wbuf = nullptr;             // whitening scratch (Q, R, R^-1), allocated on first use
   fab::Comm* comm = nullptr;          // NULL: one GPU
+  fab::CsrPlan* csr = nullptr;        // CSR operator: K1 plan (csr.cu)
   std::vector<int64_t> rank_rows;     // row_begin of every rank, plus n_global
 
   // cached Algorithm 1 graph
@@ -236,7 +238,14 @@ int run_basis_sgs(fab_ctx* c, int m);
 int run_basis_arnoldi(fab_ctx* c, int m);
 // whiten.cu (Algorithm 2 + whitening -> Algorithm 1)
 int run_basis_whiten(fab_ctx* c, int m, int k, double cond_max, int* whitened_at, double* cond_at);
-void release_long_rows(fab_ctx* c);
+// csr.cu (K1 of a CSR operator)
+int csr_grid(fab_ctx* c, int* grid);
+int csr_setup(fab_ctx* c);                   // uniform values, row blocks, column blocking
+int csr_spmv(fab_ctx* c, int col, int nw, const double* xin, double* z, cudaStream_t st, int64_t* launches,
+             int* nparts);
+int csr_passes(const fab_ctx* c);
+int64_t csr_max_blocks(const fab_ctx* c);
+void csr_release(fab_ctx* c);
 int launch_sketch_cols(fab_ctx* c, int c0, int c1, cudaStream_t st);
 // sketch.cu
 void host_sketch_rows(uint64_t seed, int64_t N, int s, int64_t* out);

@@ -431,3 +431,37 @@ def test_whitened_basis_graph_exact():
         sv.compress(mode, iters=80)
         y = sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()
         assert rel(y, exact) <= 1e-10, (mode, rel(y, exact))
+
+
+# ---- CSR K1 variants: column-blocked passes (forced at small n) ----------------
+@pytest.mark.parametrize("name,kw", [
+    ("c5", dict(n=5001, m=12, s=40)),            # random columns: entries in every block
+    ("c4", dict(n=1 << 14, m=20, s=50)),          # hubs: long rows split across passes
+    ("e4", dict(n=5001, m=15, s=40)),             # squared operator: K0 and K1 both blocked
+])
+def test_csr_column_blocked_passes(name, kw, monkeypatch):
+    """K1 as P column-blocked passes (z = A_0 x_0, z += A_j x_j, dots on the
+    last pass) -- the layout fab_init picks when x exceeds the L2 budget --
+    forced here with FAB_CSR_COLBLOCK=1000 columns per block: f_m against
+    the oracle at 1e-10 and against the unblocked CSR path at 1e-12."""
+    import torch
+    import paper_2212_12758_b200 as fab
+    p = fp.make(name, **kw)
+    ip, ix, dv = p.csr()
+    square = name == "e4"
+    f = "sign" if square else p.f
+    outs = []
+    for width in ("1000", "0"):
+        monkeypatch.setenv("FAB_CSR_COLBLOCK", width)
+        sv = fab.Solver(fab.Operator.csr(ip, ix, dv), torch.as_tensor(p.b).cuda(), p.m, p.k, p.s, square=square)
+        sv.sketch(p.s, p.sketch_seed)
+        sv.basis(p.m, p.k)
+        sv.compress("blendenpik", iters=40)
+        outs.append(sv.apply(f, p.alpha if not square else 1.0, p.sigma).cpu().numpy())
+        sv.close()
+    if square:
+        ref = ofab.sign(p.scipy(), p.b, p.m, p.k, p.s, p.sketch_seed, mode="blendenpik", lsqr_iters=40)
+    else:
+        ref = oracle_solve(p, "blendenpik")
+    assert rel(outs[0], ref["f_m"]) <= 1e-10, rel(outs[0], ref["f_m"])
+    assert rel(outs[0], outs[1]) <= 1e-12
