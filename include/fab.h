@@ -218,6 +218,21 @@ int fab_init(fab_ctx** ctx, const fab_operator* A, const double* b, const fab_op
    breakdown.  Errors: EORDER, EINVAL, ECUDA. */
 int fab_basis(fab_ctx* ctx, int m, int k);
 
+/* Multi-RHS (the paper treats one b at a time): Algorithm 2
+   (as fab_basis) for the p contexts ctx[0..p-1], 1 <= p <= 4, in one CUDA
+   graph.  The contexts must be for the same operator -- the same CSR arrays
+   (device pointers) and value_scale, or the same stencil -- on one GPU (no
+   communicator), with the same device, stream, k_max, flags and n; each has
+   its own b, workspace and sketch state.  For a CSR operator every Krylov
+   step reads the entries ONCE for all p vectors (SpMM; the column ids and
+   values are the dominant HBM stream of K1), the rest of the step is per
+   context.  Each context ends in exactly the state fab_basis(ctx[i], m, k)
+   leaves (bitwise: same kernels, grids and per-vector reduction order);
+   fab_info.ms_basis of every context is the batch's time.  Returns the
+   largest warning (FAB_BREAKDOWN if any context broke down).  Errors:
+   EINVAL (count, duplicates, mismatched contexts or capacities), ECUDA. */
+int fab_basis_batch(fab_ctx** ctx, int p, int m, int k);
+
 /* Algorithm 2 with whitening (l.106-108, l.395, l.457-458): Algorithm 2
    (truncation k, fused sketch) while monitoring Theta V_i = Q_i R_i; the
    first time ||R_i||_1 ||R_i^{-1}||_1 > cond_max (the paper: 1000), V_i <-

@@ -20,7 +20,7 @@ from . import _lib
 from ._lib import (FabError, FabInfo, FabLsqrOpts, FabOperator, FabOpts, FUNCS, GET, MODES, check,
                    lib)
 
-__all__ = ["Operator", "Solver", "FabError", "lib"]
+__all__ = ["Operator", "Solver", "FabError", "lib", "basis_batch", "solve"]
 
 
 def _torch():
@@ -234,6 +234,17 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+def basis_batch(solvers, m, k):
+    """Multi-RHS: Algorithm 2 for several Solvers of the same Operator at once
+    (fab_basis_batch: one pass over the CSR entries per Krylov step for all
+    of them); each Solver ends as after its own .basis(m, k)."""
+    arr = (C.c_void_p * len(solvers))(*[sv.ctx.value for sv in solvers])
+    st = check(lib.fab_basis_batch(arr, len(solvers), m, k), "fab_basis_batch")
+    for sv in solvers:
+        sv.status["basis"] = st
+    return st
 
 
 def solve(problem, mode="blendenpik", lsqr_iters=0, lsqr_tol=0.0, fused=True, csr=False):

@@ -24,7 +24,8 @@ MODES = {"blendenpik": FAB_BLENDENPIK, "sketch_solve": FAB_SKETCH_SOLVE, "none":
 FUNCS = {"exp": FAB_EXP, "sqrt": FAB_SQRT, "invsqrt": FAB_INVSQRT, "poly": FAB_POLY, "sign": FAB_SIGN}
 
 # every function declared in include/fab.h
-EXPORTS = ("fab_version", "fab_strerror", "fab_workspace_size", "fab_init", "fab_basis", "fab_basis_sgs", "fab_basis_arnoldi", "fab_basis_whiten",
+EXPORTS = ("fab_version", "fab_strerror", "fab_workspace_size", "fab_init", "fab_basis", "fab_basis_batch",
+           "fab_basis_sgs", "fab_basis_arnoldi", "fab_basis_whiten",
            "fab_sketch", "fab_compress", "fab_apply", "fab_get", "fab_get_column", "fab_get_vrows",
            "fab_set", "fab_last_error", "fab_destroy", "fab_comm_unique_id", "fab_comm_init",
            "fab_comm_destroy")
@@ -79,6 +80,7 @@ def load():
         "fab_workspace_size": (I, [C.POINTER(FabOperator), C.POINTER(FabOpts), C.POINTER(C.c_size_t)]),
         "fab_init": (I, [C.POINTER(P), C.POINTER(FabOperator), P, C.POINTER(FabOpts)]),
         "fab_basis": (I, [P, I, I]),
+        "fab_basis_batch": (I, [C.POINTER(P), I, I, I]),
         "fab_basis_sgs": (I, [P, I]),
         "fab_basis_arnoldi": (I, [P, I]),
         "fab_basis_whiten": (I, [P, I, I, D]),

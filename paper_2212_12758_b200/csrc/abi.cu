@@ -163,6 +163,7 @@ static void free_ctx(fab_ctx* c) {
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->gexec_sgs) cudaGraphExecDestroy(c->gexec_sgs);
   if (c->gexec_arn) cudaGraphExecDestroy(c->gexec_arn);
+  if (c->gexec_bat) cudaGraphExecDestroy(c->gexec_bat);
   if (c->wbuf) cudaFree(c->wbuf);
   if (c->part_dots) cudaFree(c->part_dots);
   if (c->own_ws && c->ws) cudaFree(c->ws);
@@ -322,15 +323,10 @@ int fab_init(fab_ctx** out, const fab_operator* A, const double* b, const fab_op
   return FAB_OK;
 }
 
-int fab_basis(fab_ctx* c, int m, int k) {
-  if (!c) return FAB_EINVAL;
-  if (k < 1 || k > c->k_max || m < 1 || m > c->m_max || m >= c->n_global) return FAB_EINVAL;
-  if (c->sketch_ready && c->s < m + 1) return FAB_EINVAL;
-  FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
-  int rc = run_basis(c, m, k);
-  if (rc != FAB_OK) return rc;
-  double ms = 0;
-  if ((rc = timed_end(c, &ms)) != FAB_OK) return rc;
+namespace fab {
+// state of a context after an Algorithm 2 basis (fab_basis, fab_basis_batch)
+static int basis_finish(fab_ctx* c, int m, int k, double ms) {
+  int rc;
   if ((rc = pull_state(c)) != FAB_OK) return rc;
   c->m = m;
   c->k = k;
@@ -353,6 +349,61 @@ int fab_basis(fab_ctx* c, int m, int k) {
   c->info.h_last = hl;
   c->info.basis_alg = 2;
   return c->breakdown ? FAB_BREAKDOWN : FAB_OK;
+}
+}  // namespace fab
+
+int fab_basis(fab_ctx* c, int m, int k) {
+  if (!c) return FAB_EINVAL;
+  if (k < 1 || k > c->k_max || m < 1 || m > c->m_max || m >= c->n_global) return FAB_EINVAL;
+  if (c->sketch_ready && c->s < m + 1) return FAB_EINVAL;
+  FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
+  int rc = run_basis(c, m, k);
+  if (rc != FAB_OK) return rc;
+  double ms = 0;
+  if ((rc = timed_end(c, &ms)) != FAB_OK) return rc;
+  return basis_finish(c, m, k, ms);
+}
+
+int fab_basis_batch(fab_ctx** cs, int p, int m, int k) {
+  if (!cs || p < 1 || p > kBatchMaxCtx) return FAB_EINVAL;
+  fab_ctx* c = cs[0];
+  for (int i = 0; i < p; ++i) {
+    fab_ctx* d = cs[i];
+    if (!d) return FAB_EINVAL;
+    for (int j = 0; j < i; ++j)
+      if (cs[j] == d) return FAB_EINVAL;
+    if (k < 1 || k > d->k_max || m < 1 || m > d->m_max || m >= d->n_global) return FAB_EINVAL;
+    if (d->sketch_ready && d->s < m + 1) return FAB_EINVAL;
+    // one operator, one device and stream, one GPU
+    if (d->comm || d->device != c->device || d->stream != c->stream) return FAB_EINVAL;
+    if (d->stencil != c->stencil || d->n != c->n || d->ld != c->ld || d->k_max != c->k_max ||
+        d->grid_spmv != c->grid_spmv || d->grid_upd != c->grid_upd || d->mf != c->mf ||
+        ((d->flags ^ c->flags) & FAB_FLAG_SQUARE))
+      return FAB_EINVAL;
+    if (c->stencil) {
+      for (int t = 0; t < 3; ++t)
+        if (d->op.dims[t] != c->op.dims[t]) return FAB_EINVAL;
+      for (int t = 0; t < 7; ++t)
+        if (d->op.coeffs[t] != c->op.coeffs[t]) return FAB_EINVAL;
+    } else if (d->op.row_ptr != c->op.row_ptr || d->op.col_idx != c->op.col_idx ||
+               d->op.values != c->op.values || d->op.value_scale != c->op.value_scale) {
+      return FAB_EINVAL;
+    }
+  }
+  FAB_CUDA(cudaSetDevice(c->device));
+  FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
+  int rc = run_basis_batch(cs, p, m, k);
+  if (rc != FAB_OK) return rc;
+  double ms = 0;
+  if ((rc = timed_end(c, &ms)) != FAB_OK) return rc;
+  int worst = FAB_OK;
+  for (int i = 0; i < p; ++i) {
+    rc = basis_finish(cs[i], m, k, ms);
+    if (rc < 0) return rc;
+    if (rc > worst) worst = rc;
+    cs[i]->info.launches_basis = c->g_bat_launches;
+  }
+  return worst;
 }
 
 int fab_basis_arnoldi(fab_ctx* c, int m) {

@@ -1169,3 +1169,83 @@ int run_basis(fab_ctx* c, int m, int k) {
 }
 
 }  // namespace fab
+
+namespace fab {
+
+// Multi-RHS (fab_basis_batch): Algorithm 2 for p contexts of one operator in
+// one graph.  CSR: each step's K0/K1 is ONE pass over the entries for all p
+// vectors (csr_spmv_multi); stencil: per-context K1 (no entries to share).
+// K2/K3, the prologue, the final scalars and the sketch stay per context, on
+// each context's own buffers, so every context's result is bitwise that of
+// fab_basis (same kernels, same grids, same per-vector arithmetic order).
+static int enqueue_batch(fab_ctx* const* cs, int p, int m, int k, cudaStream_t st, int64_t* launches) {
+  for (int i = 0; i < p; ++i) FAB_TRY(enqueue_basis_prologue(cs[i], m, cs[i]->sketch_ready, st, launches));
+  const bool sq = (cs[0]->flags & FAB_FLAG_SQUARE) != 0;
+  for (int col = 1; col <= m; ++col) {
+    const int nw = col < k ? col : k;
+    int nparts = 0;
+    if (cs[0]->stencil) {
+      for (int i = 0; i < p; ++i) FAB_TRY(enqueue_k1(cs[i], col, nw, cs[i]->vec, false, st, launches, &nparts));
+    } else {
+      const double* xin[kBatchMaxCtx];
+      double* z[kBatchMaxCtx];
+      for (int i = 0; i < p; ++i) xin[i] = cs[i]->V + (int64_t)(col - 1) * cs[i]->ld;
+      if (sq) {   // K0: t_i = A w_hat_{col-1} of every context, one pass
+        for (int i = 0; i < p; ++i) z[i] = cs[i]->sq;
+        int np0 = 0;
+        FAB_TRY(csr_spmv_multi(cs, p, col, 0, xin, z, st, launches, &np0));
+        for (int i = 0; i < p; ++i) xin[i] = cs[i]->sq;
+      }
+      for (int i = 0; i < p; ++i) z[i] = cs[i]->vec;
+      FAB_TRY(csr_spmv_multi(cs, p, col, nw, xin, z, st, launches, &nparts));
+    }
+    for (int i = 0; i < p; ++i) FAB_TRY(enqueue_k3(cs[i], col, nw, cs[i]->sketch_ready, st, launches, nparts));
+  }
+  for (int i = 0; i < p; ++i) {
+    FAB_TRY(enqueue_scalar(cs[i], m + 1, 0, 0, 1, st, launches));
+    if (cs[i]->sketch_ready) {
+      FAB_TRY(sketch_finalize(cs[i], m + 1, st));
+      ++*launches;
+    }
+  }
+  return FAB_OK;
+}
+
+int run_basis_batch(fab_ctx* const* cs, int p, int m, int k) {
+  fab_ctx* c = cs[0];
+  std::vector<fab_ctx*> key(cs, cs + p);
+  std::vector<int> fz(p), ss(p);
+  for (int i = 0; i < p; ++i) {
+    fz[i] = cs[i]->sketch_ready ? 1 : 0;
+    ss[i] = cs[i]->s;
+  }
+  if (!(c->gexec_bat && c->g_bat_ctx == key && c->g_bat_fused == fz && c->g_bat_s == ss && c->g_bat_m == m &&
+        c->g_bat_k == k)) {
+    if (c->gexec_bat) {
+      cudaGraphExecDestroy(c->gexec_bat);
+      c->gexec_bat = nullptr;
+    }
+    int64_t launches = 0;
+    FAB_CUDA(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue_batch(cs, p, m, k, c->cap, &launches);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(c->cap, &graph);
+    if (rc != FAB_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    FAB_CUDA(e);
+    FAB_CUDA(cudaGraphInstantiate(&c->gexec_bat, graph, 0));
+    cudaGraphDestroy(graph);
+    c->g_bat_ctx = key;
+    c->g_bat_fused = fz;
+    c->g_bat_s = ss;
+    c->g_bat_m = m;
+    c->g_bat_k = k;
+    c->g_bat_launches = launches;
+  }
+  FAB_CUDA(cudaGraphLaunch(c->gexec_bat, c->stream));
+  return FAB_OK;
+}
+
+}  // namespace fab

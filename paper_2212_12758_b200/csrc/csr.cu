@@ -28,12 +28,13 @@
 
 namespace fab {
 
-// entries per block: NB = 1024 (8 KB of products, 4 gathers per thread in
-// flight, 6 CTAs/SM; the default) or 2048 (16 KB, 8 gathers, 4 CTAs/SM;
-// FAB_CSR_NB=2048).  Measured per Krylov step (K1 + K3): c4 339 vs 340 us,
-// c5 4.24 vs 4.37 ms; NB = 4096 (3 CTAs/SM) was slower (420 us, 5.26 ms).
-constexpr int kCsrNBDefault = 1024;
+// entries per block: NB = 1024 (8 KB of products per vector, 4 gathers per
+// thread in flight, 6 CTAs/SM).  Measured per Krylov step (K1 + K3): NB =
+// 1024 / 2048 / 4096: c4 339 / 340 / 420 us, c5 4.24 / 4.37 / 5.26 ms.
+constexpr int kCsrNB = 1024;
 constexpr int kCsrRows = 2048;               // rows per block (cap)
+
+constexpr int kBatchMax = 4;   // multi-RHS: vectors per SpMM pass (fab_basis_batch)
 
 struct CsrArgs {
   const int64_t* rp64;     // row pointers (absolute offsets), or
@@ -43,13 +44,14 @@ struct CsrArgs {
   double vscale;
   const int64_t* blk;      // row blocks: rows [blk[b], blk[b+1])
   int64_t nblk;
-  const double* V;
   int64_t ld;
   int c, nw;               // step column c; window of nw columns ending at c-1
-  const double* xg;        // SpMV input by global column id
-  double* z;
-  double* part;            // per-CTA dot partials (DOTS)
-  const DevState* st;
+  // per right-hand side i < P (one context each)
+  const double* V[kBatchMax];
+  const double* xg[kBatchMax];   // SpMV input by global column id
+  double* z[kBatchMax];
+  double* part[kBatchMax];       // per-CTA dot partials (DOTS)
+  const DevState* st[kBatchMax];
 };
 
 // Cache policy: the entries, row pointers and z stream through once per pass
@@ -90,20 +92,30 @@ __device__ __forceinline__ int64_t rowq(const CsrArgs& a, int64_t r, uint64_t po
   return a.rp64 ? ld_s64(a.rp64 + r, pol) : (int64_t)ld_s32(a.rp32 + r, pol);
 }
 
-// ACC: z += this pass (else z =); DOTS: form the window dots of the final z
-template <int NWM, bool ACC, bool DOTS, int kCsrNB>
-__global__ void __launch_bounds__(kThreads, kCsrNB == 1024 ? 6 : 4) k_csr_stream(CsrArgs a) {
+// ACC: z += this pass (else z =); DOTS: form the window dots of the final z.
+// P right-hand sides share every entry load (multi-RHS SpMM); per vector the
+// arithmetic and its order are exactly those of P = 1.
+template <int NWM, bool ACC, bool DOTS, int P>
+__global__ void __launch_bounds__(kThreads, P == 1 ? 6 : 3) k_csr_stream(CsrArgs a) {
   constexpr int kCsrU = kCsrNB / kThreads;
-  if (a.st->breakdown) return;
-  __shared__ double prod[kCsrNB];
+  bool live[P];
+  bool any = false;
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    live[i] = !a.st[i]->breakdown;
+    any |= live[i];
+  }
+  if (!any) return;
+  __shared__ double prod[P][kCsrNB];
   __shared__ int rps[kCsrRows + 1];
-  __shared__ double red[kWarps * NWM];
-  const double* __restrict__ x = a.V + (int64_t)(a.c - 1) * a.ld;   // local rows of w_hat_{c-1}
+  __shared__ double red[kWarps * NWM * P];
   const int j0 = a.c - a.nw;
   const int tid = threadIdx.x;
-  double d[NWM];
+  double d[P][NWM];
 #pragma unroll
-  for (int t = 0; t < NWM; ++t) d[t] = 0.0;
+  for (int i = 0; i < P; ++i)
+#pragma unroll
+    for (int t = 0; t < NWM; ++t) d[i][t] = 0.0;
   const uint64_t pf = pol_first(), pl = pol_last();
 
   for (int64_t b = blockIdx.x; b < a.nblk; b += gridDim.x) {
@@ -112,53 +124,67 @@ __global__ void __launch_bounds__(kThreads, kCsrNB == 1024 ? 6 : 4) k_csr_stream
     const int64_t cnt = q1 - q0;
     if (cnt > kCsrNB) {
       // long row (r1 == r0 + 1): the whole CTA, products summed in registers
-      double acc = 0.0;
+      double acc[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) acc[i] = 0.0;
       for (int64_t base = 0; base < cnt; base += kThreads * kCsrU) {
         int col[kCsrU];
         double v[kCsrU];
 #pragma unroll
         for (int u = 0; u < kCsrU; ++u) {
-          const int64_t i = base + tid + kThreads * u;
-          col[u] = i < cnt ? ld_s32(a.ci + q0 + i, pf) : -1;
-          v[u] = (a.vals && i < cnt) ? ld_sf(a.vals + q0 + i, pf) : 1.0;
+          const int64_t q = base + tid + kThreads * u;
+          col[u] = q < cnt ? ld_s32(a.ci + q0 + q, pf) : -1;
+          v[u] = (a.vals && q < cnt) ? ld_sf(a.vals + q0 + q, pf) : 1.0;
         }
 #pragma unroll
         for (int u = 0; u < kCsrU; ++u)
-          if (col[u] >= 0) acc = fma(v[u], ld_keep(a.xg + col[u], pl), acc);
-      }
-      double a1[1] = {acc}, o1[1];
-      block_sum<1>(a1, red, o1);
-      if (tid == 0) {
-        double zr = o1[0] * a.vscale;
-        if (ACC) zr += a.z[r0];
-        a.z[r0] = zr;
-        if (DOTS) {
+          if (col[u] >= 0) {
 #pragma unroll
-          for (int t = 0; t < NWM - 1; ++t)
-            if (t < a.nw - 1) d[t] = fma(a.V[(int64_t)(j0 + t) * a.ld + r0], zr, d[t]);
-          d[NWM - 1] = fma(x[r0], zr, d[NWM - 1]);
+            for (int i = 0; i < P; ++i) acc[i] = fma(v[u], ld_keep(a.xg[i] + col[u], pl), acc[i]);
+          }
+      }
+      double o[P];
+      block_sum<P>(acc, red, o);
+      if (tid == 0) {
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          if (!live[i]) continue;
+          double zr = o[i] * a.vscale;
+          if (ACC) zr += a.z[i][r0];
+          a.z[i][r0] = zr;
+          if (DOTS) {
+#pragma unroll
+            for (int t = 0; t < NWM - 1; ++t)
+              if (t < a.nw - 1) d[i][t] = fma(a.V[i][(int64_t)(j0 + t) * a.ld + r0], zr, d[i][t]);
+            d[i][NWM - 1] = fma(a.V[i][(int64_t)(a.c - 1) * a.ld + r0], zr, d[i][NWM - 1]);
+          }
         }
       }
       continue;
     }
     const int nrows = (int)(r1 - r0);
     // stream: row pointers and products of the block's entries to shared memory
-    for (int i = tid; i <= nrows; i += kThreads) rps[i] = (int)(rowq(a, r0 + i, pf) - q0);
+    for (int q = tid; q <= nrows; q += kThreads) rps[q] = (int)(rowq(a, r0 + q, pf) - q0);
     {
       int col[kCsrU];
-      double v[kCsrU], xv[kCsrU];
+      double v[kCsrU], xv[P][kCsrU];
 #pragma unroll
       for (int u = 0; u < kCsrU; ++u) {
-        const int i = tid + kThreads * u;
-        col[u] = i < cnt ? ld_s32(a.ci + q0 + i, pf) : -1;
-        v[u] = (a.vals && i < cnt) ? ld_sf(a.vals + q0 + i, pf) : 1.0;
+        const int q = tid + kThreads * u;
+        col[u] = q < cnt ? ld_s32(a.ci + q0 + q, pf) : -1;
+        v[u] = (a.vals && q < cnt) ? ld_sf(a.vals + q0 + q, pf) : 1.0;
       }
 #pragma unroll
-      for (int u = 0; u < kCsrU; ++u) xv[u] = col[u] >= 0 ? ld_keep(a.xg + col[u], pl) : 0.0;
+      for (int u = 0; u < kCsrU; ++u)
+#pragma unroll
+        for (int i = 0; i < P; ++i) xv[i][u] = col[u] >= 0 ? ld_keep(a.xg[i] + col[u], pl) : 0.0;
 #pragma unroll
       for (int u = 0; u < kCsrU; ++u) {
-        const int i = tid + kThreads * u;
-        if (i < cnt) prod[i] = v[u] * xv[u];
+        const int q = tid + kThreads * u;
+        if (q < cnt) {
+#pragma unroll
+          for (int i = 0; i < P; ++i) prod[i][q] = v[u] * xv[i][u];
+        }
       }
     }
     __syncthreads();
@@ -166,45 +192,52 @@ __global__ void __launch_bounds__(kThreads, kCsrNB == 1024 ? 6 : 4) k_csr_stream
     const int64_t avg = cnt / nrows;
     int G = 1;
     while (G < 32 && 4 * G < avg) G <<= 1;
-    const int P = kThreads / G;
-    for (int rb = 0; rb < nrows; rb += P) {
+    const int R = kThreads / G;
+    for (int rb = 0; rb < nrows; rb += R) {
       const int rl = rb + tid / G, sub = tid & (G - 1);
       const bool own = rl < nrows && sub == 0;
       const int64_t row = r0 + rl;
-      double wv[NWM], zold = 0.0;
-      if (own) {   // issue the row's other loads before summing
-        if (ACC) zold = ld_sf(a.z + row, pf);
-        if (DOTS) {
 #pragma unroll
-          for (int t = 0; t < NWM - 1; ++t) wv[t] = (t < a.nw - 1) ? __ldg(a.V + (int64_t)(j0 + t) * a.ld + row) : 0.0;
-          wv[NWM - 1] = __ldg(x + row);
+      for (int i = 0; i < P; ++i) {
+        double wv[NWM], zold = 0.0;
+        if (own && live[i]) {   // issue the row's other loads before summing
+          if (ACC) zold = ld_sf(a.z[i] + row, pf);
+          if (DOTS) {
+#pragma unroll
+            for (int t = 0; t < NWM - 1; ++t)
+              wv[t] = (t < a.nw - 1) ? __ldg(a.V[i] + (int64_t)(j0 + t) * a.ld + row) : 0.0;
+            wv[NWM - 1] = __ldg(a.V[i] + (int64_t)(a.c - 1) * a.ld + row);
+          }
         }
-      }
-      double acc = 0.0;
-      if (rl < nrows) {
-        const int e = rps[rl + 1];
-        for (int i = rps[rl] + sub; i < e; i += G) acc += prod[i];
-      }
-      for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (own) {
-        double zr = acc * a.vscale;
-        if (ACC) zr += zold;
-        a.z[row] = zr;
-        if (DOTS) {
+        double acc = 0.0;
+        if (rl < nrows) {
+          const int e = rps[rl + 1];
+          for (int q = rps[rl] + sub; q < e; q += G) acc += prod[i][q];
+        }
+        for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (own && live[i]) {
+          double zr = acc * a.vscale;
+          if (ACC) zr += zold;
+          a.z[i][row] = zr;
+          if (DOTS) {
 #pragma unroll
-          for (int t = 0; t < NWM; ++t) d[t] = fma(wv[t], zr, d[t]);
+            for (int t = 0; t < NWM; ++t) d[i][t] = fma(wv[t], zr, d[i][t]);
+          }
         }
       }
     }
     __syncthreads();
   }
   if (DOTS) {
-    double out[NWM];
-    block_sum<NWM>(d, red, out);
-    if (tid == 0) {
-      double* p = a.part + (int64_t)blockIdx.x * (kKMax + 1);
-      for (int t = 0; t < a.nw - 1; ++t) p[t] = out[t];
-      p[a.nw - 1] = out[NWM - 1];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      double out[NWM];
+      block_sum<NWM>(d[i], red, out);
+      if (tid == 0 && live[i]) {
+        double* pp = a.part[i] + (int64_t)blockIdx.x * (kKMax + 1);
+        for (int t = 0; t < a.nw - 1; ++t) pp[t] = out[t];
+        pp[a.nw - 1] = out[NWM - 1];
+      }
     }
   }
 }
@@ -233,7 +266,6 @@ struct CsrPlan {
   std::vector<CsrPass> pass;
   std::vector<void*> owned;   // device buffers of the column-blocked copy
   int64_t width = 0;          // columns per block (0: not column-blocked)
-  int nb = kCsrNBDefault;     // entries per row block
   ~CsrPlan() {
     for (auto& p : pass)
       if (p.blk) cudaFree(p.blk);
@@ -271,17 +303,9 @@ void csr_release(fab_ctx* c) {
   c->csr = nullptr;
 }
 
-static int csr_nb_choice() {
-  const char* e = getenv("FAB_CSR_NB");
-  return (e && atoi(e) == 2048) ? 2048 : kCsrNBDefault;
-}
-
 int csr_grid(fab_ctx* c, int* grid) {
   int occ = 0;
-  if (csr_nb_choice() == 2048)
-    FAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_stream<4, false, true, 2048>, kThreads, 0));
-  else
-    FAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_stream<4, false, true, 1024>, kThreads, 0));
+  FAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_csr_stream<4, false, true, 1>, kThreads, 0));
   if (occ < 1) occ = 1;
   *grid = c->num_sms * occ;
   return FAB_OK;
@@ -293,7 +317,6 @@ int csr_setup(fab_ctx* c) {
   csr_release(c);
   CsrPlan* plan = new CsrPlan();
   c->csr = plan;
-  plan->nb = csr_nb_choice();
   // uniform values (e.g. a scaled 0/1 adjacency, c4): drop the value array
   // (8 B per entry per SpMV) and fold the value into value_scale
   if (c->op.values && c->op.nnz > 0) {
@@ -328,7 +351,7 @@ int csr_setup(fab_ctx* c) {
     p.rp64 = c->op.row_ptr;
     p.ci = c->op.col_idx;
     p.vals = c->op.values;
-    FAB_TRY(upload_blocks(build_blocks(n, plan->nb, [&](int64_t r) { return rp[r]; }), &p));
+    FAB_TRY(upload_blocks(build_blocks(n, kCsrNB, [&](int64_t r) { return rp[r]; }), &p));
     plan->pass.push_back(p);
     return FAB_OK;
   }
@@ -381,7 +404,7 @@ int csr_setup(fab_ctx* c) {
     p.rp32 = drp + (size_t)j * (n + 1);
     p.ci = dci + base[j];
     p.vals = dva ? dva + base[j] : nullptr;
-    FAB_TRY(upload_blocks(build_blocks(n, plan->nb, [&](int64_t r) { return (int64_t)rj[r]; }), &p));
+    FAB_TRY(upload_blocks(build_blocks(n, kCsrNB, [&](int64_t r) { return (int64_t)rj[r]; }), &p));
     plan->pass.push_back(p);
   }
   return FAB_OK;
@@ -396,53 +419,69 @@ int64_t csr_max_blocks(const fab_ctx* c) {
   return m;
 }
 
-template <int NWM, int NB>
-static void launch_pass_nb(const CsrArgs& a, int grid, bool acc, bool dots, cudaStream_t st) {
-  if (!acc && dots) k_csr_stream<NWM, false, true, NB><<<grid, kThreads, 0, st>>>(a);
-  else if (!acc) k_csr_stream<NWM, false, false, NB><<<grid, kThreads, 0, st>>>(a);
-  else if (dots) k_csr_stream<NWM, true, true, NB><<<grid, kThreads, 0, st>>>(a);
-  else k_csr_stream<NWM, true, false, NB><<<grid, kThreads, 0, st>>>(a);
+template <int NWM, int P>
+static void launch_pass_p(const CsrArgs& a, int grid, bool acc, bool dots, cudaStream_t st) {
+  if (!acc && dots) k_csr_stream<NWM, false, true, P><<<grid, kThreads, 0, st>>>(a);
+  else if (!acc) k_csr_stream<NWM, false, false, P><<<grid, kThreads, 0, st>>>(a);
+  else if (dots) k_csr_stream<NWM, true, true, P><<<grid, kThreads, 0, st>>>(a);
+  else k_csr_stream<NWM, true, false, P><<<grid, kThreads, 0, st>>>(a);
 }
 
 template <int NWM>
-static void launch_pass(const CsrArgs& a, int grid, int nb, bool acc, bool dots, cudaStream_t st) {
-  if (nb == 2048) launch_pass_nb<NWM, 2048>(a, grid, acc, dots, st);
-  else launch_pass_nb<NWM, 1024>(a, grid, acc, dots, st);
+static void launch_pass(const CsrArgs& a, int grid, int p, bool acc, bool dots, cudaStream_t st) {
+  switch (p) {
+    case 1: launch_pass_p<NWM, 1>(a, grid, acc, dots, st); break;
+    case 2: launch_pass_p<NWM, 2>(a, grid, acc, dots, st); break;
+    case 3: launch_pass_p<NWM, 3>(a, grid, acc, dots, st); break;
+    default: launch_pass_p<NWM, 4>(a, grid, acc, dots, st); break;
+  }
 }
 
-// z = A xin (+ the window dots when nw > 0), one launch per column block.
-int csr_spmv(fab_ctx* c, int col, int nw, const double* xin, double* z, cudaStream_t st, int64_t* launches,
-             int* nparts) {
+// z_i = A xin_i (+ the window dots when nw > 0) for the p contexts cs[i]
+// (the same operator; p = 1 is the single-RHS K1), one launch per column
+// block.  The grid and the row blocks are cs[0]'s, so per vector the
+// partials are those of a single-RHS launch.
+int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* const* xin, double* const* z,
+                   cudaStream_t st, int64_t* launches, int* nparts) {
+  fab_ctx* c = cs[0];
   CsrPlan* plan = c->csr;
-  if (!plan || plan->pass.empty()) return FAB_EORDER;
+  if (!plan || plan->pass.empty() || p < 1 || p > kBatchMax) return FAB_EORDER;
   *nparts = c->grid_spmv;
   const int np = (int)plan->pass.size();
   for (int j = 0; j < np; ++j) {
-    const CsrPass& p = plan->pass[j];
+    const CsrPass& ps = plan->pass[j];
     CsrArgs a;
-    a.rp64 = p.rp64;
-    a.rp32 = p.rp32;
-    a.ci = p.ci;
-    a.vals = p.vals;
+    memset(&a, 0, sizeof(a));
+    a.rp64 = ps.rp64;
+    a.rp32 = ps.rp32;
+    a.ci = ps.ci;
+    a.vals = ps.vals;
     a.vscale = c->op.value_scale;
-    a.blk = p.blk;
-    a.nblk = p.nblk;
-    a.V = c->V;
+    a.blk = ps.blk;
+    a.nblk = ps.nblk;
     a.ld = c->ld;
     a.c = col;
     a.nw = nw;
-    a.xg = xin;
-    a.z = z;
-    a.part = c->part_dots;
-    a.st = c->st_d;
+    for (int i = 0; i < p; ++i) {
+      a.V[i] = cs[i]->V;
+      a.xg[i] = xin[i];
+      a.z[i] = z[i];
+      a.part[i] = cs[i]->part_dots;
+      a.st[i] = cs[i]->st_d;
+    }
     const bool acc = j > 0, dots = (j == np - 1) && nw > 0;
-    if (c->k_max <= 2) launch_pass<2>(a, c->grid_spmv, plan->nb, acc, dots, st);
-    else if (c->k_max <= 4) launch_pass<4>(a, c->grid_spmv, plan->nb, acc, dots, st);
-    else launch_pass<8>(a, c->grid_spmv, plan->nb, acc, dots, st);
+    if (c->k_max <= 2) launch_pass<2>(a, c->grid_spmv, p, acc, dots, st);
+    else if (c->k_max <= 4) launch_pass<4>(a, c->grid_spmv, p, acc, dots, st);
+    else launch_pass<8>(a, c->grid_spmv, p, acc, dots, st);
     FAB_CHECK_LAUNCH();
     ++*launches;
   }
   return FAB_OK;
+}
+
+int csr_spmv(fab_ctx* c, int col, int nw, const double* xin, double* z, cudaStream_t st, int64_t* launches,
+             int* nparts) {
+  return csr_spmv_multi(&c, 1, col, nw, &xin, &z, st, launches, nparts);
 }
 
 }  // namespace fab

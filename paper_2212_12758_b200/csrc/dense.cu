@@ -228,33 +228,41 @@ static int lincomb(fab_ctx* c, int m, double a1, const double* X1, double a2, co
 }
 
 // out[0] = ||X||_1 (max column abs sum), out[1] = ||X - I||_F, out[2] = any non-finite
-__global__ void k_mat_stats(const double* X, int m, double* out) {
-  __shared__ double smax[kThreads], ssum[kThreads];
+// ||X||_1 (max column abs sum), ||X - I||_F and a non-finite flag.  One CTA
+// of 1024 threads: warp w takes columns w, w+32, ... with the lanes over the
+// rows (coalesced), per-column partials in shared memory, then thread 0
+// reduces them in column order (deterministic).
+constexpr int kStatsThreads = 1024;
+__global__ void __launch_bounds__(kStatsThreads) k_mat_stats(const double* X, int m, double* out) {
+  __shared__ double cabs[kMaxM], cdev[kMaxM];
   __shared__ int bad;
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
-  double mx = 0.0, fs = 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int b = 0;
-  for (int col = threadIdx.x; col < m; col += blockDim.x) {
-    double a = 0.0;
-    for (int r = 0; r < m; ++r) {
+  for (int col = warp; col < m; col += kStatsThreads / 32) {
+    double a = 0.0, fs = 0.0;
+    for (int r = lane; r < m; r += 32) {
       const double v = X[r + (int64_t)col * m];
       if (!isfinite(v)) b = 1;
       a += fabs(v);
       const double d = v - (r == col ? 1.0 : 0.0);
       fs = fma(d, d, fs);
     }
-    mx = fmax(mx, a);
+    a = warp_sum(a);
+    fs = warp_sum(fs);
+    if (lane == 0) {
+      cabs[col] = a;
+      cdev[col] = fs;
+    }
   }
   if (b) bad = 1;
-  smax[threadIdx.x] = mx;
-  ssum[threadIdx.x] = fs;
   __syncthreads();
   if (threadIdx.x == 0) {
     double M = 0.0, S = 0.0;
-    for (int t = 0; t < (int)blockDim.x; ++t) {
-      M = fmax(M, smax[t]);
-      S += ssum[t];
+    for (int col = 0; col < m; ++col) {
+      M = fmax(M, cabs[col]);
+      S += cdev[col];
     }
     out[0] = M;
     out[1] = sqrt(S);
@@ -353,13 +361,16 @@ k_gj_coop(double* A, double* B, int m, int nrhs, double* out) {
 // k_gj_coop (swap rows k, p and eliminate), same tie rule for the pivot.
 constexpr int kGjCl = 8;
 constexpr int kGjClMaxM = 330;
+constexpr int kGjRows = (kGjClMaxM + 31) / 32;   // rows per lane in the unrolled update
+constexpr int kGjThreads = 512;                  // 16 warps per CTA: the update is issue-bound
+constexpr int kGjWarps = kGjThreads / 32;
 
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_gj_cluster(const double* __restrict__ A, double* B, int m,
+__global__ void __launch_bounds__(kGjThreads, 1) k_gj_cluster(const double* __restrict__ A, double* B, int m,
                                                             int nrhs, double* out) {
   namespace cgx = cooperative_groups;
   cgx::cluster_group cl = cgx::this_cluster();
@@ -389,11 +400,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_gj_cluster(const double* __rest
       const double* ck = cols + (size_t)lk * m;
       double best = -1.0;
       int bi = m;
-      for (int i = k + lane; i < m; i += 32) {
-        const double a = fabs(ck[i]);
-        if (a > best) {
-          best = a;
-          bi = i;
+      double av[kGjRows];
+#pragma unroll
+      for (int r = 0; r < kGjRows; ++r) {
+        const int i = k + lane + 32 * r;
+        av[r] = i < m ? fabs(ck[i]) : -1.0;
+      }
+#pragma unroll
+      for (int r = 0; r < kGjRows; ++r) {   // ascending i per lane, as the strided loop
+        if (av[r] > best) {
+          best = av[r];
+          bi = k + lane + 32 * r;
         }
       }
 #pragma unroll
@@ -417,24 +434,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_gj_cluster(const double* __rest
     if (!(fabs(piv) > 0.0)) singular = 1;
     if (q == owner && tid == 0) logdet += log(fabs(piv));
     const double ipiv = 1.0 / piv;
-    // columns j > k of A and every column of B (j >= m)
-    for (int l = warp; l < nloc; l += kWarps) {
+    // columns j > k of A and every column of B (j >= m).  Each lane holds
+    // rows lane + 32 r (r < kGjRows) of the pivot column in registers and
+    // issues all its loads of a column before the FMAs (the row loop is
+    // fully unrolled: shared-memory latency is paid once per column, not
+    // once per row).  Same arithmetic per element as before.
+    double pr[kGjRows];
+#pragma unroll
+    for (int r = 0; r < kGjRows; ++r) {
+      const int i = lane + 32 * r;
+      pr[r] = i < m ? pc[i] : 0.0;
+    }
+    for (int l = warp; l < nloc; l += kGjWarps) {
       const int j = q + kGjCl * l;
       if (j <= k) continue;
       double* col = cols + (size_t)l * m;
       const double ap = col[p], ak = col[k];
       const double rr = ap * ipiv;
       __syncwarp();
-      for (int i = lane; i < m; i += 32) {
-        double nv;
-        if (i == k)
-          nv = rr;
-        else if (i == p)
-          nv = fma(-ckk, rr, ak);
-        else
-          nv = fma(-pc[i], rr, col[i]);
-        col[i] = nv;
+      double cv[kGjRows];
+#pragma unroll
+      for (int r = 0; r < kGjRows; ++r) {
+        const int i = lane + 32 * r;
+        cv[r] = i < m ? col[i] : 0.0;
       }
+      // every row as a generic row (branch-free), then rows k and p rewritten
+      // by their lanes: row k <- rr, row p <- a_kj - a_kk rr (the swap)
+#pragma unroll
+      for (int r = 0; r < kGjRows; ++r) {
+        const int i = lane + 32 * r;
+        if (i < m) col[i] = fma(-pr[r], rr, cv[r]);
+      }
+      __syncwarp();
+      if (lane == (k & 31)) col[k] = rr;
+      if (p != k && lane == (p & 31)) col[p] = fma(-ckk, rr, ak);
     }
     __syncthreads();
   }
@@ -465,6 +498,183 @@ __global__ void __launch_bounds__(kThreads, 1) k_gj_cluster(const double* __rest
   (void)red_log;
 }
 
+// In-place Gauss-Jordan inverse on one cluster (the Denman-Beavers M^{-1}):
+// only the m columns of A are stored -- at pivot step k column k turns into
+// column k of the running inverse (-c'/piv, 1/piv at row k) while every other
+// column takes the usual elimination -- and the row interchanges are undone
+// as a column permutation when the result is written.  Versus [A | I]: half
+// the shared memory and 2/3 of the update work; rows are handled in pairs
+// (double2 shared-memory accesses, column stride rounded up to even).  Same
+// pivot rule as k_gj_cluster.
+constexpr int kGjPairs = (kGjClMaxM + 63) / 64;   // row pairs per lane
+
+__global__ void __launch_bounds__(kGjThreads, 1) k_gj_inv_cluster(const double* __restrict__ A, double* Ainv,
+                                                                  int m, double* out) {
+  namespace cgx = cooperative_groups;
+  cgx::cluster_group cl = cgx::this_cluster();
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int pk[kGjClMaxM];
+  __shared__ int posof[kGjClMaxM];
+  const int q = (int)cl.block_rank();
+  const int mp = (m + 1) & ~1;
+  const int nloc = (m - q + kGjCl - 1) / kGjCl;   // columns j = q + kGjCl * l
+  const int nmax = (m + kGjCl - 1) / kGjCl;
+  double* cols = sm;                              // [nmax][mp]
+  double* bc = cols + (size_t)nmax * mp;          // [2][mp + 2]: column, then pivot index at [mp]
+  double* pc = bc + 2 * (mp + 2);                 // local copy of the broadcast column
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int l = 0; l < nloc; ++l) {
+    const int j = q + kGjCl * l;
+    for (int i = tid; i < mp; i += blockDim.x) cols[(size_t)l * mp + i] = i < m ? A[(int64_t)j * m + i] : 0.0;
+  }
+  double logdet = 0.0;
+  int singular = 0;
+  __syncthreads();
+  cluster_barrier();
+  for (int k = 0; k < m; ++k) {
+    const int owner = k % kGjCl, lk = k / kGjCl;
+    double* slot = bc + (size_t)(k & 1) * (mp + 2);
+    if (q == owner && warp == 0) {
+      const double* ck = cols + (size_t)lk * mp;
+      double best = -1.0;
+      int bi = m;
+      double av[kGjRows];
+#pragma unroll
+      for (int r = 0; r < kGjRows; ++r) {
+        const int i = k + lane + 32 * r;
+        av[r] = i < m ? fabs(ck[i]) : -1.0;
+      }
+#pragma unroll
+      for (int r = 0; r < kGjRows; ++r) {
+        if (av[r] > best) {
+          best = av[r];
+          bi = k + lane + 32 * r;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      const double2* c2 = reinterpret_cast<const double2*>(ck);
+      double2* s2 = reinterpret_cast<double2*>(slot);
+      for (int i = lane; i < mp / 2; i += 32) s2[i] = c2[i];
+      if (lane == 0) slot[mp] = (double)bi;
+    }
+    cluster_barrier();
+    {
+      const double2* rs = reinterpret_cast<const double2*>(cl.map_shared_rank(slot, owner));
+      double2* p2 = reinterpret_cast<double2*>(pc);
+      for (int i = tid; i <= mp / 2; i += blockDim.x) p2[i] = rs[i];   // pair mp/2 holds the pivot index
+    }
+    __syncthreads();
+    const int p = (int)pc[mp];
+    const double piv = pc[p], ckk = pc[k];
+    if (!(fabs(piv) > 0.0)) singular = 1;
+    if (q == owner && tid == 0) logdet += log(fabs(piv));
+    if (tid == 0) pk[k] = p;
+    const double ipiv = 1.0 / piv;
+    double2 pr[kGjPairs];
+    const double2* p2 = reinterpret_cast<const double2*>(pc);
+#pragma unroll
+    for (int r = 0; r < kGjPairs; ++r) {
+      const int i2 = lane + 32 * r;
+      pr[r] = 2 * i2 < mp ? p2[i2] : make_double2(0.0, 0.0);
+    }
+    for (int l = warp; l < nloc; l += kGjWarps) {
+      const int j = q + kGjCl * l;
+      double* col = cols + (size_t)l * mp;
+      double2* c2 = reinterpret_cast<double2*>(col);
+      if (j == k) {
+        // the pivot column becomes column k of the inverse: -c'/piv, 1/piv at row k
+#pragma unroll
+        for (int r = 0; r < kGjPairs; ++r) {
+          const int i2 = lane + 32 * r;
+          if (2 * i2 < mp) c2[i2] = make_double2(-pr[r].x * ipiv, -pr[r].y * ipiv);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          col[k] = ipiv;
+          if (p != k) col[p] = -ckk * ipiv;
+        }
+      } else {
+        const double ap = col[p], ak = col[k];
+        const double rr = ap * ipiv;
+        __syncwarp();
+        double2 cv[kGjPairs];
+#pragma unroll
+        for (int r = 0; r < kGjPairs; ++r) {
+          const int i2 = lane + 32 * r;
+          cv[r] = 2 * i2 < mp ? c2[i2] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int r = 0; r < kGjPairs; ++r) {
+          const int i2 = lane + 32 * r;
+          if (2 * i2 < mp) c2[i2] = make_double2(fma(-pr[r].x, rr, cv[r].x), fma(-pr[r].y, rr, cv[r].y));
+        }
+        __syncwarp();
+        if (lane == 0) {   // row k <- rr, row p <- a_kj - a_kk rr (the interchange)
+          col[k] = rr;
+          if (p != k) col[p] = fma(-ckk, rr, ak);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // undo the row interchanges as column interchanges (in reverse order):
+  // stored column s is column posof[s] of A^{-1}
+  if (tid == 0) {
+    int* colat = reinterpret_cast<int*>(pc);   // pc is free now
+    for (int s2 = 0; s2 < m; ++s2) {
+      posof[s2] = s2;
+      colat[s2] = s2;
+    }
+    for (int k = m - 1; k >= 0; --k) {
+      const int p = pk[k];
+      if (p == k) continue;
+      const int a = colat[k], b = colat[p];
+      colat[k] = b;
+      colat[p] = a;
+      posof[a] = p;
+      posof[b] = k;
+    }
+  }
+  __syncthreads();
+  for (int l = 0; l < nloc; ++l) {
+    const int j = q + kGjCl * l;
+    double* dst = Ainv + (int64_t)posof[j] * m;
+    for (int i = tid; i < m; i += blockDim.x) dst[i] = cols[(size_t)l * mp + i];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    bc[0] = logdet;
+    bc[1] = singular ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  cluster_barrier();
+  if (q == 0 && tid == 0) {
+    double lsum = 0.0, sg = 0.0;
+    for (int r = 0; r < kGjCl; ++r) {
+      const double* o = cl.map_shared_rank(bc, r);
+      lsum += o[0];
+      sg = fmax(sg, o[1]);
+    }
+    out[0] = lsum;
+    out[1] = sg;
+  }
+  cluster_barrier();
+}
+
+static size_t gj_inv_smem(int m) {
+  const int mp = (m + 1) & ~1;
+  const int nmax = (m + kGjCl - 1) / kGjCl;
+  return ((size_t)nmax * mp + 3 * ((size_t)mp + 2)) * sizeof(double);
+}
+
 static size_t gj_cluster_smem(int m, int nrhs) {
   const int nloc = (m + nrhs + kGjCl - 1) / kGjCl;
   return ((size_t)nloc * m + 3 * ((size_t)m + 2)) * sizeof(double);
@@ -482,7 +692,7 @@ static int gj_solve(fab_ctx* c, int m, const double* A, double* Awork, double* B
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kGjCl, 1, 1);
-    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.blockDim = dim3(kGjThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -505,6 +715,40 @@ static int gj_solve(fab_ctx* c, int m, const double* A, double* Awork, double* B
   return FAB_OK;
 }
 
+// A^{-1} (out[0] = log|det A|, out[1] = 1 if singular): the in-place cluster
+// inverse when it fits, else the general solve against I
+static int gj_inverse(fab_ctx* c, int m, const double* A, double* Awork, double* Ainv, double* out,
+                      cudaStream_t st);
+
+static int gj_inverse(fab_ctx* c, int m, const double* A, double* Awork, double* Ainv, double* out,
+                      cudaStream_t st) {
+  const size_t smem = gj_inv_smem(m);
+  if (m > kGjClMaxM || smem > 226 * 1024) {
+    FAB_TRY(lincomb(c, m, 0, nullptr, 0, nullptr, 0, nullptr, 1.0, Ainv, st));   // I
+    return gj_solve(c, m, A, Awork, Ainv, m, out, st);
+  }
+  static bool attr = false;
+  if (!attr) {
+    FAB_CUDA(set_max_dyn_smem((const void*)k_gj_inv_cluster, 226 * 1024));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kGjCl, 1, 1);
+  cfg.blockDim = dim3(kGjThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kGjCl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  FAB_CUDA(cudaLaunchKernelEx(&cfg, k_gj_inv_cluster, A, Ainv, m, out));
+  ++c->nlaunch;
+  return FAB_OK;
+}
+
 __global__ void k_gemv_e(const double* X, int m, const double* u, double* out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
     double a = 0.0;
@@ -521,7 +765,7 @@ __global__ void k_unit(int m, double a, double* y) {
 
 static int read_stats(fab_ctx* c, const double* X, int m, double* h, cudaStream_t st) {
   double* d = svec(c, 11);
-  k_mat_stats<<<1, kThreads, 0, st>>>(X, m, d);
+  k_mat_stats<<<1, kStatsThreads, 0, st>>>(X, m, d);
   FAB_CHECK_LAUNCH();
   FAB_CUDA(cudaMemcpyAsync(h, d, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
   FAB_CUDA(cudaStreamSynchronize(st));
@@ -705,8 +949,7 @@ static int db_e1(fab_ctx* c, int m, const double* X0, int want_inv, double* c_ou
   bool extra_done = false;
   const int maxit = 100;
   for (int it = 0; it < maxit; ++it) {
-    FAB_TRY(lincomb(c, m, 0, nullptr, 0, nullptr, 0, nullptr, 1.0, Mi, st));
-    FAB_TRY(gj_solve(c, m, M, Wk, Mi, m, gout, st));
+    FAB_TRY(gj_inverse(c, m, M, Wk, Mi, gout, st));
     double gh[2];
     FAB_CUDA(cudaMemcpyAsync(gh, gout, sizeof(gh), cudaMemcpyDeviceToHost, st));
     FAB_CUDA(cudaStreamSynchronize(st));

@@ -129,6 +129,14 @@ struct fab_ctx {
   int g_sgs_m = -1, g_sgs_s = -1;
   int64_t g_sgs_launches = 0;
 
+  // cached multi-RHS batch graph (held by the batch's first context)
+  cudaGraphExec_t gexec_bat = nullptr;
+  std::vector<fab_ctx*> g_bat_ctx;
+  std::vector<int> g_bat_fused;
+  std::vector<int> g_bat_s;
+  int g_bat_m = -1, g_bat_k = -1;
+  int64_t g_bat_launches = 0;
+
   // cached Arnoldi (CGS2) graph
   cudaGraphExec_t gexec_arn = nullptr;
   int g_arn_m = -1;
@@ -244,6 +252,10 @@ int csr_setup(fab_ctx* c);                   // uniform values, row blocks, colu
 int csr_spmv(fab_ctx* c, int col, int nw, const double* xin, double* z, cudaStream_t st, int64_t* launches,
              int* nparts);
 int csr_passes(const fab_ctx* c);
+int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* const* xin, double* const* z,
+                   cudaStream_t st, int64_t* launches, int* nparts);
+constexpr int kBatchMaxCtx = 4;              // fab_basis_batch: contexts per call
+int run_basis_batch(fab_ctx* const* cs, int p, int m, int k);
 int64_t csr_max_blocks(const fab_ctx* c);
 void csr_release(fab_ctx* c);
 int launch_sketch_cols(fab_ctx* c, int c0, int c1, cudaStream_t st);
