@@ -77,6 +77,14 @@ def test_validation_without_device():
     # null context / pointers
     assert lib.fab_basis(None, 4, 2) == _lib.FAB_EINVAL
     assert lib.fab_destroy(None) == _lib.FAB_EINVAL
+    # multi-RHS batch: null array, bad counts, null members
+    assert lib.fab_basis_batch(None, 1, 4, 2) == _lib.FAB_EINVAL
+    arr = (C.c_void_p * 5)()
+    assert lib.fab_basis_batch(arr, 0, 4, 2) == _lib.FAB_EINVAL
+    assert lib.fab_basis_batch(arr, 5, 4, 2) == _lib.FAB_EINVAL
+    assert lib.fab_basis_batch(arr, 2, 4, 2) == _lib.FAB_EINVAL          # null contexts
+    # sign needs a squared context; apply on a null context is rejected first
+    assert lib.fab_apply(None, _lib.FAB_SIGN, 1.0, 0.0, None, 0) == _lib.FAB_EINVAL
 
 
 def test_init_reports_no_device_on_cpu_box():
