@@ -164,6 +164,7 @@ static void free_ctx(fab_ctx* c) {
   if (c->gexec_sgs) cudaGraphExecDestroy(c->gexec_sgs);
   if (c->gexec_arn) cudaGraphExecDestroy(c->gexec_arn);
   if (c->gexec_bat) cudaGraphExecDestroy(c->gexec_bat);
+  if (c->xi) cudaFree(c->xi);
   if (c->wbuf) cudaFree(c->wbuf);
   if (c->part_dots) cudaFree(c->part_dots);
   if (c->own_ws && c->ws) cudaFree(c->ws);

@@ -393,7 +393,8 @@ constexpr int kChunksPerTile = kSkT / kChunk;   // 8
 constexpr int kPipeThreads = kThreads + 32;
 constexpr int kMaxStages = 16;
 constexpr int kSignPad = 16;   // doubles reserved per stage for the chunk's sign bits
-constexpr int kSmemLimit = 226 * 1024;   // dynamic smem budget per CTA (opt-in max 227 KB)
+constexpr int kPipeCtasPerSm = 2;        // resident K3/K5 CTAs per SM
+constexpr int kSmemLimit = (226 * 1024) / kPipeCtasPerSm - 2048;   // dynamic smem budget per CTA
 
 struct PipeArgs {
   double* V;
@@ -516,7 +517,7 @@ __device__ __forceinline__ double cta_det_sum(const double* p, int count, int st
 }
 
 template <bool UPDATE, bool SKETCH, int SDIM>
-__global__ void __launch_bounds__(kPipeThreads, 1) k_stream_tiles(PipeArgs a) {
+__global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(PipeArgs a) {
   if (a.st->breakdown) return;
   extern __shared__ __align__(128) double dsm[];
   __shared__ double red[kWarps];
@@ -870,9 +871,13 @@ int basis_setup_grids(fab_ctx* c) {
   // 120 us, profiles/r01_v2); needs a z-marching tile order.
   const char* mfe = getenv("FAB_MATRIX_FREE");
   c->mf = stencil_vec_path(c) && (mfe && mfe[0] == '1') && !(c->flags & FAB_FLAG_SQUARE);
-  // K3/K5 pipeline: persistent, one CTA per SM (the ring takes the smem)
+  // K3/K5 pipeline: persistent, kPipeCtasPerSm CTAs per SM (each with half the
+  // ring): 16 consumer warps per SM instead of 8 hide the consumers' FWHT /
+  // update latency (c3 basis 55.7 -> 50.2 ms although the registers are capped
+  // at 96 and the ring holds 3 stages per CTA); 3 CTAs/SM leave no room for a ring
   const int64_t ntiles = ((c->row_begin + c->n - 1) >> kSkLogT) - (c->row_begin >> kSkLogT) + 1;
-  c->grid_upd = (int)(ntiles < c->num_sms ? ntiles : c->num_sms);
+  const int64_t gmax = (int64_t)kPipeCtasPerSm * c->num_sms;
+  c->grid_upd = (int)(ntiles < gmax ? ntiles : gmax);
   if (stencil_vec_path(c)) {
     // K1 vector path: 2 CTAs/SM, blocks of kK1Block contiguous rows
     const int64_t need = (c->n + kK1Block - 1) / kK1Block;
@@ -1184,20 +1189,26 @@ static int enqueue_batch(fab_ctx* const* cs, int p, int m, int k, cudaStream_t s
   for (int col = 1; col <= m; ++col) {
     const int nw = col < k ? col : k;
     int nparts = 0;
-    if (cs[0]->stencil) {
+    if (cs[0]->stencil || !csr_interleave_fits(cs[0], p)) {
+      // no shared entry traffic worth a pass (stencil), or the p inputs would
+      // not stay in L2 (every gather would then miss for every vector):
+      // per-context K1
       for (int i = 0; i < p; ++i) FAB_TRY(enqueue_k1(cs[i], col, nw, cs[i]->vec, false, st, launches, &nparts));
     } else {
       const double* xin[kBatchMaxCtx];
       double* z[kBatchMaxCtx];
+      double* xi = cs[0]->xi;
       for (int i = 0; i < p; ++i) xin[i] = cs[i]->V + (int64_t)(col - 1) * cs[i]->ld;
       if (sq) {   // K0: t_i = A w_hat_{col-1} of every context, one pass
         for (int i = 0; i < p; ++i) z[i] = cs[i]->sq;
         int np0 = 0;
-        FAB_TRY(csr_spmv_multi(cs, p, col, 0, xin, z, st, launches, &np0));
+        FAB_TRY(csr_interleave(cs[0], p, xin, xi, st, launches));
+        FAB_TRY(csr_spmv_multi(cs, p, col, 0, xin, z, st, launches, &np0, xi));
         for (int i = 0; i < p; ++i) xin[i] = cs[i]->sq;
       }
       for (int i = 0; i < p; ++i) z[i] = cs[i]->vec;
-      FAB_TRY(csr_spmv_multi(cs, p, col, nw, xin, z, st, launches, &nparts));
+      FAB_TRY(csr_interleave(cs[0], p, xin, xi, st, launches));
+      FAB_TRY(csr_spmv_multi(cs, p, col, nw, xin, z, st, launches, &nparts, xi));
     }
     for (int i = 0; i < p; ++i) FAB_TRY(enqueue_k3(cs[i], col, nw, cs[i]->sketch_ready, st, launches, nparts));
   }
@@ -1213,6 +1224,8 @@ static int enqueue_batch(fab_ctx* const* cs, int p, int m, int k, cudaStream_t s
 
 int run_basis_batch(fab_ctx* const* cs, int p, int m, int k) {
   fab_ctx* c = cs[0];
+  if (!c->stencil && !c->xi && p > 1 && csr_interleave_fits(c, p))
+    FAB_CUDA(cudaMalloc(&c->xi, (size_t)c->n * kBatchMaxCtx * sizeof(double)));
   std::vector<fab_ctx*> key(cs, cs + p);
   std::vector<int> fz(p), ss(p);
   for (int i = 0; i < p; ++i) {

@@ -49,6 +49,8 @@ struct CsrArgs {
   // per right-hand side i < P (one context each)
   const double* V[kBatchMax];
   const double* xg[kBatchMax];   // SpMV input by global column id
+  const double* xi;              // non-null (P > 1): the P inputs interleaved, xi[col * P + i]:
+                                 // one 32-B sector serves every right-hand side of a gather
   double* z[kBatchMax];
   double* part[kBatchMax];       // per-CTA dot partials (DOTS)
   const DevState* st[kBatchMax];
@@ -86,6 +88,31 @@ __device__ __forceinline__ double ld_keep(const double* p, uint64_t pol) {
   double v;
   asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
+}
+
+__device__ __forceinline__ double2 ld_keep2(const double* p, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+
+// x_i[col] for the P right-hand sides: separate gathers, or (interleaved
+// copy) P consecutive doubles of one sector in 16-B loads
+template <int P>
+__device__ __forceinline__ void gather_x(const CsrArgs& a, int col, uint64_t pl, double (&xv)[P]) {
+  if (P > 1 && a.xi) {
+    constexpr int S = (P + 1) & ~1;   // row stride of the interleaved copy (16-B aligned rows)
+    const double* b = a.xi + (int64_t)col * S;
+#pragma unroll
+    for (int i = 0; i < P; i += 2) {
+      const double2 t = ld_keep2(b + i, pl);
+      xv[i] = t.x;
+      if (i + 1 < P) xv[i + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < P; ++i) xv[i] = ld_keep(a.xg[i] + col, pl);
+  }
 }
 
 __device__ __forceinline__ int64_t rowq(const CsrArgs& a, int64_t r, uint64_t pol) {
@@ -139,8 +166,10 @@ __global__ void __launch_bounds__(kThreads, P == 1 ? 6 : 3) k_csr_stream(CsrArgs
 #pragma unroll
         for (int u = 0; u < kCsrU; ++u)
           if (col[u] >= 0) {
+            double xg[P];
+            gather_x<P>(a, col[u], pl, xg);
 #pragma unroll
-            for (int i = 0; i < P; ++i) acc[i] = fma(v[u], ld_keep(a.xg[i] + col[u], pl), acc[i]);
+            for (int i = 0; i < P; ++i) acc[i] = fma(v[u], xg[i], acc[i]);
           }
       }
       double o[P];
@@ -167,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, P == 1 ? 6 : 3) k_csr_stream(CsrArgs
     for (int q = tid; q <= nrows; q += kThreads) rps[q] = (int)(rowq(a, r0 + q, pf) - q0);
     {
       int col[kCsrU];
-      double v[kCsrU], xv[P][kCsrU];
+      double v[kCsrU], xv[kCsrU][P];
 #pragma unroll
       for (int u = 0; u < kCsrU; ++u) {
         const int q = tid + kThreads * u;
@@ -175,15 +204,20 @@ __global__ void __launch_bounds__(kThreads, P == 1 ? 6 : 3) k_csr_stream(CsrArgs
         v[u] = (a.vals && q < cnt) ? ld_sf(a.vals + q0 + q, pf) : 1.0;
       }
 #pragma unroll
-      for (int u = 0; u < kCsrU; ++u)
+      for (int u = 0; u < kCsrU; ++u) {
+        if (col[u] >= 0) {
+          gather_x<P>(a, col[u], pl, xv[u]);
+        } else {
 #pragma unroll
-        for (int i = 0; i < P; ++i) xv[i][u] = col[u] >= 0 ? ld_keep(a.xg[i] + col[u], pl) : 0.0;
+          for (int i = 0; i < P; ++i) xv[u][i] = 0.0;
+        }
+      }
 #pragma unroll
       for (int u = 0; u < kCsrU; ++u) {
         const int q = tid + kThreads * u;
         if (q < cnt) {
 #pragma unroll
-          for (int i = 0; i < P; ++i) prod[i][q] = v[u] * xv[i][u];
+          for (int i = 0; i < P; ++i) prod[i][q] = v[u] * xv[u][i];
         }
       }
     }
@@ -412,6 +446,36 @@ int csr_setup(fab_ctx* c) {
 
 int csr_passes(const fab_ctx* c) { return c->csr ? (int)c->csr->pass.size() : 0; }
 
+// Multi-RHS: xi[r * S + i] = x_i[r], S = p rounded up to even (coalesced
+// reads of the p columns; each thread writes the values of one row)
+__global__ void k_interleave(const double* x0, const double* x1, const double* x2, const double* x3, int p,
+                             int64_t n, double* xi) {
+  const double* xs[4] = {x0, x1, x2, x3};
+  const int S = (p + 1) & ~1;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    for (int i = 0; i < S; ++i) xi[r * S + i] = i < p ? xs[i][r] : 0.0;
+}
+
+int csr_interleave(fab_ctx* c, int p, const double* const* x, double* xi, cudaStream_t st, int64_t* launches) {
+  k_interleave<<<4 * c->num_sms, kThreads, 0, st>>>(x[0], p > 1 ? x[1] : nullptr, p > 2 ? x[2] : nullptr,
+                                                    p > 3 ? x[3] : nullptr, p, c->n, xi);
+  FAB_CHECK_LAUNCH();
+  ++*launches;
+  return FAB_OK;
+}
+
+// the interleaved inputs of p right-hand sides stay in the L2 budget the
+// column blocking uses (0.4 L2), and the plan is a single pass
+bool csr_interleave_fits(const fab_ctx* c, int p) {
+  if (!c->csr || c->csr->pass.size() != 1 || c->comm) return false;
+  int l2 = 0;
+  if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device) != cudaSuccess) return false;
+  double frac = 0.75;   // X only (the entry / z streams are evict-first)
+  const char* e = getenv("FAB_BATCH_L2FRAC");
+  if (e && atof(e) > 0) frac = atof(e);
+  return (double)((p + 1) & ~1) * (double)c->n_global * 8.0 <= frac * (double)l2;
+}
+
 int64_t csr_max_blocks(const fab_ctx* c) {
   int64_t m = 0;
   if (c->csr)
@@ -442,7 +506,7 @@ static void launch_pass(const CsrArgs& a, int grid, int p, bool acc, bool dots, 
 // block.  The grid and the row blocks are cs[0]'s, so per vector the
 // partials are those of a single-RHS launch.
 int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* const* xin, double* const* z,
-                   cudaStream_t st, int64_t* launches, int* nparts) {
+                   cudaStream_t st, int64_t* launches, int* nparts, const double* xi) {
   fab_ctx* c = cs[0];
   CsrPlan* plan = c->csr;
   if (!plan || plan->pass.empty() || p < 1 || p > kBatchMax) return FAB_EORDER;
@@ -462,6 +526,7 @@ int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* con
     a.ld = c->ld;
     a.c = col;
     a.nw = nw;
+    a.xi = p > 1 ? xi : nullptr;
     for (int i = 0; i < p; ++i) {
       a.V[i] = cs[i]->V;
       a.xg[i] = xin[i];
@@ -481,7 +546,7 @@ int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* con
 
 int csr_spmv(fab_ctx* c, int col, int nw, const double* xin, double* z, cudaStream_t st, int64_t* launches,
              int* nparts) {
-  return csr_spmv_multi(&c, 1, col, nw, &xin, &z, st, launches, nparts);
+  return csr_spmv_multi(&c, 1, col, nw, &xin, &z, st, launches, nparts, nullptr);
 }
 
 }  // namespace fab

@@ -136,6 +136,7 @@ struct fab_ctx {
   std::vector<int> g_bat_s;
   int g_bat_m = -1, g_bat_k = -1;
   int64_t g_bat_launches = 0;
+  double* xi = nullptr;               // multi-RHS interleaved SpMV inputs (n x 4), allocated on first use
 
   // cached Arnoldi (CGS2) graph
   cudaGraphExec_t gexec_arn = nullptr;
@@ -253,7 +254,9 @@ int csr_spmv(fab_ctx* c, int col, int nw, const double* xin, double* z, cudaStre
              int* nparts);
 int csr_passes(const fab_ctx* c);
 int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* const* xin, double* const* z,
-                   cudaStream_t st, int64_t* launches, int* nparts);
+                   cudaStream_t st, int64_t* launches, int* nparts, const double* xi);
+int csr_interleave(fab_ctx* c, int p, const double* const* x, double* xi, cudaStream_t st, int64_t* launches);
+bool csr_interleave_fits(const fab_ctx* c, int p);
 constexpr int kBatchMaxCtx = 4;              // fab_basis_batch: contexts per call
 int run_basis_batch(fab_ctx* const* cs, int p, int m, int k);
 int64_t csr_max_blocks(const fab_ctx* c);
