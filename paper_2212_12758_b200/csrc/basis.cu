@@ -95,6 +95,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP sp, int64_t n, int64_t gbase,
                  const double* __restrict__ xin, double* __restrict__ z, double* __restrict__ part,
                  const DevState* __restrict__ st) {
+  pdl_wait();
+  pdl_trigger();
   if (st->breakdown) return;
   __shared__ double red[kWarps * NWM];
   const double* __restrict__ xw = V + (int64_t)(c - 1) * ld;   // w_hat_{c-1} (window dot)
@@ -178,6 +180,8 @@ __global__ void __launch_bounds__(kThreads)
 k_stencil_dots(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP sp, int64_t n, int64_t gbase,
                const double* __restrict__ xin, double* __restrict__ z, double* __restrict__ part,
                const DevState* __restrict__ st) {
+  pdl_wait();
+  pdl_trigger();
   if (st->breakdown) return;
   __shared__ double red[kWarps * kKMax];
   const double* __restrict__ xw = V + (int64_t)(c - 1) * ld;   // w_hat_{c-1} (window dot)
@@ -518,6 +522,8 @@ __device__ __forceinline__ double cta_det_sum(const double* p, int count, int st
 
 template <bool UPDATE, bool SKETCH, int SDIM>
 __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(PipeArgs a) {
+  pdl_wait();
+  pdl_trigger();
   if (a.st->breakdown) return;
   extern __shared__ __align__(128) double dsm[];
   __shared__ double red[kWarps];
@@ -775,7 +781,8 @@ template <bool UPDATE, bool SKETCH, int SDIM>
 static int launch_stream(fab_ctx* c, PipeArgs a, cudaStream_t st) {
   size_t smem = 0;
   a.nstage = pipe_stages(slot_geom<UPDATE, SKETCH, SDIM>(a.nw, a.apron).stage_d, SKETCH, &smem);
-  k_stream_tiles<UPDATE, SKETCH, SDIM><<<c->grid_upd, kPipeThreads, smem, st>>>(a);
+  FAB_CUDA(launch_pdl(c->pdl && !c->comm, k_stream_tiles<UPDATE, SKETCH, SDIM>, c->grid_upd, kPipeThreads, smem,
+                      st, a));
   FAB_CHECK_LAUNCH();
   return FAB_OK;
 }
@@ -869,6 +876,12 @@ int basis_setup_grids(fab_ctx* c) {
   // not the default: with the tile order of the persistent grid the +-plane
   // neighbour chunks are first-touch misses that stall the ring (K3 347 us vs
   // 120 us, profiles/r01_v2); needs a z-marching tile order.
+  // PDL between K1 and K3 is opt-in (FAB_PDL=1): measured at c3 it slows the
+  // basis from 50.8 to 60.7 ms -- with both persistent grids sized to fill
+  // the machine, the early-launched CTAs of the next kernel land unevenly as
+  // the previous kernel's CTAs exit
+  const char* pde = getenv("FAB_PDL");
+  c->pdl = (pde && pde[0] == '1');
   const char* mfe = getenv("FAB_MATRIX_FREE");
   c->mf = stencil_vec_path(c) && (mfe && mfe[0] == '1') && !(c->flags & FAB_FLAG_SQUARE);
   // K3/K5 pipeline: persistent, kPipeCtasPerSm CTAs per SM (each with half the
@@ -959,18 +972,19 @@ static int launch_k1(fab_ctx* c, int col, int nw, const double* xin, double* z, 
     const int G = c->grid_spmv;
     const int64_t gb = c->row_begin;
     const bool sq = xin != x;
+    const bool pdl = c->pdl && !c->comm;
     if (stencil_vec_path(c)) {
 #define FAB_K1V(DIM, NWM)                                                                                    \
   do {                                                                                                       \
     if (sq)                                                                                                  \
-      k_stencil_dots_v<DIM, NWM, true, true><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, xin, \
-                                                                     z, c->part_dots, c->st_d);              \
+      FAB_CUDA(launch_pdl(pdl, k_stencil_dots_v<DIM, NWM, true, true>, G, kThreads, 0, st, c->V, c->ld, col, \
+                          nw, sp, c->n, gb, xin, z, c->part_dots, (const DevState*)c->st_d));                \
     else if (!store)                                                                                         \
-      k_stencil_dots_v<DIM, NWM, false><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, xin, z,  \
-                                                                c->part_dots, c->st_d);                      \
+      FAB_CUDA(launch_pdl(pdl, k_stencil_dots_v<DIM, NWM, false>, G, kThreads, 0, st, c->V, c->ld, col, nw,  \
+                          sp, c->n, gb, xin, z, c->part_dots, (const DevState*)c->st_d));                    \
     else                                                                                                     \
-      k_stencil_dots_v<DIM, NWM, true><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, xin, z,   \
-                                                               c->part_dots, c->st_d);                       \
+      FAB_CUDA(launch_pdl(pdl, k_stencil_dots_v<DIM, NWM, true>, G, kThreads, 0, st, c->V, c->ld, col, nw,   \
+                          sp, c->n, gb, xin, z, c->part_dots, (const DevState*)c->st_d));                    \
   } while (0)
       if (c->k_max <= 2) {
         if (d3) FAB_K1V(3, 2); else FAB_K1V(2, 2);

@@ -125,6 +125,8 @@ __device__ __forceinline__ int64_t rowq(const CsrArgs& a, int64_t r, uint64_t po
 template <int NWM, bool ACC, bool DOTS, int P>
 __global__ void __launch_bounds__(kThreads, P == 1 ? 6 : 3) k_csr_stream(CsrArgs a) {
   constexpr int kCsrU = kCsrNB / kThreads;
+  pdl_wait();
+  pdl_trigger();
   bool live[P];
   bool any = false;
 #pragma unroll
@@ -484,20 +486,20 @@ int64_t csr_max_blocks(const fab_ctx* c) {
 }
 
 template <int NWM, int P>
-static void launch_pass_p(const CsrArgs& a, int grid, bool acc, bool dots, cudaStream_t st) {
-  if (!acc && dots) k_csr_stream<NWM, false, true, P><<<grid, kThreads, 0, st>>>(a);
-  else if (!acc) k_csr_stream<NWM, false, false, P><<<grid, kThreads, 0, st>>>(a);
-  else if (dots) k_csr_stream<NWM, true, true, P><<<grid, kThreads, 0, st>>>(a);
-  else k_csr_stream<NWM, true, false, P><<<grid, kThreads, 0, st>>>(a);
+static cudaError_t launch_pass_p(const CsrArgs& a, int grid, bool acc, bool dots, bool pdl, cudaStream_t st) {
+  if (!acc && dots) return launch_pdl(pdl, k_csr_stream<NWM, false, true, P>, grid, kThreads, 0, st, a);
+  if (!acc) return launch_pdl(pdl, k_csr_stream<NWM, false, false, P>, grid, kThreads, 0, st, a);
+  if (dots) return launch_pdl(pdl, k_csr_stream<NWM, true, true, P>, grid, kThreads, 0, st, a);
+  return launch_pdl(pdl, k_csr_stream<NWM, true, false, P>, grid, kThreads, 0, st, a);
 }
 
 template <int NWM>
-static void launch_pass(const CsrArgs& a, int grid, int p, bool acc, bool dots, cudaStream_t st) {
+static cudaError_t launch_pass(const CsrArgs& a, int grid, int p, bool acc, bool dots, bool pdl, cudaStream_t st) {
   switch (p) {
-    case 1: launch_pass_p<NWM, 1>(a, grid, acc, dots, st); break;
-    case 2: launch_pass_p<NWM, 2>(a, grid, acc, dots, st); break;
-    case 3: launch_pass_p<NWM, 3>(a, grid, acc, dots, st); break;
-    default: launch_pass_p<NWM, 4>(a, grid, acc, dots, st); break;
+    case 1: return launch_pass_p<NWM, 1>(a, grid, acc, dots, pdl, st);
+    case 2: return launch_pass_p<NWM, 2>(a, grid, acc, dots, pdl, st);
+    case 3: return launch_pass_p<NWM, 3>(a, grid, acc, dots, pdl, st);
+    default: return launch_pass_p<NWM, 4>(a, grid, acc, dots, pdl, st);
   }
 }
 
@@ -535,9 +537,10 @@ int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* con
       a.st[i] = cs[i]->st_d;
     }
     const bool acc = j > 0, dots = (j == np - 1) && nw > 0;
-    if (c->k_max <= 2) launch_pass<2>(a, c->grid_spmv, p, acc, dots, st);
-    else if (c->k_max <= 4) launch_pass<4>(a, c->grid_spmv, p, acc, dots, st);
-    else launch_pass<8>(a, c->grid_spmv, p, acc, dots, st);
+    const bool pdl = c->pdl && !c->comm;
+    if (c->k_max <= 2) FAB_CUDA(launch_pass<2>(a, c->grid_spmv, p, acc, dots, pdl, st));
+    else if (c->k_max <= 4) FAB_CUDA(launch_pass<4>(a, c->grid_spmv, p, acc, dots, pdl, st));
+    else FAB_CUDA(launch_pass<8>(a, c->grid_spmv, p, acc, dots, pdl, st));
     FAB_CHECK_LAUNCH();
     ++*launches;
   }

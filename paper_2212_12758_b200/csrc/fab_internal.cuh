@@ -137,6 +137,7 @@ struct fab_ctx {
   int g_bat_m = -1, g_bat_k = -1;
   int64_t g_bat_launches = 0;
   double* xi = nullptr;               // multi-RHS interleaved SpMV inputs (n x 4), allocated on first use
+  bool pdl = false;                   // PDL between K1 and K3 (opt-in: FAB_PDL=1; measured slower)
 
   // cached Arnoldi (CGS2) graph
   cudaGraphExec_t gexec_arn = nullptr;
@@ -214,6 +215,31 @@ inline cudaError_t set_max_dyn_smem(const void* fn, int want) {
 }
 
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Programmatic dependent launch (PDL) between the streaming kernels of a
+// Krylov step: the next kernel is launched while the previous one drains
+// and blocks in pdl_wait() until the previous grid has completed and its
+// memory is visible -- the launch latency and CTA rasterisation overlap the
+// tail instead of following it.  A kernel launched without the attribute
+// returns from pdl_wait() at once.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
 
 inline int64_t next_pow2(int64_t n) {
   int64_t p = 1;
