@@ -520,7 +520,9 @@ __device__ __forceinline__ double cta_det_sum(const double* p, int count, int st
   return r;   // valid in thread 0
 }
 
-template <bool UPDATE, bool SKETCH, int SDIM>
+// NWM: window capacity of the update (2, 4 or 8 >= nw), so the per-row loop
+// issues no predicated-off loads / FMAs for unused window slots
+template <bool UPDATE, bool SKETCH, int SDIM, int NWM = kKMax>
 __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(PipeArgs a) {
   pdl_wait();
   pdl_trigger();
@@ -551,9 +553,9 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
     // (CTA 0 is writing beta[c-1] concurrently), older beta_j come from memory.
     const int c = a.col0, nw = a.nw, j0 = c - nw;
     const double nu = cta_det_sum(a.part_norm_prev, gridDim.x, 1, 0, red);
-    double dj[kKMax];
+    double dj[NWM];
 #pragma unroll
-    for (int t = 0; t < kKMax; ++t) dj[t] = t < nw ? cta_det_sum(a.part_dots, a.nparts_dots, kKMax + 1, t, red) : 0.0;
+    for (int t = 0; t < NWM; ++t) dj[t] = t < nw ? cta_det_sum(a.part_dots, a.nparts_dots, kKMax + 1, t, red) : 0.0;
     if (threadIdx.x == 0) {
       const double b = sqrt(nu);
       const bool st0 = blockIdx.x == 0;
@@ -639,16 +641,16 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
   }
 
   // ---------------- consumer warps ----------------
-  double cz = 1.0, cw[kKMax];
+  double cz = 1.0, cw[NWM];
 #pragma unroll
-  for (int t = 0; t < kKMax; ++t) cw[t] = 0.0;
+  for (int t = 0; t < NWM; ++t) cw[t] = 0.0;
   bool skip = false;   // fused K2 found a breakdown: consume the ring, write nothing
   if (UPDATE) {
     const double* cf = a.fuse_k2 ? scal : a.coef + (int64_t)a.col0 * (kKMax + 1);
     skip = a.fuse_k2 && scal[kKMax + 1] != 0.0;
     cz = cf[0];
 #pragma unroll
-    for (int t = 0; t < kKMax; ++t) cw[t] = (t < a.nw) ? cf[1 + t] : 0.0;
+    for (int t = 0; t < NWM; ++t) cw[t] = (t < a.nw) ? cf[1 + t] : 0.0;
   }
   double* __restrict__ out = UPDATE ? a.V + (int64_t)a.col0 * a.ld : nullptr;
   SkRows R;
@@ -708,7 +710,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
             if (UPDATE && SDIM == 0) {
               val = cz * sb[i];
 #pragma unroll
-              for (int t = 0; t < kKMax; ++t)
+              for (int t = 0; t < NWM; ++t)
                 if (t < a.nw) val = fma(cw[t], sb[(1 + t) * kChunk + i], val);
             } else if (UPDATE) {
               // z_r = (A w_hat_{c-1})_r recomputed exactly as K1 did (stencil_row)
@@ -721,10 +723,10 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
                                                   cur[h][1], cur[h][2], cur[h][3]);
               val = cz * zr;
 #pragma unroll
-              for (int t = 0; t < kKMax - 1; ++t)
+              for (int t = 0; t < NWM - 1; ++t)
                 if (t < a.nw - 1) val = fma(cw[t], sb[xw + t * kChunk + i], val);
 #pragma unroll
-              for (int t = 0; t < kKMax; ++t)                     // j = c-1 is the last window term
+              for (int t = 0; t < NWM; ++t)                       // j = c-1 is the last window term
                 if (t == a.nw - 1) val = fma(cw[t], xc, val);
             } else {
               val = sb[i];
@@ -777,12 +779,27 @@ static int pipe_stages(int stage_d, bool sketch, size_t* smem) {
   return ns;
 }
 
+template <bool UPDATE, bool SKETCH, int SDIM, int NWM>
+static int launch_stream_w(fab_ctx* c, const PipeArgs& a, size_t smem, cudaStream_t st) {
+  static bool attr = false;   // per instantiation: allow the ring's dynamic shared memory
+  if (!attr) {
+    FAB_CUDA(set_max_dyn_smem((const void*)k_stream_tiles<UPDATE, SKETCH, SDIM, NWM>, kSmemLimit));
+    attr = true;
+  }
+  FAB_CUDA(launch_pdl(c->pdl && !c->comm, k_stream_tiles<UPDATE, SKETCH, SDIM, NWM>, c->grid_upd, kPipeThreads,
+                      smem, st, a));
+  return FAB_OK;
+}
+
 template <bool UPDATE, bool SKETCH, int SDIM>
 static int launch_stream(fab_ctx* c, PipeArgs a, cudaStream_t st) {
   size_t smem = 0;
   a.nstage = pipe_stages(slot_geom<UPDATE, SKETCH, SDIM>(a.nw, a.apron).stage_d, SKETCH, &smem);
-  FAB_CUDA(launch_pdl(c->pdl && !c->comm, k_stream_tiles<UPDATE, SKETCH, SDIM>, c->grid_upd, kPipeThreads, smem,
-                      st, a));
+  int rc;
+  if (!UPDATE || c->k_max > 4) rc = launch_stream_w<UPDATE, SKETCH, SDIM, kKMax>(c, a, smem, st);
+  else if (c->k_max > 2) rc = launch_stream_w<UPDATE, SKETCH, SDIM, 4>(c, a, smem, st);
+  else rc = launch_stream_w<UPDATE, SKETCH, SDIM, 2>(c, a, smem, st);
+  if (rc != FAB_OK) return rc;
   FAB_CHECK_LAUNCH();
   return FAB_OK;
 }
