@@ -700,13 +700,16 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
         mbar_wait(full + rp.stage, rp.phase);
         const double* sb = ring + (size_t)rp.stage * stage_d;
         const uint32_t* sgn = reinterpret_cast<const uint32_t*>(sb + sign_off);
+        // chunk entirely inside this rank's rows: no per-row bounds test
+        const int64_t rc0 = g0 + ch * kChunk - rb;
+        const bool inside = rc0 >= 0 && rc0 + kChunk <= n;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int i = tid + kThreads * h;
           const int64_t g = g0 + ch * kChunk + i;
-          const int64_t r = g - rb;
+          const int64_t r = rc0 + i;
           double val = 0.0;
-          if (r >= 0 && r < n) {
+          if (inside || (r >= 0 && r < n)) {
             if (UPDATE && SDIM == 0) {
               val = cz * sb[i];
 #pragma unroll
@@ -735,7 +738,9 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
               out[r] = val;
               nrm = fma(val, val, nrm);
             }
-            if (SKETCH && ((sgn[i >> 5] >> (i & 31)) & 1u)) val = -val;
+            if (SKETCH)   // D_tt = -1: flip the sign bit
+              val = __longlong_as_double(__double_as_longlong(val) ^
+                                         ((unsigned long long)((sgn[i >> 5] >> (i & 31)) & 1u) << 63));
           }
           v[2 * ch + h] = val;
         }
