@@ -130,6 +130,11 @@ def lsqr(matvec, rmatvec, b: np.ndarray, ncols: int, tol: float = 1e-6,
         arnorm = phibar * alpha * abs(c)
         anorm = math.sqrt(anorm2)
         info.update(iters=it, rnorm=rnorm, arnorm=arnorm, anorm=anorm)
+        if alpha == 0.0 or beta == 0.0:
+            # the bidiagonalization terminated: x is the exact LS solution (the
+            # algorithm stops here in every mode, MATLAB lsqr as well)
+            info["converged"] = True
+            break
         if iters is None:
             if rnorm / bnorm <= tol or (rnorm > 0 and arnorm / (anorm * rnorm) <= tol) \
                     or alpha == 0.0 or beta == 0.0:

@@ -332,6 +332,8 @@ int launch_tall_gemv(fab_ctx* c, int ncols, const double* p, double scal, int us
 // ---- small helpers (one CTA of kThreads) ---------------------------------
 // out_i = scale_i * sum_{j>=i} U[i,j] v_j   (U upper triangular, given as UT =
 // U^T column-major: U[i,j] = UT[j + i*m]); warp per output, fixed order.
+constexpr int kLsqrStepThreads = 1024;   // the one-CTA LSQR scalar kernels (latency-bound m-length work)
+
 __device__ void upper_gemv(const double* UT, int m, const double* v, const double* rscale, double* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int i = warp; i < m; i += nw) {
@@ -369,6 +371,11 @@ struct LsqrVecs {
 
 // fixed-order reduction of the pass partials -> g (m), returns ||t||^2.
 // nparts < 0: part_g already holds the (allreduced) g[0..m-1], ||t||^2 = part_g[m].
+// g[j] = sum_b part_g[b][j], ||t||^2 = sum_b part_tn[b] in a fixed order:
+// gs = a power of two <= min(32, blockDim / m) lanes per column j, lane u
+// summing b = u, u + gs, ... then an xor tree; the norm by warp 0 (strided,
+// then the warp tree).  (Launched with kLsqrStepThreads everywhere, so the
+// order is the same on one GPU and in the multi-GPU k_pass_reduce.)
 __device__ double reduce_pass(const double* part_g, const double* part_tn, int nparts, int m, double* g,
                               double* red) {
   if (nparts < 0) {
@@ -378,18 +385,27 @@ __device__ double reduce_pass(const double* part_g, const double* part_tn, int n
     __syncthreads();
     return tn0;
   }
-  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+  int gs = 1;
+  while (gs < 32 && 2 * gs * m <= (int)blockDim.x) gs <<= 1;
+  const int per = blockDim.x / gs;                       // columns per sweep
+  const int sub = threadIdx.x & (gs - 1);
+  for (int j0 = 0; j0 < m; j0 += per) {
+    const int j = j0 + threadIdx.x / gs;
     double a = 0.0;
-    for (int b = 0; b < nparts; ++b) a += part_g[(int64_t)b * m + j];
-    g[j] = a;
+    if (j < m)
+      for (int b = sub; b < nparts; b += gs) a += part_g[(int64_t)b * m + j];
+    for (int o = gs >> 1; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (j < m && sub == 0) g[j] = a;
   }
   __shared__ double tn;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     double a = 0.0;
-    for (int b = 0; b < nparts; ++b) a += part_tn[b];
-    tn = a;
+    for (int b = threadIdx.x; b < nparts; b += 32) a += part_tn[b];
+    a = warp_sum(a);
+    if (threadIdx.x == 0) tn = a;
   }
   __syncthreads();
+  (void)red;
   return tn;
 }
 
@@ -398,14 +414,14 @@ __device__ double reduce_pass(const double* part_g, const double* part_tn, int n
 __global__ void k_pass_reduce(const double* part_g, const double* part_tn, int nparts, int m, double* out,
                               const DevState* st) {
   if (st->lsqr_done) return;
-  __shared__ double red[kWarps];
+  __shared__ double red[kLsqrStepThreads / 32];
   const double tn = reduce_pass(part_g, part_tn, nparts, m, out, red);
   if (threadIdx.x == 0) out[m] = tn;
 }
 
 // host wrapper: out[0..ncols-1] = sum of the g partials, out[ncols] = ||t||^2
 int launch_pass_reduce(fab_ctx* c, int nparts, int ncols, double* out, cudaStream_t st) {
-  k_pass_reduce<<<1, kThreads, 0, st>>>(c->part_g, c->part_tn, nparts, ncols, out, c->st_d);
+  k_pass_reduce<<<1, kLsqrStepThreads, 0, st>>>(c->part_g, c->part_tn, nparts, ncols, out, c->st_d);
   FAB_CHECK_LAUNCH();
   return comm_allreduce(c, out, (size_t)ncols + 1, false, st);
 }
@@ -415,7 +431,7 @@ int launch_pass_reduce(fab_ctx* c, int nparts, int ncols, double* out, cudaStrea
 __global__ void k_lsqr_init(const double* part_g, const double* part_tn, int nparts, int m,
                             const double* Rinv, const double* RinvT, const double* bcol, LsqrVecs L,
                             double tol, DevState* st) {
-  __shared__ double red[kWarps];
+  __shared__ double red[kLsqrStepThreads / 32];
   const double tn = reduce_pass(part_g, part_tn, nparts, m, L.g, red);
   const double bt = sqrt(tn);
   for (int j = threadIdx.x; j < m; j += blockDim.x) L.q[j] = L.g[j] / bcol[j] / bt;
@@ -459,7 +475,7 @@ __global__ void k_lsqr_step(const double* part_g, const double* part_tn, int npa
                             const double* Rinv, const double* RinvT, const double* bcol, LsqrVecs L,
                             int tol_mode, DevState* st) {
   if (st->lsqr_done) return;
-  __shared__ double red[kWarps];
+  __shared__ double red[kLsqrStepThreads / 32];
   const double tn = reduce_pass(part_g, part_tn, nparts, m, L.g, red);
   const double beta = sqrt(tn);
   const double ib = beta > 0 ? 1.0 / beta : 0.0;
@@ -473,6 +489,10 @@ __global__ void k_lsqr_step(const double* part_g, const double* part_tn, int npa
   const double alpha = sqrt(block_norm2(L.tmp, m, red));
   const double rhobar0 = st->rhobar, phibar0 = st->phibar;
   const double rho = hypot(rhobar0, beta);
+  if (!(rho > 0.0)) {   // degenerate (both zero): nothing left to solve
+    if (threadIdx.x == 0) st->lsqr_done = 1;
+    return;
+  }
   const double cs = rhobar0 / rho, sn = beta / rho;
   const double theta = sn * alpha;
   const double phi = cs * phibar0;
@@ -503,6 +523,8 @@ __global__ void k_lsqr_step(const double* part_g, const double* part_tn, int npa
     st->phibar = phibar;
     st->scal = beta > 0 ? alpha / beta : 0.0;
     st->lsqr_iters += 1;
+    // the bidiagonalization terminated: x is the exact LS solution (every mode)
+    if (alpha == 0.0 || beta == 0.0) st->lsqr_done = 1;
     if (tol_mode) {
       const double tol = st->tol;
       if (rnorm <= tol * st->scratch[0] || (rnorm > 0 && arnorm <= tol * anorm * rnorm) || alpha == 0.0 ||
@@ -685,7 +707,7 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
         *pg = c->part_g;
         *np = G;
         if (!c->comm) return FAB_OK;
-        k_pass_reduce<<<1, kThreads, 0, st>>>(c->part_g, c->part_tn, G, m, c->red, c->st_d);
+        k_pass_reduce<<<1, kLsqrStepThreads, 0, st>>>(c->part_g, c->part_tn, G, m, c->red, c->st_d);
         FAB_CHECK_LAUNCH();
         ++launches;
         *pg = c->red;
@@ -695,7 +717,7 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
       const double* pg = nullptr;
       int np = 0;
       FAB_TRY(pass_scalars(&pg, &np));
-      k_lsqr_init<<<1, kThreads, 0, st>>>(pg, c->part_tn, np, m, Rinv, RinvT, c->beta, L, tol, c->st_d);
+      k_lsqr_init<<<1, kLsqrStepThreads, 0, st>>>(pg, c->part_tn, np, m, Rinv, RinvT, c->beta, L, tol, c->st_d);
       FAB_CHECK_LAUNCH();
       launches += 2;
       int done_iters = 0;
@@ -709,7 +731,7 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
           if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[1], st));
           ++npass;
           FAB_TRY(pass_scalars(&pg, &np));
-          k_lsqr_step<<<1, kThreads, 0, st>>>(pg, c->part_tn, np, m, Rinv, RinvT, c->beta, L, fixed ? 0 : 1,
+          k_lsqr_step<<<1, kLsqrStepThreads, 0, st>>>(pg, c->part_tn, np, m, Rinv, RinvT, c->beta, L, fixed ? 0 : 1,
                                               c->st_d);
           FAB_CHECK_LAUNCH();
           launches += 2;
