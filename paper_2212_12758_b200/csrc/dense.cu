@@ -529,43 +529,46 @@ __global__ void __launch_bounds__(kGjThreads, 1) k_gj_inv_cluster(const double* 
   }
   double logdet = 0.0;
   int singular = 0;
+  // pivot search of column kk (rows >= kk, the first largest |a|) by one warp
+  // of its owner, published with the pivot row in slot kk & 1
+  auto search_publish = [&](int kk) {
+    const double* ck = cols + (size_t)(kk / kGjCl) * mp;
+    double* slot = bc + (size_t)(kk & 1) * (mp + 2);
+    double best = -1.0;
+    int bi = m;
+    double av[kGjRows];
+#pragma unroll
+    for (int r = 0; r < kGjRows; ++r) {
+      const int i = kk + lane + 32 * r;
+      av[r] = i < m ? fabs(ck[i]) : -1.0;
+    }
+#pragma unroll
+    for (int r = 0; r < kGjRows; ++r) {
+      if (av[r] > best) {
+        best = av[r];
+        bi = kk + lane + 32 * r;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    const double2* c2 = reinterpret_cast<const double2*>(ck);
+    double2* s2 = reinterpret_cast<double2*>(slot);
+    for (int i = lane; i < mp / 2; i += 32) s2[i] = c2[i];
+    if (lane == 0) slot[mp] = (double)bi;
+  };
   __syncthreads();
+  if (q == 0 && warp == 0) search_publish(0);
   cluster_barrier();
   for (int k = 0; k < m; ++k) {
-    const int owner = k % kGjCl, lk = k / kGjCl;
-    double* slot = bc + (size_t)(k & 1) * (mp + 2);
-    if (q == owner && warp == 0) {
-      const double* ck = cols + (size_t)lk * mp;
-      double best = -1.0;
-      int bi = m;
-      double av[kGjRows];
-#pragma unroll
-      for (int r = 0; r < kGjRows; ++r) {
-        const int i = k + lane + 32 * r;
-        av[r] = i < m ? fabs(ck[i]) : -1.0;
-      }
-#pragma unroll
-      for (int r = 0; r < kGjRows; ++r) {
-        if (av[r] > best) {
-          best = av[r];
-          bi = k + lane + 32 * r;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) {
-          best = ob;
-          bi = oi;
-        }
-      }
-      const double2* c2 = reinterpret_cast<const double2*>(ck);
-      double2* s2 = reinterpret_cast<double2*>(slot);
-      for (int i = lane; i < mp / 2; i += 32) s2[i] = c2[i];
-      if (lane == 0) slot[mp] = (double)bi;
-    }
-    cluster_barrier();
+    const int owner = k % kGjCl;
+    const double* slot = bc + (size_t)(k & 1) * (mp + 2);
     {
       const double2* rs = reinterpret_cast<const double2*>(cl.map_shared_rank(slot, owner));
       double2* p2 = reinterpret_cast<double2*>(pc);
@@ -585,7 +588,7 @@ __global__ void __launch_bounds__(kGjThreads, 1) k_gj_inv_cluster(const double* 
       const int i2 = lane + 32 * r;
       pr[r] = 2 * i2 < mp ? p2[i2] : make_double2(0.0, 0.0);
     }
-    for (int l = warp; l < nloc; l += kGjWarps) {
+    auto update_col = [&](int l) {
       const int j = q + kGjCl * l;
       double* col = cols + (size_t)l * mp;
       double2* c2 = reinterpret_cast<double2*>(col);
@@ -622,8 +625,28 @@ __global__ void __launch_bounds__(kGjThreads, 1) k_gj_inv_cluster(const double* 
           if (p != k) col[p] = fma(-ckk, rr, ak);
         }
       }
+      __syncwarp();
+    };
+    // look-ahead: the owner of column k+1 updates it first (warp 0), searches
+    // its pivot and publishes it into the other slot while the remaining
+    // warps (and CTAs) update the other columns -- the search and the publish
+    // leave the per-pivot critical path.  The other slot was last read at
+    // step k-1, before the previous cluster barrier.
+    const int nk = k + 1;
+    if (nk < m && q == nk % kGjCl) {
+      const int ln = nk / kGjCl;
+      if (warp == 0) {
+        update_col(ln);
+        search_publish(nk);
+      } else {
+        for (int l = warp - 1; l < nloc; l += kGjWarps - 1)
+          if (l != ln) update_col(l);
+      }
+    } else {
+      for (int l = warp; l < nloc; l += kGjWarps) update_col(l);
     }
     __syncthreads();
+    cluster_barrier();
   }
   // undo the row interchanges as column interchanges (in reverse order):
   // stored column s is column posof[s] of A^{-1}
