@@ -23,6 +23,9 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <memory>
+#include <mutex>
+#include <thread>
 
 #include "fab_internal.cuh"
 
@@ -302,6 +305,8 @@ struct CsrPlan {
   std::vector<CsrPass> pass;
   std::vector<void*> owned;   // device buffers of the column-blocked copy
   int64_t width = 0;          // columns per block (0: not column-blocked)
+  bool uniform = false;       // every value equals v0: the value array is dropped
+  double v0 = 1.0;
   ~CsrPlan() {
     for (auto& p : pass)
       if (p.blk) cudaFree(p.blk);
@@ -334,9 +339,38 @@ static int upload_blocks(const std::vector<int64_t>& bl, CsrPass* p) {
   return FAB_OK;
 }
 
+// Plans are shared by the contexts of one operator (the multi-RHS batch
+// creates p contexts of one A): keyed by the device and the caller's arrays,
+// built once, freed with the last context.
+struct PlanKey {
+  int device;
+  const void *rp, *ci, *va;
+  int64_t n, row_begin, nnz, width;
+  bool operator==(const PlanKey& o) const {
+    return device == o.device && rp == o.rp && ci == o.ci && va == o.va && n == o.n && row_begin == o.row_begin &&
+           nnz == o.nnz && width == o.width;
+  }
+};
+static std::mutex g_plan_mu;
+static std::vector<std::pair<PlanKey, std::weak_ptr<CsrPlan>>> g_plans;
+static std::vector<std::pair<fab_ctx*, std::shared_ptr<CsrPlan>>> g_holders;
+
 void csr_release(fab_ctx* c) {
-  delete c->csr;
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  for (size_t i = 0; i < g_holders.size(); ++i)
+    if (g_holders[i].first == c) {
+      g_holders.erase(g_holders.begin() + i);
+      break;
+    }
+  for (size_t i = 0; i < g_plans.size();)
+    if (g_plans[i].second.expired()) g_plans.erase(g_plans.begin() + i);
+    else ++i;
   c->csr = nullptr;
+}
+
+static int parallel_threads() {
+  const unsigned h = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(h ? h : 1u, 32u));
 }
 
 int csr_grid(fab_ctx* c, int* grid) {
@@ -348,11 +382,47 @@ int csr_grid(fab_ctx* c, int* grid) {
 }
 
 // At fab_init: uniform-value detection, the row blocks, and (if x is larger
-// than the L2 budget) the column-blocked copy of the entries.
+// than the L2 budget) the column-blocked copy of the entries -- or the plan
+// another context of the same operator already built.
+static int build_plan(fab_ctx* c, CsrPlan* plan, int64_t width);
+
 int csr_setup(fab_ctx* c) {
   csr_release(c);
-  CsrPlan* plan = new CsrPlan();
-  c->csr = plan;
+  // column-block width: the slice of x a pass gathers from stays in ~40 % of L2
+  int l2 = 0;
+  FAB_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device));
+  int64_t width = (int64_t)(0.4 * (double)l2) / 8;
+  if (width < 1024) width = 1024;
+  const char* env = getenv("FAB_CSR_COLBLOCK");   // tests: force a width (columns)
+  if (env && atoll(env) > 0) width = atoll(env);
+  const PlanKey key{c->device, c->op.row_ptr, c->op.col_idx, c->op.values, c->n, c->row_begin, c->op.nnz, width};
+  std::shared_ptr<CsrPlan> sp;
+  {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    for (auto& e : g_plans)
+      if (e.first == key) {
+        sp = e.second.lock();
+        if (sp) break;
+      }
+  }
+  if (!sp) {
+    sp = std::make_shared<CsrPlan>();
+    const int rc = build_plan(c, sp.get(), width);
+    if (rc != FAB_OK) return rc;
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    g_plans.push_back({key, sp});
+  }
+  if (sp->uniform) {
+    c->op.values = nullptr;
+    c->op.value_scale *= sp->v0;
+  }
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  g_holders.push_back({c, sp});
+  c->csr = sp.get();
+  return FAB_OK;
+}
+
+static int build_plan(fab_ctx* c, CsrPlan* plan, int64_t width) {
   // uniform values (e.g. a scaled 0/1 adjacency, c4): drop the value array
   // (8 B per entry per SpMV) and fold the value into value_scale
   if (c->op.values && c->op.nnz > 0) {
@@ -367,59 +437,78 @@ int csr_setup(fab_ctx* c) {
     FAB_CUDA(cudaMemcpyAsync(&same, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     FAB_CUDA(cudaStreamSynchronize(c->stream));
     if (same && isfinite(v0)) {
-      c->op.values = nullptr;
-      c->op.value_scale *= v0;
+      plan->uniform = true;
+      plan->v0 = v0;
     }
   }
+  const double* values = plan->uniform ? nullptr : c->op.values;
   const int64_t n = c->n, nnz = c->op.nnz;
   std::vector<int64_t> rp(n + 1);
   FAB_CUDA(cudaMemcpy(rp.data(), c->op.row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
-  // column-block width: the slice of x a pass gathers from stays in ~40 % of L2
-  int l2 = 0;
-  FAB_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device));
-  int64_t width = (int64_t)(0.4 * (double)l2) / 8;
-  if (width < 1024) width = 1024;
-  const char* env = getenv("FAB_CSR_COLBLOCK");   // tests: force a width (columns)
-  if (env && atoll(env) > 0) width = atoll(env);
   const int64_t P = (c->n_global + width - 1) / width;
   if (P <= 1 || nnz == 0) {
     CsrPass p;
     p.rp64 = c->op.row_ptr;
     p.ci = c->op.col_idx;
-    p.vals = c->op.values;
+    p.vals = values;
     FAB_TRY(upload_blocks(build_blocks(n, kCsrNB, [&](int64_t r) { return rp[r]; }), &p));
     plan->pass.push_back(p);
     return FAB_OK;
   }
   // column-blocked copy: entries of block j (columns [j w, (j+1) w)) of every
-  // local row, rows in order, in-row order kept
+  // local row, rows in order, in-row order kept.  Host threads over row ranges:
+  // count per (range, block), offsets, scatter (deterministic: the layout
+  // does not depend on the thread count).
   std::vector<int32_t> ci(nnz);
   FAB_CUDA(cudaMemcpy(ci.data(), c->op.col_idx, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
   std::vector<double> va;
-  if (c->op.values) {
+  if (values) {
     va.resize(nnz);
-    FAB_CUDA(cudaMemcpy(va.data(), c->op.values, nnz * sizeof(double), cudaMemcpyDeviceToHost));
+    FAB_CUDA(cudaMemcpy(va.data(), values, nnz * sizeof(double), cudaMemcpyDeviceToHost));
   }
-  std::vector<int64_t> cntb(P, 0);
-  for (int64_t q = 0; q < nnz; ++q) ++cntb[ci[q] / width];
-  std::vector<int64_t> base(P + 1, 0);
+  const int T = parallel_threads();
+  std::vector<int64_t> rlo(T + 1);
+  for (int t = 0; t <= T; ++t) rlo[t] = n * t / T;
+  std::vector<int64_t> cnt((size_t)T * P, 0);
+  {
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t)
+      th.emplace_back([&, t]() {
+        int64_t* ct = cnt.data() + (size_t)t * P;
+        for (int64_t q = rp[rlo[t]]; q < rp[rlo[t + 1]]; ++q) ++ct[ci[q] / width];
+      });
+    for (auto& x : th) x.join();
+  }
+  std::vector<int64_t> base(P + 1, 0), start((size_t)T * P);
   for (int64_t j = 0; j < P; ++j) {
-    if (cntb[j] >= ((int64_t)1 << 31)) return FAB_EINVAL;   // int32 relative row pointers
-    base[j + 1] = base[j] + cntb[j];
+    int64_t acc = 0;
+    for (int t = 0; t < T; ++t) {
+      start[(size_t)t * P + j] = acc;   // relative to the block's first entry
+      acc += cnt[(size_t)t * P + j];
+    }
+    if (acc >= ((int64_t)1 << 31)) return FAB_EINVAL;   // int32 relative row pointers
+    base[j + 1] = base[j] + acc;
   }
   std::vector<int32_t> ci2(nnz), rp2((size_t)P * (n + 1));
   std::vector<double> va2(va.empty() ? 0 : nnz);
-  std::vector<int64_t> fill(P, 0);
-  for (int64_t r = 0; r < n; ++r) {
-    for (int64_t j = 0; j < P; ++j) rp2[(size_t)j * (n + 1) + r] = (int32_t)fill[j];
-    for (int64_t q = rp[r]; q < rp[r + 1]; ++q) {
-      const int64_t j = ci[q] / width;
-      const int64_t dst = base[j] + fill[j]++;
-      ci2[dst] = ci[q];
-      if (!va.empty()) va2[dst] = va[q];
-    }
+  {
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t)
+      th.emplace_back([&, t]() {
+        std::vector<int64_t> fill(start.begin() + (size_t)t * P, start.begin() + (size_t)(t + 1) * P);
+        for (int64_t r = rlo[t]; r < rlo[t + 1]; ++r) {
+          for (int64_t j = 0; j < P; ++j) rp2[(size_t)j * (n + 1) + r] = (int32_t)fill[j];
+          for (int64_t q = rp[r]; q < rp[r + 1]; ++q) {
+            const int64_t j = ci[q] / width;
+            const int64_t dst = base[j] + fill[j]++;
+            ci2[dst] = ci[q];
+            if (!va.empty()) va2[dst] = va[q];
+          }
+        }
+      });
+    for (auto& x : th) x.join();
   }
-  for (int64_t j = 0; j < P; ++j) rp2[(size_t)j * (n + 1) + n] = (int32_t)fill[j];
+  for (int64_t j = 0; j < P; ++j) rp2[(size_t)j * (n + 1) + n] = (int32_t)(base[j + 1] - base[j]);
   int32_t *dci = nullptr, *drp = nullptr;
   double* dva = nullptr;
   FAB_CUDA(cudaMalloc(&dci, nnz * sizeof(int32_t)));
@@ -434,13 +523,22 @@ int csr_setup(fab_ctx* c) {
     FAB_CUDA(cudaMemcpy(dva, va2.data(), nnz * sizeof(double), cudaMemcpyHostToDevice));
   }
   plan->width = width;
+  std::vector<std::vector<int64_t>> bls(P);
+  {
+    std::vector<std::thread> th;
+    for (int64_t j = 0; j < P; ++j)
+      th.emplace_back([&, j]() {
+        const int32_t* rj = rp2.data() + (size_t)j * (n + 1);
+        bls[j] = build_blocks(n, kCsrNB, [&](int64_t r) { return (int64_t)rj[r]; });
+      });
+    for (auto& x : th) x.join();
+  }
   for (int64_t j = 0; j < P; ++j) {
     CsrPass p;
-    const int32_t* rj = rp2.data() + (size_t)j * (n + 1);
     p.rp32 = drp + (size_t)j * (n + 1);
     p.ci = dci + base[j];
     p.vals = dva ? dva + base[j] : nullptr;
-    FAB_TRY(upload_blocks(build_blocks(n, kCsrNB, [&](int64_t r) { return (int64_t)rj[r]; }), &p));
+    FAB_TRY(upload_blocks(bls[j], &p));
     plan->pass.push_back(p);
   }
   return FAB_OK;
