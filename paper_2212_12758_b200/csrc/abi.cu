@@ -173,6 +173,9 @@ static void free_ctx(fab_ctx* c) {
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  for (int i = 0; i < kCombChunks; ++i)
+    if (c->ev_chunk[i]) cudaEventDestroy(c->ev_chunk[i]);
+  if (c->copy_st) cudaStreamDestroy(c->copy_st);
   for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
   delete c;
 }
@@ -277,6 +280,8 @@ int fab_init(fab_ctx** out, const fab_operator* A, const double* b, const fab_op
   INIT_CUDA(cudaEventCreate(&c->ev0));
   INIT_CUDA(cudaEventCreate(&c->ev1));
   INIT_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  INIT_CUDA(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking));
+  for (int i = 0; i < kCombChunks; ++i) INIT_CUDA(cudaEventCreateWithFlags(&c->ev_chunk[i], cudaEventDisableTiming));
   INIT_CUDA(cudaMallocHost(&c->st_h, sizeof(DevState)));
   // b -> V[:, 0]
   INIT_CUDA(cudaMemcpyAsync(c->V, b, c->n * sizeof(double),
@@ -583,12 +588,13 @@ int fab_apply(fab_ctx* c, int f, double alpha, double sigma, double* y, int y_lo
   int rc = dense_fe1(c, f, alpha, sigma, cvec, &iters);
   if (rc != FAB_OK) return rc;
   const bool direct = (y_location == FAB_DEVICE) && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
-  double* ydev = direct ? y : c->vec;
-  if ((rc = run_combine(c, cvec, ydev)) != FAB_OK) return rc;
-  if (!direct) {
-    FAB_CUDA(cudaMemcpyAsync(y, ydev, c->n * sizeof(double),
-                             y_location == FAB_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
-                             c->stream));
+  if (y_location == FAB_HOST) {
+    if ((rc = run_combine_host(c, cvec, y)) != FAB_OK) return rc;   // copies overlap the combination
+  } else {
+    double* ydev = direct ? y : c->vec;
+    if ((rc = run_combine(c, cvec, ydev)) != FAB_OK) return rc;
+    if (!direct)
+      FAB_CUDA(cudaMemcpyAsync(y, ydev, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   }
   double ms = 0;
   if ((rc = timed_end(c, &ms)) != FAB_OK) return rc;

@@ -3,6 +3,8 @@
 // and stored columns w_hat_j = beta_j v_j,
 //     y[r] = sum_j (gamma_b c_j / beta_j) w_hat_j[r],
 // one streaming pass over V_m (8 n m bytes read, 8 n written).
+#include <algorithm>
+
 #include "fab_internal.cuh"
 
 namespace fab {
@@ -60,6 +62,33 @@ int run_combine(fab_ctx* c, const double* cvec_d, double* y_dev) {
   FAB_CHECK_LAUNCH();
   k_combine<<<c->grid_comb, kThreads, 0, c->stream>>>(c->V, c->ld, m, c->n, coef, y_dev);
   FAB_CHECK_LAUNCH();
+  return FAB_OK;
+}
+
+// f_m into HOST memory: the combination runs in kCombChunks row chunks on the
+// context's stream, and the device-to-host copy of each chunk starts on a
+// copy stream as soon as that chunk is written, so the transfer (~2.4 ms for
+// n = 2^24 over PCIe) overlaps the remaining combination instead of
+// following it.  The context's stream waits for the last copy.
+int run_combine_host(fab_ctx* c, const double* cvec_d, double* y_host) {
+  const int m = c->m_eff;
+  double* coef = svec(c, 15);
+  k_comb_coef<<<(m + 127) / 128, 128, 0, c->stream>>>(cvec_d, c->beta, m, c->st_d, coef);
+  FAB_CHECK_LAUNCH();
+  const int64_t n = c->n;
+  const int64_t step = ((n + kCombChunks - 1) / kCombChunks + 255) / 256 * 256;   // even, 2-KB aligned rows
+  int i = 0;
+  for (int64_t r0 = 0; r0 < n; r0 += step, ++i) {
+    const int64_t nr = (n - r0) < step ? (n - r0) : step;
+    const int g = (int)std::min<int64_t>(c->grid_comb, ((nr + 1) / 2 + kThreads - 1) / kThreads);
+    k_combine<<<g, kThreads, 0, c->stream>>>(c->V + r0, c->ld, m, nr, coef, c->vec + r0);
+    FAB_CHECK_LAUNCH();
+    FAB_CUDA(cudaEventRecord(c->ev_chunk[i], c->stream));
+    FAB_CUDA(cudaStreamWaitEvent(c->copy_st, c->ev_chunk[i], 0));
+    FAB_CUDA(cudaMemcpyAsync(y_host + r0, c->vec + r0, nr * sizeof(double), cudaMemcpyDeviceToHost, c->copy_st));
+  }
+  FAB_CUDA(cudaEventRecord(c->ev_join, c->copy_st));
+  FAB_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
   return FAB_OK;
 }
 

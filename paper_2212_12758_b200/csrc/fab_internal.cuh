@@ -55,6 +55,8 @@ struct fab_ctx {
   cudaStream_t stream = nullptr;   // caller's stream
   cudaStream_t cap = nullptr;      // internal stream used for graph capture
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_join = nullptr;
+  cudaStream_t copy_st = nullptr;                 // device-to-host copies overlapped with the combination
+  cudaEvent_t ev_chunk[8] = {};                   // one per combination chunk (kCombChunks)
 
   // operator
   fab_operator op{};
@@ -302,6 +304,8 @@ int dense_qr_sketch(fab_ctx* c, int m, double* R, double* qtb, cudaStream_t st);
 int dense_tri_inverse(fab_ctx* c, const double* R, int m, double* Rinv, cudaStream_t st);
 // apply.cu
 int run_combine(fab_ctx* c, const double* coef_d, double* y_dev);
+constexpr int kCombChunks = 8;
+int run_combine_host(fab_ctx* c, const double* coef_d, double* y_host);
 
 // the dense pool layout (matrices of m_max^2 doubles)
 constexpr int kDenseMats = 14;
