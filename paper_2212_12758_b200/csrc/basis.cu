@@ -1179,6 +1179,9 @@ int run_basis(fab_ctx* c, int m, int k) {
     }
     int64_t launches = 0;
     FAB_CUDA(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
+    // (a single cooperative kernel for all m steps, two grid barriers per
+    // step, was measured slower at every size: c1 25 vs 11 us, c2 32 vs 16 us
+    // per step -- the per-step graph of K1 and K3 stays)
     int rc = enqueue_basis_prologue(c, m, fused, c->cap, &launches);
     for (int col = 1; col <= m && rc == FAB_OK; ++col) rc = enqueue_step(c, col, k, fused, c->cap, &launches);
     if (rc == FAB_OK) {
