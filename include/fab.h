@@ -69,7 +69,8 @@ enum {
 };
 
 /* ---- enums ------------------------------------------------------------ */
-enum { FAB_BLENDENPIK = 0, FAB_SKETCH_SOLVE = 1, FAB_NONE = 2, FAB_LSQR = 3 };  /* fab_compress */
+enum { FAB_BLENDENPIK = 0, FAB_SKETCH_SOLVE = 1, FAB_NONE = 2, FAB_LSQR = 3,   /* fab_compress */
+       FAB_BLENDENPIK_GRAM = 4 };
 enum { FAB_EXP = 0, FAB_SQRT = 1, FAB_INVSQRT = 2, FAB_POLY = 3,     /* fab_apply    */
        FAB_SIGN = 4 };  /* sign(A) b = (A^2)^{-1/2} (A b); needs FAB_FLAG_SQUARE */
 enum { FAB_OP_CSR = 0, FAB_OP_STENCIL = 1 };                          /* operator kind */
@@ -174,6 +175,8 @@ typedef struct {
   int whitened_at;         /* fab_basis_whiten: i of the whitening (0: not triggered) */
   int pad1;
   double whiten_cond;      /* cond_1(R_i) that triggered it                           */
+  int gram_used;           /* FAB_BLENDENPIK_GRAM: 1 = Gram path, 0 = fell back to passes */
+  int pad2;
 } fab_info;
 
 /* ---- multi-GPU (one process per GPU, NCCL over NVLink) ----
@@ -273,7 +276,12 @@ int fab_basis_arnoldi(fab_ctx* ctx, int m);
 int fab_sketch(fab_ctx* ctx, int s, uint64_t seed);
 
 /* Compression (Eq. (6)/(7)).  mode FAB_BLENDENPIK: QR of Theta V_m, LSQR on
-   V_m R^{-1} (opts NULL => tol 1e-6, maxit 4m); FAB_SKETCH_SOLVE:
+   V_m R^{-1} (opts NULL => tol 1e-6, maxit 4m), one streaming pass over V_m per
+   iteration; FAB_BLENDENPIK_GRAM (B200-specific, not in the paper): the same
+   LSQR iterates in exact arithmetic, evaluated through the Gram matrix
+   G = V_{m+1}^T V_{m+1} of ONE pass (u = M a + g c is kept in R^m), used when
+   cond(R) <= 1e4 (rounding grows like cond(R)^2), else the streaming passes
+   (fab_info.gram_used); FAB_SKETCH_SOLVE:
    y = R^{-1} Q^T Theta v_{m+1}; FAB_NONE: y = 0 (Alg 5); FAB_LSQR: plain LSQR
    on V_m (Alg 3, l.194; needs no sketch).  Warnings: ILLCOND, NOTCONV.
    Errors: EORDER, ESINGULAR, ECUDA. */

@@ -12,7 +12,7 @@ LIB_PATH = os.path.join(HERE, "libfab.so")
 FAB_OK, FAB_BREAKDOWN, FAB_ILLCOND, FAB_NOTCONV = 0, 1, 2, 3
 FAB_EINVAL, FAB_EORDER, FAB_ESINGULAR, FAB_EDOMAIN = -1, -2, -3, -4
 FAB_ENOCONV, FAB_ENOMEM, FAB_ECUDA, FAB_ENCCL, FAB_ENODEV = -5, -6, -7, -8, -9
-FAB_BLENDENPIK, FAB_SKETCH_SOLVE, FAB_NONE, FAB_LSQR = 0, 1, 2, 3
+FAB_BLENDENPIK, FAB_SKETCH_SOLVE, FAB_NONE, FAB_LSQR, FAB_BLENDENPIK_GRAM = 0, 1, 2, 3, 4
 FAB_EXP, FAB_SQRT, FAB_INVSQRT, FAB_POLY, FAB_SIGN = 0, 1, 2, 3, 4
 FAB_OP_CSR, FAB_OP_STENCIL = 0, 1
 FAB_DEVICE, FAB_HOST = 0, 1
@@ -20,7 +20,8 @@ GET = dict(info=0, H=1, V=2, SV=3, rows=4, signs=5, y=6, C=7, fc=8, R=9, beta=10
 FAB_SET_POLY, FAB_SET_B_HOST, FAB_SET_B_DEVICE = 100, 101, 102
 FAB_FLAG_PROFILE, FAB_FLAG_SQUARE = 1, 2
 
-MODES = {"blendenpik": FAB_BLENDENPIK, "sketch_solve": FAB_SKETCH_SOLVE, "none": FAB_NONE, "lsqr": FAB_LSQR}
+MODES = {"blendenpik": FAB_BLENDENPIK, "sketch_solve": FAB_SKETCH_SOLVE, "none": FAB_NONE, "lsqr": FAB_LSQR,
+         "blendenpik_gram": FAB_BLENDENPIK_GRAM}
 FUNCS = {"exp": FAB_EXP, "sqrt": FAB_SQRT, "invsqrt": FAB_INVSQRT, "poly": FAB_POLY, "sign": FAB_SIGN}
 
 # every function declared in include/fab.h
@@ -61,7 +62,8 @@ class FabInfo(C.Structure):
                 ("launches_sketch", C.c_int64), ("launches_compress", C.c_int64),
                 ("launches_apply", C.c_int64), ("ms_lsqr_pass", C.c_double),
                 ("lsqr_passes", C.c_int64), ("ms_sketch_batched", C.c_double),
-                ("whitened_at", C.c_int), ("pad1", C.c_int), ("whiten_cond", C.c_double)]
+                ("whitened_at", C.c_int), ("pad1", C.c_int), ("whiten_cond", C.c_double),
+                ("gram_used", C.c_int), ("pad2", C.c_int)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad1"}

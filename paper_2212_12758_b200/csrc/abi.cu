@@ -164,6 +164,7 @@ static void free_ctx(fab_ctx* c) {
   if (c->gexec_sgs) cudaGraphExecDestroy(c->gexec_sgs);
   if (c->gexec_arn) cudaGraphExecDestroy(c->gexec_arn);
   if (c->gexec_bat) cudaGraphExecDestroy(c->gexec_bat);
+  if (c->gram_part) cudaFree(c->gram_part);
   if (c->xi) cudaFree(c->xi);
   if (c->wbuf) cudaFree(c->wbuf);
   if (c->part_dots) cudaFree(c->part_dots);
@@ -537,10 +538,12 @@ int fab_sketch(fab_ctx* c, int s, uint64_t seed) {
 
 int fab_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o) {
   if (!c) return FAB_EINVAL;
-  if (mode != FAB_BLENDENPIK && mode != FAB_SKETCH_SOLVE && mode != FAB_NONE && mode != FAB_LSQR)
+  if (mode != FAB_BLENDENPIK && mode != FAB_SKETCH_SOLVE && mode != FAB_NONE && mode != FAB_LSQR &&
+      mode != FAB_BLENDENPIK_GRAM)
     return FAB_EINVAL;
   if (!c->basis_ready) return FAB_EORDER;
-  const bool needs_sketch = (mode == FAB_BLENDENPIK || mode == FAB_SKETCH_SOLVE);
+  if (mode == FAB_BLENDENPIK_GRAM && c->comm) return FAB_EINVAL;   // one GPU only
+  const bool needs_sketch = (mode == FAB_BLENDENPIK || mode == FAB_SKETCH_SOLVE || mode == FAB_BLENDENPIK_GRAM);
   if (needs_sketch && !c->sketch_ready) return FAB_EORDER;
   if (o && (o->iters < 0 || o->maxit < 0 || o->tol < 0)) return FAB_EINVAL;
   int rc;

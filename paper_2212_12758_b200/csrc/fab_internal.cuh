@@ -140,6 +140,8 @@ struct fab_ctx {
   int64_t g_bat_launches = 0;
   double* xi = nullptr;               // multi-RHS interleaved SpMV inputs (n x 4), allocated on first use
   bool pdl = false;                   // PDL between K1 and K3 (opt-in: FAB_PDL=1; measured slower)
+  double* gram_part = nullptr;        // FAB_BLENDENPIK_GRAM: per-CTA Gram partials (allocated on first use)
+  size_t gram_part_bytes = 0;
 
   // cached Arnoldi (CGS2) graph
   cudaGraphExec_t gexec_arn = nullptr;
@@ -304,6 +306,11 @@ int dense_qr_sketch(fab_ctx* c, int m, double* R, double* qtb, cudaStream_t st);
 int dense_tri_inverse(fab_ctx* c, const double* R, int m, double* Rinv, cudaStream_t st);
 // apply.cu
 int run_combine(fab_ctx* c, const double* coef_d, double* y_dev);
+// gram.cu (FAB_BLENDENPIK_GRAM)
+constexpr double kGramCondMax = 1e4;
+int gram_pass(fab_ctx* c, int nc, double* G, cudaStream_t st);
+int gram_lsqr(fab_ctx* c, int m, const double* G, const double* Rinv, const double* RinvT, double* x, int fixed,
+              int maxit, double tol, cudaStream_t st);
 constexpr int kCombChunks = 8;
 int run_combine_host(fab_ctx* c, const double* coef_d, double* y_host);
 

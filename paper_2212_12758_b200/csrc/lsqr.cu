@@ -621,6 +621,7 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
   c->info.lsqr_converged = 0;
   c->info.cond_R = 0.0;
   c->info.lsqr_passes = 0;
+  c->info.gram_used = 0;
   c->info.ms_lsqr_pass = 0.0;
   int64_t launches = 0;
   const bool need_ls = (mode != FAB_NONE) && !c->breakdown;
@@ -658,6 +659,42 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
       k_finish_y<<<1, kThreads, 0, st>>>(RinvT, qtb, m, y);
       FAB_CHECK_LAUNCH();
       ++launches;
+    } else if (mode == FAB_BLENDENPIK_GRAM && c->info.cond_R <= kGramCondMax) {
+      // one Gram pass over V_{m+1}, then LSQR in R^m (gram.cu)
+      const int fixed = (o && o->iters > 0) ? o->iters : 0;
+      const double tol = (o && o->tol > 0) ? o->tol : 1e-6;
+      const int maxit = fixed ? fixed : ((o && o->maxit > 0) ? o->maxit : 4 * m);
+      double* G = dmat(c, 10);                 // (m+1)^2 doubles: dmat 10 and the start of 11
+      const bool prof = (c->flags & FAB_FLAG_PROFILE) != 0;
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (prof) {
+        FAB_CUDA(cudaEventCreate(&e0));
+        FAB_CUDA(cudaEventCreate(&e1));
+        FAB_CUDA(cudaEventRecord(e0, st));
+      }
+      FAB_TRY(gram_pass(c, m + 1, G, st));
+      if (prof) FAB_CUDA(cudaEventRecord(e1, st));
+      FAB_TRY(gram_lsqr(c, m, G, Rinv, RinvT, L.x, fixed, maxit, tol, st));
+      k_finish_y<<<1, kThreads, 0, st>>>(RinvT, L.x, m, y);
+      FAB_CHECK_LAUNCH();
+      launches += 4;
+      FAB_CUDA(cudaMemcpyAsync(c->st_h, c->st_d, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+      FAB_CUDA(cudaStreamSynchronize(st));
+      c->info.gram_used = 1;
+      c->info.lsqr_iters = c->st_h->lsqr_iters;
+      c->info.lsqr_converged = c->st_h->lsqr_done;
+      c->info.lsqr_rnorm = c->st_h->rnorm;
+      c->info.lsqr_arnorm = c->st_h->arnorm;
+      c->info.lsqr_anorm = c->st_h->anorm;
+      c->info.lsqr_passes = 1;
+      if (prof) {
+        float t = 0.f;
+        FAB_CUDA(cudaEventElapsedTime(&t, e0, e1));
+        c->info.ms_lsqr_pass = t;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+      }
+      if (!fixed && !c->st_h->lsqr_done && *warn == FAB_OK) *warn = FAB_NOTCONV;
     } else {
       int jpw = 0;
       LsqrPassFn pass = pick_pass(m, &jpw);

@@ -465,3 +465,58 @@ def test_csr_column_blocked_passes(name, kw, monkeypatch):
         ref = oracle_solve(p, "blendenpik")
     assert rel(outs[0], ref["f_m"]) <= 1e-10, rel(outs[0], ref["f_m"])
     assert rel(outs[0], outs[1]) <= 1e-12
+
+
+# ---- FAB_BLENDENPIK_GRAM: the same LSQR through the Gram matrix (gram.cu) ---
+@pytest.mark.parametrize("name,kw,csr", [
+    ("c1", {}, False),
+    ("c3", dict(g=32, m=60, s=130), False),
+    ("c5", dict(n=5001, m=12, s=40), True),
+    ("c2", dict(g=200, m=60, s=130), False),
+])
+def test_blendenpik_gram_matches_lsqr(name, kw, csr):
+    """Exact arithmetic gives LSQR's iterates; in fp64 the Gram path differs
+    by rounding amplified ~cond(R)^2 (cond(R) <= 1e4 here): fixed-L f_m vs the
+    streaming Blendenpik and vs the oracle at 1e-10, tolerance mode within a
+    couple of iterations and at the LSQR tolerance's scale."""
+    import torch
+    import paper_2212_12758_b200 as fab
+    p = fp.make(name, **kw)
+    sv = fab.Solver(fab.Operator.from_problem(p, csr=csr), torch.as_tensor(p.b).cuda(), p.m, p.k, p.s)
+    sv.sketch(p.s, p.sketch_seed)
+    sv.basis(p.m, p.k)
+    ref = oracle_solve(p, "blendenpik", iters=40, tol=0)            # fixed L = 40 on both sides
+    sv.compress("blendenpik", iters=40)
+    y_pass = sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()
+    sv.compress("blendenpik_gram", iters=40)
+    inf = sv.info()
+    assert inf["gram_used"] == 1 and inf["lsqr_iters"] == 40
+    y_gram = sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()
+    assert rel(y_gram, y_pass) <= 1e-10, rel(y_gram, y_pass)
+    assert rel(y_gram, ref["f_m"]) <= 1e-10, rel(y_gram, ref["f_m"])
+    sv.compress("blendenpik", tol=1e-6)
+    L_pass = sv.info()["lsqr_iters"]
+    y_tp = sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()
+    sv.compress("blendenpik_gram", tol=1e-6)
+    L_gram = sv.info()["lsqr_iters"]
+    y_tg = sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()
+    assert abs(L_gram - L_pass) <= 2, (L_gram, L_pass)
+    assert rel(y_tg, y_tp) <= 1e-6
+
+
+def test_blendenpik_gram_falls_back_when_ill_conditioned():
+    """c4's truncated basis is numerically singular (cond(R) ~ 1e15): the Gram
+    path would square that, so fab_compress runs the streaming passes."""
+    import torch
+    import paper_2212_12758_b200 as fab
+    p = fp.make("c4", n=1 << 14, m=60, s=130)
+    sv = fab.Solver(fab.Operator.from_problem(p), torch.as_tensor(p.b).cuda(), p.m, p.k, p.s)
+    sv.sketch(p.s, p.sketch_seed)
+    sv.basis(p.m, p.k)
+    sv.compress("blendenpik", iters=30)
+    y0 = sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()
+    sv.compress("blendenpik_gram", iters=30)
+    inf = sv.info()
+    assert inf["cond_R"] > 1e4 and inf["gram_used"] == 0
+    y1 = sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()
+    assert np.array_equal(y0, y1)
