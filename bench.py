@@ -237,13 +237,13 @@ def main():
     sv = fab.Solver(op, b, m_max=p.m, k_max=p.k, s_max=p.s, device=dev, profile=True, comm=comm)
     y = torch.empty(n_loc, dtype=torch.float64, device=f"cuda:{dev}")
 
-    def step(mode="blendenpik", fused=True):
+    def step(mode="blendenpik", fused=True, iters=0):
         if mode != "none" and fused:
             sv.sketch(p.s, p.sketch_seed)
         sv.basis(p.m, p.k)
         if mode != "none" and not fused:
             sv.sketch(p.s, p.sketch_seed)
-        sv.compress(mode, tol=1e-6)
+        sv.compress(mode, iters=iters, tol=0.0 if iters else 1e-6)
         sv.apply(p.f, p.alpha, p.sigma, out=y)
         return sv.info()
 
@@ -349,6 +349,16 @@ def main():
                                           "compress_ms": inf["ms_compress"],
                                           "gram_gflops": 2.0 * n_loc * (m + 1) ** 2 / 2 /
                                           max(inf["ms_lsqr_pass"], 1e-9) / 1e6}
+        # parity mode (fixed L = 40 LSQR iterations)
+        step("blendenpik", iters=40)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step("blendenpik", iters=40)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        modes["blendenpik_L40"] = 1e3 / e0.elapsed_time(e1)
         modes["blendenpik"] = value
         out["solves_per_s_by_mode"] = modes
         # API-order variant: sketch after the basis (batched SRHT pass)
@@ -410,6 +420,14 @@ def main():
         out["cpu_baseline"] = {"value": 1.0 / T, "unit": "solves/s", "cores": cpu_cores(),
                                "kind": "oracle", "sample": desc,
                                "krylov_iters_per_s": 1.0 / parts["t_iter"]}
+        try:   # the same sample on ONE core (BLAS threads limited)
+            from threadpoolctl import threadpool_limits
+            with threadpool_limits(limits=1):
+                T1, desc1, parts1 = oracle_sample(p, A, int(round(out["lsqr_iters"])), small=True)
+            out["cpu_baseline_1core"] = {"value": 1.0 / T1, "unit": "solves/s", "cores": 1, "kind": "oracle",
+                                         "sample": desc1, "krylov_iters_per_s": 1.0 / parts1["t_iter"]}
+        except Exception as e:   # report, do not fail the bench line
+            out["cpu_baseline_1core"] = {"error": repr(e)}
     sv.close()
     if comm is not None:
         comm.close()
