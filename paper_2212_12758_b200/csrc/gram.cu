@@ -17,6 +17,8 @@
 // amplifies by ||R^{-1}||^2 ~ cond(R)^2 / m; fab_compress therefore uses it
 // only when cond(R) <= kGramCondMax and otherwise runs the explicit passes
 // (fab_info.gram_used says which).
+#include <stdlib.h>
+
 #include "fab_internal.cuh"
 
 namespace fab {
@@ -121,6 +123,144 @@ k_gram(const double* __restrict__ V, int64_t ld, int64_t n, int nc, int ngroups,
         const int ci = I * kGB + u, cj = J * kGB + v;
         if (ci < nc && cj < nc) P[ci + (int64_t)cj * nc] = acc[u][v];
       }
+  }
+}
+
+// fp64 tensor-core variant (mma.sync m8n8k4 f64, DMMA): a warp owns a 4 x 4
+// tile of 8 x 8 blocks (TI <= TJ over the 4-block tiles of the upper
+// triangle), 32 accumulators per thread; per k-step of 4 rows it loads one
+// A/B fragment per block row / column (the same fragment serves as A for
+// block row X and as B for block column X: A[i][k] = B[k][i] = x[k][8X+i])
+// and issues 16 DMMAs -- 8 shared-memory loads per 4096 FMAs per warp instead
+// of 16 loads per 64 FMAs per thread in k_gram.  Warp tiles are dealt to
+// kGmWarps-warp groups; a CTA of group g sweeps every row chunk for its tiles.
+constexpr int kGmT = 4;          // blocks per warp-tile side
+constexpr int kGmWarps = 16;     // warps (tiles) per CTA group
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__host__ __device__ inline int gm_tile_str(int nbk) {
+  // row stride of the staged tile (doubles): 8-column blocks kGBS apart, then
+  // padded to 8 mod 16 so the 4 rows of a fragment load hit 2 disjoint
+  // halves of the banks
+  int s = nbk * kGBS;
+  while (s % 16 != 8) ++s;
+  return s;
+}
+
+__global__ void __launch_bounds__(kGmWarps * 32, 1)
+k_gram_mma(const double* __restrict__ V, int64_t ld, int64_t n, int nc, int ngroups, double* __restrict__ part) {
+  extern __shared__ __align__(16) double tile[];   // [2][kGRows][str]
+  const int nbk = (nc + kGB - 1) / kGB;
+  const int nwt = (nbk + kGmT - 1) / kGmT;
+  const int ntiles = nwt * (nwt + 1) / 2;
+  const int str = gm_tile_str(nbk);
+  const int group = blockIdx.x % ngroups;
+  const int cta_in_group = blockIdx.x / ngroups;
+  const int ctas_per_group = gridDim.x / ngroups;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wt = group * kGmWarps + warp;
+  const bool active = wt < ntiles;
+  int TI = 0, TJ = 0;
+  if (active) {
+    int rem = wt;
+    while (rem >= nwt - TI) {
+      rem -= nwt - TI;
+      ++TI;
+    }
+    TJ = TI + rem;
+  }
+  double acc[kGmT][kGmT][2];
+#pragma unroll
+  for (int a = 0; a < kGmT; ++a)
+#pragma unroll
+    for (int b = 0; b < kGmT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int64_t nchunks = (n + kGRows - 1) / kGRows;
+  const int ncol_pad = nbk * kGB;
+  const int nel = ncol_pad * kGRows;
+  auto load_chunk = [&](int64_t ch2, double* T) {
+    const int64_t r0 = ch2 * kGRows;
+    for (int e = threadIdx.x; e < nel; e += blockDim.x) {
+      const int j = e / kGRows, r = e - j * kGRows;
+      const bool ok = j < nc && r0 + r < n;
+      const double* src = ok ? V + (int64_t)j * ld + r0 + r : V;
+      const uint32_t dst =
+          static_cast<uint32_t>(__cvta_generic_to_shared(T + r * str + (j / kGB) * kGBS + (j % kGB)));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  // this lane's fragment offset inside a 4-row k-step: row (lane & 3), column (lane >> 2)
+  const int foff = (lane & 3) * str + (lane >> 2);
+  int64_t ch = cta_in_group;
+  int buf = 0;
+  if (ch < nchunks) load_chunk(ch, tile);
+  for (; ch < nchunks; ch += ctas_per_group) {
+    const int64_t nx = ch + ctas_per_group;
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    if (nx < nchunks) load_chunk(nx, tile + (size_t)(buf ^ 1) * kGRows * str);
+    const double* T = tile + (size_t)buf * kGRows * str;
+    if (active) {
+#pragma unroll 2
+      for (int ks = 0; ks < kGRows / 4; ++ks) {
+        const double* Tk = T + (4 * ks) * str + foff;
+        double fa[kGmT], fb[kGmT];
+#pragma unroll
+        for (int a = 0; a < kGmT; ++a) {
+          const int bi = TI * kGmT + a, bj = TJ * kGmT + a;
+          fa[a] = bi < nbk ? Tk[bi * kGBS] : 0.0;
+          fb[a] = bj < nbk ? Tk[bj * kGBS] : 0.0;
+        }
+#pragma unroll
+        for (int a = 0; a < kGmT; ++a)
+#pragma unroll
+          for (int b = 0; b < kGmT; ++b) dmma(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+      }
+    }
+    buf ^= 1;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (active) {
+    double* P = part + (int64_t)blockIdx.x * nc * nc;
+#pragma unroll
+    for (int a = 0; a < kGmT; ++a)
+#pragma unroll
+      for (int b = 0; b < kGmT; ++b) {
+        const int I = TI * kGmT + a, J = TJ * kGmT + b;
+        if (I > J || J >= nbk) continue;
+        const int ci = I * kGB + (lane >> 2);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cj = J * kGB + 2 * (lane & 3) + h;
+          if (ci < nc && cj < nc) P[ci + (int64_t)cj * nc] = acc[a][b][h];
+        }
+      }
+  }
+}
+
+// G from the k_gram_mma partials: the group owning block (I, J) is that of
+// its warp tile (I / 4, J / 4)
+__global__ void k_gram_mma_reduce(const double* part, int nc, int ngroups, int nctas, double* G) {
+  const int64_t total = (int64_t)nc * nc;
+  const int nbk = (nc + kGB - 1) / kGB;
+  const int nwt = (nbk + kGmT - 1) / kGmT;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int ci = (int)(e % nc), cj = (int)(e / nc);
+    const int I = ci / kGB, J = cj / kGB;
+    if (I > J) continue;
+    const int TI = I / kGmT, TJ = J / kGmT;
+    const int wt = TI * nwt - TI * (TI - 1) / 2 + (TJ - TI);
+    const int g = wt / kGmWarps;
+    double a = 0.0;
+    for (int c = g; c < nctas; c += ngroups) a += part[(int64_t)c * total + e];
+    G[ci + (int64_t)cj * nc] = a;
+    G[cj + (int64_t)ci * nc] = a;
   }
 }
 
@@ -289,7 +429,40 @@ static size_t gram_smem(int nc) {
 
 // G = V_hat^T V_hat of the stored columns 0..m (nc = m+1) into G (nc x nc,
 // column-major); uses c->wbuf-style scratch for the per-CTA partials.
+static int gram_pass_mma(fab_ctx* c, int nc, double* G, cudaStream_t st) {
+  const int nbk = (nc + kGB - 1) / kGB;
+  const int nwt = (nbk + kGmT - 1) / kGmT;
+  const int ntiles = nwt * (nwt + 1) / 2;
+  const int ngroups = (ntiles + kGmWarps - 1) / kGmWarps;
+  int grid = c->num_sms / ngroups * ngroups;
+  if (grid < ngroups) grid = ngroups;
+  const size_t need = (size_t)grid * nc * nc * sizeof(double);
+  if (c->gram_part_bytes < need) {
+    if (c->gram_part) cudaFree(c->gram_part);
+    c->gram_part = nullptr;
+    c->gram_part_bytes = 0;
+    FAB_CUDA(cudaMalloc(&c->gram_part, need));
+    c->gram_part_bytes = need;
+  }
+  const size_t smem = (size_t)2 * kGRows * gm_tile_str(nbk) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    FAB_CUDA(set_max_dyn_smem((const void*)k_gram_mma, 200 * 1024));
+    attr = true;
+  }
+  k_gram_mma<<<grid, kGmWarps * 32, smem, st>>>(c->V, c->ld, c->n, nc, ngroups, c->gram_part);
+  FAB_CHECK_LAUNCH();
+  k_gram_mma_reduce<<<(nc * nc + 255) / 256, 256, 0, st>>>(c->gram_part, nc, ngroups, grid, G);
+  FAB_CHECK_LAUNCH();
+  return FAB_OK;
+}
+
 int gram_pass(fab_ctx* c, int nc, double* G, cudaStream_t st) {
+  // the DMMA variant is opt-in (FAB_GRAM_MMA=1): measured at c3 51 ms vs
+  // 36.7 ms for the DFMA k_gram (two CTA groups each stage every row chunk,
+  // and the m8n8k4 f64 path does not outrun the FP64 FMA pipe here)
+  const char* e = getenv("FAB_GRAM_MMA");
+  if (e && e[0] == '1') return gram_pass_mma(c, nc, G, st);
   const int nbk = (nc + kGB - 1) / kGB;
   const int nblocks = nbk * (nbk + 1) / 2;
   const int ngroups = (nblocks + kGThreadsMax - 1) / kGThreadsMax;

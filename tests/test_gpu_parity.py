@@ -504,6 +504,24 @@ def test_blendenpik_gram_matches_lsqr(name, kw, csr):
     assert rel(y_tg, y_tp) <= 1e-6
 
 
+def test_blendenpik_gram_dmma_variant(monkeypatch):
+    """The opt-in fp64 tensor-core (mma.sync m8n8k4 DMMA) Gram kernel gives
+    the same f_m as the streaming LSQR at fixed L."""
+    import torch
+    import paper_2212_12758_b200 as fab
+    monkeypatch.setenv("FAB_GRAM_MMA", "1")
+    p = fp.make("c3", g=32, m=60, s=130)
+    sv = fab.Solver(fab.Operator.from_problem(p), torch.as_tensor(p.b).cuda(), p.m, p.k, p.s)
+    sv.sketch(p.s, p.sketch_seed)
+    sv.basis(p.m, p.k)
+    sv.compress("blendenpik", iters=40)
+    y0 = sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()
+    sv.compress("blendenpik_gram", iters=40)
+    assert sv.info()["gram_used"] == 1
+    y1 = sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()
+    assert rel(y1, y0) <= 1e-10
+
+
 def test_blendenpik_gram_falls_back_when_ill_conditioned():
     """c4's truncated basis is numerically singular (cond(R) ~ 1e15): the Gram
     path would square that, so fab_compress runs the streaming passes."""
