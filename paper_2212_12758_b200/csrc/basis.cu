@@ -419,6 +419,7 @@ struct PipeArgs {
   // kernel's prologue -- every CTA reduces the K1 / norm partials in
   // k_scalar's order (bitwise the same), CTA 0 stores beta, H and the state
   int fuse_k2;
+  const double* sums;   // fused K2 on several GPUs: the allreduced step scalars (k_step_reduce + C2)
   int nparts_dots;
   const double* part_dots;
   const double* part_norm_prev;
@@ -552,10 +553,17 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
     // CTA's consumer warps; only CTA 0 stores.  beta_{c-1} is this step's b
     // (CTA 0 is writing beta[c-1] concurrently), older beta_j come from memory.
     const int c = a.col0, nw = a.nw, j0 = c - nw;
-    const double nu = cta_det_sum(a.part_norm_prev, gridDim.x, 1, 0, red);
+    double nu;
     double dj[NWM];
+    if (a.sums) {   // several GPUs: the scalars were reduced and allreduced already
+      nu = a.sums[nw];
 #pragma unroll
-    for (int t = 0; t < NWM; ++t) dj[t] = t < nw ? cta_det_sum(a.part_dots, a.nparts_dots, kKMax + 1, t, red) : 0.0;
+      for (int t = 0; t < NWM; ++t) dj[t] = t < nw ? a.sums[t] : 0.0;
+    } else {
+      nu = cta_det_sum(a.part_norm_prev, gridDim.x, 1, 0, red);
+#pragma unroll
+      for (int t = 0; t < NWM; ++t) dj[t] = t < nw ? cta_det_sum(a.part_dots, a.nparts_dots, kKMax + 1, t, red) : 0.0;
+    }
     if (threadIdx.x == 0) {
       const double b = sqrt(nu);
       const bool st0 = blockIdx.x == 0;
@@ -1081,7 +1089,8 @@ int square_rhs(fab_ctx* c) {
 // K3 of step col: w_hat_col from z and the window, its norm partials and
 // (fused) its sketch partials.  nparts_k2 > 0: K2 of the step (k_scalar) is
 // done in K3's prologue from nparts_k2 K1 dot partials (one GPU only).
-int enqueue_k3(fab_ctx* c, int col, int nw, bool fused, cudaStream_t st, int64_t* launches, int nparts_k2 = 0) {
+int enqueue_k3(fab_ctx* c, int col, int nw, bool fused, cudaStream_t st, int64_t* launches, int nparts_k2 = 0,
+               const double* sums = nullptr) {
   PipeArgs a{};
   a.V = c->V;
   a.ld = c->ld;
@@ -1100,6 +1109,7 @@ int enqueue_k3(fab_ctx* c, int col, int nw, bool fused, cudaStream_t st, int64_t
   a.st = c->st_d;
   if (nparts_k2 > 0) {
     a.fuse_k2 = 1;
+    a.sums = sums;
     a.nparts_dots = nparts_k2;
     a.part_dots = c->part_dots;
     a.part_norm_prev = norm_parts(c, col - 1);
@@ -1129,9 +1139,15 @@ static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st,
   const int nw = col < k ? col : k;
   int nparts = 0;
   FAB_TRY(enqueue_k1(c, col, nw, c->vec, false, st, launches, &nparts));
-  if (c->comm) {   // C2: the scalars come from the allreduce
-    FAB_TRY(enqueue_scalar(c, col, nw, nparts, 0, st, launches));
-    return enqueue_k3(c, col, nw, fused, st, launches);
+  if (c->comm) {
+    // C2: this rank's scalars in k_scalar's order, ONE allreduce of k+1
+    // doubles, then K3 forms the step scalars from the sums in its prologue
+    k_step_reduce<<<1, kThreads, 0, st>>>(nw, nparts, c->grid_upd, c->part_dots, norm_parts(c, col - 1), c->red,
+                                         c->st_d);
+    FAB_CHECK_LAUNCH();
+    ++*launches;
+    FAB_TRY(comm_allreduce(c, c->red, (size_t)nw + 1, false, st));
+    return enqueue_k3(c, col, nw, fused, st, launches, nparts, c->red);
   }
   return enqueue_k3(c, col, nw, fused, st, launches, nparts);   // K2 fused into K3
 }

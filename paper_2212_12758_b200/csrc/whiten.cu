@@ -26,7 +26,8 @@ int enqueue_basis_prologue(fab_ctx* c, int m, bool fused, cudaStream_t st, int64
 int enqueue_k1(fab_ctx* c, int col, int nw, double* z, bool need_z, cudaStream_t st, int64_t* launches,
                int* nparts);
 int enqueue_scalar(fab_ctx* c, int col, int nw, int nparts, int final_step, cudaStream_t st, int64_t* launches);
-int enqueue_k3(fab_ctx* c, int col, int nw, bool fused, cudaStream_t st, int64_t* launches, int nparts_k2);
+int enqueue_k3(fab_ctx* c, int col, int nw, bool fused, cudaStream_t st, int64_t* launches, int nparts_k2,
+               const double* sums);
 int enqueue_col_sketch_reduce(fab_ctx* c, int col, double* p, cudaStream_t st, int64_t* launches);
 int enqueue_sgs_column(fab_ctx* c, int col, int m, cudaStream_t st, int64_t* launches);
 
@@ -214,7 +215,7 @@ int run_basis_whiten(fab_ctx* c, int m, int k, double cond_max, int* whitened_at
         break;
       }
     }
-    FAB_TRY(enqueue_k3(c, col, nw, true, st, &launches, 0));
+    FAB_TRY(enqueue_k3(c, col, nw, true, st, &launches, 0, nullptr));
   }
   if (iw == 0) {
     // no trigger: the plain Algorithm 2 basis (final lagged norm, Theta V)
