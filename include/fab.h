@@ -231,7 +231,9 @@ int fab_basis(fab_ctx* ctx, int m, int k);
    values are the dominant HBM stream of K1), the rest of the step is per
    context.  Each context ends in exactly the state fab_basis(ctx[i], m, k)
    leaves (bitwise: same kernels, grids and per-vector reduction order);
-   fab_info.ms_basis of every context is the batch's time.  Returns the
+   fab_info.ms_basis of every context is the batch's time.  For a CSR
+   operator whose p inputs fit the L2 budget, the first call allocates an
+   n x 4 interleaved input buffer (cudaMalloc, outside the workspace).  Returns the
    largest warning (FAB_BREAKDOWN if any context broke down).  Errors:
    EINVAL (count, duplicates, mismatched contexts or capacities), ECUDA. */
 int fab_basis_batch(fab_ctx** ctx, int p, int m, int k);
@@ -281,7 +283,8 @@ int fab_sketch(fab_ctx* ctx, int s, uint64_t seed);
    LSQR iterates in exact arithmetic, evaluated through the Gram matrix
    G = V_{m+1}^T V_{m+1} of ONE pass (u = M a + g c is kept in R^m), used when
    cond(R) <= 1e4 (rounding grows like cond(R)^2), else the streaming passes
-   (fab_info.gram_used); FAB_SKETCH_SOLVE:
+   (fab_info.gram_used); its first use allocates (cudaMalloc, outside the
+   workspace) #SMs x (m+1)^2 doubles of per-CTA Gram partials; FAB_SKETCH_SOLVE:
    y = R^{-1} Q^T Theta v_{m+1}; FAB_NONE: y = 0 (Alg 5); FAB_LSQR: plain LSQR
    on V_m (Alg 3, l.194; needs no sketch).  Warnings: ILLCOND, NOTCONV.
    Errors: EORDER, ESINGULAR, ECUDA. */

@@ -8,7 +8,23 @@
 
 #include "fab_internal.cuh"
 
+#include <mutex>
+
 namespace fab {
+
+cudaError_t ensure_dyn_smem(const void* fn, int want) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& d : done)
+    if (d.first == fn && d.second == dev) return cudaSuccess;
+  e = set_max_dyn_smem(fn, want);
+  if (e == cudaSuccess) done.push_back({fn, dev});
+  return e;
+}
 
 static thread_local char g_err[512] = "";
 

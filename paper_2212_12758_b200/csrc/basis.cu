@@ -794,11 +794,7 @@ static int pipe_stages(int stage_d, bool sketch, size_t* smem) {
 
 template <bool UPDATE, bool SKETCH, int SDIM, int NWM>
 static int launch_stream_w(fab_ctx* c, const PipeArgs& a, size_t smem, cudaStream_t st) {
-  static bool attr = false;   // per instantiation: allow the ring's dynamic shared memory
-  if (!attr) {
-    FAB_CUDA(set_max_dyn_smem((const void*)k_stream_tiles<UPDATE, SKETCH, SDIM, NWM>, kSmemLimit));
-    attr = true;
-  }
+  FAB_CUDA(ensure_dyn_smem((const void*)k_stream_tiles<UPDATE, SKETCH, SDIM, NWM>, kSmemLimit));
   FAB_CUDA(launch_pdl(c->pdl && !c->comm, k_stream_tiles<UPDATE, SKETCH, SDIM, NWM>, c->grid_upd, kPipeThreads,
                       smem, st, a));
   return FAB_OK;

@@ -708,11 +708,7 @@ static int gj_solve(fab_ctx* c, int m, const double* A, double* Awork, double* B
                     cudaStream_t st) {
   const size_t smem = gj_cluster_smem(m, nrhs);
   if (m <= kGjClMaxM && smem <= 226 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      FAB_CUDA(set_max_dyn_smem((const void*)k_gj_cluster, 226 * 1024));
-      attr = true;
-    }
+    FAB_CUDA(ensure_dyn_smem((const void*)k_gj_cluster, 226 * 1024));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kGjCl, 1, 1);
     cfg.blockDim = dim3(kGjThreads, 1, 1);
@@ -750,11 +746,7 @@ static int gj_inverse(fab_ctx* c, int m, const double* A, double* Awork, double*
     FAB_TRY(lincomb(c, m, 0, nullptr, 0, nullptr, 0, nullptr, 1.0, Ainv, st));   // I
     return gj_solve(c, m, A, Awork, Ainv, m, out, st);
   }
-  static bool attr = false;
-  if (!attr) {
-    FAB_CUDA(set_max_dyn_smem((const void*)k_gj_inv_cluster, 226 * 1024));
-    attr = true;
-  }
+  FAB_CUDA(ensure_dyn_smem((const void*)k_gj_inv_cluster, 226 * 1024));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kGjCl, 1, 1);
   cfg.blockDim = dim3(kGjThreads, 1, 1);

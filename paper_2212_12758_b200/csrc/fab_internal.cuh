@@ -218,6 +218,10 @@ inline cudaError_t set_max_dyn_smem(const void* fn, int want) {
   return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, want < cap ? want : cap);
 }
 
+// set_max_dyn_smem once per (kernel, device) of this process (the attribute
+// belongs to the device context; a process may drive several GPUs)
+cudaError_t ensure_dyn_smem(const void* fn, int want);
+
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 // Programmatic dependent launch (PDL) between the streaming kernels of a

@@ -445,11 +445,7 @@ static int gram_pass_mma(fab_ctx* c, int nc, double* G, cudaStream_t st) {
     c->gram_part_bytes = need;
   }
   const size_t smem = (size_t)2 * kGRows * gm_tile_str(nbk) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    FAB_CUDA(set_max_dyn_smem((const void*)k_gram_mma, 200 * 1024));
-    attr = true;
-  }
+  FAB_CUDA(ensure_dyn_smem((const void*)k_gram_mma, 200 * 1024));
   k_gram_mma<<<grid, kGmWarps * 32, smem, st>>>(c->V, c->ld, c->n, nc, ngroups, c->gram_part);
   FAB_CHECK_LAUNCH();
   k_gram_mma_reduce<<<(nc * nc + 255) / 256, 256, 0, st>>>(c->gram_part, nc, ngroups, grid, G);
@@ -479,11 +475,7 @@ int gram_pass(fab_ctx* c, int nc, double* G, cudaStream_t st) {
     FAB_CUDA(cudaMalloc(&c->gram_part, need));
     c->gram_part_bytes = need;
   }
-  static bool attr = false;
-  if (!attr) {
-    FAB_CUDA(set_max_dyn_smem((const void*)k_gram, 200 * 1024));
-    attr = true;
-  }
+  FAB_CUDA(ensure_dyn_smem((const void*)k_gram, 200 * 1024));
   k_gram<<<grid, threads, gram_smem(nc), st>>>(c->V, c->ld, c->n, nc, ngroups, per_group, c->gram_part);
   FAB_CHECK_LAUNCH();
   k_gram_reduce<<<(nc * nc + 255) / 256, 256, 0, st>>>(c->gram_part, nc, ngroups, grid, G);
