@@ -26,7 +26,7 @@ namespace fab {
 constexpr int kGB = 8;          // 8 x 8 block of G per thread
 constexpr int kGBS = 10;        // shared-memory stride of an 8-column block (doubles)
 constexpr int kGRows = 32;      // rows per chunk
-constexpr int kGThreadsMax = 384;
+constexpr int kGThreadsMax = 352;   // 186 registers per thread at one CTA per SM
 
 // Upper-triangular 8 x 8 blocks (I <= J) of an (nc x nc) Gram matrix, block b
 // of group gi handled by thread b - gi * per_group.  Partials per CTA:
@@ -92,18 +92,36 @@ k_gram(const double* __restrict__ V, int64_t ld, int64_t n, int nc, int ngroups,
     if (nx < nchunks) load_chunk(nx, tile + (size_t)(buf ^ 1) * kGRows * str);   // in flight during the FMAs
     const double* T = tile + (size_t)buf * kGRows * str;
     if (active) {
-#pragma unroll 2
+      // software-pipelined: row r+1's eight 16-B loads are issued before row
+      // r's 64 FMAs, so the FMAs never wait on shared memory
+      double2 fi[kGB / 2], fj[kGB / 2];
+      {
+        const double2* pi = reinterpret_cast<const double2*>(T + I * kGBS);
+        const double2* pj = reinterpret_cast<const double2*>(T + J * kGBS);
+#pragma unroll
+        for (int u = 0; u < kGB / 2; ++u) {
+          fi[u] = pi[u];
+          fj[u] = pj[u];
+        }
+      }
+#pragma unroll 1
       for (int r = 0; r < kGRows; ++r) {
-        const double2* pi = reinterpret_cast<const double2*>(T + r * str + I * kGBS);
-        const double2* pj = reinterpret_cast<const double2*>(T + r * str + J * kGBS);
         double xi[kGB], xj[kGB];
 #pragma unroll
         for (int u = 0; u < kGB / 2; ++u) {
-          const double2 a2 = pi[u], b2 = pj[u];
-          xi[2 * u] = a2.x;
-          xi[2 * u + 1] = a2.y;
-          xj[2 * u] = b2.x;
-          xj[2 * u + 1] = b2.y;
+          xi[2 * u] = fi[u].x;
+          xi[2 * u + 1] = fi[u].y;
+          xj[2 * u] = fj[u].x;
+          xj[2 * u + 1] = fj[u].y;
+        }
+        if (r + 1 < kGRows) {
+          const double2* pi = reinterpret_cast<const double2*>(T + (r + 1) * str + I * kGBS);
+          const double2* pj = reinterpret_cast<const double2*>(T + (r + 1) * str + J * kGBS);
+#pragma unroll
+          for (int u = 0; u < kGB / 2; ++u) {
+            fi[u] = pi[u];
+            fj[u] = pj[u];
+          }
         }
 #pragma unroll
         for (int u = 0; u < kGB; ++u)
