@@ -538,3 +538,41 @@ def test_blendenpik_gram_falls_back_when_ill_conditioned():
     assert inf["cond_R"] > 1e4 and inf["gram_used"] == 0
     y1 = sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()
     assert np.array_equal(y0, y1)
+
+
+# ---- seeded random sweep over shapes, operators, modes and functions -------
+def _sweep_cases():
+    rng = np.random.default_rng(20240611)
+    cases = []
+    for i in range(12):
+        kind = ["c1", "c3", "c5", "c4"][i % 4]
+        if kind == "c1":
+            kw = dict(g=int(rng.integers(20, 90)))
+        elif kind == "c3":
+            kw = dict(g=int(rng.integers(8, 26)))
+        elif kind == "c5":
+            kw = dict(n=int(rng.integers(1500, 9000)))
+        else:
+            kw = dict(n=int(2 ** rng.integers(11, 14)))
+        m = int(rng.integers(3, 31))
+        kw.update(m=m, k=int(rng.integers(1, 5)), s=int(m + 1 + rng.integers(0, 2 * m)))
+        mode = ["blendenpik", "sketch_solve", "none"][int(rng.integers(0, 3))]
+        csr = bool(rng.integers(0, 2)) if kind in ("c1", "c3") else True
+        cases.append((kind, kw, mode, csr))
+    return cases
+
+
+@pytest.mark.parametrize("kind,kw,mode,csr", _sweep_cases())
+def test_random_sweep_parity(kind, kw, mode, csr):
+    """Ragged sizes, every k, CSR and stencil, all three modes, the config's f:
+    f_m against the oracle at BASELINE's 1e-10 (fixed L = 40), where the
+    oracle's own MGS/CGS floor allows (G-24); breakdowns must agree."""
+    p = fp.make(kind, **kw)
+    y, sv = gpu_solve(p, mode, iters=40, csr=csr)
+    ref = oracle_solve(p, mode, iters=40, tol=0.0)
+    inf = sv.info()
+    assert inf["m_eff"] == ref["m_eff"] and bool(inf["breakdown"]) == bool(ref["breakdown"])
+    floor = rel(ofab.solve(p.scipy(), p.b, p.m, p.k, p.s, p.sketch_seed, mode=mode, f=p.f, alpha=p.alpha,
+                           sigma=p.sigma, lsqr_iters=40, variant="mgs", keep=False)["f_m"], ref["f_m"])
+    assert rel(y, ref["f_m"]) <= max(1e-10, 10 * floor), (rel(y, ref["f_m"]), floor)
+    sv.close()
