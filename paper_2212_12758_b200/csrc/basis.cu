@@ -397,6 +397,17 @@ constexpr int kChunksPerTile = kSkT / kChunk;   // 8
 constexpr int kPipeThreads = kThreads + 32;
 constexpr int kMaxStages = 16;
 constexpr int kSignPad = 16;   // doubles reserved per stage for the chunk's sign bits
+// K5 (!UPDATE: one vector, sketch only) stages a whole 4096-row tile per ring
+// stage: one bulk copy of 32 KB (+ 512 B of sign bits) and one mbarrier
+// round trip per tile instead of eight, which matters because K5 moves one
+// vector per FWHT (in K3 the FWHT hides behind 5-6 vectors of traffic)
+template <bool UPDATE>
+struct ChunkGeo {
+  static constexpr int CH = UPDATE ? kChunk : kSkT;          // rows per stage
+  static constexpr int NCH = kSkT / CH;                      // stages per tile
+  static constexpr int RPT = CH / kThreads;                  // rows per consumer thread per stage
+  static constexpr int SIGND = UPDATE ? kSignPad : kSkT / 64;   // doubles of sign bits (128-B multiple)
+};
 constexpr int kPipeCtasPerSm = 2;        // resident K3/K5 CTAs per SM
 constexpr int kSmemLimit = (226 * 1024) / kPipeCtasPerSm - 2048;   // dynamic smem budget per CTA
 
@@ -431,6 +442,7 @@ struct PipeArgs {
   StencilP sp;
   int64_t hal;          // halo rows held in each column's padding (0 on one GPU)
   int apron;            // rows of w_hat_{c-1} staged either side of a chunk (16)
+  int64_t sign_words;   // allocated 32-bit words of the sign bitmap (16-B multiple)
 };
 
 // Ring-stage slots (doubles) of one 512-row chunk [r0, r0+512):
@@ -451,7 +463,7 @@ __host__ __device__ __forceinline__ SlotGeom slot_geom(int nw, int apron) {
   SlotGeom g;
   if (!UPDATE) {
     g.nslot = 1;
-    g.stage_d = kChunk;
+    g.stage_d = ChunkGeo<false>::CH;
   } else if (SDIM == 0) {
     g.nslot = 1 + nw;
     g.stage_d = (1 + nw) * kChunk;
@@ -459,7 +471,7 @@ __host__ __device__ __forceinline__ SlotGeom slot_geom(int nw, int apron) {
     g.nslot = 1 + (nw - 1);
     g.stage_d = (kChunk + 2 * apron) + (nw - 1) * kChunk;
   }
-  g.stage_d += SKETCH ? kSignPad : 0;
+  g.stage_d += SKETCH ? ChunkGeo<UPDATE>::SIGND : 0;
   return g;
 }
 
@@ -468,8 +480,8 @@ template <bool UPDATE, int SDIM>
 __device__ __forceinline__ void slot_copy(const PipeArgs& a, int v, int col, int64_t r0, const double** src,
                                           int* dst_off, int64_t* lo, int64_t* hi) {
   const int j0 = a.col0 - a.nw;
-  int64_t base = r0, len = kChunk, clo = 0, chi = a.n;
-  int off = v * kChunk;
+  int64_t base = r0, len = ChunkGeo<UPDATE>::CH, clo = 0, chi = a.n;
+  int off = v * ChunkGeo<UPDATE>::CH;
   if (!UPDATE) {
     *src = a.V + (int64_t)col * a.ld;
   } else if (SDIM == 0) {
@@ -534,7 +546,8 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
   const SlotGeom geo = slot_geom<UPDATE, SKETCH, SDIM>(a.nw, a.apron);
   const int nstage = a.nstage;
   const int stage_d = geo.stage_d;
-  const int sign_off = stage_d - (SKETCH ? kSignPad : 0);
+  using CG = ChunkGeo<UPDATE>;
+  const int sign_off = stage_d - (SKETCH ? CG::SIGND : 0);
   double* ring = dsm;
   double* fw = ring + (size_t)nstage * stage_d;
   uint64_t* full = reinterpret_cast<uint64_t*>(fw + (SKETCH ? kSkSmem : 0));
@@ -608,9 +621,15 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
     RingPos rp;
     for (int col = a.col0; col < a.col1; ++col) {
       for (int64_t tile = t_first + blockIdx.x; tile <= t_last; tile += gridDim.x) {
-        for (int ch = 0; ch < kChunksPerTile; ++ch) {
-          const int64_t r0 = (tile << kSkLogT) + ch * kChunk - rb;
-          const bool any = (r0 + kChunk > 0) && (r0 < n);   // the chunk holds local rows
+        for (int ch = 0; ch < CG::NCH; ++ch) {
+          const int64_t r0 = (tile << kSkLogT) + ch * CG::CH - rb;
+          const bool any = (r0 + CG::CH > 0) && (r0 < n);   // the chunk holds local rows
+          // sign words of global rows [g, g + CH): g is CH-aligned; clamp to
+          // the bitmap's allocation (a tile past N only holds zero rows)
+          const int64_t gw = ((tile << kSkLogT) + ch * CG::CH) >> 5;
+          const int64_t sw_left = a.sign_words - gw;
+          const uint32_t sbytes =
+              SKETCH ? (uint32_t)(sw_left <= 0 ? 0 : (sw_left < CG::CH / 32 ? sw_left * 4 : CG::CH / 8)) : 0u;
           mbar_wait(empty + rp.stage, rp.phase ^ 1u);
           if (any) {
             double* sb = ring + (size_t)rp.stage * stage_d;
@@ -618,7 +637,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
             int doff = 0;
             int64_t lo = 0, hi = 0;
             if (lane == 0) {
-              uint32_t total = SKETCH ? 64u : 0u;
+              uint32_t total = sbytes;
               for (int v = 0; v < geo.nslot; ++v) {
                 slot_copy<UPDATE, SDIM>(a, v, col, r0, &src, &doff, &lo, &hi);
                 if (hi > lo) total += (uint32_t)((hi - lo) * 8);
@@ -631,11 +650,8 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
               const bool xslot = UPDATE && SDIM > 0 && (lane == 0 || lane >= a.nw);
               if (hi > lo)
                 bulk_g2s(sb + doff, src + lo, (uint32_t)((hi - lo) * 8), full + rp.stage, xslot ? pol_x : pol);
-            } else if (SKETCH && lane == geo.nslot) {
-              // sign words of global rows [g, g+512): g is 512-aligned, the
-              // bitmap is padded to 256 B, so the 64 B are always in bounds
-              const int64_t gw = ((tile << kSkLogT) + ch * kChunk) >> 5;
-              bulk_g2s(sb + sign_off, a.signs + gw, 64u, full + rp.stage, pol);
+            } else if (SKETCH && lane == geo.nslot && sbytes > 0) {
+              bulk_g2s(sb + sign_off, a.signs + gw, sbytes, full + rp.stage, pol);
             }
           } else if (lane == 0) {
             mbar_arrive(full + rp.stage);
@@ -693,7 +709,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
       const int64_t g0 = tile << kSkLogT;
       double v[kSkPer];
 #pragma unroll
-      for (int ch = 0; ch < kChunksPerTile; ++ch) {
+      for (int ch = 0; ch < CG::NCH; ++ch) {
         double cur[2][4];
         if (UPDATE && SDIM > 0) {
 #pragma unroll
@@ -709,12 +725,12 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
         const double* sb = ring + (size_t)rp.stage * stage_d;
         const uint32_t* sgn = reinterpret_cast<const uint32_t*>(sb + sign_off);
         // chunk entirely inside this rank's rows: no per-row bounds test
-        const int64_t rc0 = g0 + ch * kChunk - rb;
-        const bool inside = rc0 >= 0 && rc0 + kChunk <= n;
+        const int64_t rc0 = g0 + ch * CG::CH - rb;
+        const bool inside = rc0 >= 0 && rc0 + CG::CH <= n;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < CG::RPT; ++h) {
           const int i = tid + kThreads * h;
-          const int64_t g = g0 + ch * kChunk + i;
+          const int64_t g = g0 + ch * CG::CH + i;
           const int64_t r = rc0 + i;
           double val = 0.0;
           if (inside || (r >= 0 && r < n)) {
@@ -750,7 +766,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
               val = __longlong_as_double(__double_as_longlong(val) ^
                                          ((unsigned long long)((sgn[i >> 5] >> (i & 31)) & 1u) << 63));
           }
-          v[2 * ch + h] = val;
+          v[CG::RPT * ch + h] = val;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + rp.stage);
@@ -1099,6 +1115,7 @@ int enqueue_k3(fab_ctx* c, int col, int nw, bool fused, cudaStream_t st, int64_t
   a.row_begin = c->row_begin;
   a.part_norm = norm_parts(c, col);
   a.signs = c->signs_d;
+  a.sign_words = round_up((c->N + 31) / 32, 4);   // 16-B multiple, inside the 256-B carve
   a.rows = c->rows_d;
   a.s = c->s;
   a.part_sk = c->part_sk;
@@ -1158,6 +1175,7 @@ int launch_sketch_cols(fab_ctx* c, int c0, int c1, cudaStream_t st) {
   a.n = c->n;
   a.row_begin = c->row_begin;
   a.signs = c->signs_d;
+  a.sign_words = round_up((c->N + 31) / 32, 4);   // 16-B multiple, inside the 256-B carve
   a.rows = c->rows_d;
   a.s = c->s;
   a.part_sk = c->part_sk;
