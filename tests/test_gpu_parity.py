@@ -576,3 +576,15 @@ def test_random_sweep_parity(kind, kw, mode, csr):
                            sigma=p.sigma, lsqr_iters=40, variant="mgs", keep=False)["f_m"], ref["f_m"])
     assert rel(y, ref["f_m"]) <= max(1e-10, 10 * floor), (rel(y, ref["f_m"]), floor)
     sv.close()
+
+
+@pytest.mark.parametrize("name", ["c5", "c1"])
+def test_large_m_dense_fallback(name):
+    """m > 330: the dense step leaves the one-cluster Gauss-Jordan (the
+    m x m matrix no longer fits 8 CTAs' shared memory) for the grid-wide
+    cooperative kernel -- Denman-Beavers (c5: invsqrt) and Pade (c1: exp)."""
+    p = fp.make(name, **(dict(n=3000) if name == "c5" else dict(g=60)), m=400, k=2, s=0)
+    y, sv = gpu_solve(p, "none")
+    ref = oracle_solve(p, "none", tol=0.0)
+    assert rel(y, ref["f_m"]) <= 1e-10, rel(y, ref["f_m"])
+    sv.close()
