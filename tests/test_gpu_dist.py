@@ -37,12 +37,12 @@ def comm():
     dist.destroy_process_group()
 
 
-def _solve(p, comm, csr=False, mode="blendenpik", fused=True):
+def _solve(p, comm, csr=False, mode="blendenpik", fused=True, square=False):
     import torch
     import paper_2212_12758_b200 as fab
     from paper_2212_12758_b200 import dist as fdist
     op = fdist.local_operator(p, 0, p.n, csr=csr) if comm is not None else fab.Operator.from_problem(p, csr=csr)
-    sv = fab.Solver(op, torch.as_tensor(p.b).cuda(), m_max=p.m, k_max=p.k, s_max=p.s, comm=comm)
+    sv = fab.Solver(op, torch.as_tensor(p.b).cuda(), m_max=p.m, k_max=p.k, s_max=p.s, comm=comm, square=square)
     sv._op = op
     if fused:
         sv.sketch(p.s, p.sketch_seed)
@@ -50,7 +50,7 @@ def _solve(p, comm, csr=False, mode="blendenpik", fused=True):
     if not fused:
         sv.sketch(p.s, p.sketch_seed)
     sv.compress(mode, iters=40)
-    y = sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()
+    y = sv.apply("sign" if square else p.f, 1.0 if square else p.alpha, p.sigma).cpu().numpy()
     out = dict(y=y, H=sv.get("H"), SV=sv.get("SV"), info=sv.info())
     sv.close()
     return out
@@ -69,6 +69,18 @@ def test_one_rank_nccl_path_is_bitwise_single_gpu(comm, name, kw, csr):
     assert np.array_equal(a["SV"], b["SV"])
     assert np.array_equal(a["y"], b["y"])
     assert a["info"]["lsqr_iters"] == b["info"]["lsqr_iters"] == 40
+
+
+@pytest.mark.parametrize("name,kw,csr", [
+    ("e4", dict(n=5000, m=20, s=48), True),       # CSR: x and A x gathered
+    ("e5", dict(g=16, m=20, s=48), False),       # stencil: halo of x and of A x
+])
+def test_one_rank_nccl_squared_operator(comm, name, kw, csr):
+    """FAB_FLAG_SQUARE on the NCCL path (two C1 exchanges per step)."""
+    p = fp.make(name, **kw)
+    a = _solve(p, None, csr=csr, square=True)
+    b = _solve(p, comm, csr=csr, square=True)
+    assert np.array_equal(a["H"], b["H"]) and np.array_equal(a["y"], b["y"])
 
 
 def test_one_rank_nccl_batched_sketch(comm):
