@@ -23,7 +23,7 @@ int launch_tall_gemv(fab_ctx* c, int ncols, const double* p, double scal, int us
                      const double* t_old, double* t_new, cudaStream_t st, int* nparts_out);
 int launch_pass_reduce(fab_ctx* c, int nparts, int ncols, double* out, cudaStream_t st);
 int enqueue_k1(fab_ctx* c, int col, int nw, double* z, bool need_z, cudaStream_t st, int64_t* launches,
-               int* nparts);
+               int* nparts, double* step_sums = nullptr);
 
 __global__ void k_arn_reset(DevState* st, int m) {
   st->breakdown = 0;

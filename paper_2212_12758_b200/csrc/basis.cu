@@ -94,7 +94,7 @@ template <int DIM, int NWM, bool STORE_Z, bool SQ = false, int U = (NWM <= 4 ? k
 __global__ void __launch_bounds__(kThreads, 2)
 k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP sp, int64_t n, int64_t gbase,
                  const double* __restrict__ xin, double* __restrict__ z, double* __restrict__ part,
-                 const DevState* __restrict__ st) {
+                 const DevState* __restrict__ st, StepRed sr) {
   pdl_wait();
   pdl_trigger();
   if (st->breakdown) return;
@@ -172,6 +172,7 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
     for (int t = 0; t < nw - 1; ++t) p[t] = out[t];
     p[nw - 1] = out[NWM - 1];
   }
+  step_red_tail(sr, part, gridDim.x, nw, red);
 }
 
 // scalar fallback (odd gx): one row per thread, grid-stride
@@ -179,7 +180,7 @@ template <int DIM>
 __global__ void __launch_bounds__(kThreads)
 k_stencil_dots(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP sp, int64_t n, int64_t gbase,
                const double* __restrict__ xin, double* __restrict__ z, double* __restrict__ part,
-               const DevState* __restrict__ st) {
+               const DevState* __restrict__ st, StepRed sr) {
   pdl_wait();
   pdl_trigger();
   if (st->breakdown) return;
@@ -216,6 +217,7 @@ k_stencil_dots(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP
     for (int t = 0; t < nw - 1; ++t) p[t] = out[t];
     p[nw - 1] = out[kKMax - 1];
   }
+  step_red_tail(sr, part, gridDim.x, nw, red);
 }
 
 // ---------------------------------------------------------------------------
@@ -1005,7 +1007,7 @@ int enqueue_scalar(fab_ctx* c, int col, int nw, int nparts, int final_step, cuda
 // = V[:, col-1], which is xin unless the operator is squared).  xin: stencil --
 // local rows with their halo slots filled; CSR -- indexed by global column id.
 static int launch_k1(fab_ctx* c, int col, int nw, const double* xin, double* z, bool store, cudaStream_t st,
-                     int64_t* launches, int* nparts) {
+                     int64_t* launches, int* nparts, StepRed sr = StepRed{}) {
   *nparts = c->grid_spmv;
   const double* x = c->V + (int64_t)(col - 1) * c->ld;
   if (c->stencil) {
@@ -1020,13 +1022,13 @@ static int launch_k1(fab_ctx* c, int col, int nw, const double* xin, double* z, 
   do {                                                                                                       \
     if (sq)                                                                                                  \
       FAB_CUDA(launch_pdl(pdl, k_stencil_dots_v<DIM, NWM, true, true>, G, kThreads, 0, st, c->V, c->ld, col, \
-                          nw, sp, c->n, gb, xin, z, c->part_dots, (const DevState*)c->st_d));                \
+                          nw, sp, c->n, gb, xin, z, c->part_dots, (const DevState*)c->st_d, sr));            \
     else if (!store)                                                                                         \
       FAB_CUDA(launch_pdl(pdl, k_stencil_dots_v<DIM, NWM, false>, G, kThreads, 0, st, c->V, c->ld, col, nw,  \
-                          sp, c->n, gb, xin, z, c->part_dots, (const DevState*)c->st_d));                    \
+                          sp, c->n, gb, xin, z, c->part_dots, (const DevState*)c->st_d, sr));                \
     else                                                                                                     \
       FAB_CUDA(launch_pdl(pdl, k_stencil_dots_v<DIM, NWM, true>, G, kThreads, 0, st, c->V, c->ld, col, nw,   \
-                          sp, c->n, gb, xin, z, c->part_dots, (const DevState*)c->st_d));                    \
+                          sp, c->n, gb, xin, z, c->part_dots, (const DevState*)c->st_d, sr));                \
   } while (0)
       if (c->k_max <= 2) {
         if (d3) FAB_K1V(3, 2); else FAB_K1V(2, 2);
@@ -1038,16 +1040,16 @@ static int launch_k1(fab_ctx* c, int col, int nw, const double* xin, double* z, 
 #undef FAB_K1V
     } else if (d3) {
       k_stencil_dots<3><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, xin, z, c->part_dots,
-                                                c->st_d);
+                                                c->st_d, sr);
     } else {
       k_stencil_dots<2><<<G, kThreads, 0, st>>>(c->V, c->ld, col, nw, sp, c->n, gb, xin, z, c->part_dots,
-                                                c->st_d);
+                                                c->st_d, sr);
     }
     FAB_CHECK_LAUNCH();
     ++*launches;
     return FAB_OK;
   }
-  return csr_spmv(c, col, nw, xin, z, st, launches, nparts);
+  return csr_spmv(c, col, nw, xin, z, st, launches, nparts, sr);
 }
 
 // The SpMV input for a product with the local vector x (local rows): C1 on
@@ -1073,7 +1075,7 @@ static int spmv_input(fab_ctx* c, double* x, cudaStream_t st, const double** xin
 // then a K0 pass (the same kernel, no dots) writes t = A w_hat_{col-1} to the
 // padded scratch c->sq first.  *nparts = partial slots written.
 int enqueue_k1(fab_ctx* c, int col, int nw, double* z, bool need_z, cudaStream_t st, int64_t* launches,
-               int* nparts) {
+               int* nparts, double* step_sums = nullptr) {
   double* x = c->V + (int64_t)(col - 1) * c->ld;
   const double* xin = nullptr;
   FAB_TRY(spmv_input(c, x, st, &xin));
@@ -1082,7 +1084,14 @@ int enqueue_k1(fab_ctx* c, int col, int nw, double* z, bool need_z, cudaStream_t
     FAB_TRY(launch_k1(c, col, 0, xin, c->sq, true, st, launches, &np0));   // K0: t = A w_hat_{col-1}
     FAB_TRY(spmv_input(c, c->sq, st, &xin));
   }
-  return launch_k1(c, col, nw, xin, z, need_z || !c->mf, st, launches, nparts);
+  StepRed sr{};
+  if (step_sums) {   // C2 on several GPUs: the last K1 CTA forms this rank's step sums
+    sr.count = &c->st_d->pad[0];
+    sr.sums = step_sums;
+    sr.part_norm = norm_parts(c, col - 1);
+    sr.nparts_norm = c->grid_upd;
+  }
+  return launch_k1(c, col, nw, xin, z, need_z || !c->mf, st, launches, nparts, sr);
 }
 
 // FAB_FLAG_SQUARE: the starting vector of the Krylov space of A^2 is A b
@@ -1151,17 +1160,15 @@ int enqueue_k3(fab_ctx* c, int col, int nw, bool fused, cudaStream_t st, int64_t
 static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st, int64_t* launches) {
   const int nw = col < k ? col : k;
   int nparts = 0;
-  FAB_TRY(enqueue_k1(c, col, nw, c->vec, false, st, launches, &nparts));
   if (c->comm) {
-    // C2: this rank's scalars in k_scalar's order, ONE allreduce of k+1
-    // doubles, then K3 forms the step scalars from the sums in its prologue
-    k_step_reduce<<<1, kThreads, 0, st>>>(nw, nparts, c->grid_upd, c->part_dots, norm_parts(c, col - 1), c->red,
-                                         c->st_d);
-    FAB_CHECK_LAUNCH();
-    ++*launches;
+    // C2: the last K1 CTA reduces this rank's scalars in k_scalar's order,
+    // ONE allreduce of k+1 doubles, then K3 forms the step scalars from the
+    // sums in its prologue: K1, allreduce, K3
+    FAB_TRY(enqueue_k1(c, col, nw, c->vec, false, st, launches, &nparts, c->red));
     FAB_TRY(comm_allreduce(c, c->red, (size_t)nw + 1, false, st));
     return enqueue_k3(c, col, nw, fused, st, launches, nparts, c->red);
   }
+  FAB_TRY(enqueue_k1(c, col, nw, c->vec, false, st, launches, &nparts));
   return enqueue_k3(c, col, nw, fused, st, launches, nparts);   // K2 fused into K3
 }
 

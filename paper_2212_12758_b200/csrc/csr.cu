@@ -57,6 +57,7 @@ struct CsrArgs {
   double* z[kBatchMax];
   double* part[kBatchMax];       // per-CTA dot partials (DOTS)
   const DevState* st[kBatchMax];
+  StepRed sr;                    // P == 1 on several GPUs: fused step reduction (last DOTS pass)
 };
 
 // Cache policy: the entries, row pointers and z stream through once per pass
@@ -278,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, P == 1 ? 6 : 3) k_csr_stream(CsrArgs
         pp[a.nw - 1] = out[NWM - 1];
       }
     }
+    if (P == 1) step_red_tail(a.sr, a.part[0], gridDim.x, a.nw, red);
   }
 }
 
@@ -606,7 +608,7 @@ static cudaError_t launch_pass(const CsrArgs& a, int grid, int p, bool acc, bool
 // block.  The grid and the row blocks are cs[0]'s, so per vector the
 // partials are those of a single-RHS launch.
 int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* const* xin, double* const* z,
-                   cudaStream_t st, int64_t* launches, int* nparts, const double* xi) {
+                   cudaStream_t st, int64_t* launches, int* nparts, const double* xi, StepRed sr) {
   fab_ctx* c = cs[0];
   CsrPlan* plan = c->csr;
   if (!plan || plan->pass.empty() || p < 1 || p > kBatchMax) return FAB_EORDER;
@@ -635,6 +637,7 @@ int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* con
       a.st[i] = cs[i]->st_d;
     }
     const bool acc = j > 0, dots = (j == np - 1) && nw > 0;
+    a.sr = (dots && p == 1) ? sr : StepRed{};
     const bool pdl = c->pdl && !c->comm;
     if (c->k_max <= 2) FAB_CUDA(launch_pass<2>(a, c->grid_spmv, p, acc, dots, pdl, st));
     else if (c->k_max <= 4) FAB_CUDA(launch_pass<4>(a, c->grid_spmv, p, acc, dots, pdl, st));
@@ -646,8 +649,8 @@ int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* con
 }
 
 int csr_spmv(fab_ctx* c, int col, int nw, const double* xin, double* z, cudaStream_t st, int64_t* launches,
-             int* nparts) {
-  return csr_spmv_multi(&c, 1, col, nw, &xin, &z, st, launches, nparts, nullptr);
+             int* nparts, StepRed sr) {
+  return csr_spmv_multi(&c, 1, col, nw, &xin, &z, st, launches, nparts, nullptr, sr);
 }
 
 }  // namespace fab

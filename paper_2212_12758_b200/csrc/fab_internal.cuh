@@ -43,6 +43,17 @@ struct DevState {
   double scratch[8];
 };
 
+// Multi-GPU step reduction folded into K1 (C2): the last K1 CTA to finish
+// (arrival counter) reduces every CTA's dot partials and the previous
+// column's norm partials in k_scalar's fixed order into sums[0..nw] for the
+// allreduce.  sums == nullptr: off (one GPU: K3 reduces in its prologue).
+struct StepRed {
+  int* count;               // arrival counter (DevState::pad[0]), reset by the last CTA
+  double* sums;
+  const double* part_norm;  // norm partials of w_hat_{c-1}
+  int nparts_norm;
+};
+
 struct Comm;   // comm.cu: NCCL communicator of the row-partitioned path
 struct CsrPlan;   // csr.cu: row blocks / column-blocked copy of a CSR operator
 
@@ -205,6 +216,38 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* smem, double 
   __syncthreads();
 }
 
+// det_sum reading through L2 (other CTAs' partials of the same launch)
+__device__ __forceinline__ double det_sum_cg(const double* p, int count, int stride, int off, double* red) {
+  double a = 0.0;
+  for (int b = threadIdx.x; b < count; b += blockDim.x) a += __ldcg(p + (int64_t)b * stride + off);
+  double v1[1] = {a}, o1[1];
+  block_sum<1>(v1, red, o1);
+  return o1[0];
+}
+
+// called by EVERY thread of each K1 CTA after its partial (part + cta row) is
+// stored by thread 0: the last CTA forms the sums (same order as k_step_reduce)
+__device__ __forceinline__ void step_red_tail(const StepRed& sr, const double* part_dots, int nparts_dots, int nw,
+                                              double* red) {
+  if (!sr.sums) return;
+  __shared__ int last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(sr.count, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const double nu = det_sum_cg(sr.part_norm, sr.nparts_norm, 1, 0, red);
+  if (threadIdx.x == 0) sr.sums[nw] = nu;
+  for (int t = 0; t < nw; ++t) {
+    const double dv = det_sum_cg(part_dots, nparts_dots, kKMax + 1, t, red);
+    if (threadIdx.x == 0) sr.sums[t] = dv;
+  }
+  if (threadIdx.x == 0) *sr.count = 0;
+}
+
 // Raise a kernel's dynamic shared-memory cap to min(want, opt-in max - its
 // static shared memory).
 inline cudaError_t set_max_dyn_smem(const void* fn, int want) {
@@ -285,10 +328,10 @@ int run_basis_whiten(fab_ctx* c, int m, int k, double cond_max, int* whitened_at
 int csr_grid(fab_ctx* c, int* grid);
 int csr_setup(fab_ctx* c);                   // uniform values, row blocks, column blocking
 int csr_spmv(fab_ctx* c, int col, int nw, const double* xin, double* z, cudaStream_t st, int64_t* launches,
-             int* nparts);
+             int* nparts, StepRed sr = StepRed{});
 int csr_passes(const fab_ctx* c);
 int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* const* xin, double* const* z,
-                   cudaStream_t st, int64_t* launches, int* nparts, const double* xi);
+                   cudaStream_t st, int64_t* launches, int* nparts, const double* xi, StepRed sr = StepRed{});
 int csr_interleave(fab_ctx* c, int p, const double* const* x, double* xi, cudaStream_t st, int64_t* launches);
 bool csr_interleave_fits(const fab_ctx* c, int p);
 constexpr int kBatchMaxCtx = 4;              // fab_basis_batch: contexts per call

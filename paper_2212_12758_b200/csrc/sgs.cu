@@ -118,7 +118,7 @@ __global__ void k_sgs_reset(DevState* st, int m) {
 int launch_tall_gemv(fab_ctx* c, int ncols, const double* p, double scal, int use_state_scal,
                      const double* t_old, double* t_new, cudaStream_t st, int* nparts_out);
 int enqueue_k1(fab_ctx* c, int col, int nw, double* z, bool need_z, cudaStream_t st, int64_t* launches,
-               int* nparts);
+               int* nparts, double* step_sums = nullptr);
 
 // p = Theta w_hat_col from its sketch partials (already in part_sk), C3 on several GPUs
 int enqueue_col_sketch_reduce(fab_ctx* c, int col, double* p, cudaStream_t st, int64_t* launches) {

@@ -24,7 +24,7 @@ namespace fab {
 
 int enqueue_basis_prologue(fab_ctx* c, int m, bool fused, cudaStream_t st, int64_t* launches);
 int enqueue_k1(fab_ctx* c, int col, int nw, double* z, bool need_z, cudaStream_t st, int64_t* launches,
-               int* nparts);
+               int* nparts, double* step_sums = nullptr);
 int enqueue_scalar(fab_ctx* c, int col, int nw, int nparts, int final_step, cudaStream_t st, int64_t* launches);
 int enqueue_k3(fab_ctx* c, int col, int nw, bool fused, cudaStream_t st, int64_t* launches, int nparts_k2,
                const double* sums);
