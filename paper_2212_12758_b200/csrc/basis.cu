@@ -800,6 +800,110 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
   }
 }
 
+// K5 (sketch only): the tiles, the tile -> CTA order, the FWHT and the
+// gather of k_stream_tiles<false, true> -- the partials are bitwise the same
+// -- but each thread loads its 16 values of layout A straight from global
+// memory into registers, one (column, tile) item ahead, instead of through
+// the bulk-copy ring.  K5 moves one vector per FWHT, so shared memory, not
+// HBM, bounds it: the ring's copy-in and read-back were two of the tile's
+// seven 32-KB shared-memory passes.  No producer warp; grid = grid_upd.
+__device__ __forceinline__ double ld_first(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+__global__ void __launch_bounds__(kThreads, kPipeCtasPerSm) k_sketch_direct(PipeArgs a) {
+  if (a.st->breakdown) return;
+  // two FWHT buffers, alternating per tile: the next tile's first transpose
+  // cannot overwrite slots this tile's gather still reads, so the barrier
+  // after the gather goes away
+  extern __shared__ __align__(128) double fwb[];
+  const int tid = threadIdx.x;
+  const int64_t n = a.n, rb = a.row_begin;
+  const int64_t t_first = rb >> kSkLogT;
+  const int64_t t_last = (rb + n - 1) >> kSkLogT;
+  const int64_t mine = t_first + blockIdx.x <= t_last ? (t_last - t_first - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t items = mine * (a.col1 - a.col0);
+  if (items == 0) {   // no tile here (grid_upd <= tiles, so not at present): zero partials
+    for (int col = a.col0; col < a.col1; ++col)
+      for (int p = tid; p < a.s; p += kThreads) a.part_sk[((int64_t)col * gridDim.x + blockIdx.x) * a.s + p] = 0.0;
+    return;
+  }
+  SkRows R;
+  load_sk_rows(a.rows, a.s, tid, R);
+  const uint64_t pol = policy_evict_first();
+  const int sh = 31 - (tid & 31);   // this thread's sign bit, moved to bit 31
+  double x[kSkPer];
+  uint32_t w[kSkPer];
+  // the (column, tile) items of this CTA in the pipeline's order: columns
+  // outer, this CTA's tiles inner; counters instead of divisions
+  auto issue = [&](int col, int64_t tile) {
+    const double* src = a.V + (int64_t)col * a.ld;
+    const int64_t g0 = tile << kSkLogT, rc0 = g0 - rb;
+    const uint32_t* sg = a.signs + (g0 >> 5) + (tid >> 5);
+    if (rc0 >= 0 && rc0 + kSkT <= n) {
+      const double* p = src + rc0 + tid;
+#pragma unroll
+      for (int q = 0; q < kSkPer; ++q) {
+        x[q] = ld_first(p + kThreads * q, pol);
+        w[q] = __ldg(sg + 8 * q);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < kSkPer; ++q) {
+        const int64_t r = rc0 + tid + kThreads * q;
+        const bool in = r >= 0 && r < n;
+        x[q] = in ? ld_first(src + r, pol) : 0.0;
+        w[q] = in ? __ldg(sg + 8 * q) : 0u;
+      }
+    }
+  };
+  int col = a.col0, ncol = a.col0;
+  int64_t ti = 0, nti = 0;
+  int buf = 0;
+  issue(ncol, t_first + blockIdx.x);
+  double acc[kSkAcc] = {0.0, 0.0, 0.0};
+  while (col < a.col1) {
+    const int64_t tile = t_first + blockIdx.x + ti * gridDim.x;
+    const int64_t rc0 = (tile << kSkLogT) - rb;
+    double v[kSkPer];
+    // D_tt = -1: flip the sign bit (rows outside [0, n) stay +0.0, as in the ring path)
+    if (rc0 >= 0 && rc0 + kSkT <= n) {
+#pragma unroll
+      for (int q = 0; q < kSkPer; ++q)
+        v[q] = __hiloint2double(__double2hiint(x[q]) ^ (int)((w[q] << sh) & 0x80000000u), __double2loint(x[q]));
+    } else {
+#pragma unroll
+      for (int q = 0; q < kSkPer; ++q) {
+        const int64_t r = rc0 + tid + kThreads * q;
+        v[q] = (r >= 0 && r < n)
+                   ? __hiloint2double(__double2hiint(x[q]) ^ (int)((w[q] << sh) & 0x80000000u), __double2loint(x[q]))
+                   : 0.0;
+      }
+    }
+    if (++nti == mine) {
+      nti = 0;
+      ++ncol;
+    }
+    if (ncol < a.col1) issue(ncol, t_first + blockIdx.x + nti * gridDim.x);   // overlaps this tile's FWHT
+    double* fw = fwb + (buf ? kSkSmem : 0);
+    buf ^= 1;
+    tile_fwht(v, fw, tid);
+    tile_gather(fw, R, a.s, tile, tid, acc);
+    if (++ti == mine) {
+#pragma unroll
+      for (int q = 0; q < kSkAcc; ++q) {
+        const int p = tid + kThreads * q;
+        if (p < a.s) a.part_sk[((int64_t)col * gridDim.x + blockIdx.x) * a.s + p] = acc[q];
+        acc[q] = 0.0;
+      }
+      ti = 0;
+      ++col;
+    }
+  }
+}
+
 static int pipe_stages(int stage_d, bool sketch, size_t* smem) {
   const size_t stage = (size_t)stage_d * sizeof(double);
   const size_t fixed = (sketch ? kSkSmem * sizeof(double) : 0) + 1024;
@@ -1172,7 +1276,7 @@ static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st,
   return enqueue_k3(c, col, nw, fused, st, launches, nparts);   // K2 fused into K3
 }
 
-// K5 / column 0: sketch partials of columns [c0, c1) (no writes)
+// K5 / column 0: sketch partials of columns [c0, c1) (no writes) -- k_sketch_direct
 int launch_sketch_cols(fab_ctx* c, int c0, int c1, cudaStream_t st) {
   PipeArgs a{};
   a.V = c->V;
@@ -1187,7 +1291,13 @@ int launch_sketch_cols(fab_ctx* c, int c0, int c1, cudaStream_t st) {
   a.s = c->s;
   a.part_sk = c->part_sk;
   a.st = c->st_d;
-  return launch_stream<false, true, 0>(c, a, st);
+  const char* re = getenv("FAB_SKETCH_RING");   // the bulk-copy ring version (A/B)
+  if (re && re[0] == '1') return launch_stream<false, true, 0>(c, a, st);
+  const int smem = 2 * kSkSmem * (int)sizeof(double);
+  FAB_CUDA(ensure_dyn_smem((const void*)k_sketch_direct, smem));
+  k_sketch_direct<<<c->grid_upd, kThreads, smem, st>>>(a);
+  FAB_CHECK_LAUNCH();
+  return FAB_OK;
 }
 
 // Before step 1 of Algorithm 2: reset the device state, zero underline-H
