@@ -295,6 +295,150 @@ static LsqrPassFn pick_pass(int m, int* jpw) {
   return nullptr;
 }
 
+// Narrow tall GEMV (ncols <= 64: Algorithm 1's first steps, Arnoldi's
+// passes): the same t_new = W p - scal t_old, g = W^T t_new, ||t_new||^2 as
+// k_lsqr_pipe, but row-parallel -- SPLIT lanes of one warp own one row of an
+// R-row chunk (each a contiguous block of CAP / SPLIT columns) and combine
+// their parts of t with lane shuffles, so a chunk needs no cross-warp
+// reduction and no CTA barrier.  k_lsqr_pipe's 32-row chunks cost ~900
+// cycles each in barriers and mbarrier round trips whatever the width (1.7
+// ms per pass at n = 2^24 for 2 columns).  One TMA box of R rows x ncols
+// columns (+ the t_old rows) per ring stage; 8 consumer warps; R = 256 / SPLIT
+// keeps a stage <= 67 KB and the ring >= 3 deep.
+template <int CAP>
+struct RowsGeo {
+  static constexpr int SPLIT = CAP <= 32 ? 1 : 2;                      // lanes per row
+  static constexpr int CPT = CAP / SPLIT;                              // columns per lane
+  static constexpr int RPW = 32 / SPLIT;                               // rows per warp
+  static constexpr int NW = 8;                                         // consumer warps
+  static constexpr int R = NW * RPW;                                   // rows per chunk
+};
+
+template <int CAP>
+__global__ void __launch_bounds__(RowsGeo<CAP>::NW * 32 + 32, 1)
+k_gemv_rows(const __grid_constant__ CUtensorMap tmW, int m, int64_t n, const double* __restrict__ p,
+            double scal_arg, const double* t_old, double* t_new, double* __restrict__ part_g,
+            double* __restrict__ part_tn, const DevState* __restrict__ st, int use_state_scal, int nstage) {
+  using G = RowsGeo<CAP>;
+  constexpr int NW = G::NW, R = G::R, CPT = G::CPT, RPW = G::RPW;
+  if (st->lsqr_done) return;
+  extern __shared__ __align__(128) double ring[];
+  __shared__ double sp[CAP];
+  __shared__ double red[NW][CAP + 1];
+  const int stage_d = (m + 1) * R;   // W box (column-major, R rows per column) + t_old rows
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)nstage * stage_d);
+  uint64_t* empty = full + nstage;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int j = tid; j < m; j += blockDim.x) sp[j] = p[j];
+  if (tid == 0) {
+    for (int i = 0; i < nstage; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, NW);
+    }
+    fence_barrier_init();
+  }
+  const double scal = use_state_scal ? st->scal : scal_arg;
+  __syncthreads();
+  const int64_t nch = (n + R - 1) / R;
+  if (warp == NW) {
+    // ---------------- producer warp ----------------
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      RingPos rp;
+      for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+        const int64_t r0 = ch * R;
+        int64_t rows = n - r0 < R ? n - r0 : R;
+        rows = (rows + 1) & ~(int64_t)1;   // 16-B multiple (inside the padded vector)
+        const uint32_t tbytes = (uint32_t)(rows * 8);
+        mbar_wait(empty + rp.stage, rp.phase ^ 1u);
+        double* sb = ring + (size_t)rp.stage * stage_d;
+        mbar_arrive_expect_tx(full + rp.stage, (uint32_t)(m * R * 8) + tbytes);
+        tma_load_2d(sb, &tmW, (int)r0, 0, full + rp.stage, pol);
+        bulk_g2s(sb + (size_t)m * R, t_old + r0, tbytes, full + rp.stage, pol);
+        rp.advance(nstage);
+      }
+    }
+    return;
+  }
+  // ---------------- consumer warps: SPLIT lanes per row ----------------
+  const int q = lane / RPW;               // column block of this lane
+  const int i = warp * RPW + lane % RPW;  // row within the chunk
+  const int j0 = q * CPT;
+  double acc[CPT];
+#pragma unroll
+  for (int jj = 0; jj < CPT; ++jj) acc[jj] = 0.0;
+  double tn = 0.0;
+  RingPos rp;
+  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+    const int64_t r = ch * R + i;
+    const bool valid = r < n;
+    mbar_wait(full + rp.stage, rp.phase);
+    const double* sb = ring + (size_t)rp.stage * stage_d + i;
+    double t = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < CPT; ++jj)
+      if (j0 + jj < m) t = fma(sb[(j0 + jj) * R], sp[j0 + jj], t);
+    // blocks combined pairwise (lane q and q^1, then the pairs): a + b == b + a,
+    // so every lane of the row holds the same bits
+#pragma unroll
+    for (int o = RPW; o < 32; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    t = valid ? fma(-scal, sb[m * R], t) : 0.0;
+    if (valid && q == 0) {
+      t_new[r] = t;
+      tn = fma(t, t, tn);
+    }
+#pragma unroll
+    for (int jj = 0; jj < CPT; ++jj)
+      if (j0 + jj < m) acc[jj] = fma(sb[(j0 + jj) * R], t, acc[jj]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + rp.stage);
+    rp.advance(nstage);
+  }
+  // per-CTA partials: trees over the rows of a warp, then the warps in order
+#pragma unroll
+  for (int jj = 0; jj < CPT; ++jj) {
+    double a = acc[jj];
+#pragma unroll
+    for (int o = 1; o < RPW; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane % RPW == 0 && j0 + jj < m) red[warp][j0 + jj] = a;
+  }
+  {
+    const double a = warp_sum(tn);
+    if (lane == 0) red[warp][CAP] = a;
+  }
+  consumer_sync(1, NW * 32);
+  for (int j = tid; j <= m; j += NW * 32) {
+    const int jj = j < m ? j : CAP;
+    double s = 0.0;
+    for (int w = 0; w < NW; ++w) s += red[w][jj];
+    if (j < m) part_g[(int64_t)blockIdx.x * m + j] = s;
+    else part_tn[blockIdx.x] = s;
+  }
+}
+
+template <int CAP>
+static int launch_gemv_rows(fab_ctx* c, int ncols, const double* p, double scal, int use_state_scal,
+                            const double* t_old, double* t_new, cudaStream_t st, int* nparts_out) {
+  constexpr int R = RowsGeo<CAP>::R;
+  const size_t stage = (size_t)(ncols + 1) * R * sizeof(double);
+  const int limit = 200 * 1024;
+  int ns = (int)(limit / (stage + 16));
+  if (ns > kLsMaxStages) ns = kLsMaxStages;
+  if (ns < 2) return FAB_EINVAL;
+  const size_t smem = (size_t)ns * stage + 2 * ns * sizeof(uint64_t);
+  FAB_CUDA(ensure_dyn_smem((const void*)k_gemv_rows<CAP>, limit + 1024));
+  CUtensorMap tm;
+  FAB_TRY(make_tmap_cols(c->V, c->n, ncols, c->ld, R, ncols, &tm));
+  const int64_t nch = (c->n + R - 1) / R;
+  const int G = (int)(nch < c->num_sms ? nch : c->num_sms);
+  k_gemv_rows<CAP><<<G, RowsGeo<CAP>::NW * 32 + 32, smem, st>>>(tm, ncols, c->n, p, scal, t_old, t_new,
+                                                                 c->part_g, c->part_tn, c->st_d, use_state_scal,
+                                                                 ns);
+  FAB_CHECK_LAUNCH();
+  if (nparts_out) *nparts_out = G;
+  return FAB_OK;
+}
+
 // One streaming pass over the first ncols stored columns W of V (K6):
 // t_new = W p - scal t_old (scal from st->scal if use_state_scal), with the
 // g = W^T t_new, ||t_new||^2 partials into part_g / part_tn.  Used by LSQR
@@ -303,6 +447,18 @@ static LsqrPassFn pick_pass(int m, int* jpw) {
 // (graph-capture safe: the map is a by-value kernel parameter).
 int launch_tall_gemv(fab_ctx* c, int ncols, const double* p, double scal, int use_state_scal,
                      const double* t_old, double* t_new, cudaStream_t st, int* nparts_out) {
+  static const bool rows_off = [] {
+    const char* e = getenv("FAB_GEMV_ROWS");
+    return e && e[0] == '0';
+  }();
+  // (a CAP = 128 variant, 4 lanes per row, measured slower than k_lsqr_pipe
+  // above 64 columns: 2552 vs 2232 us at 100 columns, n = 2^24)
+  if (!rows_off && ncols >= 1 && ncols <= 64) {
+    if (ncols <= 8) return launch_gemv_rows<8>(c, ncols, p, scal, use_state_scal, t_old, t_new, st, nparts_out);
+    if (ncols <= 16) return launch_gemv_rows<16>(c, ncols, p, scal, use_state_scal, t_old, t_new, st, nparts_out);
+    if (ncols <= 32) return launch_gemv_rows<32>(c, ncols, p, scal, use_state_scal, t_old, t_new, st, nparts_out);
+    return launch_gemv_rows<64>(c, ncols, p, scal, use_state_scal, t_old, t_new, st, nparts_out);
+  }
   LsqrPipeFn pipe = pick_pipe(ncols);
   size_t smem = 0;
   const int ns = lsqr_pipe_stages(ncols, &smem);
