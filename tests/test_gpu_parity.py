@@ -336,6 +336,7 @@ def test_alg3_breakdown_diagonal_exact():
     ("c1", dict(m=30), False),
     ("c3", dict(g=20, m=40, s=90), False),
     ("c5", dict(n=4000, m=12, s=30), True),
+    ("c5", dict(n=4999, m=70, s=150), True),     # odd n; GEMV widths 1..69 (K6n <= 64, then K6)
 ])
 def test_arnoldi_fom_parity(name, kw, csr):
     import torch
