@@ -28,7 +28,8 @@ __global__ void k_sketch_col_raw(const double* __restrict__ part, int nparts, in
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < s; q += gridDim.x * blockDim.x) {
     const double* src = part + (int64_t)col * nparts * s + q;
     double a = 0.0;
-    for (int b = 0; b < nparts; ++b) a += src[(int64_t)b * s];
+#pragma unroll 16
+    for (int b = 0; b < nparts; ++b) a += src[(int64_t)b * s];   // loads batched, adds in order
     p[q] = a / sqrt((double)s);
   }
 }
@@ -75,6 +76,7 @@ __global__ void k_sgs_step(int c, int s, const double* __restrict__ praw, double
   for (int j = warp; j < c; j += kWarps) {
     const double* sj = SV + (int64_t)j * s;
     double a = 0.0;
+#pragma unroll 8
     for (int q = lane; q < s; q += 32) a = fma(sj[q], praw[q] * bsc, a);
     a = warp_sum(a);
     if (lane == 0) rr[j] = a;
@@ -84,6 +86,7 @@ __global__ void k_sgs_step(int c, int s, const double* __restrict__ praw, double
   double a = 0.0;
   for (int q = threadIdx.x; q < s; q += blockDim.x) {
     double v = praw[q] * bsc;
+#pragma unroll 16
     for (int j = 0; j < c; ++j) v = fma(-SV[(int64_t)j * s + q], rr[j], v);
     sbuf[q] = v;
     a = fma(v, v, a);
