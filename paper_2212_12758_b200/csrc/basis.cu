@@ -395,7 +395,6 @@ __device__ __forceinline__ void tile_gather(const double* sm, const SkRows& R, i
 //          and (SKETCH) the pruned-FWHT partials of w_hat_c.
 //   !UPDATE (K5 / column 0): vector 0 = column col; sketch partials only.
 constexpr int kChunk = 512;
-constexpr int kChunksPerTile = kSkT / kChunk;   // 8
 constexpr int kPipeThreads = kThreads + 32;
 constexpr int kMaxStages = 16;
 constexpr int kSignPad = 16;   // doubles reserved per stage for the chunk's sign bits
@@ -449,10 +448,12 @@ struct PipeArgs {
 
 // Ring-stage slots (doubles) of one 512-row chunk [r0, r0+512):
 //   SDIM == 0, UPDATE : z | window columns j0 .. c-1                (512 each)
-//   SDIM  > 0, UPDATE : w_hat_{c-1} rows [r0-16, r0+528) (the x neighbours,
-//                       one 128-B aligned copy) | window columns j0 .. c-2;
-//                       the y / z neighbours (+-gx, +-gx*gy rows: L2 hits)
-//                       are loaded by the consumers one chunk ahead
+//   SDIM  > 0, UPDATE : w_hat_{c-1} rows [r0-apron, r0+512+apron), apron >=
+//                       gx+1 (the x and y neighbours, one 128-B aligned copy) |
+//                       window columns j0 .. c-2 | (SDIM == 3) the rows
+//                       [r0-+plane, r0-+plane+512) of w_hat_{c-1} (the z
+//                       neighbours; L2 hits, the neighbouring tiles' CTAs
+//                       stream them at about the same time)
 //   !UPDATE           : column col
 //   + (SKETCH) the chunk's 512 sign bits (64 B, padded to 128 B)
 struct SlotGeom {
@@ -470,8 +471,8 @@ __host__ __device__ __forceinline__ SlotGeom slot_geom(int nw, int apron) {
     g.nslot = 1 + nw;
     g.stage_d = (1 + nw) * kChunk;
   } else {
-    g.nslot = 1 + (nw - 1);
-    g.stage_d = (kChunk + 2 * apron) + (nw - 1) * kChunk;
+    g.nslot = 1 + (nw - 1) + (SDIM == 3 ? 2 : 0);
+    g.stage_d = (kChunk + 2 * apron) + (nw - 1) * kChunk + (SDIM == 3 ? 2 * kChunk : 0);
   }
   g.stage_d += SKETCH ? ChunkGeo<UPDATE>::SIGND : 0;
   return g;
@@ -499,9 +500,16 @@ __device__ __forceinline__ void slot_copy(const PipeArgs& a, int v, int col, int
       off = 0;
       clo = -hale;
       chi = a.n + a.hal;
-    } else {                                    // window column j0 + v - 1
+    } else if (v < a.nw) {                      // window column j0 + v - 1
       *src = a.V + (int64_t)(j0 + v - 1) * a.ld;
       off = xw + (v - 1) * kChunk;
+    } else {                                    // SDIM == 3: the -plane / +plane rows
+      const int64_t pl = (int64_t)a.sp.gx * a.sp.gy;
+      *src = x;
+      base = r0 + (v == a.nw ? -pl : pl);
+      off = xw + (a.nw - 1 + (v - a.nw)) * kChunk;
+      clo = -hale;
+      chi = a.n + a.hal;
     }
   }
   int64_t l = base > clo ? base : clo;
@@ -683,28 +691,6 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
   if (SKETCH) load_sk_rows(a.rows, a.s, tid, R);
   double nrm = 0.0;
   RingPos rp;
-  // SDIM > 0: y / z neighbours of the rows (tid, tid+256) of the next chunk,
-  // loaded from global (L2) one chunk ahead: nbr[h][0..3] = x[r-gx], x[r+gx],
-  // x[r-plane], x[r+plane] (0 outside the grid)
-  double nbr[2][4];
-  const double* xcol = (UPDATE && SDIM > 0) ? a.V + (int64_t)(a.col0 - 1) * a.ld : nullptr;
-  auto load_nbr = [&](int64_t g0c) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t g = g0c + tid + kThreads * h, r = g - rb;
-      nbr[h][0] = nbr[h][1] = nbr[h][2] = nbr[h][3] = 0.0;
-      if (r >= 0 && r < n) {
-        uint32_t ix, iy, iz;
-        grid_coords(a.sp, (uint32_t)g, ix, iy, iz);
-        const int64_t gx = a.sp.gx, pl = (int64_t)a.sp.gx * a.sp.gy;
-        if (iy > 0) nbr[h][0] = __ldg(xcol + r - gx);
-        if (iy + 1 < (uint32_t)a.sp.gy) nbr[h][1] = __ldg(xcol + r + gx);
-        if (SDIM == 3 && iz > 0) nbr[h][2] = __ldg(xcol + r - pl);
-        if (SDIM == 3 && iz + 1 < (uint32_t)a.sp.gz) nbr[h][3] = __ldg(xcol + r + pl);
-      }
-    }
-  };
-  if (UPDATE && SDIM > 0 && t_first + blockIdx.x <= t_last) load_nbr((t_first + blockIdx.x) << kSkLogT);
   for (int col = a.col0; col < a.col1; ++col) {
     double acc[kSkAcc] = {0.0, 0.0, 0.0};
     for (int64_t tile = t_first + blockIdx.x; tile <= t_last; tile += gridDim.x) {
@@ -712,17 +698,6 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
       double v[kSkPer];
 #pragma unroll
       for (int ch = 0; ch < CG::NCH; ++ch) {
-        double cur[2][4];
-        if (UPDATE && SDIM > 0) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) cur[h][q] = nbr[h][q];
-          // issue the next chunk's neighbour loads before waiting on this one
-          const int64_t gn = ch + 1 < kChunksPerTile ? g0 + (ch + 1) * kChunk
-                                                     : ((tile + gridDim.x) << kSkLogT);
-          if (ch + 1 < kChunksPerTile || tile + gridDim.x <= t_last) load_nbr(gn);
-        }
         mbar_wait(full + rp.stage, rp.phase);
         const double* sb = ring + (size_t)rp.stage * stage_d;
         const uint32_t* sgn = reinterpret_cast<const uint32_t*>(sb + sign_off);
@@ -742,14 +717,18 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
               for (int t = 0; t < NWM; ++t)
                 if (t < a.nw) val = fma(cw[t], sb[(1 + t) * kChunk + i], val);
             } else if (UPDATE) {
-              // z_r = (A w_hat_{c-1})_r recomputed exactly as K1 did (stencil_row)
+              // z_r = (A w_hat_{c-1})_r recomputed exactly as K1 did (stencil_row);
+              // every neighbour is in this stage (out-of-grid ones are not used)
               uint32_t ix, iy, iz;
               grid_coords(a.sp, (uint32_t)g, ix, iy, iz);
               const int xw = kChunk + 2 * a.apron;
               const double* xs = sb + a.apron;                    // row i at xs[i]
               const double xc = xs[i];
-              const double zr = stencil_row<SDIM>(a.sp, ix, iy, iz, xc, xs[i - 1], xs[i + 1], cur[h][0],
-                                                  cur[h][1], cur[h][2], cur[h][3]);
+              const int gx = a.sp.gx;
+              const double* zs = sb + xw + (a.nw - 1) * kChunk;   // -plane rows, then +plane rows
+              const double zr = stencil_row<SDIM>(a.sp, ix, iy, iz, xc, xs[i - 1], xs[i + 1], xs[i - gx],
+                                                  xs[i + gx], SDIM == 3 ? zs[i] : 0.0,
+                                                  SDIM == 3 ? zs[kChunk + i] : 0.0);
               val = cz * zr;
 #pragma unroll
               for (int t = 0; t < NWM - 1; ++t)
@@ -1004,6 +983,22 @@ static StencilP stencil_params(const fab_ctx* c) {
   return p;
 }
 
+// matrix-free K3: the x-slot apron covers the +-1 and +-gx neighbours
+static int mf_apron(const fab_ctx* c) { return (int)round_up((int64_t)c->op.dims[0] + 1, 16); }
+
+// the staged matrix-free K3 fits: apron <= one chunk, 16-row aligned planes,
+// a ring of >= 2 stages at the largest window
+static bool mf_fits(const fab_ctx* c) {
+  const int apron = mf_apron(c);
+  if (apron > kChunk) return false;
+  const bool d3 = c->op.dims[2] > 1;
+  if (d3 && (((int64_t)c->op.dims[0] * c->op.dims[1]) % 16) != 0) return false;
+  const int nw = c->k_max;
+  const int stage_d = (kChunk + 2 * apron) + (nw - 1) * kChunk + (d3 ? 2 * kChunk : 0) + kSignPad;
+  size_t smem = 0;
+  return pipe_stages(stage_d, true, &smem) >= 2;
+}
+
 bool stencil_vec_path(const fab_ctx* c) {
   // row pairs never straddle a grid line, and double2 accesses stay aligned
   return c->stencil && (c->op.dims[0] % 2 == 0) && (c->row_begin % 2 == 0);
@@ -1019,11 +1014,12 @@ int basis_setup_grids(fab_ctx* c) {
   FAB_CUDA(set_max_dyn_smem((const void*)k_stream_tiles<true, true, 3>, kSmemLimit));
   FAB_CUDA(set_max_dyn_smem((const void*)k_stream_tiles<true, false, 3>, kSmemLimit));
   // matrix-free stencil (FAB_MATRIX_FREE=1): z = A w_hat_{c-1} is recomputed
-  // in K3 from w_hat_{c-1} and its neighbour chunks instead of round-tripping
+  // in K3 from w_hat_{c-1} and its neighbour rows instead of round-tripping
   // through HBM (72 instead of 88 B/row at k = 4).  Correct and tested, but
-  // not the default: with the tile order of the persistent grid the +-plane
-  // neighbour chunks are first-touch misses that stall the ring (K3 347 us vs
-  // 120 us, profiles/r01_v2); needs a z-marching tile order.
+  // not the default: every neighbour is staged in the ring (x with a gx+1
+  // apron, the -+plane rows) and hits L2 -- K3's DRAM traffic is the
+  // algorithmic 671 MB at c3 -- but a 29-KB stage leaves a 2-deep ring per
+  // CTA, so K3 is latency-bound at 3.4 TB/s (196 vs 128 us; K1 93 vs 106 us).
   // PDL between K1 and K3 is opt-in (FAB_PDL=1): measured at c3 it slows the
   // basis from 50.8 to 60.7 ms -- with both persistent grids sized to fill
   // the machine, the early-launched CTAs of the next kernel land unevenly as
@@ -1031,7 +1027,7 @@ int basis_setup_grids(fab_ctx* c) {
   const char* pde = getenv("FAB_PDL");
   c->pdl = (pde && pde[0] == '1');
   const char* mfe = getenv("FAB_MATRIX_FREE");
-  c->mf = stencil_vec_path(c) && (mfe && mfe[0] == '1') && !(c->flags & FAB_FLAG_SQUARE);
+  c->mf = stencil_vec_path(c) && (mfe && mfe[0] == '1') && !(c->flags & FAB_FLAG_SQUARE) && mf_fits(c);
   // K3/K5 pipeline: persistent, kPipeCtasPerSm CTAs per SM (each with half the
   // ring): 16 consumer warps per SM instead of 8 hide the consumers' FWHT /
   // update latency (c3 basis 55.7 -> 50.2 ms although the registers are capped
@@ -1248,7 +1244,7 @@ int enqueue_k3(fab_ctx* c, int col, int nw, bool fused, cudaStream_t st, int64_t
   if (c->mf) {
     a.sp = stencil_params(c);
     a.hal = c->hal;
-    a.apron = 16;
+    a.apron = mf_apron(c);
     if (c->op.dims[2] > 1)
       rc = fused ? launch_stream<true, true, 3>(c, a, st) : launch_stream<true, false, 3>(c, a, st);
     else

@@ -589,3 +589,25 @@ def test_large_m_dense_fallback(name):
     ref = oracle_solve(p, "none", tol=0.0)
     assert rel(y, ref["f_m"]) <= 1e-10, rel(y, ref["f_m"])
     sv.close()
+
+
+# ---- matrix-free K3 option: z recomputed in K3 ---------------
+@pytest.mark.parametrize("name,kw", [("c3", dict(g=64, m=60, s=120)), ("c1", dict(m=30))])
+def test_matrix_free_option_bitwise(name, kw, monkeypatch):
+    """FAB_MATRIX_FREE=1 recomputes z = A w_hat_{c-1} inside K3 from staged
+    neighbour rows with K1's stencil_row arithmetic: H, Theta V and f_m are
+    bitwise those of the default path (z stored by K1)."""
+    import torch
+    import paper_2212_12758_b200 as fab
+    p = fp.make(name, **kw)
+    out = []
+    for mf in ("0", "1"):
+        monkeypatch.setenv("FAB_MATRIX_FREE", mf)
+        sv = fab.Solver(fab.Operator.from_problem(p), torch.as_tensor(p.b).cuda(), p.m, p.k, p.s)
+        sv.sketch(p.s, p.sketch_seed)
+        sv.basis(p.m, p.k)
+        sv.compress("blendenpik", iters=30)
+        out.append((sv.get("H"), sv.get("SV"), sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()))
+        sv.close()
+    for a, b in zip(*out):
+        assert np.array_equal(a, b)
