@@ -611,3 +611,65 @@ def test_matrix_free_option_bitwise(name, kw, monkeypatch):
         sv.close()
     for a, b in zip(*out):
         assert np.array_equal(a, b)
+
+
+# ---- CSR rows longer than a row block (the whole-CTA long-row path) ---------
+def _hub_matrix(n=6000, seed=4242):
+    """Seeded random sparse matrix whose hub rows hold 1500-5000 entries
+    (> kCsrNB = 1024, so each is a block of its own, summed by the whole CTA)
+    and whose column 7 is referenced by every fourth row (a hub column)."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(seed)
+    rows, cols, vals = [], [], []
+    for r in range(n):
+        c = rng.choice(n, 8, replace=False)
+        rows += [r] * 8
+        cols += list(c)
+        vals += list(rng.standard_normal(8) / 8)
+        if r % 4 == 0:
+            rows.append(r); cols.append(7); vals.append(0.05)
+    for r, deg in ((10, 3000), (2500, 1500), (n - 1, 5000)):
+        c = rng.choice(n, deg, replace=False)
+        rows += [r] * deg
+        cols += list(c)
+        vals += list(rng.standard_normal(deg) / (4 * np.sqrt(deg)))
+    A = sp.csr_matrix((vals, (rows, cols)), shape=(n, n))
+    A.sum_duplicates()
+    A = A - 2.0 * sp.identity(n, format="csr")
+    A.sort_indices()
+    b = rng.standard_normal(n)
+    return A.tocsr(), b
+
+
+@pytest.mark.parametrize("colblock", [None, "1000"])
+def test_csr_long_rows(colblock, monkeypatch):
+    """The long-row path of the CSR K1 (rows with 1500-5000 entries, one
+    block each) against the oracle at 1e-10, unblocked and with forced column
+    blocks (a long row split over the passes), and the multi-RHS batch over
+    the same rows bitwise equal to single solves."""
+    import torch
+    import paper_2212_12758_b200 as fab
+    if colblock:
+        monkeypatch.setenv("FAB_CSR_COLBLOCK", colblock)
+    A, b = _hub_matrix()
+    assert np.diff(A.indptr).max() > 1024
+    m, k, s, seed = 30, 2, 80, 77
+    op = fab.Operator.csr(A.indptr, A.indices, A.data)
+    ref = ofab.solve(A, b, m, k, s, seed, mode="blendenpik", f="exp", lsqr_iters=40, keep=False)
+    svs = []
+    for bb in (b, np.random.default_rng(5).standard_normal(A.shape[0])):
+        sv = fab.Solver(op, torch.as_tensor(bb).cuda(), m, k, s)
+        sv.sketch(s, seed)
+        svs.append(sv)
+    fab.basis_batch(svs, m, k)
+    single = fab.Solver(op, torch.as_tensor(b).cuda(), m, k, s)
+    single.sketch(s, seed)
+    single.basis(m, k)
+    assert np.array_equal(svs[0].get("H"), single.get("H"))
+    assert np.array_equal(svs[0].get("SV"), single.get("SV"))
+    for sv in (svs[0], single):
+        sv.compress("blendenpik", iters=40)
+        y = sv.apply("exp", 1.0, 0.0).cpu().numpy()
+        assert rel(y, ref["f_m"]) <= 1e-10, rel(y, ref["f_m"])
+    for sv in svs + [single]:
+        sv.close()
