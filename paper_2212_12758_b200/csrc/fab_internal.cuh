@@ -194,6 +194,42 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// a + sum_{i < count} p[i * stride], added in order of i, the loads issued
+// B at a time (the GPU issues in order: a load whose sum waits on the
+// previous load's value would otherwise expose one memory latency per term)
+template <int B>
+__device__ __forceinline__ double ordered_sum(const double* p, int64_t stride, int count, double a = 0.0) {
+  for (int i0 = 0; i0 < count; i0 += B) {
+    double t[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) t[u] = (i0 + u < count) ? p[(int64_t)(i0 + u) * stride] : 0.0;
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+      if (i0 + u < count) a += t[u];
+  }
+  return a;
+}
+
+// a + sum_{i < count} p[i * stride] * q[i * qstride] as an fma chain in order
+// of i, loads issued B at a time
+template <int B>
+__device__ __forceinline__ double ordered_dot(const double* p, int64_t stride, const double* q, int64_t qstride,
+                                              int count, double a = 0.0) {
+  for (int i0 = 0; i0 < count; i0 += B) {
+    double t[B], r[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const bool ok = i0 + u < count;
+      t[u] = ok ? p[(int64_t)(i0 + u) * stride] : 0.0;
+      r[u] = ok ? q[(int64_t)(i0 + u) * qstride] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+      if (i0 + u < count) a = fma(t[u], r[u], a);
+  }
+  return a;
+}
+
 // Fixed-order block reduction of NV values per thread; result valid in
 // thread 0 (out[j]).  smem must hold kWarps*NV doubles.
 template <int NV>

@@ -490,47 +490,27 @@ int launch_tall_gemv(fab_ctx* c, int ncols, const double* p, double scal, int us
 // U^T column-major: U[i,j] = UT[j + i*m]); warp per output, fixed order.
 constexpr int kLsqrStepThreads = 1024;   // the one-CTA LSQR scalar kernels (latency-bound m-length work)
 
-// (Both are latency-bound single-CTA loops over L2-resident m x m data: a
-// warp takes its outputs two at a time and the inner loops are unrolled, so
-// several loads per lane are in flight; each output's sum keeps its order.)
+// (Both are latency-bound single-CTA loops over L2-resident m x m data: the
+// loads of an output's terms are issued in batches; each output's fma chain
+// keeps its order.)
 __device__ void upper_gemv(const double* UT, int m, const double* v, const double* rscale, double* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int i0 = warp; i0 < m; i0 += 2 * nw) {
-    const int i1 = i0 + nw;
-    double a0 = 0.0, a1 = 0.0;
-#pragma unroll 4
-    for (int j0 = i0 + lane; j0 < m; j0 += 32) {   // j1 = i1 + lane + 32 k runs beside j0
-      const int j1 = j0 + (i1 - i0);
-      a0 = fma(UT[j0 + (int64_t)i0 * m], v[j0], a0);
-      if (j1 < m) a1 = fma(UT[j1 + (int64_t)i1 * m], v[j1], a1);
-    }
-    a0 = warp_sum(a0);
-    a1 = warp_sum(a1);
-    if (lane == 0) {
-      out[i0] = rscale ? a0 * rscale[i0] : a0;
-      if (i1 < m) out[i1] = rscale ? a1 * rscale[i1] : a1;
-    }
+  for (int i = warp; i < m; i += nw) {
+    const int j = i + lane;
+    const int cnt = j < m ? (m - 1 - j) / 32 + 1 : 0;        // j, j+32, ... < m
+    double a = ordered_dot<8>(UT + j + (int64_t)i * m, 32, v + j, 32, cnt);
+    a = warp_sum(a);
+    if (lane == 0) out[i] = rscale ? a * rscale[i] : a;
   }
 }
 // out_i = sum_{j<=i} U[j,i] q_j   (U^T q; column i of U is contiguous)
 __device__ void upperT_gemv(const double* U, int m, const double* q, double* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int i0 = warp; i0 < m; i0 += 2 * nw) {
-    const int i1 = i0 + nw;
-    double a0 = 0.0, a1 = 0.0;
-    const int jmax = i1 < m ? i1 : i0;
-#pragma unroll 4
-    for (int j = lane; j <= jmax; j += 32) {
-      const double qj = q[j];
-      if (j <= i0) a0 = fma(U[j + (int64_t)i0 * m], qj, a0);
-      if (i1 < m) a1 = fma(U[j + (int64_t)i1 * m], qj, a1);
-    }
-    a0 = warp_sum(a0);
-    a1 = warp_sum(a1);
-    if (lane == 0) {
-      out[i0] = a0;
-      if (i1 < m) out[i1] = a1;
-    }
+  for (int i = warp; i < m; i += nw) {
+    const int cnt = lane <= i ? (i - lane) / 32 + 1 : 0;     // lane, lane+32, ... <= i
+    double a = ordered_dot<8>(U + lane + (int64_t)i * m, 32, q + lane, 32, cnt);
+    a = warp_sum(a);
+    if (lane == 0) out[i] = a;
   }
 }
 
@@ -572,18 +552,15 @@ __device__ double reduce_pass(const double* part_g, const double* part_tn, int n
   for (int j0 = 0; j0 < m; j0 += per) {
     const int j = j0 + threadIdx.x / gs;
     double a = 0.0;
-    if (j < m) {
-#pragma unroll 16
-      for (int b = sub; b < nparts; b += gs) a += part_g[(int64_t)b * m + j];   // loads batched, adds in order
-    }
+    if (j < m && sub < nparts)   // b = sub, sub + gs, ... < nparts, in order
+      a = ordered_sum<16>(part_g + (int64_t)sub * m + j, (int64_t)gs * m, (nparts - 1 - sub) / gs + 1);
     for (int o = gs >> 1; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     if (j < m && sub == 0) g[j] = a;
   }
   __shared__ double tn;
   if (threadIdx.x < 32) {
     double a = 0.0;
-#pragma unroll 8
-    for (int b = threadIdx.x; b < nparts; b += 32) a += part_tn[b];
+    if ((int)threadIdx.x < nparts) a = ordered_sum<8>(part_tn + threadIdx.x, 32, (nparts - 1 - threadIdx.x) / 32 + 1);
     a = warp_sum(a);
     if (threadIdx.x == 0) tn = a;
   }

@@ -28,8 +28,7 @@ __global__ void k_sketch_col_raw(const double* __restrict__ part, int nparts, in
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < s; q += gridDim.x * blockDim.x) {
     const double* src = part + (int64_t)col * nparts * s + q;
     double a = 0.0;
-#pragma unroll 16
-    for (int b = 0; b < nparts; ++b) a += src[(int64_t)b * s];   // loads batched, adds in order
+    for (int b = 0; b < nparts; ++b) a += src[(int64_t)b * s];
     p[q] = a / sqrt((double)s);
   }
 }

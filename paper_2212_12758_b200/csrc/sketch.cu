@@ -98,8 +98,7 @@ __global__ void k_sketch_finalize(const double* __restrict__ part, int nparts, i
     }
     const double* q = part + (int64_t)col * nparts * s + p;
     double a = 0.0;
-#pragma unroll 16
-    for (int b = 0; b < nparts; ++b) a += q[(int64_t)b * s];   // loads batched, adds in order
+    for (int b = 0; b < nparts; ++b) a += q[(int64_t)b * s];
     SV[i] = a / (sqrt((double)s) * beta[col]);
   }
 }
