@@ -973,11 +973,15 @@ static int db_e1(fab_ctx* c, int m, const double* X0, int want_inv, double* c_ou
     if (err > 1e-2) mu = exp(-gh[0] / (2.0 * m));
     const double imu2 = 1.0 / (mu * mu);
     FAB_TRY(lincomb(c, m, imu2, Mi, 0, nullptr, 0, nullptr, 1.0, T, st));   // I + mu^-2 M^-1
-    FAB_TRY(gemm(c, m, Y, T, 0.5 * mu, 0.0, nullptr, 0.0, Y2, st));
-    FAB_TRY(gemm(c, m, Z, T, 0.5 * mu, 0.0, nullptr, 0.0, Z2, st));
+    // only the wanted factor is carried (the iteration itself runs on M)
     double* t;
-    t = Y; Y = Y2; Y2 = t;
-    t = Z; Z = Z2; Z2 = t;
+    if (want_inv) {
+      FAB_TRY(gemm(c, m, Z, T, 0.5 * mu, 0.0, nullptr, 0.0, Z2, st));
+      t = Z; Z = Z2; Z2 = t;
+    } else {
+      FAB_TRY(gemm(c, m, Y, T, 0.5 * mu, 0.0, nullptr, 0.0, Y2, st));
+      t = Y; Y = Y2; Y2 = t;
+    }
     FAB_TRY(lincomb(c, m, 0.25 * mu * mu, M, 0.25 * imu2, Mi, 0, nullptr, 0.5, M, st));
     FAB_TRY(read_stats(c, M, m, h, st));
     if (h[2] != 0.0) return FAB_EDOMAIN;
