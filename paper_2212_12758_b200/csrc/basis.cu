@@ -525,22 +525,48 @@ __device__ __forceinline__ void slot_copy(const PipeArgs& a, int v, int col, int
   *dst_off = off + (int)(l - base);
 }
 
-// k_scalar's det_sum inside the pipeline CTA: the 256 consumer threads sum
-// p[b*stride+off], b = t, t+256, ..., then the 8 warp sums in order -- the
-// same operations in the same order as det_sum in a 256-thread CTA.  Called
-// by the consumer warps only (named barrier 2), so the producer warp starts
-// streaming while the scalars are formed.
-__device__ __forceinline__ double cta_det_sum(const double* p, int count, int stride, int off, double* red) {
-  double a = 0.0;
-  for (int b = threadIdx.x; b < count; b += kThreads) a += p[(int64_t)b * stride + off];
-  a = warp_sum(a);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+// k_scalar's sums inside the pipeline CTA, all at once (the lagged norm from
+// pn, the nw window dots from pd): thread t sums p[b] for b = t, t+256, ...,
+// then the 8 warp sums in order -- the order of det_sum in a 256-thread CTA
+// (k_scalar), called by the consumer warps only (named barrier 2, so the
+// producer warp streams meanwhile).  The loads of every quantity are issued
+// together and the warp partials cross one barrier, so the consumers wait one
+// L2 round trip instead of nw + 1 before their first chunk.
+template <int NWM>
+__device__ __forceinline__ void cta_det_sums(const double* pn, int cn, const double* pd, int cd, int nw,
+                                             double* red, double& nu, double (&dj)[NWM]) {
+  double a[NWM + 1];
+#pragma unroll
+  for (int q = 0; q <= NWM; ++q) a[q] = 0.0;
+  const int cmax = cn > cd ? cn : cd;
+  for (int b = threadIdx.x; b < cmax; b += kThreads) {
+    double v[NWM + 1];
+    v[0] = b < cn ? pn[b] : 0.0;
+#pragma unroll
+    for (int t = 0; t < NWM; ++t) v[1 + t] = (t < nw && b < cd) ? pd[(int64_t)b * (kKMax + 1) + t] : 0.0;
+    if (b < cn) a[0] += v[0];
+#pragma unroll
+    for (int t = 0; t < NWM; ++t)
+      if (t < nw && b < cd) a[1 + t] += v[1 + t];
+  }
+  const int warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q <= NWM; ++q) {
+    const double w = warp_sum(a[q]);
+    if ((threadIdx.x & 31) == 0) red[q * kWarps + warp] = w;
+  }
   consumer_sync(2, kThreads);
-  double r = 0.0;
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0) {
+    double r = 0.0;
     for (int w = 0; w < kWarps; ++w) r += red[w];
-  consumer_sync(2, kThreads);
-  return r;   // valid in thread 0
+    nu = r;
+#pragma unroll
+    for (int t = 0; t < NWM; ++t) {
+      r = 0.0;
+      for (int w = 0; w < kWarps; ++w) r += red[(1 + t) * kWarps + w];
+      dj[t] = t < nw ? r : 0.0;
+    }
+  }
 }
 
 // NWM: window capacity of the update (2, 4 or 8 >= nw), so the per-row loop
@@ -583,9 +609,8 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
 #pragma unroll
       for (int t = 0; t < NWM; ++t) dj[t] = t < nw ? a.sums[t] : 0.0;
     } else {
-      nu = cta_det_sum(a.part_norm_prev, gridDim.x, 1, 0, red);
-#pragma unroll
-      for (int t = 0; t < NWM; ++t) dj[t] = t < nw ? cta_det_sum(a.part_dots, a.nparts_dots, kKMax + 1, t, red) : 0.0;
+      __shared__ double red2[(NWM + 1) * kWarps];
+      cta_det_sums<NWM>(a.part_norm_prev, gridDim.x, a.part_dots, a.nparts_dots, nw, red2, nu, dj);
     }
     if (threadIdx.x == 0) {
       const double b = sqrt(nu);
