@@ -97,7 +97,9 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
                  const DevState* __restrict__ st, StepRed sr) {
   pdl_wait();
   pdl_trigger();
-  if (st->breakdown) return;
+  // the breakdown flag is tested after the first rows' loads are issued, so
+  // its L2 round trip overlaps them instead of preceding them
+  const bool bd = st->breakdown != 0;
   __shared__ double red[kWarps * NWM];
   const double* __restrict__ xw = V + (int64_t)(c - 1) * ld;   // w_hat_{c-1} (window dot)
   const double* __restrict__ x = SQ ? xin : xw;                // SpMV input
@@ -144,6 +146,7 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
         if (SQ) xd[u] = ld2(xw + r);
       }
     }
+    if (bd) return;   // uniform over the grid: nothing is written after a breakdown
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (!ok[u]) continue;
@@ -165,6 +168,7 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
       d[NWM - 1] = fma(xl2.y, a1, d[NWM - 1]);
     }
   }
+  if (bd) return;
   double out[NWM];
   block_sum<NWM>(d, red, out);
   if (threadIdx.x == 0 && nw > 0) {
