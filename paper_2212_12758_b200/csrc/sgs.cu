@@ -21,15 +21,21 @@
 
 namespace fab {
 
-// p = (sum_b part[col][b][:]) / sqrt(s)  (Theta w without any column scale)
+// p = (sum_b part[col][b][:]) / sqrt(s)  (Theta w without any column scale).
+// One warp per sketch row q: lane l sums the partials b = l, l+32, ... (its
+// loads issued together), then the fixed xor tree -- s = 400 rows x 296
+// partials as 400 warps instead of 400 threads walking 296 loads each.
 __global__ void k_sketch_col_raw(const double* __restrict__ part, int nparts, int s, int col,
                                  double* __restrict__ p, const DevState* __restrict__ st) {
   if (st->breakdown) return;
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < s; q += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < s; q += nwarps) {
     const double* src = part + (int64_t)col * nparts * s + q;
     double a = 0.0;
-    for (int b = 0; b < nparts; ++b) a += src[(int64_t)b * s];
-    p[q] = a / sqrt((double)s);
+    if (lane < nparts) a = ordered_sum<8>(src + (int64_t)lane * s, 32 * (int64_t)s, (nparts - 1 - lane) / 32 + 1);
+    a = warp_sum(a);
+    if (lane == 0) p[q] = a / sqrt((double)s);
   }
 }
 
@@ -75,8 +81,18 @@ __global__ void k_sgs_step(int c, int s, const double* __restrict__ praw, double
   for (int j = warp; j < c; j += kWarps) {
     const double* sj = SV + (int64_t)j * s;
     double a = 0.0;
-#pragma unroll 8
-    for (int q = lane; q < s; q += 32) a = fma(sj[q], praw[q] * bsc, a);
+    for (int q0 = lane; q0 < s; q0 += 32 * 8) {   // loads issued 8 at a time, fmas in order of q
+      double x[8], y[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = q0 + 32 * u;
+        x[u] = q < s ? sj[q] : 0.0;
+        y[u] = q < s ? praw[q] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (q0 + 32 * u < s) a = fma(x[u], y[u] * bsc, a);
+    }
     a = warp_sum(a);
     if (lane == 0) rr[j] = a;
   }
@@ -85,8 +101,14 @@ __global__ void k_sgs_step(int c, int s, const double* __restrict__ praw, double
   double a = 0.0;
   for (int q = threadIdx.x; q < s; q += blockDim.x) {
     double v = praw[q] * bsc;
-#pragma unroll 16
-    for (int j = 0; j < c; ++j) v = fma(-SV[(int64_t)j * s + q], rr[j], v);
+    for (int j0 = 0; j0 < c; j0 += 8) {   // loads issued 8 at a time, fmas in order of j
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = j0 + u < c ? SV[(int64_t)(j0 + u) * s + q] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j0 + u < c) v = fma(-x[u], rr[j0 + u], v);
+    }
     sbuf[q] = v;
     a = fma(v, v, a);
   }
@@ -124,8 +146,8 @@ int enqueue_k1(fab_ctx* c, int col, int nw, double* z, bool need_z, cudaStream_t
 
 // p = Theta w_hat_col from its sketch partials (already in part_sk), C3 on several GPUs
 int enqueue_col_sketch_reduce(fab_ctx* c, int col, double* p, cudaStream_t st, int64_t* launches) {
-  k_sketch_col_raw<<<(c->s + kThreads - 1) / kThreads, kThreads, 0, st>>>(c->part_sk, c->grid_upd, c->s, col,
-                                                                          p, c->st_d);
+  k_sketch_col_raw<<<(c->s * 32 + kThreads - 1) / kThreads, kThreads, 0, st>>>(c->part_sk, c->grid_upd, c->s,
+                                                                               col, p, c->st_d);
   FAB_CHECK_LAUNCH();
   ++*launches;
   return comm_allreduce(c, p, (size_t)c->s, false, st);
