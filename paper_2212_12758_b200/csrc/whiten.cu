@@ -72,10 +72,22 @@ __global__ void k_wh_qr_step(int j, int s, const double* __restrict__ praw, cons
   if (st->breakdown) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double bs = 1.0 / beta[j];
+  // (the loops below issue their loads 8 at a time; every sum keeps its order)
   for (int l = warp; l < j; l += kWarps) {            // r_l = q_l^T p
     const double* ql = Q + (int64_t)l * s;
     double a = 0.0;
-    for (int q = lane; q < s; q += 32) a = fma(ql[q], praw[q] * bs, a);
+    for (int q0 = lane; q0 < s; q0 += 32 * 8) {
+      double x[8], y[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = q0 + 32 * u;
+        x[u] = q < s ? ql[q] : 0.0;
+        y[u] = q < s ? praw[q] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (q0 + 32 * u < s) a = fma(x[u], y[u] * bs, a);
+    }
     a = warp_sum(a);
     if (lane == 0) rr[l] = a;
   }
@@ -83,7 +95,14 @@ __global__ void k_wh_qr_step(int j, int s, const double* __restrict__ praw, cons
   double a = 0.0;
   for (int q = threadIdx.x; q < s; q += blockDim.x) {
     double v = praw[q] * bs;
-    for (int l = 0; l < j; ++l) v = fma(-Q[(int64_t)l * s + q], rr[l], v);
+    for (int l0 = 0; l0 < j; l0 += 8) {
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = l0 + u < j ? Q[(int64_t)(l0 + u) * s + q] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (l0 + u < j) v = fma(-x[u], rr[l0 + u], v);
+    }
     Q[(int64_t)j * s + q] = v;
     a = fma(v, v, a);
   }
@@ -95,7 +114,14 @@ __global__ void k_wh_qr_step(int j, int s, const double* __restrict__ praw, cons
   // new column of R^{-1}: x_j = 1/r_jj, x_l = -(1/r_jj) sum_{t=l}^{j-1} Ri[l,t] r_t
   for (int l = threadIdx.x; l < j; l += blockDim.x) {
     double acc = 0.0;
-    for (int t = l; t < j; ++t) acc = fma(Ri[l + (int64_t)t * ldr], rr[t], acc);
+    for (int t0 = l; t0 < j; t0 += 8) {
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = t0 + u < j ? Ri[l + (int64_t)(t0 + u) * ldr] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (t0 + u < j) acc = fma(x[u], rr[t0 + u], acc);
+    }
     xs[l] = -acc / rjj;
   }
   if (threadIdx.x == 0) xs[j] = 1.0 / rjj;
