@@ -127,17 +127,39 @@ int dense_qr_sketch(fab_ctx* c, int m, double* R, double* qtb, cudaStream_t st) 
 // R^{-1} for upper triangular R (column-major m x m): CTA j solves R x = e_j
 // by column-oriented back substitution (x_i = 0 for i > j).
 // ---------------------------------------------------------------------------
+// Column l of R (and its diagonal) is loaded one step ahead, so a step waits
+// on shared memory and barriers only, not on an L2 round trip (m <= 1024:
+// 8 rows per thread at 128 threads).  Same operations in the same order.
 __global__ void k_tri_inverse(const double* R, int m, double* Rinv) {
   extern __shared__ double b[];
+  constexpr int kPer = (kMaxM + 127) / 128;
   const int j = blockIdx.x;
   for (int i = threadIdx.x; i < m; i += blockDim.x) b[i] = (i == j) ? 1.0 : 0.0;
+  double rc[kPer], rn[kPer], dg, dn = 0.0;
+  auto load_col = [&](int l, double (&r)[kPer], double& d) {
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int i = threadIdx.x + 128 * u;
+      r[u] = (l >= 0 && i < l) ? R[i + (int64_t)l * m] : 0.0;
+    }
+    d = l >= 0 ? R[l + (int64_t)l * m] : 1.0;
+  };
+  load_col(j, rc, dg);
   __syncthreads();
   for (int l = j; l >= 0; --l) {
-    const double xl = b[l] / R[l + (int64_t)l * m];
+    load_col(l - 1, rn, dn);   // next column, in flight during this step
+    const double xl = b[l] / dg;
     __syncthreads();
     if (threadIdx.x == 0) b[l] = xl;
-    for (int i = threadIdx.x; i < l; i += blockDim.x) b[i] = fma(-R[i + (int64_t)l * m], xl, b[i]);
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int i = threadIdx.x + 128 * u;
+      if (i < l) b[i] = fma(-rc[u], xl, b[i]);
+    }
     __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) rc[u] = rn[u];
+    dg = dn;
   }
   for (int i = threadIdx.x; i < m; i += blockDim.x) Rinv[i + (int64_t)j * m] = (i <= j) ? b[i] : 0.0;
 }
