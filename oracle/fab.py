@@ -17,7 +17,8 @@ Compression (Eq. (6), l.167-171): V_m^+ A V_m = H_m + h_{m+1,m} (V_m^+ v_{m+1})
 e_m^T, gamma_b = ||b||_2 for Alg 2 (l.172).  f is applied as
 f(alpha C + sigma I) (reading G-17).  Reading G-12: Blendenpik reuses the
 basis sketch Theta (one fab_sketch call), so SV_{m+1} = Theta V_{m+1} feeds
-both the Blendenpik R and sketch-and-solve.
+both the Blendenpik R and sketch-and-solve -- unless `precond=(s2, seed2)`
+asks for Blendenpik's own sketch Theta' of V_m.
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 """
@@ -29,8 +30,12 @@ from .srht import SRHT
 MODES = ("blendenpik", "sketch_solve", "none")
 
 
-def compress(dec, SV, mode, lsqr_tol=1e-6, lsqr_iters=None, lsqr_maxit=None, rinv="solve"):
-    """y and C_m = H_m + h_{m+1,m} y e_m^T from an Alg 2 decomposition."""
+def compress(dec, SV, mode, lsqr_tol=1e-6, lsqr_iters=None, lsqr_maxit=None, rinv="solve", precond=None):
+    """y and C_m = H_m + h_{m+1,m} y e_m^T from an Alg 2 decomposition.
+    precond=(s2, seed2): Blendenpik takes its preconditioner from its own
+    SRHT Theta' = SRHT(n, s2, seed2) of V_m ("computes a
+    random sketch of the basis using, once again, a SRHT"; reading G-12's
+    precond_s / precond_seed) instead of reusing SV = Theta V."""
     V, H, m = dec["V"], dec["H"], dec["m_eff"]
     Hm = H[:m, :m].copy()
     info = {}
@@ -40,7 +45,10 @@ def compress(dec, SV, mode, lsqr_tol=1e-6, lsqr_iters=None, lsqr_maxit=None, rin
         if mode != "none" and SV is not None:
             R, _ = lsq.householder_qr(SV[:, :m])
     elif mode == "blendenpik":
-        y, R, info = lsq.blendenpik(V[:, :m], V[:, m], SV[:, :m], tol=lsqr_tol,
+        SVp = SV[:, :m]
+        if precond is not None:
+            SVp = SRHT(V.shape[0], precond[0], precond[1]).apply(V[:, :m])      # Theta' V_m
+        y, R, info = lsq.blendenpik(V[:, :m], V[:, m], SVp, tol=lsqr_tol,
                                     maxit=lsqr_maxit, iters=lsqr_iters, rinv=rinv)
     elif mode == "sketch_solve":
         y, R = lsq.sketch_and_solve(SV[:, :m], SV[:, m])
@@ -54,7 +62,7 @@ def compress(dec, SV, mode, lsqr_tol=1e-6, lsqr_iters=None, lsqr_maxit=None, rin
 
 def solve(A, b, m, k, s, seed, mode="blendenpik", f="exp", alpha=1.0,
           sigma=0.0, poly=None, lsqr_tol=1e-6, lsqr_iters=None,
-          lsqr_maxit=None, variant="cgs", keep=True, lsqr_rinv="solve"):
+          lsqr_maxit=None, variant="cgs", keep=True, lsqr_rinv="solve", precond=None):
     """One f(A)b approximation by Alg 4 / Remark 2 / Alg 5.  Returns a dict
     with f_m and every intermediate (V, H, SV, rows, signs, y, C, c)."""
     dec = krylov.truncated_arnoldi(A, b, m, k, variant=variant)     # Alg 2
@@ -65,7 +73,7 @@ def solve(A, b, m, k, s, seed, mode="blendenpik", f="exp", alpha=1.0,
         if me + 1 > s:
             raise ValueError("InvalidSketchSize: need s >= m+1")
         SV = th.apply(dec["V"])                                     # Theta V_{m+1}
-    y, C, R, info = compress(dec, SV, mode, lsqr_tol, lsqr_iters, lsqr_maxit, lsqr_rinv)
+    y, C, R, info = compress(dec, SV, mode, lsqr_tol, lsqr_iters, lsqr_maxit, lsqr_rinv, precond)
     c = matfun.f_e1(f, C, alpha, sigma, poly)                       # f(C) e_1
     fm = dec["gamma"] * (dec["V"][:, :me] @ c)                      # ||b|| V_m c
     out = dict(f_m=fm, H=dec["H"], gamma=dec["gamma"], m_eff=me,

@@ -213,3 +213,45 @@ def test_whitened_alg4_on_graph_matches_dense_exp():
                                lsqr_iters=60)
         assert r["whitened_at"] > 0
         assert np.linalg.norm(r["f_m"] - ref) <= 1e-10 * np.linalg.norm(ref), mode
+
+
+# ---- Blendenpik's own preconditioner sketch (reading G-12) --
+def test_precond_same_sketch_is_default():
+    """precond=(s, seed) is the basis sketch Theta itself: the same R, y, f_m."""
+    p = fp.make("c2", g=60, m=30, s=60)
+    a = fab.solve(p.scipy(), p.b, p.m, p.k, p.s, p.sketch_seed, mode="blendenpik", f=p.f, alpha=p.alpha,
+                  lsqr_iters=20)
+    b = fab.solve(p.scipy(), p.b, p.m, p.k, p.s, p.sketch_seed, mode="blendenpik", f=p.f, alpha=p.alpha,
+                  lsqr_iters=20, precond=(p.s, p.sketch_seed))
+    assert np.array_equal(a["R"], b["R"]) and np.array_equal(a["f_m"], b["f_m"])
+
+
+def test_precond_isometric_sketch_makes_lsqr_one_step():
+    """With s' = N the SRHT is an isometry (Theta'^T Theta' = I, G-9), so R is
+    V_m's own R factor and V_m R^{-1} has orthonormal columns: LSQR on it
+    terminates with the exact least-squares solution within two iterations
+    (one distinct singular value), whatever the conditioning of V_m."""
+    p = fp.make("c3", g=16, m=12, k=4, s=30)            # n = 4096 = N
+    dec = krylov.truncated_arnoldi(p.scipy(), p.b, p.m, p.k, variant="cgs")
+    from oracle.srht import SRHT
+    SV = SRHT(p.n, p.s, p.sketch_seed).apply(dec["V"])
+    y, C, R, info = fab.compress(dec, SV, "blendenpik", lsqr_tol=1e-12, precond=(p.n, 99))
+    V = dec["V"]
+    ref = np.linalg.lstsq(V[:, :p.m], V[:, p.m], rcond=None)[0]
+    assert info["iters"] <= 2
+    assert rel(y, ref) <= 1e-10
+    Q = V[:, :p.m] @ np.linalg.inv(R)
+    assert np.abs(Q.T @ Q - np.eye(p.m)).max() <= 1e-12
+
+
+def test_precond_larger_sketch_fewer_iterations():
+    """A larger preconditioner sketch gives a better-conditioned V_m R^{-1}
+    (embedding distortion ~ sqrt(m/s')): fewer LSQR iterations to the MATLAB
+    tolerance 1e-6 (l.359), and the same compression within that tolerance."""
+    p = fp.make("c5", n=1 << 14, m=60, s=120)
+    A = p.scipy()
+    a = fab.solve(A, p.b, p.m, p.k, p.s, p.sketch_seed, mode="blendenpik", f=p.f, alpha=p.alpha)
+    b = fab.solve(A, p.b, p.m, p.k, p.s, p.sketch_seed, mode="blendenpik", f=p.f, alpha=p.alpha,
+                  precond=(4 * p.m, 12345))
+    assert b["lsqr"]["iters"] < a["lsqr"]["iters"]
+    assert rel(b["f_m"], a["f_m"]) <= 1e-8
