@@ -40,6 +40,40 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+def workload_config(p, world):
+    """The config dict of BOTH arms (the driver compares them)."""
+    return {"workload": WORKLOAD, "n": p.n, "m": p.m, "k": p.k, "s": p.s,
+            "mode": "blendenpik (LSQR tol 1e-6)", "f": "sqrt", "sigma": p.sigma,
+            "l2": "inputs larger than L2 (V_{m+1} = 27 GB >> 126 MB L2), no flush needed",
+            "parallelism": "1 GPU" if world == 1 else
+            f"{world} GPUs: one solve, z-slab row blocks, NCCL halo + allreduce"}
+
+
+def oracle_lsqr_iters():
+    """LSQR iterations of the ORACLE's own full-size c3 run at tol 1e-6
+    (tests/golden/c3_full.npz, written by the oracle-only script
+    tests/golden/make_c3_golden.py): the reference arm scales its LSQR sample
+    by it, so neither arm's count comes from the other."""
+    path = os.path.join(ROOT, "tests", "golden", "c3_full.npz")
+    import numpy as np
+    with np.load(path) as g:
+        meta = json.loads(bytes(g["meta_json"]).decode())
+    return int(round(meta["blendenpik_lsqr"]["iters"])), "oracle full-size c3 run (tests/golden/c3_full.npz)"
+
+
+def relaunch_distributed(args):
+    """--gpus N > 1 without torchrun: start N ranks of this same command
+    (torch.distributed.run, 127.0.0.1) and return their exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    log("[bench] launching", " ".join(cmd))
+    return subprocess.call(cmd)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -48,7 +82,9 @@ def parse():
     ap.add_argument("--impl", default="fab", choices=["fab", "reference"])
     ap.add_argument("--g", type=int, default=256, help="grid side (256 = BASELINE c3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-extras", action="store_true", help="skip mode / e2e side measurements")
+    ap.add_argument("--no-extras", action="store_true", help="skip the c3 side measurements (modes, API order)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the c4 / c5 side lines")
+    ap.add_argument("--config-reps", type=int, default=2, help="timed solves per mode for c4 / c5")
     return ap.parse_args()
 
 
@@ -178,6 +214,35 @@ def oracle_sample(p, A, lsqr_iters, small=False):
                          t_final=t_final)
 
 
+def src_sha(files):
+    import hashlib
+    h = hashlib.sha256()
+    for f in files:
+        with open(os.path.join(ROOT, "paper_2212_12758_b200", "csrc", f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+TRAFFIC_SRC = ("lsqr.cu", "pipe.cuh", "fab_internal.cuh")
+
+
+def lsqr_pass_traffic(n_loc, m):
+    """dram__bytes_read.sum + dram__bytes_write.sum of ONE K6 launch from the
+    `ncu --set full` capture recorded in profiles/lsqr_pass_traffic.json --
+    used only if that capture was taken on the kernel source as it is now
+    (hash of its files) and at this n, m; else None with the reason."""
+    tp = os.path.join(ROOT, "profiles", "lsqr_pass_traffic.json")
+    if not os.path.exists(tp):
+        return None, "no capture"
+    d = json.load(open(tp))
+    cur = src_sha(TRAFFIC_SRC)
+    if d.get("src_sha") != cur:
+        return None, f"capture {d.get('capture')} is of another kernel source ({d.get('src_sha')} != {cur})"
+    if d.get("n") != n_loc or d.get("m") != m:
+        return None, "capture at another size"
+    return d["dram_bytes_per_launch"], f"ncu --set full capture {d.get('capture')} (src {cur})"
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -189,28 +254,36 @@ def run_reference(args):
     import numpy as np  # noqa: F401
     import fab_problems as fp
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
     p = fp.make("c3", g=args.g)
     log(f"[reference] building CSR of the c3 operator (n={p.n}) for the oracle ...")
     A = p.scipy()
-    L = 26   # LSQR iterations of the GPU run at c3 (tol 1e-6); used to scale the sample
-    Ts = []
+    L, L_src = oracle_lsqr_iters()
+    Ts, walls = [], []
     for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
         T, desc, parts = oracle_sample(p, A, L)   # the cpu_baseline sample (~20 s at c3)
         if i >= args.warmup:
             Ts.append(T)
+            walls.append(time.perf_counter() - t0)
         log(f"[reference] step {i}: estimated {T:.1f} s/solve {parts}")
     T = statistics.mean(Ts)
     val = 1.0 / T
     cores = cpu_cores()
     out = {
         "metric": METRIC, "value": val, "unit": "solves/s", "impl": "reference",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": T * 1e3, "higher_is_better": True, "scaling": "strong",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        # one step = one bounded oracle sample (its wall time); value is the
+        # sample extrapolated to one full c3 solve (see cpu_baseline.sample)
+        "ms_per_step": statistics.mean(walls) * 1e3,
+        "extrapolated_ms_per_solve": T * 1e3,
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n": p.n, "m": p.m, "k": p.k, "s": p.s},
+        "config": workload_config(p, world),
         "krylov_iters_per_s": 1.0 / parts["t_iter"],
+        "lsqr_iters": L, "lsqr_iters_source": L_src,
         "cpu_baseline": {"value": val, "unit": "solves/s", "cores": cores, "kind": "oracle",
                          "sample": desc},
         "e2e": {"value": val, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -222,8 +295,82 @@ def run_reference(args):
 # ----------------------------------------------------------------------------
 # GPU arm
 # ----------------------------------------------------------------------------
+def other_config(name, world, rank, dev, comm, dist, reps):
+    """BASELINE c4 (power-law graph, CSR, exp) or c5 (random sparse, CSR,
+    column-blocked K1, invsqrt) at full size: Krylov it/s (fused sketch) and
+    solves/s per mode (median of `reps` timed solves after one warm-up),
+    one solve over all ranks (nnz-balanced / equal row blocks)."""
+    import numpy as np
+    import torch
+    import fab_problems as fp
+    import paper_2212_12758_b200 as fab
+    t0 = time.perf_counter()
+    p = fp.make(name)
+    t_gen = time.perf_counter() - t0
+    if comm is not None:
+        from paper_2212_12758_b200 import dist as fdist
+        ip = p.csr()[0]
+        cuts = fdist.csr_blocks(ip, world) if name == "c4" else fdist.row_blocks(p.n, world)
+        r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+        op = fdist.local_operator(p, r0, r1)
+    else:
+        r0, r1 = 0, p.n
+        op = fab.Operator.from_problem(p)
+    b = torch.as_tensor(np.ascontiguousarray(p.b[r0:r1])).cuda(dev)
+    sv = fab.Solver(op, b, m_max=p.m, k_max=p.k, s_max=p.s, device=dev, profile=True, comm=comm)
+    yv = torch.empty(r1 - r0, dtype=torch.float64, device=f"cuda:{dev}")
+    st = torch.cuda.current_stream(dev)
+
+    def solve(mode):
+        if mode != "none":
+            sv.sketch(p.s, p.sketch_seed)
+        sv.basis(p.m, p.k)
+        sv.compress(mode, tol=1e-6)
+        sv.apply(p.f, p.alpha, p.sigma, out=yv)
+        return sv.info()
+
+    res = {"n": p.n, "m": p.m, "k": p.k, "s": p.s, "f": p.f, "nnz": int(p.meta["nnz"]), "gen_s": t_gen}
+    for mode in ("blendenpik", "sketch_solve", "none"):
+        solve(mode)
+        times, infs = [], []
+        for _ in range(reps):
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            infs.append(solve(mode))
+            e1.record(st)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            if dist:
+                t = torch.tensor([ms], device=f"cuda:{dev}")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t.item())
+            times.append(ms)
+        ms = statistics.median(times)
+        r = {"solves_per_s": 1e3 / ms, "ms_per_solve": ms,
+             "basis_ms": statistics.median(i["ms_basis"] for i in infs)}
+        if mode == "blendenpik":
+            r["lsqr_iters"] = infs[-1]["lsqr_iters"]
+            r["cond_R"] = infs[-1]["cond_R"]
+            res["krylov_iters_per_s"] = p.m / (r["basis_ms"] * 1e-3)
+        res[mode] = r
+    sv.close()
+    del sv, op
+    torch.cuda.empty_cache()
+    return res
+
+
 def main():
     args = parse()
+    world_env = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and world_env is None:
+        return relaunch_distributed(args)
+    if world_env is not None and int(world_env) != args.gpus:
+        log(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world_env}: launch one rank per GPU "
+            f"(torchrun --nproc-per-node {args.gpus}) or drop --gpus")
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     import numpy as np
@@ -308,13 +455,7 @@ def main():
     pass_ms = sum(i["ms_lsqr_pass"] for i in infos) / max(passes, 1)
     pass_bytes = 8.0 * n_loc * (m + 2)       # this GPU's rows
     achieved = pass_bytes / (pass_ms * 1e-3) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "lsqr_pass_traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    traffic, traffic_src = lsqr_pass_traffic(n_loc, m)
     # basis: algorithmic bytes per Krylov step of this implementation:
     # K1 reads k window columns and writes z (8n(k+1)); K3 reads z + k columns and
     # writes one (8n(k+2)) -> 8n(2k+3) = 88 B/row at k = 4
@@ -333,11 +474,7 @@ def main():
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n": n, "m": m, "k": k, "s": s,
-                   "mode": "blendenpik (LSQR tol 1e-6)", "f": "sqrt", "sigma": p.sigma,
-                   "l2": "inputs larger than L2 (V_{m+1} = 27 GB >> 126 MB L2), no flush needed",
-                   "parallelism": "1 GPU" if world == 1 else
-                   f"{world} GPUs: one solve, z-slab row blocks, NCCL halo + allreduce"},
+        "config": workload_config(p, world),
         "krylov_iters_per_s": m / (basis_ms * 1e-3),
         "phase_ms": {"sketch": avg("ms_sketch"), "basis": basis_ms, "compress": avg("ms_compress"),
                      "apply": avg("ms_apply")},
@@ -346,113 +483,141 @@ def main():
         "roofline": {"kernel": "k_lsqr_pass (Blendenpik-LSQR fused V p / V^T t pass)",
                      "bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": peak_src,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": pass_bytes, "avg_launch_ms": pass_ms,
                      "launches_timed": passes},
         "gpu_launches": launches,
         "clocks": clocks,
     }
 
+    # ---- e2e: through the ABI, b from / f_m to pinned host memory ---------
+    bh = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
+    bh.copy_(torch.as_tensor(b_np))
+    yh = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
+    bh_np, yh_np = bh.numpy(), yh.numpy()
+
+    def e2e_step():
+        sv.set_b(bh_np)
+        sv.sketch(p.s, p.sketch_seed)
+        sv.basis(p.m, p.k)
+        sv.compress("blendenpik", tol=1e-6)
+        sv.apply(p.f, p.alpha, p.sigma, out=yh_np, host=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    ne = max(2, min(args.steps, 3))
+    for _ in range(ne):
+        e2e_step()
+    torch.cuda.synchronize()
+    te = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([te], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        te = float(t.item())
+    # bytes of the whole job per step: every rank copies its n_loc rows of b in and of f_m out
+    out["e2e"] = {"value": ne / te, "unit": "solves/s", "h2d_bytes_per_step": 8 * n,
+                  "d2h_bytes_per_step": 8 * n, "output_finite": bool(np.isfinite(yh_np).all())}
+
     # ---- side measurements (not part of value) ----------------------------
-    if not args.no_extras:
-        modes = {}
-        for mode in ("sketch_solve", "none", "blendenpik_gram"):
-            step(mode)
-            torch.cuda.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            inf = step(mode)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            modes[mode] = 1e3 / e0.elapsed_time(e1)
-            if mode == "blendenpik_gram":
-                # the same LSQR iterates through the Gram matrix of V_{m+1} (one
-                # fp64 SYRK pass instead of L+1 streaming passes)
-                out["blendenpik_gram"] = {"solves_per_s": modes[mode], "gram_used": inf["gram_used"],
-                                          "lsqr_iters": inf["lsqr_iters"], "gram_pass_ms": inf["ms_lsqr_pass"],
-                                          "compress_ms": inf["ms_compress"],
-                                          "gram_gflops": 2.0 * n_loc * (m + 1) ** 2 / 2 /
-                                          max(inf["ms_lsqr_pass"], 1e-9) / 1e6}
-        # parity mode (fixed L = 40 LSQR iterations)
-        step("blendenpik", iters=40)
+    errors = {}
+
+    def side(name, fn):
+        """One side measurement; an error is reported, not fatal (the line
+        must still print).  Every rank runs the same calls in the same order."""
+        try:
+            fn()
+        except Exception as e:   # noqa: BLE001
+            errors[name] = repr(e)[:300]
+            log(f"[bench] side measurement {name} failed: {e!r}")
+
+    def timed(fn):
+        fn()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        step("blendenpik", iters=40)
+        r = fn()
         e1.record(stream)
         torch.cuda.synchronize()
-        modes["blendenpik_L40"] = 1e3 / e0.elapsed_time(e1)
-        modes["blendenpik"] = value
+        return e0.elapsed_time(e1), r
+
+    if not args.no_extras:
+        modes = {"blendenpik": value}
         out["solves_per_s_by_mode"] = modes
-        # API-order variant: sketch after the basis (batched SRHT pass)
-        step("blendenpik", fused=False)
-        inf = step("blendenpik", fused=False)
-        out["api_order_sketch_ms"] = inf["ms_sketch_batched"]
-        # the paper's basis comparison (Table 1) on
-        # the same operator: Alg 2 (the step above), Alg 1 (sketched GS, O(n m^2)
-        # bytes, one pass over V_i per step) and full Arnoldi (CGS2, three passes)
-        algs = {"alg2_truncated_k%d" % k: avg("ms_basis")}
-        sv.sketch(p.s, p.sketch_seed)
-        sv.basis_sgs(p.m)
-        algs["alg1_sketched_gs"] = sv.info()["ms_basis"]
-        sv.compress("lsqr", tol=1e-6)
-        sv.apply(p.f, p.alpha, p.sigma, out=y)
-        a3 = sv.info()
-        sv.basis_arnoldi(p.m)
-        algs["arnoldi_cgs2"] = sv.info()["ms_basis"]
-        out["basis_ms_by_algorithm"] = algs
-        out["alg3_solve_ms"] = a3["ms_basis"] + a3["ms_compress"] + a3["ms_apply"]
-        out["alg3_lsqr_iters"] = a3["lsqr_iters"]
-        # e2e: b from pinned host memory, f_m back to pinned host memory, every step
-        bh = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
-        bh.copy_(torch.as_tensor(b_np))
-        yh = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
-        bh_np, yh_np = bh.numpy(), yh.numpy()
+        for mode in ("sketch_solve", "none"):
+            side(mode, lambda mode=mode: modes.__setitem__(mode, 1e3 / timed(lambda: step(mode))[0]))
+        # parity mode (fixed L = 40 LSQR iterations, SURVEY §8d-1)
+        side("blendenpik_L40", lambda: modes.__setitem__(
+            "blendenpik_L40", 1e3 / timed(lambda: step("blendenpik", iters=40))[0]))
+        if comm is None:   # the Gram variant is one-GPU only (fab_compress: EINVAL with a communicator)
+            def gram():
+                ms, inf = timed(lambda: step("blendenpik_gram"))
+                modes["blendenpik_gram"] = 1e3 / ms
+                # the same LSQR iterates through the Gram matrix of V_{m+1} (one
+                # fp64 SYRK pass instead of L+1 streaming passes; DESIGN.md)
+                out["blendenpik_gram"] = {"solves_per_s": modes["blendenpik_gram"], "gram_used": inf["gram_used"],
+                                          "lsqr_iters": inf["lsqr_iters"], "gram_pass_ms": inf["ms_lsqr_pass"],
+                                          "compress_ms": inf["ms_compress"],
+                                          "gram_gflops": 2.0 * n_loc * (m + 1) ** 2 / 2 /
+                                          max(inf["ms_lsqr_pass"], 1e-9) / 1e6}
+            side("blendenpik_gram", gram)
 
-        def e2e_step():
-            sv.set_b(bh_np)
+        def api_order():
+            # API-order variant: sketch after the basis (batched SRHT pass)
+            step("blendenpik", fused=False)
+            inf = step("blendenpik", fused=False)
+            out["api_order_sketch_ms"] = inf["ms_sketch_batched"]
+        side("api_order", api_order)
+
+        def algs():
+            # the paper's basis comparison (Table 1, P:262-269; P:72, P:415-421)
+            # on the same operator: Alg 2 (the step above), Alg 1 (sketched GS,
+            # O(n m^2) bytes) and full Arnoldi (CGS2, three passes)
+            al = {"alg2_truncated_k%d" % k: avg("ms_basis")}
             sv.sketch(p.s, p.sketch_seed)
-            sv.basis(p.m, p.k)
-            sv.compress("blendenpik", tol=1e-6)
-            sv.apply(p.f, p.alpha, p.sigma, out=yh_np, host=True)
-
-        e2e_step()
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        t0 = time.perf_counter()
-        ne = max(2, min(args.steps, 3))
-        for _ in range(ne):
-            e2e_step()
-        torch.cuda.synchronize()
-        te = time.perf_counter() - t0
-        if dist:
-            t = torch.tensor([te], device=f"cuda:{dev}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            te = float(t.item())
-        out["e2e"] = {"value": ne / te, "unit": "solves/s", "h2d_bytes_per_step": 8 * n,
-                      "d2h_bytes_per_step": 8 * n}
-        ok = np.isfinite(yh_np).all()
-        out["e2e"]["output_finite"] = bool(ok)
+            sv.basis_sgs(p.m)
+            al["alg1_sketched_gs"] = sv.info()["ms_basis"]
+            sv.compress("lsqr", tol=1e-6)
+            sv.apply(p.f, p.alpha, p.sigma, out=y)
+            a3 = sv.info()
+            sv.basis_arnoldi(p.m)
+            al["arnoldi_cgs2"] = sv.info()["ms_basis"]
+            out["basis_ms_by_algorithm"] = al
+            out["alg3_solve_ms"] = a3["ms_basis"] + a3["ms_compress"] + a3["ms_apply"]
+            out["alg3_lsqr_iters"] = a3["lsqr_iters"]
+        side("basis_algorithms", algs)
 
     # ---- CPU oracle baseline (rank 0, N = 1 only) ---------------------------
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        log("[cpu_baseline] building the c3 CSR for the oracle ...")
-        A = p.scipy()
-        T, desc, parts = oracle_sample(p, A, int(round(out["lsqr_iters"])))
-        out["cpu_baseline"] = {"value": 1.0 / T, "unit": "solves/s", "cores": cpu_cores(),
-                               "kind": "oracle", "sample": desc,
-                               "krylov_iters_per_s": 1.0 / parts["t_iter"]}
-        try:   # the same sample on ONE core (BLAS threads limited)
-            from threadpoolctl import threadpool_limits
+        def cpu():
+            log("[cpu_baseline] building the c3 CSR for the oracle ...")
+            A = p.scipy()
+            T, desc, parts = oracle_sample(p, A, int(round(out["lsqr_iters"])))
+            out["cpu_baseline"] = {"value": 1.0 / T, "unit": "solves/s", "cores": cpu_cores(),
+                                   "kind": "oracle", "sample": desc,
+                                   "krylov_iters_per_s": 1.0 / parts["t_iter"]}
+            from threadpoolctl import threadpool_limits   # the same sample on ONE core (SURVEY §8d-6)
             with threadpool_limits(limits=1):
                 T1, desc1, parts1 = oracle_sample(p, A, int(round(out["lsqr_iters"])), small=True)
             out["cpu_baseline_1core"] = {"value": 1.0 / T1, "unit": "solves/s", "cores": 1, "kind": "oracle",
                                          "sample": desc1, "krylov_iters_per_s": 1.0 / parts1["t_iter"]}
-        except Exception as e:   # report, do not fail the bench line
-            out["cpu_baseline_1core"] = {"error": repr(e)}
+        side("cpu_baseline", cpu)
     sv.close()
+    del sv
+    torch.cuda.empty_cache()
+
+    # ---- the other large configs (BASELINE c4, c5; north star: "synthetic
+    # stencil and random-graph matrices"), Krylov it/s and solves/s per mode
+    if not args.no_configs:
+        out["configs"] = {}
+        for name in ("c4", "c5"):
+            side(name, lambda name=name: out["configs"].__setitem__(
+                name, other_config(name, world, rank, dev, comm, dist, args.config_reps)))
+    if errors:
+        out["side_errors"] = errors
     if comm is not None:
         comm.close()
     if rank == 0:

@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define FAB_ABI_VERSION 1
+#define FAB_ABI_VERSION 2   /* 2: fab_lsqr_opts.precond_*, fab_info.precond_*, loopback comms */
 
 /* ---- status codes ---------------------------------------------------- */
 enum {
@@ -151,6 +151,17 @@ typedef struct {
   int iters;               /* > 0: run exactly this many LSQR iterations (parity)   */
   int maxit;               /* tolerance mode cap; 0 => 4m               */
   double tol;              /* tolerance mode: MATLAB lsqr test (l.359); 0 => 1e-6    */
+  /* Blendenpik's preconditioner sketch (l.183: Blendenpik "computes a random
+     sketch of the basis using, once again, a SRHT"; reading G-12).  By
+     default it reuses fab_sketch's Theta (R = qr(Theta V_m)).  A different
+     precond_s and/or precond_seed draws Theta' = SRHT(precond_s, seed') and
+     takes R = qr(Theta' V_m): one extra batched pass over V_m (8 n m bytes);
+     a larger s' gives a better-conditioned V_m R^{-1}, so fewer LSQR passes
+     (8 n (m+2) bytes each).  Used by FAB_BLENDENPIK / FAB_BLENDENPIK_GRAM
+     only.  m_eff <= precond_s <= min(s_max, N), else EINVAL.            */
+  int precond_s;           /* 0 => s of fab_sketch                                   */
+  int precond_pad;
+  int64_t precond_seed;    /* < 0 => the seed of fab_sketch                          */
 } fab_lsqr_opts;
 
 typedef struct {
@@ -177,6 +188,9 @@ typedef struct {
   double whiten_cond;      /* cond_1(R_i) that triggered it                           */
   int gram_used;           /* FAB_BLENDENPIK_GRAM: 1 = Gram path, 0 = fell back to passes */
   int pad2;
+  int precond_s;           /* rows of the sketch R came from (s, or fab_lsqr_opts.precond_s) */
+  int precond_fresh;       /* 1 if R came from a separate Theta' (precond_s / precond_seed) */
+  double ms_precond_sketch;/* device time of the Theta' V_m pass (0 when Theta is reused)  */
 } fab_info;
 
 /* ---- multi-GPU (one process per GPU, NCCL over NVLink) ----
@@ -197,6 +211,21 @@ int fab_comm_unique_id(unsigned char id[128]);
 /* Communicator for rank `rank` of `nranks` on CUDA device `device` (collective
    over the ranks).  *comm is passed as fab_opts.comm.  Errors: EINVAL, ENCCL. */
 int fab_comm_init(void** comm, const unsigned char id[128], int rank, int nranks, int device);
+
+/* Loopback communicators (test tier T3'): the nranks ranks of
+   ONE row-partitioned solve, all on CUDA device `device`, driven by nranks
+   host threads of one process -- comms[r] is passed as fab_opts.comm by the
+   thread of rank r, which must use its own stream.  Every collective moves
+   the same data as over NCCL, stream-ordered: halo rows and all-gather
+   slices by device-to-device copies from the peer's buffer, allreduce by a
+   sum over the ranks' buffers in rank order 0..nranks-1 (every rank gets
+   bitwise the same result; NCCL's order may differ), synchronised by CUDA
+   events and a host barrier (no kernel waits on another rank, so the ranks
+   cannot deadlock on one GPU).  Collectives are host-synchronised, so calls
+   on a loopback rank are enqueued eagerly (no CUDA graph).  For testing the
+   partitioned path's data movement with one GPU; 1 <= nranks <= 8.  Each
+   comms[r] is released with fab_comm_destroy.  Errors: EINVAL, ENOMEM, ECUDA. */
+int fab_comm_init_loopback(void** comms, int nranks, int device);
 
 /* Destroy a communicator (after every context using it is destroyed). */
 int fab_comm_destroy(void* comm);

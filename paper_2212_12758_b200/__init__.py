@@ -157,8 +157,10 @@ class Solver:
         self.status["sketch"] = st
         return st
 
-    def compress(self, mode="blendenpik", iters=0, tol=0.0, maxit=0):
-        o = FabLsqrOpts(iters, maxit, tol)
+    def compress(self, mode="blendenpik", iters=0, tol=0.0, maxit=0, precond_s=0, precond_seed=-1):
+        """precond_s / precond_seed: Blendenpik's own preconditioner sketch
+        Theta' (reading G-12); defaults reuse the Theta of sketch()."""
+        o = FabLsqrOpts(iters, maxit, tol, precond_s, precond_seed)
         st = check(lib.fab_compress(self.ctx, MODES[mode], C.byref(o)), "fab_compress")
         self.status["compress"] = st
         return st

@@ -29,7 +29,7 @@ EXPORTS = ("fab_version", "fab_strerror", "fab_workspace_size", "fab_init", "fab
            "fab_basis_sgs", "fab_basis_arnoldi", "fab_basis_whiten",
            "fab_sketch", "fab_compress", "fab_apply", "fab_get", "fab_get_column", "fab_get_vrows",
            "fab_set", "fab_last_error", "fab_destroy", "fab_comm_unique_id", "fab_comm_init",
-           "fab_comm_destroy")
+           "fab_comm_init_loopback", "fab_comm_destroy")
 
 
 class FabOperator(C.Structure):
@@ -47,7 +47,11 @@ class FabOpts(C.Structure):
 
 
 class FabLsqrOpts(C.Structure):
-    _fields_ = [("iters", C.c_int), ("maxit", C.c_int), ("tol", C.c_double)]
+    _fields_ = [("iters", C.c_int), ("maxit", C.c_int), ("tol", C.c_double), ("precond_s", C.c_int),
+                ("precond_pad", C.c_int), ("precond_seed", C.c_int64)]
+
+    def __init__(self, iters=0, maxit=0, tol=0.0, precond_s=0, precond_seed=-1):
+        super().__init__(iters, maxit, tol, precond_s, 0, precond_seed)
 
 
 class FabInfo(C.Structure):
@@ -63,10 +67,11 @@ class FabInfo(C.Structure):
                 ("launches_apply", C.c_int64), ("ms_lsqr_pass", C.c_double),
                 ("lsqr_passes", C.c_int64), ("ms_sketch_batched", C.c_double),
                 ("whitened_at", C.c_int), ("pad1", C.c_int), ("whiten_cond", C.c_double),
-                ("gram_used", C.c_int), ("pad2", C.c_int)]
+                ("gram_used", C.c_int), ("pad2", C.c_int), ("precond_s", C.c_int),
+                ("precond_fresh", C.c_int), ("ms_precond_sketch", C.c_double)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad1"}
+        return {k: getattr(self, k) for k, _ in self._fields_ if k not in ("pad1", "pad2")}
 
 
 def load():
@@ -96,6 +101,7 @@ def load():
         "fab_destroy": (I, [P]),
         "fab_comm_unique_id": (I, [P]),
         "fab_comm_init": (I, [C.POINTER(P), P, I, I, I]),
+        "fab_comm_init_loopback": (I, [P, I, I]),
         "fab_comm_destroy": (I, [P]),
     }
     for name, (res, args) in sig.items():

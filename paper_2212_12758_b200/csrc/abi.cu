@@ -8,6 +8,8 @@
 
 #include "fab_internal.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <mutex>
 
 namespace fab {
@@ -26,6 +28,13 @@ cudaError_t ensure_dyn_smem(const void* fn, int want) {
   return e;
 }
 
+// NVTX range over one ABI call (visible in nsys / ncu --nvtx; header-only NVTX3,
+// a no-op when no tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 static thread_local char g_err[512] = "";
 
 void set_last_cuda_error(cudaError_t e, const char* what, const char* file, int line) {
@@ -34,7 +43,7 @@ void set_last_cuda_error(cudaError_t e, const char* what, const char* file, int 
 }
 
 struct Layout {
-  size_t V, vec, H, beta, coef, part_norm, part_sk, SV, rows, signs, part_g, part_tn, small, dense, qr, red, xg, sq, st;
+  size_t V, vec, H, beta, coef, part_norm, part_sk, SV, rows, signs, rows2, signs2, part_g, part_tn, small, dense, qr, red, xg, sq, st;
   size_t total;
 };
 
@@ -58,6 +67,8 @@ static Layout make_layout(const fab_ctx* c) {
   L.SV = carve(cur, (size_t)(c->s_max > 0 ? c->s_max : 1) * m1 * 8);
   L.rows = carve(cur, (size_t)(c->s_max > 0 ? c->s_max : 1) * 8);
   L.signs = carve(cur, (size_t)((c->N + 31) / 32) * 4);
+  L.rows2 = carve(cur, (size_t)(c->s_max > 0 ? c->s_max : 1) * 8);
+  L.signs2 = carve(cur, c->s_max > 0 ? (size_t)((c->N + 31) / 32) * 4 : 8);
   L.part_g = carve(cur, (size_t)c->grid_lsqr * c->m_max * 8);
   L.part_tn = carve(cur, (size_t)c->grid_lsqr * 8);
   L.small = carve(cur, (size_t)kSmallVecs * kSmall * 8);
@@ -163,6 +174,8 @@ static void assign_buffers(fab_ctx* c) {
   c->SV = reinterpret_cast<double*>(w + L.SV);
   c->rows_d = reinterpret_cast<int64_t*>(w + L.rows);
   c->signs_d = reinterpret_cast<uint32_t*>(w + L.signs);
+  c->rows2_d = reinterpret_cast<int64_t*>(w + L.rows2);
+  c->signs2_d = reinterpret_cast<uint32_t*>(w + L.signs2);
   c->part_g = reinterpret_cast<double*>(w + L.part_g);
   c->part_tn = reinterpret_cast<double*>(w + L.part_tn);
   c->small = reinterpret_cast<double*>(w + L.small);
@@ -252,6 +265,7 @@ int fab_workspace_size(const fab_operator* A, const fab_opts* o, size_t* bytes) 
 }
 
 int fab_init(fab_ctx** out, const fab_operator* A, const double* b, const fab_opts* o) {
+  NvtxRange nvtx__("fab_init");
   if (!out || !b) return FAB_EINVAL;
   *out = nullptr;
   int rc = validate_operator(A);
@@ -376,6 +390,7 @@ static int basis_finish(fab_ctx* c, int m, int k, double ms) {
 }  // namespace fab
 
 int fab_basis(fab_ctx* c, int m, int k) {
+  NvtxRange nvtx__("fab_basis");
   if (!c) return FAB_EINVAL;
   if (k < 1 || k > c->k_max || m < 1 || m > c->m_max || m >= c->n_global) return FAB_EINVAL;
   if (c->sketch_ready && c->s < m + 1) return FAB_EINVAL;
@@ -388,6 +403,7 @@ int fab_basis(fab_ctx* c, int m, int k) {
 }
 
 int fab_basis_batch(fab_ctx** cs, int p, int m, int k) {
+  NvtxRange nvtx__("fab_basis_batch");
   if (!cs || p < 1 || p > kBatchMaxCtx) return FAB_EINVAL;
   fab_ctx* c = cs[0];
   for (int i = 0; i < p; ++i) {
@@ -430,6 +446,7 @@ int fab_basis_batch(fab_ctx** cs, int p, int m, int k) {
 }
 
 int fab_basis_arnoldi(fab_ctx* c, int m) {
+  NvtxRange nvtx__("fab_basis_arnoldi");
   if (!c) return FAB_EINVAL;
   if (m < 1 || m > c->m_max || m >= c->n_global) return FAB_EINVAL;
   FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
@@ -461,6 +478,7 @@ int fab_basis_arnoldi(fab_ctx* c, int m) {
 }
 
 int fab_basis_whiten(fab_ctx* c, int m, int k, double cond_max) {
+  NvtxRange nvtx__("fab_basis_whiten");
   if (!c) return FAB_EINVAL;
   if (!c->sketch_ready) return FAB_EORDER;   // the monitor and Algorithm 1 need Theta
   if (k < 1 || k > c->k_max || m < 1 || m > c->m_max || m >= c->n_global || c->s < m + 1) return FAB_EINVAL;
@@ -498,6 +516,7 @@ int fab_basis_whiten(fab_ctx* c, int m, int k, double cond_max) {
 }
 
 int fab_basis_sgs(fab_ctx* c, int m) {
+  NvtxRange nvtx__("fab_basis_sgs");
   if (!c) return FAB_EINVAL;
   if (!c->sketch_ready) return FAB_EORDER;   // Algorithm 1 sketches every new vector
   if (m < 1 || m > c->m_max || m >= c->n_global || c->s < m + 1) return FAB_EINVAL;
@@ -530,6 +549,7 @@ int fab_basis_sgs(fab_ctx* c, int m) {
 }
 
 int fab_sketch(fab_ctx* c, int s, uint64_t seed) {
+  NvtxRange nvtx__("fab_sketch");
   if (!c) return FAB_EINVAL;
   if (s < 1 || s > c->s_max || (int64_t)s > c->N) return FAB_EINVAL;
   if (c->basis_ready && s < (c->breakdown ? c->m_eff : c->m + 1)) return FAB_EINVAL;
@@ -553,6 +573,7 @@ int fab_sketch(fab_ctx* c, int s, uint64_t seed) {
 }
 
 int fab_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o) {
+  NvtxRange nvtx__("fab_compress");
   if (!c) return FAB_EINVAL;
   if (mode != FAB_BLENDENPIK && mode != FAB_SKETCH_SOLVE && mode != FAB_NONE && mode != FAB_LSQR &&
       mode != FAB_BLENDENPIK_GRAM)
@@ -561,7 +582,10 @@ int fab_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o) {
   if (mode == FAB_BLENDENPIK_GRAM && c->comm) return FAB_EINVAL;   // one GPU only
   const bool needs_sketch = (mode == FAB_BLENDENPIK || mode == FAB_SKETCH_SOLVE || mode == FAB_BLENDENPIK_GRAM);
   if (needs_sketch && !c->sketch_ready) return FAB_EORDER;
-  if (o && (o->iters < 0 || o->maxit < 0 || o->tol < 0)) return FAB_EINVAL;
+  if (o && (o->iters < 0 || o->maxit < 0 || o->tol < 0 || o->precond_s < 0)) return FAB_EINVAL;
+  if (o && o->precond_s > 0 &&
+      (o->precond_s < c->m_eff || o->precond_s > c->s_max || (int64_t)o->precond_s > c->N))
+    return FAB_EINVAL;
   int rc;
   const int64_t l0 = c->nlaunch;
   if (needs_sketch && !c->sketch_in_V) {
@@ -591,6 +615,7 @@ int fab_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o) {
 }
 
 int fab_apply(fab_ctx* c, int f, double alpha, double sigma, double* y, int y_location) {
+  NvtxRange nvtx__("fab_apply");
   if (!c || !y) return FAB_EINVAL;
   if (f < FAB_EXP || f > FAB_SIGN) return FAB_EINVAL;
   if (f == FAB_SIGN) {   // (A^2)^{-1/2} (A b) (l.406): invsqrt on the squared operator's compression
@@ -756,6 +781,7 @@ int fab_set(fab_ctx* c, int what, const void* src, size_t bytes) {
 }
 
 int fab_destroy(fab_ctx* c) {
+  NvtxRange nvtx__("fab_destroy");
   if (!c) return FAB_EINVAL;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);

@@ -83,48 +83,55 @@ __global__ void k_arn_norm(int c, const double* red, double* beta, double* H, in
   }
 }
 
+static int enqueue_arnoldi_all(fab_ctx* c, int m, cudaStream_t st, int64_t* launches) {
+  double* pvec = svec(c, 22);
+  double* h1 = svec(c, 21);
+  double* red = c->red;
+  int G = 0;
+  k_arn_reset<<<1, 1, 0, st>>>(c->st_d, m);
+  ++*launches;
+  FAB_CUDA(cudaMemsetAsync(c->H, 0, (size_t)c->ldH * m * sizeof(double), st));
+  FAB_CUDA(cudaMemsetAsync(pvec, 0, sizeof(double) * kSmall, st));
+  // pass 0 over [b]: ||b||^2 (t = b into the scratch vector)
+  FAB_TRY(launch_tall_gemv(c, 1, pvec, 0.0, 1, c->V, c->vec, st, &G));
+  FAB_TRY(launch_pass_reduce(c, G, 1, red, st));
+  k_arn_first<<<1, kThreads, 0, st>>>(red, c->m_max, c->beta, c->st_d);
+  *launches += 3;
+  for (int col = 1; col <= m; ++col) {
+    double* w = c->V + (int64_t)col * c->ld;
+    int nparts = 0;
+    FAB_TRY(enqueue_k1(c, col, 1, w, true, st, launches, &nparts));
+    for (int phase = 1; phase <= 3; ++phase) {
+      if (phase == 1) FAB_CUDA(cudaMemsetAsync(pvec, 0, sizeof(double) * col, st));   // pass 1: t = w / beta_{c-1}
+      FAB_TRY(launch_tall_gemv(c, col, pvec, 0.0, 1, w, w, st, &G));
+      FAB_TRY(launch_pass_reduce(c, G, col, red, st));
+      *launches += 2;
+      if (phase < 3)
+        k_arn_coef<<<1, kThreads, 0, st>>>(col, phase, red, c->beta, c->H, c->ldH, pvec, h1, c->st_d);
+      else
+        k_arn_norm<<<1, 32, 0, st>>>(col, red, c->beta, c->H, c->ldH, col == m ? 1 : 0, c->st_d);
+      ++*launches;
+    }
+  }
+  return FAB_OK;
+}
+
 int run_basis_arnoldi(fab_ctx* c, int m) {
+  if (!comm_graphable(c)) {   // loopback ranks: eager
+    int64_t launches = 0;
+    FAB_TRY(enqueue_arnoldi_all(c, m, c->stream, &launches));
+    c->info.launches_basis = launches;
+    return FAB_OK;
+  }
   if (!(c->gexec_arn && c->g_arn_m == m)) {
     if (c->gexec_arn) {
       cudaGraphExecDestroy(c->gexec_arn);
       c->gexec_arn = nullptr;
     }
-    double* pvec = svec(c, 22);
-    double* h1 = svec(c, 21);
-    double* red = c->red;
     int64_t launches = 0;
     cudaStream_t st = c->cap;
     FAB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    int rc = FAB_OK;
-    int G = 0;
-    k_arn_reset<<<1, 1, 0, st>>>(c->st_d, m);
-    ++launches;
-    cudaMemsetAsync(c->H, 0, (size_t)c->ldH * m * sizeof(double), st);
-    cudaMemsetAsync(pvec, 0, sizeof(double) * kSmall, st);
-    // pass 0 over [b]: ||b||^2 (t = b into the scratch vector)
-    rc = launch_tall_gemv(c, 1, pvec, 0.0, 1, c->V, c->vec, st, &G);
-    if (rc == FAB_OK) rc = launch_pass_reduce(c, G, 1, red, st);
-    if (rc == FAB_OK) {
-      k_arn_first<<<1, kThreads, 0, st>>>(red, c->m_max, c->beta, c->st_d);
-      launches += 3;
-    }
-    for (int col = 1; col <= m && rc == FAB_OK; ++col) {
-      double* w = c->V + (int64_t)col * c->ld;
-      int nparts = 0;
-      rc = enqueue_k1(c, col, 1, w, true, st, &launches, &nparts);
-      for (int phase = 1; phase <= 3 && rc == FAB_OK; ++phase) {
-        if (phase == 1) cudaMemsetAsync(pvec, 0, sizeof(double) * col, st);   // pass 1: t = w / beta_{c-1}
-        rc = launch_tall_gemv(c, col, pvec, 0.0, 1, w, w, st, &G);
-        if (rc == FAB_OK) rc = launch_pass_reduce(c, G, col, red, st);
-        launches += 2;
-        if (rc != FAB_OK) break;
-        if (phase < 3)
-          k_arn_coef<<<1, kThreads, 0, st>>>(col, phase, red, c->beta, c->H, c->ldH, pvec, h1, c->st_d);
-        else
-          k_arn_norm<<<1, 32, 0, st>>>(col, red, c->beta, c->H, c->ldH, col == m ? 1 : 0, c->st_d);
-        ++launches;
-      }
-    }
+    int rc = enqueue_arnoldi_all(c, m, st, &launches);
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(st, &graph);
     if (rc != FAB_OK) {

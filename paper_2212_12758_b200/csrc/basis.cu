@@ -1342,8 +1342,31 @@ int enqueue_basis_prologue(fab_ctx* c, int m, bool fused, cudaStream_t st, int64
   return FAB_OK;
 }
 
+// Every launch of an Algorithm 2 basis (prologue, m steps, final scalars,
+// sketch reduction) on stream st.
+static int enqueue_basis_all(fab_ctx* c, int m, int k, bool fused, cudaStream_t st, int64_t* launches) {
+  // (a single cooperative kernel for all m steps, two grid barriers per
+  // step, was measured slower at every size: c1 25 vs 11 us, c2 32 vs 16 us
+  // per step -- the per-step graph of K1 and K3 stays)
+  FAB_TRY(enqueue_basis_prologue(c, m, fused, st, launches));
+  for (int col = 1; col <= m; ++col) FAB_TRY(enqueue_step(c, col, k, fused, st, launches));
+  // final lagged norm: beta_m = h_{m+1,m}; breakdown test of the last step
+  FAB_TRY(enqueue_scalar(c, m + 1, 0, 0, 1, st, launches));
+  if (fused) {
+    FAB_TRY(sketch_finalize(c, m + 1, st));
+    ++*launches;
+  }
+  return FAB_OK;
+}
+
 int run_basis(fab_ctx* c, int m, int k) {
   const bool fused = c->sketch_ready;
+  if (!comm_graphable(c)) {   // loopback ranks: host-synchronised collectives, no capture
+    int64_t launches = 0;
+    FAB_TRY(enqueue_basis_all(c, m, k, fused, c->stream, &launches));
+    c->info.launches_basis = launches;
+    return FAB_OK;
+  }
   if (!(c->gexec && c->g_m == m && c->g_k == k && c->g_fused == fused && (!fused || c->g_s == c->s))) {
     if (c->gexec) {
       cudaGraphExecDestroy(c->gexec);
@@ -1351,19 +1374,7 @@ int run_basis(fab_ctx* c, int m, int k) {
     }
     int64_t launches = 0;
     FAB_CUDA(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
-    // (a single cooperative kernel for all m steps, two grid barriers per
-    // step, was measured slower at every size: c1 25 vs 11 us, c2 32 vs 16 us
-    // per step -- the per-step graph of K1 and K3 stays)
-    int rc = enqueue_basis_prologue(c, m, fused, c->cap, &launches);
-    for (int col = 1; col <= m && rc == FAB_OK; ++col) rc = enqueue_step(c, col, k, fused, c->cap, &launches);
-    if (rc == FAB_OK) {
-      // final lagged norm: beta_m = h_{m+1,m}; breakdown test of the last step
-      rc = enqueue_scalar(c, m + 1, 0, 0, 1, c->cap, &launches);
-      if (rc == FAB_OK && fused) {
-        rc = sketch_finalize(c, m + 1, c->cap);
-        ++launches;
-      }
-    }
+    int rc = enqueue_basis_all(c, m, k, fused, c->cap, &launches);
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(c->cap, &graph);
     if (rc != FAB_OK) {

@@ -17,8 +17,26 @@
 // NCCL is loaded at run time (dlopen of libnccl.so.2, normally the copy the
 // torch process already mapped), so libfab.so loads and runs on one GPU, and
 // its CPU-side tests run, without NCCL.
+//
+// Loopback communicator (SURVEY §4 tier T3'): P ranks of the
+// SAME row-partitioned path as P host threads on ONE GPU, each rank with its
+// own context, workspace and stream.  Its collectives move the same data as
+// the NCCL ones, stream-ordered: a rank publishes its buffer pointer and
+// records an event, the P host threads meet at a barrier, each stream waits
+// on its peers' events and then copies (halo, all-gather: cudaMemcpyAsync
+// from the peer's buffer) or sums (allreduce: one kernel per rank adding the
+// P buffers in rank order 0..P-1, so every rank holds bitwise the same sum),
+// and a second event + barrier keeps a buffer alive until every peer has
+// read it.  No kernel ever waits on another rank's kernel (waits are stream
+// dependencies on events already recorded), so the ranks cannot deadlock
+// on one GPU.  Host-synchronised collectives cannot be captured in a CUDA
+// graph: under a loopback communicator every fab_* call enqueues eagerly.
 #include <dlfcn.h>
 #include <nccl.h>
+
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
 
 #include "fab_internal.cuh"
 
@@ -36,10 +54,119 @@ struct NcclApi {
   const char* (*errorString)(ncclResult_t);
 };
 
+// one virtual partition of P loopback ranks
+struct LoopGroup {
+  int P = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  int refs = 0;
+  std::vector<const void*> ptr;          // published buffer of each rank
+  std::vector<cudaEvent_t> ev_ready;     // buffer ready (recorded after its producer)
+  std::vector<cudaEvent_t> ev_done;      // this rank finished reading its peers' buffers
+
+  bool broken = false;                   // a rank timed out at a barrier: every later collective fails
+
+  // false if a peer never arrived (it returned an error before this
+  // collective): the group is then broken and every rank's call fails
+  // with FAB_ENCCL instead of hanging
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (broken) return false;
+    const uint64_t g = gen;
+    if (++arrived == P) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return true;
+    }
+    if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g || broken; }) || broken) {
+      broken = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
+  }
+};
+
 struct Comm {
   ncclComm_t nc = nullptr;
   int rank = 0, nranks = 1, device = 0;
+  LoopGroup* loop = nullptr;            // loopback rank (no NCCL)
+  void* scratch = nullptr;              // loopback allreduce result before the copy back
+  size_t scratch_bytes = 0;
 };
+
+bool comm_graphable(const fab_ctx* c) { return !(c->comm && c->comm->loop); }
+
+// out[i] = in_0[i] (+|max) in_1[i] ... in_{P-1}[i], ranks in order
+template <typename T>
+__global__ void k_loop_reduce(const T* const* __restrict__ ptrs, int P, size_t count, int use_max, T* out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    T a = ptrs[0][i];
+    for (int q = 1; q < P; ++q) {
+      const T v = ptrs[q][i];
+      a = use_max ? (v > a ? v : a) : a + v;
+    }
+    out[i] = a;
+  }
+}
+
+static int loop_publish(fab_ctx* c, const void* p, cudaStream_t st) {
+  LoopGroup* g = c->comm->loop;
+  const int r = c->comm->rank;
+  g->ptr[r] = p;
+  FAB_CUDA(cudaEventRecord(g->ev_ready[r], st));
+  return g->barrier() ? FAB_OK : FAB_ENCCL;
+}
+
+static int loop_wait(fab_ctx* c, const std::vector<cudaEvent_t>& evs, int q, cudaStream_t st) {
+  FAB_CUDA(cudaStreamWaitEvent(st, evs[q], 0));
+  return FAB_OK;
+}
+
+// every rank has finished reading the published buffers
+static int loop_release(fab_ctx* c, cudaStream_t st) {
+  LoopGroup* g = c->comm->loop;
+  const int r = c->comm->rank;
+  FAB_CUDA(cudaEventRecord(g->ev_done[r], st));
+  if (!g->barrier()) return FAB_ENCCL;
+  for (int q = 0; q < g->P; ++q)
+    if (q != r) FAB_TRY(loop_wait(c, g->ev_done, q, st));
+  return FAB_OK;
+}
+
+template <typename T>
+static int loop_allreduce(fab_ctx* c, T* buf, size_t count, bool use_max, cudaStream_t st) {
+  Comm* cm = c->comm;
+  LoopGroup* g = cm->loop;
+  const size_t bytes = count * sizeof(T) + 8 * sizeof(void*);
+  if (cm->scratch_bytes < bytes) {
+    // grows once to the largest collective (the s x (m+1) sketch partials);
+    // a loopback rank runs eagerly, never inside a graph capture
+    if (cm->scratch) cudaFree(cm->scratch);
+    cm->scratch = nullptr;
+    cm->scratch_bytes = 0;
+    FAB_CUDA(cudaMalloc(&cm->scratch, bytes));
+    cm->scratch_bytes = bytes;
+  }
+  FAB_TRY(loop_publish(c, buf, st));
+  for (int q = 0; q < g->P; ++q)
+    if (q != cm->rank) FAB_TRY(loop_wait(c, g->ev_ready, q, st));
+  const T** dptrs = reinterpret_cast<const T**>(cm->scratch);
+  T* out = reinterpret_cast<T*>(reinterpret_cast<char*>(cm->scratch) + 8 * sizeof(void*));
+  std::vector<const void*> hp(g->ptr.begin(), g->ptr.end());
+  FAB_CUDA(cudaMemcpyAsync(dptrs, hp.data(), g->P * sizeof(void*), cudaMemcpyHostToDevice, st));
+  const int grid = (int)((count + 255) / 256 < 1024 ? (count + 255) / 256 : 1024);
+  k_loop_reduce<T><<<grid > 0 ? grid : 1, 256, 0, st>>>(dptrs, g->P, count, use_max ? 1 : 0, out);
+  FAB_CHECK_LAUNCH();
+  FAB_TRY(loop_release(c, st));
+  FAB_CUDA(cudaMemcpyAsync(buf, out, count * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  // the host pointer array must outlive the copy: synchronous enough here
+  // (hp is consumed by the H2D copy above, which is pageable -> staged at call)
+  return FAB_OK;
+}
 
 static NcclApi* nccl_api() {
   static NcclApi api;
@@ -94,6 +221,7 @@ int comm_size(const fab_ctx* c) { return c->comm ? c->comm->nranks : 1; }
 
 int comm_allreduce(fab_ctx* c, double* buf, size_t count, bool use_max, cudaStream_t st) {
   if (!c->comm) return FAB_OK;   // one GPU: nothing to reduce (1-rank comms still call NCCL)
+  if (c->comm->loop) return loop_allreduce<double>(c, buf, count, use_max, st);
   NcclApi* api = nccl_api();
   if (!api) return FAB_ENCCL;
   FAB_NCCL(api->allReduce(buf, buf, count, ncclFloat64, use_max ? ncclMax : ncclSum, c->comm->nc, st));
@@ -102,6 +230,7 @@ int comm_allreduce(fab_ctx* c, double* buf, size_t count, bool use_max, cudaStre
 
 // raw allreduce of int64 (used once at init to gather the row ranges)
 static int allreduce_i64(fab_ctx* c, int64_t* buf, size_t count, cudaStream_t st) {
+  if (c->comm->loop) return loop_allreduce<int64_t>(c, buf, count, false, st);
   NcclApi* api = nccl_api();
   if (!api) return FAB_ENCCL;
   FAB_NCCL(api->allReduce(buf, buf, count, ncclInt64, ncclSum, c->comm->nc, st));
@@ -112,10 +241,25 @@ static int allreduce_i64(fab_ctx* c, int64_t* buf, size_t count, cudaStream_t st
 // x points at local row 0 of a V column (halo slots are in its padding)
 int comm_halo(fab_ctx* c, double* x, cudaStream_t st) {
   if (!c->comm || c->comm->nranks == 1 || c->hal == 0) return FAB_OK;
-  NcclApi* api = nccl_api();
-  if (!api) return FAB_ENCCL;
   const int r = c->comm->rank, P = c->comm->nranks;
   const size_t h = (size_t)c->hal;
+  if (c->comm->loop) {
+    LoopGroup* g = c->comm->loop;
+    FAB_TRY(loop_publish(c, x, st));
+    if (r > 0) {   // the last h rows of rank r-1
+      FAB_TRY(loop_wait(c, g->ev_ready, r - 1, st));
+      const int64_t nprev = c->rank_rows[r] - c->rank_rows[r - 1];
+      const double* src = static_cast<const double*>(g->ptr[r - 1]) + nprev - (int64_t)h;
+      FAB_CUDA(cudaMemcpyAsync(x - h, src, h * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+    if (r + 1 < P) {   // the first h rows of rank r+1
+      FAB_TRY(loop_wait(c, g->ev_ready, r + 1, st));
+      FAB_CUDA(cudaMemcpyAsync(x + c->n, g->ptr[r + 1], h * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+    return loop_release(c, st);
+  }
+  NcclApi* api = nccl_api();
+  if (!api) return FAB_ENCCL;
   FAB_NCCL(api->groupStart());
   if (r > 0) {
     FAB_NCCL(api->send(x, h, ncclFloat64, r - 1, c->comm->nc, st));
@@ -134,9 +278,21 @@ int comm_gather_x(fab_ctx* c, const double* x, cudaStream_t st) {
   if (!c->comm) return FAB_OK;
   FAB_CUDA(cudaMemcpyAsync(c->xg + c->row_begin, x, (size_t)c->n * sizeof(double), cudaMemcpyDeviceToDevice, st));
   if (c->comm->nranks == 1) return FAB_OK;
+  const int r = c->comm->rank, P = c->comm->nranks;
+  if (c->comm->loop) {
+    LoopGroup* g = c->comm->loop;
+    FAB_TRY(loop_publish(c, x, st));
+    for (int q = 0; q < P; ++q) {
+      if (q == r) continue;
+      FAB_TRY(loop_wait(c, g->ev_ready, q, st));
+      const int64_t b0 = c->rank_rows[q], b1 = c->rank_rows[q + 1];
+      FAB_CUDA(cudaMemcpyAsync(c->xg + b0, g->ptr[q], (size_t)(b1 - b0) * sizeof(double), cudaMemcpyDeviceToDevice,
+                               st));
+    }
+    return loop_release(c, st);
+  }
   NcclApi* api = nccl_api();
   if (!api) return FAB_ENCCL;
-  const int r = c->comm->rank, P = c->comm->nranks;
   FAB_NCCL(api->groupStart());
   for (int d = 1; d < P; ++d) {
     const int to = (r + d) % P, from = (r - d + P) % P;
@@ -223,9 +379,56 @@ int fab_comm_init(void** comm, const unsigned char id[128], int rank, int nranks
   return FAB_OK;
 }
 
+int fab_comm_init_loopback(void** comms, int nranks, int device) {
+  if (!comms || nranks < 1 || nranks > 8) return FAB_EINVAL;
+  for (int r = 0; r < nranks; ++r) comms[r] = nullptr;
+  FAB_CUDA(cudaSetDevice(device));
+  LoopGroup* g = new (std::nothrow) LoopGroup();
+  if (!g) return FAB_ENOMEM;
+  g->P = nranks;
+  g->refs = nranks;
+  g->ptr.assign(nranks, nullptr);
+  g->ev_ready.assign(nranks, nullptr);
+  g->ev_done.assign(nranks, nullptr);
+  for (int r = 0; r < nranks; ++r) {
+    if (cudaEventCreateWithFlags(&g->ev_ready[r], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->ev_done[r], cudaEventDisableTiming) != cudaSuccess) {
+      for (cudaEvent_t e : g->ev_ready) if (e) cudaEventDestroy(e);
+      for (cudaEvent_t e : g->ev_done) if (e) cudaEventDestroy(e);
+      delete g;
+      return FAB_ECUDA;
+    }
+  }
+  for (int r = 0; r < nranks; ++r) {
+    Comm* cm = new Comm();
+    cm->rank = r;
+    cm->nranks = nranks;
+    cm->device = device;
+    cm->loop = g;
+    comms[r] = cm;
+  }
+  return FAB_OK;
+}
+
 int fab_comm_destroy(void* comm) {
   if (!comm) return FAB_EINVAL;
   Comm* cm = static_cast<Comm*>(comm);
+  if (cm->loop) {
+    LoopGroup* g = cm->loop;
+    if (cm->scratch) cudaFree(cm->scratch);
+    bool last;
+    {
+      std::lock_guard<std::mutex> lk(g->mu);
+      last = --g->refs == 0;
+    }
+    if (last) {
+      for (cudaEvent_t e : g->ev_ready) cudaEventDestroy(e);
+      for (cudaEvent_t e : g->ev_done) cudaEventDestroy(e);
+      delete g;
+    }
+    delete cm;
+    return FAB_OK;
+  }
   NcclApi* api = nccl_api();
   if (api && cm->nc) api->commDestroy(cm->nc);
   delete cm;

@@ -91,8 +91,9 @@ __global__ void k_qr_extract(const double* A, int rows, int m, const double* dia
     const int r = (int)(i % m), col = (int)(i / m);
     R[i] = (r < col) ? A[r + (int64_t)col * rows] : (r == col ? diag[r] : 0.0);
   }
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
-    qtb[i] = A[i + (int64_t)m * rows];
+  if (qtb)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+      qtb[i] = A[i + (int64_t)m * rows];
 }
 
 static int coop_grid(fab_ctx* c, const void* fn, int want) {
@@ -107,20 +108,27 @@ static int coop_grid(fab_ctx* c, const void* fn, int want) {
 
 double* qr_work(fab_ctx* c);   // abi.cu
 
-int dense_qr_sketch(fab_ctx* c, int m, double* R, double* qtb, cudaStream_t st) {
-  const int s = c->s;
-  if (s > 32 * kQrNQ) return FAB_EINVAL;
+// QR of the rows x ntot matrix already in the QR work area (lda = rows):
+// R of its first m columns; qtb = Q^T column m when ntot > m (else NULL).
+int dense_qr_work(fab_ctx* c, int m, int rows, int ntot, double* R, double* qtb, cudaStream_t st) {
+  if (rows > 32 * kQrNQ) return FAB_EINVAL;
   double* A = qr_work(c);
   double* diag = svec(c, 10);
-  FAB_CUDA(cudaMemcpyAsync(A, c->SV, (size_t)s * (m + 1) * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  int rows = s, nf = m, ntot = m + 1;
+  int nf = m;
   void* args[] = {&A, &rows, &nf, &ntot, &diag};
   const int grid = coop_grid(c, (const void*)k_qr_coop, (ntot + kWarps - 1) / kWarps);
   FAB_CUDA(cudaLaunchCooperativeKernel((const void*)k_qr_coop, grid, kThreads, args, 0, st));
   ++c->nlaunch;
-  k_qr_extract<<<(m * m + kThreads - 1) / kThreads, kThreads, 0, st>>>(A, s, m, diag, R, qtb);
+  k_qr_extract<<<(m * m + kThreads - 1) / kThreads, kThreads, 0, st>>>(A, rows, m, diag, R, ntot > m ? qtb : nullptr);
   FAB_CHECK_LAUNCH();
   return FAB_OK;
+}
+
+int dense_qr_sketch(fab_ctx* c, int m, double* R, double* qtb, cudaStream_t st) {
+  const int s = c->s;
+  if (s > 32 * kQrNQ) return FAB_EINVAL;
+  FAB_CUDA(cudaMemcpyAsync(qr_work(c), c->SV, (size_t)s * (m + 1) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  return dense_qr_work(c, m, s, m + 1, R, qtb, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -129,17 +137,18 @@ int dense_qr_sketch(fab_ctx* c, int m, double* R, double* qtb, cudaStream_t st) 
 // ---------------------------------------------------------------------------
 // Column l of R (and its diagonal) is loaded one step ahead, so a step waits
 // on shared memory and barriers only, not on an L2 round trip (m <= 1024:
-// 8 rows per thread at 128 threads).  Same operations in the same order.
-__global__ void k_tri_inverse(const double* R, int m, double* Rinv) {
+// 8 rows per thread at kTriThreads = 128).  Same operations in the same order.
+constexpr int kTriThreads = 128;
+__global__ void __launch_bounds__(kTriThreads) k_tri_inverse(const double* R, int m, double* Rinv) {
   extern __shared__ double b[];
-  constexpr int kPer = (kMaxM + 127) / 128;
+  constexpr int kPer = (kMaxM + kTriThreads - 1) / kTriThreads;
   const int j = blockIdx.x;
-  for (int i = threadIdx.x; i < m; i += blockDim.x) b[i] = (i == j) ? 1.0 : 0.0;
+  for (int i = threadIdx.x; i < m; i += kTriThreads) b[i] = (i == j) ? 1.0 : 0.0;
   double rc[kPer], rn[kPer], dg, dn = 0.0;
   auto load_col = [&](int l, double (&r)[kPer], double& d) {
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
-      const int i = threadIdx.x + 128 * u;
+      const int i = threadIdx.x + kTriThreads * u;
       r[u] = (l >= 0 && i < l) ? R[i + (int64_t)l * m] : 0.0;
     }
     d = l >= 0 ? R[l + (int64_t)l * m] : 1.0;
@@ -153,7 +162,7 @@ __global__ void k_tri_inverse(const double* R, int m, double* Rinv) {
     if (threadIdx.x == 0) b[l] = xl;
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
-      const int i = threadIdx.x + 128 * u;
+      const int i = threadIdx.x + kTriThreads * u;
       if (i < l) b[i] = fma(-rc[u], xl, b[i]);
     }
     __syncthreads();
@@ -161,11 +170,11 @@ __global__ void k_tri_inverse(const double* R, int m, double* Rinv) {
     for (int u = 0; u < kPer; ++u) rc[u] = rn[u];
     dg = dn;
   }
-  for (int i = threadIdx.x; i < m; i += blockDim.x) Rinv[i + (int64_t)j * m] = (i <= j) ? b[i] : 0.0;
+  for (int i = threadIdx.x; i < m; i += kTriThreads) Rinv[i + (int64_t)j * m] = (i <= j) ? b[i] : 0.0;
 }
 
 int dense_tri_inverse(fab_ctx* c, const double* R, int m, double* Rinv, cudaStream_t st) {
-  k_tri_inverse<<<m, 128, m * sizeof(double), st>>>(R, m, Rinv);
+  k_tri_inverse<<<m, kTriThreads, m * sizeof(double), st>>>(R, m, Rinv);
   FAB_CHECK_LAUNCH();
   return FAB_OK;
 }

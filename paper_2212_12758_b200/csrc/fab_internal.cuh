@@ -103,6 +103,10 @@ struct fab_ctx {
   double* SV = nullptr;          // s_max x (m_max+1)
   int64_t* rows_d = nullptr;     // s_max
   uint32_t* signs_d = nullptr;   // N/32 words
+  uint32_t* signs2_d = nullptr;  // N/32 words: Blendenpik's own Theta' (precond_s / precond_seed)
+  int64_t* rows2_d = nullptr;    // s_max
+  int pre_s = 0;                 // Theta' currently drawn in signs2_d / rows2_d (0: none)
+  uint64_t pre_seed = 0;
   double* part_g = nullptr;      // grid_lsqr * (m_max+1)
   double* part_tn = nullptr;     // grid_lsqr
   double* small = nullptr;       // small vectors (LSQR, dense)
@@ -348,6 +352,7 @@ int comm_allreduce(fab_ctx* c, double* buf, size_t count, bool use_max, cudaStre
 int comm_halo(fab_ctx* c, double* x, cudaStream_t st);
 int comm_gather_x(fab_ctx* c, const double* x, cudaStream_t st);
 int comm_setup_partition(fab_ctx* c);
+bool comm_graphable(const fab_ctx* c);       // false for a loopback rank: enqueue eagerly
 const char* nccl_last_error();
 // basis.cu
 int basis_setup_grids(fab_ctx* c);
@@ -380,12 +385,17 @@ void host_sketch_rows(uint64_t seed, int64_t N, int s, int64_t* out);
 int sketch_draw(fab_ctx* c, int s, uint64_t seed);
 int sketch_batched(fab_ctx* c);              // K5: Theta V_{m+1} after the basis
 int sketch_finalize(fab_ctx* c, int ncols, cudaStream_t st);
+// Blendenpik's own sketch Theta' (s2 rows, seed2; fab_lsqr_opts.precond_*):
+// Theta' V_m -> dst (s2 x m, the QR work area), one batched pass over V_m
+int sketch_precond(fab_ctx* c, int s2, uint64_t seed2, int m, double* dst, cudaStream_t st);
 // lsqr.cu / compress
 int lsqr_setup(fab_ctx* c);
 int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn);
 // dense.cu
 int dense_fe1(fab_ctx* c, int f, double alpha, double sigma, double* c_out, int* iters);
 int dense_qr_sketch(fab_ctx* c, int m, double* R, double* qtb, cudaStream_t st);
+int dense_qr_work(fab_ctx* c, int m, int rows, int ntot, double* R, double* qtb, cudaStream_t st);
+double* qr_work(fab_ctx* c);                 // abi.cu: s_max x (m_max+1) QR work area
 int dense_tri_inverse(fab_ctx* c, const double* R, int m, double* Rinv, cudaStream_t st);
 // apply.cu
 int run_combine(fab_ctx* c, const double* coef_d, double* y_dev);

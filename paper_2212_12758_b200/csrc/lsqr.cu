@@ -783,6 +783,9 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
   c->info.lsqr_passes = 0;
   c->info.gram_used = 0;
   c->info.ms_lsqr_pass = 0.0;
+  c->info.precond_s = 0;
+  c->info.precond_fresh = 0;
+  c->info.ms_precond_sketch = 0.0;
   int64_t launches = 0;
   const bool need_ls = (mode != FAB_NONE) && !c->breakdown;
   if (mode != FAB_NONE && mode != FAB_LSQR && !c->sketch_in_V) return FAB_EORDER;
@@ -795,8 +798,41 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
     launches += 3;
     c->info.cond_R = 1.0;
   } else if (need_ls) {
-    // QR of Theta V_m (s x m) with Theta v_{m+1} as an extra column
-    int rc = dense_qr_sketch(c, m, R, qtb, st);
+    // Blendenpik's preconditioner sketch: Theta of fab_sketch, or its own
+    // Theta' when fab_lsqr_opts.precond_s / precond_seed ask for one (G-12)
+    const bool bp = (mode == FAB_BLENDENPIK || mode == FAB_BLENDENPIK_GRAM);
+    int s2 = c->s;
+    uint64_t seed2 = c->seed;
+    if (bp && o) {
+      if (o->precond_s > 0) s2 = o->precond_s;
+      if (o->precond_seed >= 0) seed2 = (uint64_t)o->precond_seed;
+    }
+    const bool fresh = bp && (s2 != c->s || seed2 != c->seed);
+    c->info.precond_s = s2;
+    c->info.precond_fresh = fresh ? 1 : 0;
+    c->info.ms_precond_sketch = 0.0;
+    int rc;
+    if (fresh) {
+      // R = qr(Theta' V_m): one batched pass over V_m into the QR work area
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      FAB_CUDA(cudaEventCreate(&e0));
+      FAB_CUDA(cudaEventCreate(&e1));
+      FAB_CUDA(cudaEventRecord(e0, st));
+      rc = sketch_precond(c, s2, seed2, m, qr_work(c), st);
+      if (rc == FAB_OK) rc = dense_qr_work(c, m, s2, m, R, nullptr, st);
+      cudaEventRecord(e1, st);
+      if (rc == FAB_OK && cudaEventSynchronize(e1) == cudaSuccess) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, e0, e1);
+        c->info.ms_precond_sketch = t;
+      }
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      launches += 3;
+    } else {
+      // QR of Theta V_m (s x m) with Theta v_{m+1} as an extra column
+      rc = dense_qr_sketch(c, m, R, qtb, st);
+    }
     if (rc != FAB_OK) return rc;
     rc = dense_tri_inverse(c, R, m, Rinv, st);
     if (rc != FAB_OK) return rc;

@@ -177,26 +177,34 @@ int enqueue_sgs_column(fab_ctx* c, int col, int m, cudaStream_t st, int64_t* lau
   return FAB_OK;
 }
 
+static int enqueue_sgs_all(fab_ctx* c, int m, cudaStream_t st, int64_t* launches) {
+  double* praw = svec(c, 20);
+  k_sgs_reset<<<1, 1, 0, st>>>(c->st_d, m);
+  ++*launches;
+  FAB_CUDA(cudaMemsetAsync(c->H, 0, (size_t)c->ldH * m * sizeof(double), st));
+  FAB_TRY(enqueue_col_sketch(c, 0, praw, st, launches));
+  k_sgs_first<<<1, kThreads, 0, st>>>(praw, c->s, c->m_max, c->SV, c->beta, c->st_d);
+  ++*launches;
+  for (int col = 1; col <= m; ++col) FAB_TRY(enqueue_sgs_column(c, col, m, st, launches));
+  return FAB_OK;
+}
+
 int run_basis_sgs(fab_ctx* c, int m) {
+  if (!comm_graphable(c)) {   // loopback ranks: eager
+    int64_t launches = 0;
+    FAB_TRY(enqueue_sgs_all(c, m, c->stream, &launches));
+    c->info.launches_basis = launches;
+    return FAB_OK;
+  }
   if (!(c->gexec_sgs && c->g_sgs_m == m && c->g_sgs_s == c->s)) {
     if (c->gexec_sgs) {
       cudaGraphExecDestroy(c->gexec_sgs);
       c->gexec_sgs = nullptr;
     }
-    double* praw = svec(c, 20);
     int64_t launches = 0;
     cudaStream_t st = c->cap;
     FAB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    int rc = FAB_OK;
-    k_sgs_reset<<<1, 1, 0, st>>>(c->st_d, m);
-    ++launches;
-    cudaMemsetAsync(c->H, 0, (size_t)c->ldH * m * sizeof(double), st);
-    rc = enqueue_col_sketch(c, 0, praw, st, &launches);
-    if (rc == FAB_OK) {
-      k_sgs_first<<<1, kThreads, 0, st>>>(praw, c->s, c->m_max, c->SV, c->beta, c->st_d);
-      ++launches;
-    }
-    for (int col = 1; col <= m && rc == FAB_OK; ++col) rc = enqueue_sgs_column(c, col, m, st, &launches);
+    int rc = enqueue_sgs_all(c, m, st, &launches);
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(st, &graph);
     if (rc != FAB_OK) {

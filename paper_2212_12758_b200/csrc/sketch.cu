@@ -65,18 +65,23 @@ __global__ void k_signs(uint32_t* __restrict__ bits, int64_t nwords, uint64_t ke
   }
 }
 
-int sketch_draw(fab_ctx* c, int s, uint64_t seed) {
+// rows (host Floyd, uploaded) and the sign bitmap of the SRHT (s, seed)
+static int draw_into(fab_ctx* c, int s, uint64_t seed, int64_t* rows_d, uint32_t* signs_d) {
   std::vector<int64_t> rows(s);
   host_sketch_rows(seed, c->N, s, rows.data());
   // rows go through a pinned-free synchronous copy: s <= 768 int64
-  FAB_CUDA(cudaMemcpyAsync(c->rows_d, rows.data(), s * sizeof(int64_t), cudaMemcpyHostToDevice,
-                           c->stream));
+  FAB_CUDA(cudaMemcpyAsync(rows_d, rows.data(), s * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
   const int64_t nwords = (c->N + 31) / 32;
   const int grid = (int)((nwords + kThreads - 1) / kThreads < 4096 ? (nwords + kThreads - 1) / kThreads : 4096);
-  k_signs<<<grid, kThreads, 0, c->stream>>>(c->signs_d, nwords, mix64(seed ^ kTagSign));
+  k_signs<<<grid, kThreads, 0, c->stream>>>(signs_d, nwords, mix64(seed ^ kTagSign));
   FAB_CHECK_LAUNCH();
   // the host vector must outlive the async copy
   FAB_CUDA(cudaStreamSynchronize(c->stream));
+  return FAB_OK;
+}
+
+int sketch_draw(fab_ctx* c, int s, uint64_t seed) {
+  FAB_TRY(draw_into(c, s, seed, c->rows_d, c->signs_d));
   c->s = s;
   c->seed = seed;
   return FAB_OK;
@@ -112,6 +117,38 @@ int sketch_finalize(fab_ctx* c, int ncols, cudaStream_t st) {
   // C3: every rank sketched its own rows on globally aligned tiles (R-1);
   // the sum over ranks is Theta V (nothing else crosses GPUs for the SRHT)
   return comm_allreduce(c, c->SV, (size_t)c->s * ncols, false, st);
+}
+
+// Blendenpik with its own SRHT Theta' (Blendenpik "computes
+// a random sketch of the basis using, once again, a SRHT"; reading G-12's
+// precond_s / precond_seed): draw Theta' once per (s2, seed2), then K5 over
+// the m columns of V_m with Theta' in place of Theta (the same per-tile
+// algorithm and fixed-order reduction), finalized into dst (s2 x m).  The
+// per-CTA partial buffer of the basis sketch is reused (Theta V is already
+// reduced into SV by then).
+int sketch_precond(fab_ctx* c, int s2, uint64_t seed2, int m, double* dst, cudaStream_t st) {
+  if (s2 < m || s2 > c->s_max || (int64_t)s2 > c->N) return FAB_EINVAL;
+  if (c->pre_s != s2 || c->pre_seed != seed2) {
+    FAB_TRY(draw_into(c, s2, seed2, c->rows2_d, c->signs2_d));
+    c->pre_s = s2;
+    c->pre_seed = seed2;
+  }
+  uint32_t* sg = c->signs_d;
+  int64_t* rw = c->rows_d;
+  const int s = c->s;
+  c->signs_d = c->signs2_d;
+  c->rows_d = c->rows2_d;
+  c->s = s2;
+  int rc = launch_sketch_cols(c, 0, m, st);
+  c->signs_d = sg;
+  c->rows_d = rw;
+  c->s = s;
+  if (rc != FAB_OK) return rc;
+  const int64_t total = (int64_t)s2 * m;
+  const int grid = (int)((total + kThreads - 1) / kThreads);
+  k_sketch_finalize<<<grid, kThreads, 0, st>>>(c->part_sk, c->grid_upd, s2, m, c->beta, dst, c->st_d);
+  FAB_CHECK_LAUNCH();
+  return comm_allreduce(c, dst, (size_t)total, false, st);   // C3 for Theta'
 }
 
 // K5: the sketch drawn after the basis -- one batched streaming pass over

@@ -135,6 +135,64 @@ class Comm:
             pass
 
 
-__all__ = ["Comm", "row_blocks", "stencil_blocks", "csr_blocks", "local_csr", "local_operator",
+class LoopbackComm:
+    """One rank of a loopback group (fab_comm_init_loopback): same interface
+    as Comm (.rank, .size, .handle); owned by its LoopbackGroup."""
+
+    def __init__(self, handle, rank, size, device):
+        self.handle = C.c_void_p(handle)
+        self.rank, self.size, self.device = rank, size, device
+
+    def close(self):
+        if self.handle:
+            lib.fab_comm_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+
+class LoopbackGroup:
+    """P ranks of one row-partitioned solve on ONE GPU (SURVEY §4 tier T3'):
+    the path's halo / all-gather / allreduce data movement without NCCL.
+    Drive rank r from its own host thread and its own CUDA stream (`run`)."""
+
+    def __init__(self, nranks, device=0):
+        arr = (C.c_void_p * nranks)()
+        check(lib.fab_comm_init_loopback(C.cast(arr, C.c_void_p), nranks, device), "fab_comm_init_loopback")
+        self.comms = [LoopbackComm(arr[r], r, nranks, device) for r in range(nranks)]
+
+    def run(self, fn):
+        """fn(rank, comm, stream) on P threads at once; returns the P results
+        (re-raises the first exception)."""
+        import threading
+
+        import torch
+        out = [None] * len(self.comms)
+        errs = [None] * len(self.comms)
+        dev = self.comms[0].device
+
+        def body(r):
+            try:
+                torch.cuda.set_device(dev)
+                st = torch.cuda.Stream(device=dev)
+                with torch.cuda.stream(st):
+                    out[r] = fn(r, self.comms[r], st)
+                st.synchronize()
+            except BaseException as e:   # noqa: BLE001
+                errs[r] = e
+        ts = [threading.Thread(target=body, args=(r,)) for r in range(len(self.comms))]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        for e in errs:
+            if e is not None:
+                raise e
+        return out
+
+    def close(self):
+        for cm in self.comms:
+            cm.close()
+
+
+__all__ = ["Comm", "LoopbackGroup", "LoopbackComm", "row_blocks", "stencil_blocks", "csr_blocks", "local_csr", "local_operator",
            "stencil_halo", "ALIGN"]
 _ = _lib

@@ -22,11 +22,39 @@ def test_reference_arm_json_line():
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "solves/s"
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    # the same config dict as the GPU arm (bench.workload_config)
+    for key in ("workload", "n", "m", "k", "s", "mode", "f", "sigma", "l2", "parallelism"):
+        assert key in d["config"], key
+    assert d["lsqr_iters"] > 0 and "oracle" in d["lsqr_iters_source"]
 
 
 def test_reference_arm_other_ranks_exit_quietly():
     env = dict(os.environ, RANK="1", WORLD_SIZE="2")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
-                        "--warmup", "0", "--g", "16"], capture_output=True, text=True, timeout=300, cwd=ROOT,
-                       env=env)
+                        "--warmup", "0", "--g", "16", "--gpus", "2"], capture_output=True, text=True, timeout=300,
+                       cwd=ROOT, env=env)
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def test_gpus_must_match_world_size():
+    """--gpus N under a launcher whose WORLD_SIZE differs is an error (the
+    line would otherwise report the wrong n_gpus)."""
+    env = dict(os.environ, RANK="0", WORLD_SIZE="2")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "0", "--g", "16", "--gpus", "4"], capture_output=True, text=True, timeout=300,
+                       cwd=ROOT, env=env)
+    assert r.returncode == 2 and "WORLD_SIZE" in r.stderr
+
+
+def test_gpus_n_without_launcher_spawns_ranks():
+    """--gpus 2 without torchrun starts 2 ranks itself (torch.distributed.run
+    on 127.0.0.1); the reference arm prints one line from rank 0 with n_gpus 2."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "0", "--g", "16", "--gpus", "2"], capture_output=True, text=True, timeout=600,
+                       cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"

@@ -1,0 +1,181 @@
+"""The row-partitioned multi-GPU path with P ranks on ONE GPU (SURVEY §4 tier
+T3', VERDICT r01 "missing" #1): P host threads, each a rank with its own
+context, workspace and stream, joined by a loopback communicator
+(fab_comm_init_loopback) that moves the same halo / all-gather / allreduce
+data as NCCL does, stream-ordered.  This runs the product's rank-boundary
+code on the real kernels: global grid coordinates of a row block (gbase),
+halo slots in V's padding, SRHT tiles cut at rank boundaries (reading R-1:
+the pruned tile partials of every rank sum to Theta V), the
+gathered-x CSR buffer, the per-rank K1 step sums + allreduce (C2), the
+sketch allreduce (C3) and the per-rank LSQR pass partials (C4).
+
+Checked against the fp64 oracle (f_m <= 1e-10, H <= 1e-12, Theta V <= 1e-13;
+BASELINE north star) and for P-invariance: sampled rows / signs bit-exact
+and every replicated quantity (H, Theta V, y, C) bitwise equal on all ranks;
+f_m within 1e-12 of the one-GPU run (only the reduction order
+changes with P).
+"""
+import numpy as np
+import pytest
+
+import fab_problems as fp
+from oracle import fab as ofab
+from oracle import krylov as okrylov
+from oracle import rng as orng
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b))
+
+
+def cuts_for(p, P, csr=False):
+    from paper_2212_12758_b200 import dist as fdist
+    if p.kind == "stencil" and not csr:
+        return fdist.stencil_blocks(p.dims, P)
+    if p.name == "c4":
+        return fdist.csr_blocks(p.csr()[0], P)
+    return fdist.row_blocks(p.n, P)
+
+
+def run_partitioned(p, P, mode, iters=40, csr=False, alg="alg2", square=False, f=None):
+    """One solve over P loopback ranks; returns (cuts, per-rank dicts)."""
+    import torch
+    import paper_2212_12758_b200 as fab
+    from paper_2212_12758_b200 import dist as fdist
+    cuts = cuts_for(p, P, csr)
+    grp = fdist.LoopbackGroup(P, 0)
+
+    def body(r, comm, st):
+        r0, r1 = int(cuts[r]), int(cuts[r + 1])
+        op = fdist.local_operator(p, r0, r1, csr=csr)
+        b = torch.as_tensor(np.ascontiguousarray(p.b[r0:r1])).cuda()
+        sv = fab.Solver(op, b, m_max=p.m, k_max=p.k, s_max=p.s, stream=st, comm=comm, square=square)
+        if alg == "alg2":
+            if mode != "none":
+                sv.sketch(p.s, p.sketch_seed)
+            sv.basis(p.m, p.k)
+        elif alg == "alg1":
+            sv.sketch(p.s, p.sketch_seed)
+            sv.basis_sgs(p.m)
+        elif alg == "arnoldi":
+            sv.basis_arnoldi(p.m)
+        sv.compress(mode, iters=iters)
+        y = sv.apply(f or p.f, p.alpha, p.sigma)
+        st.synchronize()
+        out = dict(y=y.cpu().numpy(), H=sv.get("H"), info=sv.info(), C=sv.get("C"), yls=sv.get("y"))
+        if mode != "none" or alg == "alg1":
+            out.update(SV=sv.get("SV"))
+        if mode != "none":
+            out.update(rows=sv.get("rows"))
+        sv.close()
+        del op
+        return out
+
+    try:
+        res = grp.run(body)
+    finally:
+        grp.close()
+    return cuts, res
+
+
+def one_gpu(p, mode, iters=40, csr=False):
+    import torch
+    import paper_2212_12758_b200 as fab
+    sv = fab.Solver(fab.Operator.from_problem(p, csr=csr), torch.as_tensor(p.b).cuda(), p.m, p.k, p.s)
+    if mode != "none":
+        sv.sketch(p.s, p.sketch_seed)
+    sv.basis(p.m, p.k)
+    sv.compress(mode, iters=iters)
+    y = sv.apply(p.f, p.alpha, p.sigma).cpu().numpy()
+    H = sv.get("H")
+    sv.close()
+    return y, H
+
+
+def check_replicated(res, keys):
+    for key in keys:
+        for r in range(1, len(res)):
+            assert np.array_equal(res[r][key], res[0][key]), key
+
+
+CASES = [
+    # c3 z-slabs of whole 32x32 planes (halo = one plane in V's padding)
+    ("c3", dict(g=32, m=60, s=120), 2, False),
+    ("c3", dict(g=32, m=60, s=120), 3, False),
+    ("c3", dict(g=32, m=60, s=120), 4, False),
+    # c1 2D: 100-row lines are not 32-aligned -> aligned row blocks cut
+    # mid-line and mid 4096-row sketch tile (halo = one line)
+    ("c1", {}, 3, False),
+    # c5 CSR: all-gather of x into the global-length buffer, ragged n
+    ("c5", dict(n=20000 + 77, m=40, s=80), 2, False),
+    ("c5", dict(n=20000 + 77, m=40, s=80), 3, False),
+    # c4 CSR: nnz-balanced blocks (hub rows at low ids), uniform values
+    ("c4", dict(n=1 << 15, m=20, s=40), 4, False),
+    # c3 as CSR (the stencil's rows, gathered x instead of halo planes)
+    ("c3", dict(g=20, m=30, s=60), 2, True),
+]
+IDS = [f"{c}-P{P}{'-csr' if csr else ''}" for c, _, P, csr in CASES]
+
+
+@pytest.mark.parametrize("name,kw,P,csr", CASES, ids=IDS)
+def test_loopback_partitioned_parity(name, kw, P, csr):
+    p = fp.make(name, **kw)
+    A = p.scipy()
+    for mode in ("blendenpik", "sketch_solve", "none"):
+        cuts, res = run_partitioned(p, P, mode, csr=csr)
+        y = np.concatenate([r["y"] for r in res])
+        assert len(y) == p.n and all(len(r["y"]) == int(cuts[i + 1] - cuts[i]) for i, r in enumerate(res))
+        ref = ofab.solve(A, p.b, p.m, p.k, p.s, p.sketch_seed, mode=mode, f=p.f, alpha=p.alpha,
+                         sigma=p.sigma, lsqr_iters=40)
+        assert rel(y, ref["f_m"]) <= 1e-10, (mode, rel(y, ref["f_m"]))
+        keys = ["H", "C", "yls"] + (["SV", "rows"] if mode != "none" else [])
+        check_replicated(res, keys)
+        assert rel(res[0]["H"], ref["H"]) <= 1e-12
+        if mode != "none":
+            N = 1 << max(0, (p.n - 1).bit_length())
+            assert np.array_equal(res[0]["rows"], orng.rows(p.sketch_seed, N, p.s))
+            assert np.abs(res[0]["SV"] - ref["SV"]).max() <= 1e-13 * np.abs(ref["SV"]).max()
+        y1, H1 = one_gpu(p, mode, csr=csr)
+        assert rel(y, y1) <= 1e-12, (mode, rel(y, y1))
+        assert res[0]["info"]["m_eff"] == ref["m_eff"]
+
+
+def test_loopback_other_bases_and_sign():
+    """Algorithm 1 (+ Algorithm 3), full Arnoldi (+ FOM) and sign(A) b (the
+    squared operator: halo / all-gather of t = A w) over loopback ranks."""
+    p = fp.make("c3", g=24, m=30, k=4, s=70)
+    A = p.scipy()
+    cuts, res = run_partitioned(p, 2, "lsqr", iters=150, alg="alg1")
+    y = np.concatenate([r["y"] for r in res])
+    ref = ofab.alg3(A, p.b, p.m, p.s, p.sketch_seed, f=p.f, alpha=p.alpha, sigma=p.sigma, lsqr_iters=150)
+    assert rel(y, ref["f_m"]) <= 1e-10
+    check_replicated(res, ["H", "SV", "C"])
+    cuts, res = run_partitioned(p, 3, "none", alg="arnoldi")
+    y = np.concatenate([r["y"] for r in res])
+    assert rel(y, ofab.fom(A, p.b, p.m, f=p.f, alpha=p.alpha, sigma=p.sigma)) <= 1e-10
+    check_replicated(res, ["H", "C"])
+    # sign: e4's recipe (spectrum in both half planes), squared operator
+    q = fp.make("e4", n=6000, m=20, s=40)
+    cuts, res = run_partitioned(q, 2, "sketch_solve", square=True, f="sign")
+    y = np.concatenate([r["y"] for r in res])
+    ref = ofab.sign(q.scipy(), q.b, q.m, q.k, q.s, q.sketch_seed, mode="sketch_solve")
+    assert rel(y, ref["f_m"]) <= 1e-10
+
+
+def test_loopback_oracle_mgs_floor_c3():
+    # the tolerance above is meaningful: the oracle's own MGS-vs-CGS basis
+    # gap at the c3 case is far below it
+    p = fp.make("c3", g=32, m=60, s=120)
+    a = okrylov.truncated_arnoldi(p.scipy(), p.b, p.m, p.k, variant="cgs")
+    b = okrylov.truncated_arnoldi(p.scipy(), p.b, p.m, p.k, variant="mgs")
+    assert np.abs(a["V"] - b["V"]).max() <= 1e-12
