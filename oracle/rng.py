@@ -76,9 +76,14 @@ def signs(seed: int, N: int, start: int = 0, count: int = None) -> np.ndarray:
 
 def rows(seed: int, N: int, s: int) -> np.ndarray:
     """s distinct row indices in [0, N), sorted ascending (Floyd)."""
+    return rows_from_key(key(seed, TAG_ROWS), N, s)
+
+
+def rows_from_key(k: int, N: int, s: int) -> np.ndarray:
+    """Floyd's sampling driven by the SplitMix64 stream of state k (q_i =
+    h(k, i) = output i of SplitMix64(state = k))."""
     if not (1 <= s <= N):
         raise ValueError("need 1 <= s <= N")
-    k = key(seed, TAG_ROWS)
     chosen = set()
     for j in range(N - s, N):
         q = h(k, j - N + s)

@@ -42,6 +42,19 @@ def test_rows_structure_and_floyd():
         rng.rows(1, 8, 9)
 
 
+def test_rows_floyd_hand_trace():
+    """Floyd's sampler step by step on the published SplitMix64 stream (two
+    collisions: the 'take j' branch runs at j = 2 and j = 3); a uniform but
+    different sampler fails this."""
+    g = json.load(open(os.path.join(GOLD, "floyd_trace.json")))
+    qs = rng.splitmix64_stream(g["state"], g["s"])
+    for st, q in zip(g["trace"], qs):
+        assert f"{q / 2.0 ** 64:.4f}" == st["q_over_2_64"]
+        assert (q * (st["j"] + 1)) >> 64 == st["t"]
+    assert rng.rows_from_key(g["state"], g["N"], g["s"]).tolist() == g["rows"]
+    assert sorted(st["taken"] for st in g["trace"]) == g["rows"]
+
+
 def test_rows_uniform_chi2():
     # each index of [0, 32) should be chosen with probability s/N = 1/4
     N, s, T = 32, 8, 4000
