@@ -192,6 +192,8 @@ static void free_ctx(fab_ctx* c) {
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->gexec_sgs) cudaGraphExecDestroy(c->gexec_sgs);
   if (c->gexec_arn) cudaGraphExecDestroy(c->gexec_arn);
+  if (c->gexec_lsqr) cudaGraphExecDestroy(c->gexec_lsqr);
+  if (c->cap2) cudaStreamDestroy(c->cap2);
   if (c->gexec_bat) cudaGraphExecDestroy(c->gexec_bat);
   if (c->gram_part) cudaFree(c->gram_part);
   if (c->xi) cudaFree(c->xi);

@@ -158,6 +158,13 @@ struct fab_ctx {
   double* gram_part = nullptr;        // FAB_BLENDENPIK_GRAM: per-CTA Gram partials (allocated on first use)
   size_t gram_part_bytes = 0;
 
+  // cached LSQR graph (init + conditional WHILE node over one iteration)
+  cudaGraphExec_t gexec_lsqr = nullptr;
+  cudaStream_t cap2 = nullptr;        // second capture stream (the while body)
+  int gl_m = -1, gl_G = -1, gl_ns = -1, gl_fixed = -1, gl_maxit = -1;
+  bool gl_pipe = false;
+  double gl_tol = -1.0;
+
   // cached Arnoldi (CGS2) graph
   cudaGraphExec_t gexec_arn = nullptr;
   int g_arn_m = -1;

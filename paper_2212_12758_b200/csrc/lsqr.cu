@@ -631,10 +631,21 @@ __global__ void k_lsqr_init(const double* part_g, const double* part_tn, int npa
 }
 
 // one LSQR iteration's scalar work after the pass t_new = M v - alpha u
+// Inside the graph-resident loop (cond_while != 0) it also sets the while
+// node's condition: continue iff not done and fewer than maxit iterations.
+__device__ __forceinline__ void lsqr_set_cond(unsigned long long h, int use, const DevState* st, int maxit) {
+  if (use && threadIdx.x == 0)
+    cudaGraphSetConditional((cudaGraphConditionalHandle)h, (!st->lsqr_done && st->lsqr_iters < maxit) ? 1u : 0u);
+}
+
 __global__ void k_lsqr_step(const double* part_g, const double* part_tn, int nparts, int m,
                             const double* Rinv, const double* RinvT, const double* bcol, LsqrVecs L,
-                            int tol_mode, DevState* st) {
-  if (st->lsqr_done) return;
+                            int tol_mode, DevState* st, unsigned long long cond_h = 0, int cond_while = 0,
+                            int maxit = 0) {
+  if (st->lsqr_done) {
+    lsqr_set_cond(cond_h, cond_while, st, maxit);
+    return;
+  }
   __shared__ double red[kLsqrStepThreads / 32];
   const double tn = reduce_pass(part_g, part_tn, nparts, m, L.g, red);
   const double beta = sqrt(tn);
@@ -651,6 +662,7 @@ __global__ void k_lsqr_step(const double* part_g, const double* part_tn, int npa
   const double rho = hypot(rhobar0, beta);
   if (!(rho > 0.0)) {   // degenerate (both zero): nothing left to solve
     if (threadIdx.x == 0) st->lsqr_done = 1;
+    lsqr_set_cond(cond_h, cond_while, st, maxit);
     return;
   }
   const double cs = rhobar0 / rho, sn = beta / rho;
@@ -692,6 +704,7 @@ __global__ void k_lsqr_step(const double* part_g, const double* part_tn, int npa
         st->lsqr_done = 1;
     }
   }
+  lsqr_set_cond(cond_h, cond_while, st, maxit);
 }
 
 // y = R^{-1} x ;  C = H_m + h_{m+1,m} y e_m^T
@@ -905,15 +918,7 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
       if (pipe && make_tmap_cols(c->V, c->n, m, c->ld, kLsR, boxc, &tmW) != FAB_OK) pipe = nullptr;
       const int64_t nchunks = (c->n + kLsR - 1) / kLsR;
       const int G = pipe ? (int)(nchunks < c->num_sms ? nchunks : c->num_sms) : c->grid_lsqr;
-      // one streaming pass over V_m: t_new = W p - scal t_old, g = W^T t_new, ||t_new||^2
-      auto launch_pass = [&](double scal, const double* t_old, int use_state) {
-        if (pipe)
-          pipe<<<G, kLsPipeThreads, pipe_smem, st>>>(tmW, boxc, ncopies, m, c->n, L.p, scal, t_old, c->vec,
-                                                    c->part_g, c->part_tn, c->st_d, use_state, pipe_ns);
-        else
-          pass<<<G, kLsqrThreads, 0, st>>>(c->V, c->ld, m, c->n, L.p, scal, t_old, c->vec, c->part_g,
-                                           c->part_tn, c->st_d, use_state);
-      };
+      // one streaming pass over V_m: t_new = W p - scal t_old, g = W^T t_new, ||t_new||^2 (launch_pass_on)
       const int fixed = (o && o->iters > 0) ? o->iters : 0;
       const double tol = (o && o->tol > 0) ? o->tol : 1e-6;
       const int maxit = fixed ? fixed : ((o && o->maxit > 0) ? o->maxit : 4 * m);
@@ -927,60 +932,164 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
         }
         return &c->prof_ev[2 * i];
       };
-      // init pass: p = 0, t_old = w_hat_m, scal = -1  ->  t = w_hat_m, g = W^T t
-      FAB_CUDA(cudaMemsetAsync(L.p, 0, m * sizeof(double), st));
-      k_reset_lsqr<<<1, 1, 0, st>>>(c->st_d);
-      if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[0], st));
-      launch_pass(-1.0, c->V + (int64_t)m * c->ld, 0);
-      FAB_CHECK_LAUNCH();
-      if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[1], st));
-      ++npass;
+      // the stream the LSQR launches go to (the caller's, or a capture stream)
+      cudaStream_t ls = st;
       // C4 on several GPUs: reduce this rank's partials, allreduce m+1 scalars
       auto pass_scalars = [&](const double** pg, int* np) -> int {
         *pg = c->part_g;
         *np = G;
         if (!c->comm) return FAB_OK;
-        k_pass_reduce<<<1, kLsqrStepThreads, 0, st>>>(c->part_g, c->part_tn, G, m, c->red, c->st_d);
+        k_pass_reduce<<<1, kLsqrStepThreads, 0, ls>>>(c->part_g, c->part_tn, G, m, c->red, c->st_d);
         FAB_CHECK_LAUNCH();
         ++launches;
         *pg = c->red;
         *np = -1;
-        return comm_allreduce(c, c->red, (size_t)m + 1, false, st);
+        return comm_allreduce(c, c->red, (size_t)m + 1, false, ls);
       };
-      const double* pg = nullptr;
-      int np = 0;
-      FAB_TRY(pass_scalars(&pg, &np));
-      k_lsqr_init<<<1, kLsqrStepThreads, 0, st>>>(pg, c->part_tn, np, m, Rinv, RinvT, c->beta, L, tol, c->st_d);
-      FAB_CHECK_LAUNCH();
-      launches += 2;
-      int done_iters = 0;
-      const int chunk = fixed ? maxit : 4;
-      while (done_iters < maxit) {
-        const int nit = (maxit - done_iters) < chunk ? (maxit - done_iters) : chunk;
-        for (int it = 0; it < nit; ++it) {
-          if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[0], st));
-          launch_pass(0.0, c->vec, 1);
-          FAB_CHECK_LAUNCH();
-          if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[1], st));
-          ++npass;
-          FAB_TRY(pass_scalars(&pg, &np));
-          k_lsqr_step<<<1, kLsqrStepThreads, 0, st>>>(pg, c->part_tn, np, m, Rinv, RinvT, c->beta, L, fixed ? 0 : 1,
-                                              c->st_d);
-          FAB_CHECK_LAUNCH();
-          launches += 2;
+      auto launch_pass_on = [&](double scal, const double* t_old, int use_state) {
+        if (pipe)
+          pipe<<<G, kLsPipeThreads, pipe_smem, ls>>>(tmW, boxc, ncopies, m, c->n, L.p, scal, t_old, c->vec,
+                                                    c->part_g, c->part_tn, c->st_d, use_state, pipe_ns);
+        else
+          pass<<<G, kLsqrThreads, 0, ls>>>(c->V, c->ld, m, c->n, L.p, scal, t_old, c->vec, c->part_g,
+                                           c->part_tn, c->st_d, use_state);
+      };
+      // init pass: p = 0, t_old = w_hat_m, scal = -1  ->  t = w_hat_m, g = W^T t
+      auto enqueue_init = [&]() -> int {
+        FAB_CUDA(cudaMemsetAsync(L.p, 0, m * sizeof(double), ls));
+        k_reset_lsqr<<<1, 1, 0, ls>>>(c->st_d);
+        if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[0], ls));
+        launch_pass_on(-1.0, c->V + (int64_t)m * c->ld, 0);
+        FAB_CHECK_LAUNCH();
+        if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[1], ls));
+        ++npass;
+        const double* pg = nullptr;
+        int np = 0;
+        FAB_TRY(pass_scalars(&pg, &np));
+        k_lsqr_init<<<1, kLsqrStepThreads, 0, ls>>>(pg, c->part_tn, np, m, Rinv, RinvT, c->beta, L, tol, c->st_d);
+        FAB_CHECK_LAUNCH();
+        launches += 2;
+        return FAB_OK;
+      };
+      // one iteration: the pass, its scalars, the recurrence (+ the while condition)
+      auto enqueue_iter = [&](unsigned long long h, int use_cond) -> int {
+        if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[0], ls));
+        launch_pass_on(0.0, c->vec, 1);
+        FAB_CHECK_LAUNCH();
+        if (prof) FAB_CUDA(cudaEventRecord(ev_pair(npass)[1], ls));
+        ++npass;
+        const double* pg = nullptr;
+        int np = 0;
+        FAB_TRY(pass_scalars(&pg, &np));
+        k_lsqr_step<<<1, kLsqrStepThreads, 0, ls>>>(pg, c->part_tn, np, m, Rinv, RinvT, c->beta, L, fixed ? 0 : 1,
+                                                    c->st_d, h, use_cond, maxit);
+        FAB_CHECK_LAUNCH();
+        launches += 2;
+        return FAB_OK;
+      };
+      // Graph-resident loop (one GPU, not profiling): init, then a CUDA-graph
+      // conditional WHILE node whose body is one iteration; k_lsqr_step sets
+      // the condition on the device (not done and < maxit), so the
+      // tolerance test of l.359 needs no host round trip.  FAB_FLAG_PROFILE
+      // keeps the host-driven loop: event nodes are not allowed in a
+      // conditional body, and the bench times every pass with CUDA events.
+      const char* eg = getenv("FAB_LSQR_GRAPH");
+      const bool graph_loop = !prof && !c->comm && !(eg && eg[0] == '0');
+      if (graph_loop) {
+        const bool hit = c->gexec_lsqr && c->gl_m == m && c->gl_G == G && c->gl_pipe == (pipe != nullptr) &&
+                         c->gl_ns == pipe_ns && c->gl_fixed == fixed && c->gl_maxit == maxit && c->gl_tol == tol;
+        if (!hit) {
+          if (c->gexec_lsqr) {
+            cudaGraphExecDestroy(c->gexec_lsqr);
+            c->gexec_lsqr = nullptr;
+          }
+          if (!c->cap2) FAB_CUDA(cudaStreamCreateWithFlags(&c->cap2, cudaStreamNonBlocking));
+          const int64_t nl0 = c->nlaunch;   // captured launches are counted per replay below
+          ls = c->cap;
+          FAB_CUDA(cudaStreamBeginCapture(ls, cudaStreamCaptureModeThreadLocal));
+          int rc = enqueue_init();
+          cudaGraph_t g = nullptr;
+          cudaGraphNode_t cn = nullptr;
+          cudaGraphConditionalHandle h = 0;
+          if (rc == FAB_OK) {
+            cudaStreamCaptureStatus cs;
+            const cudaGraphNode_t* deps = nullptr;
+            size_t nd = 0;
+            cudaError_t e = cudaStreamGetCaptureInfo(ls, &cs, nullptr, &g, &deps, &nd);
+            if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+            cudaGraphNodeParams np = {};
+            np.type = cudaGraphNodeTypeConditional;
+            np.conditional.handle = h;
+            np.conditional.type = cudaGraphCondTypeWhile;
+            np.conditional.size = 1;
+            if (e == cudaSuccess) e = cudaGraphAddNode(&cn, g, deps, nd, &np);
+            if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(ls, &cn, 1, cudaStreamSetCaptureDependencies);
+            if (e == cudaSuccess) {
+              cudaGraph_t body = np.conditional.phGraph_out[0];
+              ls = c->cap2;
+              e = cudaStreamBeginCaptureToGraph(ls, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+              if (e == cudaSuccess) {
+                rc = enqueue_iter((unsigned long long)h, 1);
+                cudaGraph_t bg = nullptr;
+                const cudaError_t e2 = cudaStreamEndCapture(ls, &bg);
+                if (rc == FAB_OK && e2 != cudaSuccess) e = e2;
+              }
+              ls = c->cap;
+            }
+            if (e != cudaSuccess && rc == FAB_OK) {
+              set_last_cuda_error(e, "LSQR while-node graph", __FILE__, __LINE__);
+              rc = FAB_ECUDA;
+            }
+          }
+          if (rc == FAB_OK) {
+            k_finish_y<<<1, kThreads, 0, ls>>>(RinvT, L.x, m, y);
+            ++launches;
+          }
+          cudaGraph_t graph = nullptr;
+          const cudaError_t e = cudaStreamEndCapture(c->cap, &graph);
+          ls = st;
+          if (rc != FAB_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return rc;
+          }
+          FAB_CUDA(e);
+          FAB_CUDA(cudaGraphInstantiate(&c->gexec_lsqr, graph, 0));
+          cudaGraphDestroy(graph);
+          c->nlaunch = nl0;
+          c->gl_m = m;
+          c->gl_G = G;
+          c->gl_pipe = pipe != nullptr;
+          c->gl_ns = pipe_ns;
+          c->gl_fixed = fixed;
+          c->gl_maxit = maxit;
+          c->gl_tol = tol;
         }
-        done_iters += nit;
-        if (fixed) break;
-        FAB_CUDA(cudaMemcpyAsync(c->st_h, c->st_d, sizeof(DevState), cudaMemcpyDeviceToHost, st));
-        FAB_CUDA(cudaStreamSynchronize(st));
-        if (c->st_h->lsqr_done) break;
+        FAB_CUDA(cudaGraphLaunch(c->gexec_lsqr, st));
+        launches += 3;
+      } else {
+        FAB_TRY(enqueue_init());
+        int done_iters = 0;
+        const int chunk = fixed ? maxit : 4;
+        while (done_iters < maxit) {
+          const int nit = (maxit - done_iters) < chunk ? (maxit - done_iters) : chunk;
+          for (int it = 0; it < nit; ++it) FAB_TRY(enqueue_iter(0, 0));
+          done_iters += nit;
+          if (fixed) break;
+          FAB_CUDA(cudaMemcpyAsync(c->st_h, c->st_d, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+          FAB_CUDA(cudaStreamSynchronize(st));
+          if (c->st_h->lsqr_done) break;
+        }
+        k_finish_y<<<1, kThreads, 0, st>>>(RinvT, L.x, m, y);
+        FAB_CHECK_LAUNCH();
+        ++launches;
       }
-      k_finish_y<<<1, kThreads, 0, st>>>(RinvT, L.x, m, y);
-      FAB_CHECK_LAUNCH();
-      ++launches;
       FAB_CUDA(cudaMemcpyAsync(c->st_h, c->st_d, sizeof(DevState), cudaMemcpyDeviceToHost, st));
       FAB_CUDA(cudaStreamSynchronize(st));
       c->info.lsqr_iters = c->st_h->lsqr_iters;
+      // graph replay: reset + init pass + init scalars + finish, and per
+      // iteration (the body ran iters times, once more when it ended on done)
+      // one pass and one step kernel
+      if (graph_loop) c->nlaunch += 4 + 2 * (int64_t)c->st_h->lsqr_iters;
       // passes after convergence exit immediately; count the ones that ran
       c->info.lsqr_passes = 1 + c->st_h->lsqr_iters;
       c->info.ms_lsqr_pass = 0.0;

@@ -20,13 +20,21 @@ Steps, each the oracle's own (no shortcuts):
         sketch_solve  Remark 2 (y = R^{-1} Q^T Theta v_{m+1})
         blendenpik40  Blendenpik-LSQR with exactly L = 40 iterations (G-14)
         blendenpik    Blendenpik-LSQR at the MATLAB tolerance 1e-6 (l.359)
+        blendenpik120 Blendenpik-LSQR with L = 120 iterations: converged to
+                      the least-squares solution (contraction ~0.7 per
+                      iteration at s = 2m), so y is determined by the data
+        blendenpik40_inv  the L = 40 run with R^{-1} applied as an explicit
+                      inverse instead of by substitution: the same method in
+                      other rounding -- its distance to blendenpik40 is the
+                      oracle's own noise floor for an unconverged iterate
+                      (reading R-3)
   * c = sqrt(C_m + sigma I) e_1 (scipy sqrtm, l.356) and f_m = gamma V_m c
     (Algorithm 4 line 3, l.207).
 
 f_m has 2^24 entries (128 MB), too large to commit; the file keeps, per mode,
 every 4096th row (4096 values), the sums over the 4096 consecutive blocks of
 4096 rows (every entry of f_m enters one of them), and ||f_m||.  The full
-H, Theta V, R, y and c are kept.  Needs ~32 GB RAM and ~15-25 min on 8 cores.
+H, Theta V, R, y and c are kept.  Needs ~32 GB RAM and ~45 min on 8 cores.
 """
 import argparse
 import hashlib
@@ -89,11 +97,13 @@ def main():
                 signs_sha256=hashlib.sha256((th.signs < 0).astype(np.uint8).tobytes()).hexdigest())
     modes = {"none": dict(mode="none"), "sketch_solve": dict(mode="sketch_solve"),
              "blendenpik40": dict(mode="blendenpik", lsqr_iters=40),
-             "blendenpik": dict(mode="blendenpik", lsqr_tol=1e-6)}
+             "blendenpik": dict(mode="blendenpik", lsqr_tol=1e-6),
+             "blendenpik120": dict(mode="blendenpik", lsqr_iters=120),
+             "blendenpik40_inv": dict(mode="blendenpik", lsqr_iters=40, rinv="inverse")}
     for key, kw in modes.items():
         t0 = time.perf_counter()
         y, C, R, info = ofab.compress(dec, SV, kw["mode"], lsqr_tol=kw.get("lsqr_tol", 1e-6),
-                                      lsqr_iters=kw.get("lsqr_iters"))         # Eq. (6)/(7)
+                                      lsqr_iters=kw.get("lsqr_iters"), rinv=kw.get("rinv", "solve"))  # Eq. (6)/(7)
         c = matfun.f_e1(p.f, C, p.alpha, p.sigma)                              # f(C_m) e_1
         fm = dec["gamma"] * (V[:, :m] @ c)                                     # l.207
         s = fm_summary(fm)

@@ -131,6 +131,14 @@ IDS = [f"{c}-P{P}{'-csr' if csr else ''}" for c, _, P, csr in CASES]
 def test_loopback_partitioned_parity(name, kw, P, csr):
     p = fp.make(name, **kw)
     A = p.scipy()
+    # the data's own rounding floor (reading G-24): the oracle's MGS vs CGS
+    # bases.  c4's Krylov space saturates (H and late V columns are
+    # rounding-dominated there: MGS/CGS differ by ~5e-11 in H, 4e-6 in V), so
+    # H / Theta V are held to 10x that floor, f_m always to 1e-10
+    cg = okrylov.truncated_arnoldi(A, p.b, p.m, p.k, variant="cgs")
+    mg = okrylov.truncated_arnoldi(A, p.b, p.m, p.k, variant="mgs")
+    nH = rel(mg["H"], cg["H"])
+    nV = float(np.abs(mg["V"] - cg["V"]).max())
     for mode in ("blendenpik", "sketch_solve", "none"):
         cuts, res = run_partitioned(p, P, mode, csr=csr)
         y = np.concatenate([r["y"] for r in res])
@@ -140,13 +148,14 @@ def test_loopback_partitioned_parity(name, kw, P, csr):
         assert rel(y, ref["f_m"]) <= 1e-10, (mode, rel(y, ref["f_m"]))
         keys = ["H", "C", "yls"] + (["SV", "rows"] if mode != "none" else [])
         check_replicated(res, keys)
-        assert rel(res[0]["H"], ref["H"]) <= 1e-12
+        assert rel(res[0]["H"], ref["H"]) <= max(1e-12, 10 * nH), (rel(res[0]["H"], ref["H"]), nH)
         if mode != "none":
             N = 1 << max(0, (p.n - 1).bit_length())
             assert np.array_equal(res[0]["rows"], orng.rows(p.sketch_seed, N, p.s))
-            assert np.abs(res[0]["SV"] - ref["SV"]).max() <= 1e-13 * np.abs(ref["SV"]).max()
+            assert np.abs(res[0]["SV"] - ref["SV"]).max() <= max(1e-13, 10 * nV) * np.abs(ref["SV"]).max()
         y1, H1 = one_gpu(p, mode, csr=csr)
         assert rel(y, y1) <= 1e-12, (mode, rel(y, y1))
+        assert rel(res[0]["H"], H1) <= max(1e-13, 10 * nH)
         assert res[0]["info"]["m_eff"] == ref["m_eff"]
 
 
