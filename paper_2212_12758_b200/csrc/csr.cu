@@ -344,15 +344,65 @@ static int upload_blocks(const std::vector<int64_t>& bl, CsrPass* p) {
 // Plans are shared by the contexts of one operator (the multi-RHS batch
 // creates p contexts of one A): keyed by the device and the caller's arrays,
 // built once, freed with the last context.
+// A plan is shared by the contexts of one operator.  The key holds the
+// caller's device pointers AND a content fingerprint of the arrays (all row
+// pointers, up to 2^20 sampled column ids and values), so an address the
+// caching allocator hands to a different operator does not reuse a stale
+// plan.  (Arrays edited in place while a context is alive are still the
+// caller's error: fab.h, operator arrays are borrowed and must not change.)
 struct PlanKey {
   int device;
   const void *rp, *ci, *va;
   int64_t n, row_begin, nnz, width;
+  unsigned long long fp;
   bool operator==(const PlanKey& o) const {
     return device == o.device && rp == o.rp && ci == o.ci && va == o.va && n == o.n && row_begin == o.row_begin &&
-           nnz == o.nnz && width == o.width;
+           nnz == o.nnz && width == o.width && fp == o.fp;
   }
 };
+
+__device__ __forceinline__ unsigned long long fp_mix(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// out += sum over sampled i of mix(salt + i phi ^ word_i): order independent
+template <typename W>
+__global__ void k_fingerprint(const W* __restrict__ a, int64_t count, int64_t stride, unsigned long long salt,
+                              unsigned long long* out) {
+  unsigned long long acc = 0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k * stride < count;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = k * stride;
+    acc += fp_mix((salt + (unsigned long long)i * 0x9E3779B97F4A7C15ull) ^ (unsigned long long)a[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
+static int operator_fingerprint(fab_ctx* c, unsigned long long* fp) {
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(c->vec);
+  FAB_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), c->stream));
+  const int grid = 2 * c->num_sms;
+  k_fingerprint<int64_t><<<grid, kThreads, 0, c->stream>>>(c->op.row_ptr, c->n + 1, 1, 1, d);
+  FAB_CHECK_LAUNCH();
+  const int64_t nnz = c->op.nnz;
+  const int64_t stride = nnz > (1 << 20) ? nnz / (1 << 20) : 1;
+  if (nnz > 0) {
+    k_fingerprint<int32_t><<<grid, kThreads, 0, c->stream>>>(c->op.col_idx, nnz, stride, 2, d);
+    FAB_CHECK_LAUNCH();
+    if (c->op.values) {
+      k_fingerprint<int64_t><<<grid, kThreads, 0, c->stream>>>(reinterpret_cast<const int64_t*>(c->op.values), nnz,
+                                                               stride, 3, d);
+      FAB_CHECK_LAUNCH();
+    }
+  }
+  FAB_CUDA(cudaMemcpyAsync(fp, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+  FAB_CUDA(cudaStreamSynchronize(c->stream));
+  return FAB_OK;
+}
 static std::mutex g_plan_mu;
 static std::vector<std::pair<PlanKey, std::weak_ptr<CsrPlan>>> g_plans;
 static std::vector<std::pair<fab_ctx*, std::shared_ptr<CsrPlan>>> g_holders;
@@ -397,7 +447,9 @@ int csr_setup(fab_ctx* c) {
   if (width < 1024) width = 1024;
   const char* env = getenv("FAB_CSR_COLBLOCK");   // tests: force a width (columns)
   if (env && atoll(env) > 0) width = atoll(env);
-  const PlanKey key{c->device, c->op.row_ptr, c->op.col_idx, c->op.values, c->n, c->row_begin, c->op.nnz, width};
+  unsigned long long fp = 0;
+  FAB_TRY(operator_fingerprint(c, &fp));
+  const PlanKey key{c->device, c->op.row_ptr, c->op.col_idx, c->op.values, c->n, c->row_begin, c->op.nnz, width, fp};
   std::shared_ptr<CsrPlan> sp;
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);

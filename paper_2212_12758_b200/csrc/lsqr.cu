@@ -588,7 +588,7 @@ int launch_pass_reduce(fab_ctx* c, int nparts, int ncols, double* out, cudaStrea
 
 // LSQR initialisation after the pass t = w_hat_m, g = W^T t:
 //   beta_1 u_1 = v_{m+1} (unit), alpha_1 v_1 = M^T u_1, w_1 = v_1, x_0 = 0
-__global__ void k_lsqr_init(const double* part_g, const double* part_tn, int nparts, int m,
+__global__ void __launch_bounds__(kLsqrStepThreads) k_lsqr_init(const double* part_g, const double* part_tn, int nparts, int m,
                             const double* Rinv, const double* RinvT, const double* bcol, LsqrVecs L,
                             double tol, DevState* st) {
   __shared__ double red[kLsqrStepThreads / 32];
@@ -638,7 +638,7 @@ __device__ __forceinline__ void lsqr_set_cond(unsigned long long h, int use, con
     cudaGraphSetConditional((cudaGraphConditionalHandle)h, (!st->lsqr_done && st->lsqr_iters < maxit) ? 1u : 0u);
 }
 
-__global__ void k_lsqr_step(const double* part_g, const double* part_tn, int nparts, int m,
+__global__ void __launch_bounds__(kLsqrStepThreads) k_lsqr_step(const double* part_g, const double* part_tn, int nparts, int m,
                             const double* Rinv, const double* RinvT, const double* bcol, LsqrVecs L,
                             int tol_mode, DevState* st, unsigned long long cond_h = 0, int cond_while = 0,
                             int maxit = 0) {
