@@ -223,7 +223,7 @@ def src_sha(files):
     return h.hexdigest()[:16]
 
 
-TRAFFIC_SRC = ("lsqr.cu", "pipe.cuh", "fab_internal.cuh")
+TRAFFIC_SRC = ("lsqr.cu", "pipe.cuh")
 
 
 def lsqr_pass_traffic(n_loc, m):

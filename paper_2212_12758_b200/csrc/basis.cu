@@ -912,6 +912,188 @@ __global__ void __launch_bounds__(kThreads, kPipeCtasPerSm) k_sketch_direct(Pipe
   }
 }
 
+// ---------------------------------------------------------------------------
+// K5 v2 (default batched sketch): tile groups with a two-round FWHT.
+//
+// k_sketch_direct spends five 32-KB shared-memory passes per 4096-row tile
+// (three radix-16 rounds) and ties 256 threads to one tile, so the tile's
+// FWHT serialises behind CTA-wide barriers (ncu: L1/TEX 78 %, 0.51 of the
+// copy bandwidth at c3).  Here a group of 64 threads owns a tile with 64
+// values per thread, so the 12 butterfly stages are two radix-64 rounds in
+// registers around ONE transpose through a padded 64 x 65 shared matrix
+// (write + read), plus the final write the gather reads: three passes.  The
+// stage ORDER is k_sketch_direct's / K3's -- idx bits 8,9,10,11,0,1 in
+// round 1, 2..7 in round 2 -- so every butterfly output is bitwise the same
+// (a stage's rounding depends only on the stages before it), and the
+// gathered terms are added per virtual CTA b (b = K3's CTA index, tiles
+// b, b + nvirt, ... in order, starting from 0.0) exactly as K3 / k_sketch_
+// direct add them: the partials are bitwise equal to the fused sketch's.
+//
+// A CTA (one per SM) runs kSkG groups that take consecutive tiles of one
+// virtual b; each group adds its tile's s terms into the CTA's accumulators
+// in tile order (a shared turn counter), so groups overlap each other's
+// loads, butterflies and transposes without CTA-wide barriers.
+//   load layout  : thread t holds idx = j | t << 2 | qh << 8, q = qh + 16 j
+//                  (one 256-bit load per qh: idx bits 0,1 contiguous)
+//   matrix       : M[a][b], a = idx bits 2..7, b = idx bits {0,1,8..11}
+//   round-2 layout: thread t' = b holds a = 0..63
+// ---------------------------------------------------------------------------
+constexpr int kSkG = 5;                   // tile groups per CTA
+constexpr int kSkGT = 64;                 // threads per group
+constexpr int kSkGV = 64;                 // values per thread
+constexpr int kSkGLd = 65;                // padded row of the 64 x 64 matrix
+constexpr int kSkGBuf = 64 * kSkGLd;      // doubles per group buffer
+constexpr int kSkGR = (3 * kThreads + kSkGT - 1) / kSkGT;   // gathered rows per thread (s <= 768)
+
+__device__ __forceinline__ void reg_fwht64(double (&v)[kSkGV]) {
+#pragma unroll
+  for (int h = 1; h < kSkGV; h <<= 1) {
+#pragma unroll
+    for (int q = 0; q < kSkGV; ++q) {
+      if ((q & h) == 0) {
+        const double x = v[q], y = v[q + h];
+        v[q] = x + y;
+        v[q + h] = x - y;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void ld256_first(const double* p, uint64_t pol, double& a, double& b, double& c,
+                                            double& d) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+               : "l"(p), "l"(pol));
+}
+
+__device__ __forceinline__ void group_sync(int g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(kSkGT) : "memory");
+}
+
+__global__ void __maxnreg__(200) k_sketch_groups(PipeArgs a, int nvirt) {
+  if (a.st->breakdown) return;
+  extern __shared__ __align__(128) double sk_smem[];
+  double* acc = sk_smem + kSkG * kSkGBuf;                       // s accumulators of the current b
+  int* loc_t = reinterpret_cast<int*>(acc + 3 * kThreads);       // sampled rows: r mod T
+  long long* hi_t = reinterpret_cast<long long*>(loc_t + 3 * kThreads);   // r / T
+  __shared__ int turn;
+  const int g = threadIdx.x / kSkGT, t = threadIdx.x % kSkGT;
+  double* buf = sk_smem + g * kSkGBuf;
+  const int s = a.s;
+  for (int p = threadIdx.x; p < s; p += blockDim.x) {
+    const int64_t r = a.rows[p];
+    loc_t[p] = (int)(r & (kSkT - 1));
+    hi_t[p] = r >> kSkLogT;
+    acc[p] = 0.0;
+  }
+  const int64_t n = a.n, rb = a.row_begin;
+  const int64_t t_first = rb >> kSkLogT, t_last = (rb + n - 1) >> kSkLogT;
+  const int ncols = a.col1 - a.col0;
+  const uint64_t pol = policy_evict_first();
+  double v[kSkGV];
+  uint32_t w[16];
+  // item it of virtual CTA b: column col0 + it / mine, tile t_first + b + (it % mine) nvirt
+  auto issue = [&](int64_t b, int64_t mine, int64_t it) {
+    const int col = a.col0 + (int)(it / mine);
+    const int64_t tile = t_first + b + (it % mine) * nvirt;
+    const int64_t g0 = tile << kSkLogT, rc0 = g0 - rb;
+    const double* src = a.V + (int64_t)col * a.ld + rc0;
+    const uint32_t* sg = a.signs + (g0 >> 5) + (t >> 3);
+#pragma unroll
+    for (int qh = 0; qh < 16; ++qh) w[qh] = __ldg(sg + (qh << 3));
+    if (rc0 >= 0 && rc0 + kSkT <= n) {
+#pragma unroll
+      for (int qh = 0; qh < 16; ++qh)
+        ld256_first(src + (qh << 8) + (t << 2), pol, v[qh], v[qh + 16], v[qh + 32], v[qh + 48]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < kSkGV; ++q) {
+        const int64_t r = rc0 + ((q >> 4) | (t << 2) | ((q & 15) << 8));
+        v[q] = (r >= 0 && r < n) ? ld_first(src + (r - rc0), pol) : 0.0;
+      }
+    }
+  };
+  for (int64_t b = blockIdx.x; b < nvirt; b += gridDim.x) {
+    const int64_t mine = t_first + b <= t_last ? (t_last - t_first - b) / nvirt + 1 : 0;
+    if (mine == 0) {   // no tile for this virtual CTA: zero partials
+      for (int col = a.col0; col < a.col1; ++col)
+        for (int p = threadIdx.x; p < s; p += blockDim.x) a.part_sk[((int64_t)col * nvirt + b) * s + p] = 0.0;
+      continue;
+    }
+    const int64_t items = mine * ncols;
+    if (threadIdx.x == 0) turn = 0;
+    __syncthreads();
+    int64_t it = g;
+    if (it < items) issue(b, mine, it);
+    for (; it < items; it += kSkG) {
+      const int64_t ti = it % mine;
+      const int col = a.col0 + (int)(it / mine);
+      const int64_t tile = t_first + b + ti * nvirt;
+      const int64_t rc0 = (tile << kSkLogT) - rb;
+      // D_tt = -1: flip the sign bit; bit of idx = j | t << 2 | qh << 8 is
+      // bit (4 (t & 7) + j) of word qh (rows outside [0, n) stay +0.0)
+      const int bs = 4 * (t & 7);
+#pragma unroll
+      for (int q = 0; q < kSkGV; ++q) {
+        const uint32_t bit = (w[q & 15] >> (bs + (q >> 4))) & 1u;
+        v[q] = __hiloint2double(__double2hiint(v[q]) ^ (int)(bit << 31), __double2loint(v[q]));
+      }
+      if (!(rc0 >= 0 && rc0 + kSkT <= n)) {
+#pragma unroll
+        for (int q = 0; q < kSkGV; ++q) {
+          const int64_t r = rc0 + ((q >> 4) | (t << 2) | ((q & 15) << 8));
+          if (!(r >= 0 && r < n)) v[q] = 0.0;
+        }
+      }
+      reg_fwht64(v);                                    // idx bits 8, 9, 10, 11, 0, 1
+#pragma unroll
+      for (int q = 0; q < kSkGV; ++q) buf[t * kSkGLd + ((q >> 4) | ((q & 15) << 2))] = v[q];   // M[a = t][b]
+      group_sync(g);
+#pragma unroll
+      for (int q = 0; q < kSkGV; ++q) v[q] = buf[q * kSkGLd + t];                             // column b = t
+      reg_fwht64(v);                                    // idx bits 2 .. 7
+#pragma unroll
+      for (int q = 0; q < kSkGV; ++q) buf[q * kSkGLd + t] = v[q];
+      if (it + kSkG < items) issue(b, mine, it + kSkG);   // the next tile's loads overlap the gather
+      group_sync(g);
+      // gather: term p = (-1)^popcount((r_p / T) & tile) * out[r_p mod T]
+      double gv[kSkGR];
+#pragma unroll
+      for (int r = 0; r < kSkGR; ++r) {
+        const int p = t + kSkGT * r;
+        gv[r] = 0.0;
+        if (p < s) {
+          const int l = loc_t[p];
+          const double x = buf[((l >> 2) & 63) * kSkGLd + ((l & 3) | ((l >> 8) << 2))];
+          gv[r] = (__popcll((unsigned long long)(hi_t[p] & tile)) & 1) ? -x : x;
+        }
+      }
+      // add in tile order (the turn counter), flush the column's partial
+      if (t == 0)
+        while (*(volatile int*)&turn != (int)it) __nanosleep(32);
+      group_sync(g);
+      const bool last = (ti == mine - 1);
+#pragma unroll
+      for (int r = 0; r < kSkGR; ++r) {
+        const int p = t + kSkGT * r;
+        if (p < s) {
+          const double sum = acc[p] + gv[r];
+          if (last) {
+            a.part_sk[((int64_t)col * nvirt + b) * s + p] = sum;
+            acc[p] = 0.0;
+          } else {
+            acc[p] = sum;
+          }
+        }
+      }
+      __threadfence_block();
+      group_sync(g);
+      if (t == 0) *(volatile int*)&turn = (int)it + 1;
+    }
+    __syncthreads();
+  }
+}
+
 static int pipe_stages(int stage_d, bool sketch, size_t* smem) {
   const size_t stage = (size_t)stage_d * sizeof(double);
   const size_t fixed = (sketch ? kSkSmem * sizeof(double) : 0) + 1024;
@@ -1318,9 +1500,19 @@ int launch_sketch_cols(fab_ctx* c, int c0, int c1, cudaStream_t st) {
   a.st = c->st_d;
   const char* re = getenv("FAB_SKETCH_RING");   // the bulk-copy ring version (A/B)
   if (re && re[0] == '1') return launch_stream<false, true, 0>(c, a, st);
-  const int smem = 2 * kSkSmem * (int)sizeof(double);
-  FAB_CUDA(ensure_dyn_smem((const void*)k_sketch_direct, smem));
-  k_sketch_direct<<<c->grid_upd, kThreads, smem, st>>>(a);
+  const char* kv = getenv("FAB_SKETCH_K5");      // "2": k_sketch_groups (A/B); default: k_sketch_direct
+  if (!(kv && kv[0] == '2')) {
+    const int smem = 2 * kSkSmem * (int)sizeof(double);
+    FAB_CUDA(ensure_dyn_smem((const void*)k_sketch_direct, smem));
+    k_sketch_direct<<<c->grid_upd, kThreads, smem, st>>>(a);
+    FAB_CHECK_LAUNCH();
+    return FAB_OK;
+  }
+  // the same partial slots (virtual CTAs = K3's grid) on one CTA per SM
+  const int smem = (kSkG * kSkGBuf + 3 * kThreads) * (int)sizeof(double) + 3 * kThreads * (4 + 8);
+  FAB_CUDA(ensure_dyn_smem((const void*)k_sketch_groups, smem));
+  const int grid = c->num_sms < c->grid_upd ? c->num_sms : c->grid_upd;
+  k_sketch_groups<<<grid, kSkG * kSkGT, smem, st>>>(a, c->grid_upd);
   FAB_CHECK_LAUNCH();
   return FAB_OK;
 }

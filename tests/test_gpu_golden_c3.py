@@ -53,6 +53,7 @@ def run():
     res = {}
     runs = {"none": dict(mode="none"), "sketch_solve": dict(mode="sketch_solve"),
             "blendenpik40": dict(mode="blendenpik", iters=40),
+            "blendenpik120": dict(mode="blendenpik", iters=120),
             "blendenpik": dict(mode="blendenpik", tol=1e-6)}
     for key, kw in runs.items():
         sv.sketch(p.s, p.sketch_seed)                   # fused sketch: the bench's order
@@ -86,7 +87,7 @@ def test_golden_basis_and_sketch(run):
     assert rel(r["R"], g["R"]) <= 1e-11
 
 
-@pytest.mark.parametrize("key", ["none", "sketch_solve", "blendenpik40", "blendenpik"])
+@pytest.mark.parametrize("key", ["none", "sketch_solve", "blendenpik40", "blendenpik120", "blendenpik"])
 def test_golden_fm_per_mode(run, key):
     p, g, meta, res = run
     r = res[key]
@@ -102,15 +103,22 @@ def test_golden_y_per_mode(run):
     p, g, meta, res = run
     assert not np.any(res["none"]["y"])
     assert rel(res["sketch_solve"]["y"], g["sketch_solve_y"]) <= 1e-10
-    # fixed L = 40 (parity mode, G-14): the same iterate on both sides
+    # L = 120: LSQR converged to the least-squares y of Eq. (7), which the
+    # data determine -- the headline kernel k_lsqr_pipe<13> held to 1e-10
+    r = res["blendenpik120"]
+    assert r["info"]["lsqr_iters"] == 120
+    assert rel(r["y"], g["blendenpik120_y"]) <= 1e-10, rel(r["y"], g["blendenpik120_y"])
+    # fixed L = 40 (parity mode, G-14): an unconverged iterate carries the
+    # implementation's rounding (reading R-3): held to 20x the oracle's own
+    # floor (the same run with R^{-1} as an explicit inverse), at least 1e-10
     r = res["blendenpik40"]
     assert r["info"]["lsqr_iters"] == 40
-    assert rel(r["y"], g["blendenpik40_y"]) <= 1e-10, rel(r["y"], g["blendenpik40_y"])
-    # tolerance mode (l.359): the oracle's iteration count; the iterate at
-    # ||M^T r|| <= 1e-6 ||M|| ||r|| is rounding-sensitive (reading R-3), so y
-    # is held to 1e-7 here and to 1e-10 in the fixed-L mode above; f_m (the
-    # output) to 1e-10 in test_golden_fm_per_mode
+    ny = rel(g["blendenpik40_inv_y"], g["blendenpik40_y"])
+    assert rel(r["y"], g["blendenpik40_y"]) <= max(1e-10, 20 * ny), (rel(r["y"], g["blendenpik40_y"]), ny)
+    # tolerance mode (l.359): the oracle's iteration count; its iterate at
+    # ||M^T r|| <= 1e-6 ||M|| ||r|| likewise at the oracle's floor; f_m (the
+    # output) at 1e-10 in test_golden_fm_per_mode
     r = res["blendenpik"]
     L = int(meta["blendenpik_lsqr"]["iters"])
     assert r["info"]["lsqr_converged"] == 1 and abs(r["info"]["lsqr_iters"] - L) <= 1
-    assert rel(r["y"], g["blendenpik_y"]) <= 1e-7, rel(r["y"], g["blendenpik_y"])
+    assert rel(r["y"], g["blendenpik_y"]) <= max(1e-10, 20 * ny), (rel(r["y"], g["blendenpik_y"]), ny)
