@@ -208,6 +208,11 @@ static void free_ctx(fab_ctx* c) {
   for (int i = 0; i < kCombChunks; ++i)
     if (c->ev_chunk[i]) cudaEventDestroy(c->ev_chunk[i]);
   if (c->copy_st) cudaStreamDestroy(c->copy_st);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+  for (cudaEvent_t e : c->ev_peer)
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
   delete c;
 }
@@ -316,6 +321,15 @@ int fab_init(fab_ctx** out, const fab_operator* A, const double* b, const fab_op
   INIT_CUDA(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking));
   for (int i = 0; i < kCombChunks; ++i) INIT_CUDA(cudaEventCreateWithFlags(&c->ev_chunk[i], cudaEventDisableTiming));
   INIT_CUDA(cudaMallocHost(&c->st_h, sizeof(DevState)));
+  if (c->comm && comm_size(c) > 1) {   // C1 on a side stream, overlapped with K1 (basis.cu)
+    INIT_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    INIT_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    INIT_CUDA(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+    if (!c->stencil) {
+      c->ev_peer.assign(comm_size(c), nullptr);
+      for (auto& e : c->ev_peer) INIT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+  }
   // b -> V[:, 0]
   INIT_CUDA(cudaMemcpyAsync(c->V, b, c->n * sizeof(double),
                             o->b_location == FAB_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,

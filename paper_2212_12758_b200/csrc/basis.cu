@@ -90,11 +90,19 @@ __device__ __forceinline__ double2 ld2(const double* p) {
 // SQ (squared operator, FAB_FLAG_SQUARE): the SpMV input is xin = A w_hat_{c-1}
 // (written by a K0 = this kernel with nw = 0), so z = A^2 w_hat_{c-1}; the
 // j = c-1 window dot then reads w_hat_{c-1} itself (one more column load).
+// Rows a launch covers: virtual rows v in [begin, end), row r = v (v < split)
+// or v + shift -- the whole block {0, n, n, 0}; on several GPUs the interior
+// {hal, n - hal, n, 0} runs while the halo is in flight and the two boundary
+// slabs {0, 2 hal, hal, n - 2 hal} after it.
+struct RowMap {
+  int64_t begin, end, split, shift;
+};
+
 template <int DIM, int NWM, bool STORE_Z, bool SQ = false, int U = (NWM <= 4 ? kK1U : 1)>
 __global__ void __launch_bounds__(kThreads, 2)
 k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, StencilP sp, int64_t n, int64_t gbase,
                  const double* __restrict__ xin, double* __restrict__ z, double* __restrict__ part,
-                 const DevState* __restrict__ st, StepRed sr) {
+                 const DevState* __restrict__ st, StepRed sr, RowMap rm, int part_off) {
   pdl_wait();
   pdl_trigger();
   // the breakdown flag is tested after the first rows' loads are issued, so
@@ -109,7 +117,7 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
   for (int t = 0; t < NWM; ++t) d[t] = 0.0;
   const int64_t gx = sp.gx, plane = (int64_t)sp.gx * sp.gy;
   const double2 zero2 = make_double2(0.0, 0.0);
-  for (int64_t base = (int64_t)blockIdx.x * (kThreads * 2 * U); base < n;
+  for (int64_t base = rm.begin + (int64_t)blockIdx.x * (kThreads * 2 * U); base < rm.end;
        base += (int64_t)gridDim.x * (kThreads * 2 * U)) {
     double2 xc[U], ym[U], yp[U], zm[U], zp[U], w[U][NWM > 1 ? NWM - 1 : 1], xd[U];
     double xl[U], xr[U];
@@ -117,8 +125,9 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
     bool ok[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t r = base + 2 * threadIdx.x + 2 * kThreads * u;
-      ok[u] = r < n;                       // n even on this path: r+1 < n too
+      const int64_t rv = base + 2 * threadIdx.x + 2 * kThreads * u;
+      const int64_t r = rv < rm.split ? rv : rv + rm.shift;
+      ok[u] = rv < rm.end;                 // n, begin, split, shift even on this path: r+1 < n too
       xc[u] = ym[u] = yp[u] = zm[u] = zp[u] = xd[u] = zero2;
       xl[u] = xr[u] = 0.0;
       ixs[u] = iys[u] = izs[u] = 0;
@@ -150,7 +159,8 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (!ok[u]) continue;
-      const int64_t r = base + 2 * threadIdx.x + 2 * kThreads * u;
+      const int64_t rv = base + 2 * threadIdx.x + 2 * kThreads * u;
+      const int64_t r = rv < rm.split ? rv : rv + rm.shift;
       const double a0 = stencil_row<DIM>(sp, ixs[u], iys[u], izs[u], xc[u].x, xl[u], xc[u].y, ym[u].x, yp[u].x,
                                          zm[u].x, zp[u].x);
       const double a1 = stencil_row<DIM>(sp, ixs[u] + 1, iys[u], izs[u], xc[u].y, xc[u].x, xr[u], ym[u].y,
@@ -172,11 +182,11 @@ k_stencil_dots_v(const double* __restrict__ V, int64_t ld, int c, int nw, Stenci
   double out[NWM];
   block_sum<NWM>(d, red, out);
   if (threadIdx.x == 0 && nw > 0) {
-    double* p = part + (int64_t)blockIdx.x * (kKMax + 1);
+    double* p = part + (int64_t)(part_off + blockIdx.x) * (kKMax + 1);
     for (int t = 0; t < nw - 1; ++t) p[t] = out[t];
     p[nw - 1] = out[NWM - 1];
   }
-  step_red_tail(sr, part, gridDim.x, nw, red);
+  step_red_tail(sr, part, part_off + gridDim.x, nw, red);
 }
 
 // scalar fallback (odd gx): one row per thread, grid-stride
@@ -1281,8 +1291,9 @@ int init_vector_norm(fab_ctx* c) {
     const int64_t nb = csr_max_blocks(c);
     if (nb < c->grid_spmv) c->grid_spmv = (int)(nb > 0 ? nb : 1);
   }
-  // per-step dot partials: one slot per CTA of K1
-  const int64_t slots = (int64_t)c->grid_spmv;
+  // per-step dot partials: one slot per CTA of K1 (two launches' worth when
+  // the halo overlaps K1 on several GPUs: interior + boundary slabs)
+  const int64_t slots = (int64_t)c->grid_spmv * (c->comm ? 2 : 1);
   if (c->part_dots) cudaFree(c->part_dots);
   FAB_CUDA(cudaMalloc(&c->part_dots, slots * (kKMax + 1) * sizeof(double)));
   return FAB_OK;
@@ -1318,13 +1329,15 @@ int enqueue_scalar(fab_ctx* c, int col, int nw, int nparts, int final_step, cuda
 // = V[:, col-1], which is xin unless the operator is squared).  xin: stencil --
 // local rows with their halo slots filled; CSR -- indexed by global column id.
 static int launch_k1(fab_ctx* c, int col, int nw, const double* xin, double* z, bool store, cudaStream_t st,
-                     int64_t* launches, int* nparts, StepRed sr = StepRed{}) {
+                     int64_t* launches, int* nparts, StepRed sr = StepRed{}, const RowMap* rmap = nullptr,
+                     int part_off = 0, int grid = 0) {
   *nparts = c->grid_spmv;
+  const RowMap rm = rmap ? *rmap : RowMap{0, c->n, c->n, 0};
   const double* x = c->V + (int64_t)(col - 1) * c->ld;
   if (c->stencil) {
     StencilP sp = stencil_params(c);
     const bool d3 = c->op.dims[2] > 1;
-    const int G = c->grid_spmv;
+    const int G = grid > 0 ? grid : c->grid_spmv;
     const int64_t gb = c->row_begin;
     const bool sq = xin != x;
     const bool pdl = c->pdl && !c->comm;
@@ -1333,13 +1346,13 @@ static int launch_k1(fab_ctx* c, int col, int nw, const double* xin, double* z, 
   do {                                                                                                       \
     if (sq)                                                                                                  \
       FAB_CUDA(launch_pdl(pdl, k_stencil_dots_v<DIM, NWM, true, true>, G, kThreads, 0, st, c->V, c->ld, col, \
-                          nw, sp, c->n, gb, xin, z, c->part_dots, (const DevState*)c->st_d, sr));            \
+                          nw, sp, c->n, gb, xin, z, c->part_dots, (const DevState*)c->st_d, sr, rm, part_off)); \
     else if (!store)                                                                                         \
       FAB_CUDA(launch_pdl(pdl, k_stencil_dots_v<DIM, NWM, false>, G, kThreads, 0, st, c->V, c->ld, col, nw,  \
-                          sp, c->n, gb, xin, z, c->part_dots, (const DevState*)c->st_d, sr));                \
+                          sp, c->n, gb, xin, z, c->part_dots, (const DevState*)c->st_d, sr, rm, part_off));    \
     else                                                                                                     \
       FAB_CUDA(launch_pdl(pdl, k_stencil_dots_v<DIM, NWM, true>, G, kThreads, 0, st, c->V, c->ld, col, nw,   \
-                          sp, c->n, gb, xin, z, c->part_dots, (const DevState*)c->st_d, sr));                \
+                          sp, c->n, gb, xin, z, c->part_dots, (const DevState*)c->st_d, sr, rm, part_off));    \
   } while (0)
       if (c->k_max <= 2) {
         if (d3) FAB_K1V(3, 2); else FAB_K1V(2, 2);
@@ -1403,6 +1416,78 @@ int enqueue_k1(fab_ctx* c, int col, int nw, double* z, bool need_z, cudaStream_t
     sr.nparts_norm = c->grid_upd;
   }
   return launch_k1(c, col, nw, xin, z, need_z || !c->mf, st, launches, nparts, sr);
+}
+
+// Several GPUs, stencil: C1 overlapped with K1.  The halo of
+// w_hat_{col-1} goes out on a side stream while K1 runs over the interior
+// rows [hal, n - hal) -- they read no halo slot -- and K1 over the two
+// boundary slabs [0, hal) and [n - hal, n) follows the halo's arrival.  The
+// two launches write disjoint partial slots (interior 0..Gi-1, boundary
+// Gi..Gi+Gb-1); the boundary launch's last CTA forms the step sums over all
+// of them (fixed order).  The result differs from the unsplit K1 only in the
+// dots' grouping (rounding).
+bool k1_split_ok(const fab_ctx* c) {
+  const char* e = getenv("FAB_HALO_OVERLAP");
+  return c->side && stencil_vec_path(c) && !(c->flags & FAB_FLAG_SQUARE) && !c->mf && c->hal > 0 &&
+         c->hal % 2 == 0 && c->n % 2 == 0 && c->n >= 4 * c->hal && !(e && e[0] == '0');
+}
+
+// CSR on several GPUs: this rank's rows into xg, then the all-gather as R-1
+// pipelined steps on the side stream; K1's column blocks are ordered by the
+// rank that owns their columns (own first), and each waits only for its
+// slice (csr_spmv, peer_ev).
+bool csr_pipe_ok(const fab_ctx* c) {
+  const char* e = getenv("FAB_HALO_OVERLAP");
+  return c->side && !c->stencil && !(c->flags & FAB_FLAG_SQUARE) && (int)c->ev_peer.size() == comm_size(c) &&
+         !(e && e[0] == '0');
+}
+
+static int enqueue_k1_csr_pipe(fab_ctx* c, int col, int nw, double* z, cudaStream_t st, int64_t* launches,
+                               int* nparts, double* step_sums) {
+  const double* x = c->V + (int64_t)(col - 1) * c->ld;
+  FAB_CUDA(cudaMemcpyAsync(c->xg + c->row_begin, x, (size_t)c->n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  FAB_CUDA(cudaEventRecord(c->ev_fork, st));
+  FAB_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+  for (int d = 1; d < comm_size(c); ++d) {
+    FAB_TRY(comm_gather_step(c, x, d, c->side));
+    FAB_CUDA(cudaEventRecord(c->ev_peer[d], c->side));
+  }
+  StepRed sr{};
+  if (step_sums) {
+    sr.count = &c->st_d->pad[0];
+    sr.sums = step_sums;
+    sr.part_norm = norm_parts(c, col - 1);
+    sr.nparts_norm = c->grid_upd;
+  }
+  return csr_spmv(c, col, nw, c->xg, z, st, launches, nparts, sr, c->ev_peer.data());
+}
+
+static int enqueue_k1_split(fab_ctx* c, int col, int nw, double* z, cudaStream_t st, int64_t* launches,
+                            int* nparts, double* step_sums) {
+  double* x = c->V + (int64_t)(col - 1) * c->ld;
+  FAB_CUDA(cudaEventRecord(c->ev_fork, st));
+  FAB_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+  FAB_TRY(comm_halo(c, x, c->side));
+  FAB_CUDA(cudaEventRecord(c->ev_halo, c->side));
+  const int64_t hal = c->hal, per = (int64_t)kThreads * 2 * kK1U;
+  const int gb_need = (int)((2 * hal + per - 1) / per);
+  const int Gb = gb_need < c->grid_spmv ? gb_need : c->grid_spmv;
+  const int Gi = c->grid_spmv;
+  const RowMap ri{hal, c->n - hal, c->n, 0};
+  const RowMap rb{0, 2 * hal, hal, c->n - 2 * hal};
+  int np = 0;
+  FAB_TRY(launch_k1(c, col, nw, x, z, true, st, launches, &np, StepRed{}, &ri, 0, Gi));   // interior
+  FAB_CUDA(cudaStreamWaitEvent(st, c->ev_halo, 0));
+  StepRed sr{};
+  if (step_sums) {
+    sr.count = &c->st_d->pad[0];
+    sr.sums = step_sums;
+    sr.part_norm = norm_parts(c, col - 1);
+    sr.nparts_norm = c->grid_upd;
+  }
+  FAB_TRY(launch_k1(c, col, nw, x, z, true, st, launches, &np, sr, &rb, Gi, Gb));           // boundary slabs
+  *nparts = Gi + Gb;
+  return FAB_OK;
 }
 
 // FAB_FLAG_SQUARE: the starting vector of the Krylov space of A^2 is A b
@@ -1475,7 +1560,12 @@ static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st,
     // C2: the last K1 CTA reduces this rank's scalars in k_scalar's order,
     // ONE allreduce of k+1 doubles, then K3 forms the step scalars from the
     // sums in its prologue: K1, allreduce, K3
-    FAB_TRY(enqueue_k1(c, col, nw, c->vec, false, st, launches, &nparts, c->red));
+    if (k1_split_ok(c))
+      FAB_TRY(enqueue_k1_split(c, col, nw, c->vec, st, launches, &nparts, c->red));
+    else if (csr_pipe_ok(c))
+      FAB_TRY(enqueue_k1_csr_pipe(c, col, nw, c->vec, st, launches, &nparts, c->red));
+    else
+      FAB_TRY(enqueue_k1(c, col, nw, c->vec, false, st, launches, &nparts, c->red));
     FAB_TRY(comm_allreduce(c, c->red, (size_t)nw + 1, false, st));
     return enqueue_k3(c, col, nw, fused, st, launches, nparts, c->red);
   }

@@ -304,6 +304,30 @@ int comm_gather_x(fab_ctx* c, const double* x, cudaStream_t st) {
   return FAB_OK;
 }
 
+// C1 (CSR), pipelined: step d of the all-gather -- this rank's rows go to rank
+// - d, rank + d's rows arrive in xg (the caller copied its own rows into xg
+// first).  K1 runs the column block of rank + d as soon as step d is done.
+int comm_gather_step(fab_ctx* c, const double* x, int d, cudaStream_t st) {
+  const int r = c->comm->rank, P = c->comm->nranks;
+  const int to = (r - d + P) % P, from = (r + d) % P;
+  const int64_t b0 = c->rank_rows[from], b1 = c->rank_rows[from + 1];
+  if (c->comm->loop) {
+    LoopGroup* g = c->comm->loop;
+    FAB_TRY(loop_publish(c, x, st));
+    FAB_TRY(loop_wait(c, g->ev_ready, from, st));
+    FAB_CUDA(cudaMemcpyAsync(c->xg + b0, g->ptr[from], (size_t)(b1 - b0) * sizeof(double), cudaMemcpyDeviceToDevice,
+                             st));
+    return loop_release(c, st);
+  }
+  NcclApi* api = nccl_api();
+  if (!api) return FAB_ENCCL;
+  FAB_NCCL(api->groupStart());
+  FAB_NCCL(api->send(x, (size_t)c->n, ncclFloat64, to, c->comm->nc, st));
+  FAB_NCCL(api->recv(c->xg + b0, (size_t)(b1 - b0), ncclFloat64, from, c->comm->nc, st));
+  FAB_NCCL(api->groupEnd());
+  return FAB_OK;
+}
+
 // Collect every rank's [row_begin, row_end) and check that the blocks are
 // contiguous, in rank order and cover [0, n): rank_rows[p] = row_begin of p.
 int comm_setup_partition(fab_ctx* c) {

@@ -305,6 +305,7 @@ struct CsrPass {
 
 struct CsrPlan {
   std::vector<CsrPass> pass;
+  std::vector<int> ord;       // several GPUs: pass j reads x of rank (rank + ord[j]) mod P (0 = own rows)
   std::vector<void*> owned;   // device buffers of the column-blocked copy
   int64_t width = 0;          // columns per block (0: not column-blocked)
   bool uniform = false;       // every value equals v0: the value array is dropped
@@ -355,9 +356,10 @@ struct PlanKey {
   const void *rp, *ci, *va;
   int64_t n, row_begin, nnz, width;
   unsigned long long fp;
+  int nranks;
   bool operator==(const PlanKey& o) const {
     return device == o.device && rp == o.rp && ci == o.ci && va == o.va && n == o.n && row_begin == o.row_begin &&
-           nnz == o.nnz && width == o.width && fp == o.fp;
+           nnz == o.nnz && width == o.width && fp == o.fp && nranks == o.nranks;
   }
 };
 
@@ -449,7 +451,8 @@ int csr_setup(fab_ctx* c) {
   if (env && atoll(env) > 0) width = atoll(env);
   unsigned long long fp = 0;
   FAB_TRY(operator_fingerprint(c, &fp));
-  const PlanKey key{c->device, c->op.row_ptr, c->op.col_idx, c->op.values, c->n, c->row_begin, c->op.nnz, width, fp};
+  const PlanKey key{c->device, c->op.row_ptr, c->op.col_idx, c->op.values, c->n, c->row_begin, c->op.nnz, width, fp,
+                    comm_size(c)};
   std::shared_ptr<CsrPlan> sp;
   {
     std::lock_guard<std::mutex> lk(g_plan_mu);
@@ -499,7 +502,47 @@ static int build_plan(fab_ctx* c, CsrPlan* plan, int64_t width) {
   const int64_t n = c->n, nnz = c->op.nnz;
   std::vector<int64_t> rp(n + 1);
   FAB_CUDA(cudaMemcpy(rp.data(), c->op.row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
-  const int64_t P = (c->n_global + width - 1) / width;
+  // Column blocks.  One GPU: [j w, (j+1) w).  Several GPUs (R ranks): the
+  // own columns first (pieces of <= w columns), then the other ranks' in
+  // the order the pipelined all-gather delivers them (C1 step o brings rank
+  // + o's slice), merged greedily into blocks of <= w columns (a slice wider
+  // than w is cut into pieces).  K1 runs the blocks in order, each as soon
+  // as the last slice it reads has arrived, so the gather overlaps the SpMV;
+  // merging keeps the number of z = / z += passes near the one-GPU count.
+  const int R = comm_size(c), me = comm_rank(c);
+  const bool split = R > 1;
+  std::vector<std::vector<int64_t>> piece_blk(R);   // block of piece p of rank me + o
+  std::vector<int> blk_ord;                          // last delivery step a block waits for
+  int64_t P;
+  if (split) {
+    int64_t cur = -1, cur_cols = 0;
+    for (int o = 0; o < R; ++o) {
+      const int q = (me + o) % R;
+      const int64_t len = c->rank_rows[q + 1] - c->rank_rows[q];
+      const int64_t np = (len + width - 1) / width;
+      for (int64_t p = 0; p < np; ++p) {
+        const int64_t pl = (p + 1) * width < len ? width : len - p * width;
+        if (o == 0 || cur < 0 || blk_ord[cur] == 0 || cur_cols + pl > width) {
+          blk_ord.push_back(o);
+          cur = (int64_t)blk_ord.size() - 1;
+          cur_cols = 0;
+        }
+        blk_ord[cur] = o;
+        cur_cols += pl;
+        piece_blk[o].push_back(cur);
+      }
+    }
+    P = (int64_t)blk_ord.size();
+  } else {
+    P = (c->n_global + width - 1) / width;
+  }
+  auto block_of = [&](int64_t col) -> int64_t {
+    if (!split) return col / width;
+    const int q = (int)(std::upper_bound(c->rank_rows.begin(), c->rank_rows.end(), col) - c->rank_rows.begin()) - 1;
+    const int o = (q - me + R) % R;
+    return piece_blk[o][(col - c->rank_rows[q]) / width];
+  };
+  auto ord_of_block = [&](int64_t j) -> int { return split ? blk_ord[j] : 0; };
   if (P <= 1 || nnz == 0) {
     CsrPass p;
     p.rp64 = c->op.row_ptr;
@@ -507,6 +550,7 @@ static int build_plan(fab_ctx* c, CsrPlan* plan, int64_t width) {
     p.vals = values;
     FAB_TRY(upload_blocks(build_blocks(n, kCsrNB, [&](int64_t r) { return rp[r]; }), &p));
     plan->pass.push_back(p);
+    plan->ord.push_back(0);
     return FAB_OK;
   }
   // column-blocked copy: entries of block j (columns [j w, (j+1) w)) of every
@@ -529,7 +573,7 @@ static int build_plan(fab_ctx* c, CsrPlan* plan, int64_t width) {
     for (int t = 0; t < T; ++t)
       th.emplace_back([&, t]() {
         int64_t* ct = cnt.data() + (size_t)t * P;
-        for (int64_t q = rp[rlo[t]]; q < rp[rlo[t + 1]]; ++q) ++ct[ci[q] / width];
+        for (int64_t q = rp[rlo[t]]; q < rp[rlo[t + 1]]; ++q) ++ct[block_of(ci[q])];
       });
     for (auto& x : th) x.join();
   }
@@ -553,7 +597,7 @@ static int build_plan(fab_ctx* c, CsrPlan* plan, int64_t width) {
         for (int64_t r = rlo[t]; r < rlo[t + 1]; ++r) {
           for (int64_t j = 0; j < P; ++j) rp2[(size_t)j * (n + 1) + r] = (int32_t)fill[j];
           for (int64_t q = rp[r]; q < rp[r + 1]; ++q) {
-            const int64_t j = ci[q] / width;
+            const int64_t j = block_of(ci[q]);
             const int64_t dst = base[j] + fill[j]++;
             ci2[dst] = ci[q];
             if (!va.empty()) va2[dst] = va[q];
@@ -588,12 +632,15 @@ static int build_plan(fab_ctx* c, CsrPlan* plan, int64_t width) {
     for (auto& x : th) x.join();
   }
   for (int64_t j = 0; j < P; ++j) {
+    // an empty block is skipped, except the first (z = ... starts there)
+    if (j > 0 && base[j + 1] == base[j]) continue;
     CsrPass p;
     p.rp32 = drp + (size_t)j * (n + 1);
     p.ci = dci + base[j];
     p.vals = dva ? dva + base[j] : nullptr;
     FAB_TRY(upload_blocks(bls[j], &p));
     plan->pass.push_back(p);
+    plan->ord.push_back(ord_of_block(j));
   }
   return FAB_OK;
 }
@@ -660,13 +707,17 @@ static cudaError_t launch_pass(const CsrArgs& a, int grid, int p, bool acc, bool
 // block.  The grid and the row blocks are cs[0]'s, so per vector the
 // partials are those of a single-RHS launch.
 int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* const* xin, double* const* z,
-                   cudaStream_t st, int64_t* launches, int* nparts, const double* xi, StepRed sr) {
+                   cudaStream_t st, int64_t* launches, int* nparts, const double* xi, StepRed sr,
+                   const cudaEvent_t* peer_ev) {
   fab_ctx* c = cs[0];
   CsrPlan* plan = c->csr;
   if (!plan || plan->pass.empty() || p < 1 || p > kBatchMax) return FAB_EORDER;
   *nparts = c->grid_spmv;
   const int np = (int)plan->pass.size();
+  int waited = 0;   // peer_ev[o]: the slice of rank (rank + o) has arrived in xin (pipelined C1)
   for (int j = 0; j < np; ++j) {
+    if (peer_ev)
+      while (waited < plan->ord[j]) FAB_CUDA(cudaStreamWaitEvent(st, peer_ev[++waited], 0));
     const CsrPass& ps = plan->pass[j];
     CsrArgs a;
     memset(&a, 0, sizeof(a));
@@ -697,12 +748,14 @@ int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* con
     FAB_CHECK_LAUNCH();
     ++*launches;
   }
+  if (peer_ev)   // join every gather step (the side stream ends inside this step)
+    while (waited < comm_size(c) - 1) FAB_CUDA(cudaStreamWaitEvent(st, peer_ev[++waited], 0));
   return FAB_OK;
 }
 
 int csr_spmv(fab_ctx* c, int col, int nw, const double* xin, double* z, cudaStream_t st, int64_t* launches,
-             int* nparts, StepRed sr) {
-  return csr_spmv_multi(&c, 1, col, nw, &xin, &z, st, launches, nparts, nullptr, sr);
+             int* nparts, StepRed sr, const cudaEvent_t* peer_ev) {
+  return csr_spmv_multi(&c, 1, col, nw, &xin, &z, st, launches, nparts, nullptr, sr, peer_ev);
 }
 
 }  // namespace fab

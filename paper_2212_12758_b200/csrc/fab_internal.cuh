@@ -67,6 +67,9 @@ struct fab_ctx {
   cudaStream_t cap = nullptr;      // internal stream used for graph capture
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_join = nullptr;
   cudaStream_t copy_st = nullptr;                 // device-to-host copies overlapped with the combination
+  cudaStream_t side = nullptr;                    // several GPUs: C1 halo overlapped with K1's interior
+  cudaEvent_t ev_fork = nullptr, ev_halo = nullptr;
+  std::vector<cudaEvent_t> ev_peer;               // CSR on several GPUs: step d of the pipelined all-gather done
   cudaEvent_t ev_chunk[8] = {};                   // one per combination chunk (kCombChunks)
 
   // operator
@@ -358,6 +361,7 @@ int comm_size(const fab_ctx* c);
 int comm_allreduce(fab_ctx* c, double* buf, size_t count, bool use_max, cudaStream_t st);
 int comm_halo(fab_ctx* c, double* x, cudaStream_t st);
 int comm_gather_x(fab_ctx* c, const double* x, cudaStream_t st);
+int comm_gather_step(fab_ctx* c, const double* x, int d, cudaStream_t st);   // pipelined C1: slice of rank + d
 int comm_setup_partition(fab_ctx* c);
 bool comm_graphable(const fab_ctx* c);       // false for a loopback rank: enqueue eagerly
 const char* nccl_last_error();
@@ -376,10 +380,11 @@ int run_basis_whiten(fab_ctx* c, int m, int k, double cond_max, int* whitened_at
 int csr_grid(fab_ctx* c, int* grid);
 int csr_setup(fab_ctx* c);                   // uniform values, row blocks, column blocking
 int csr_spmv(fab_ctx* c, int col, int nw, const double* xin, double* z, cudaStream_t st, int64_t* launches,
-             int* nparts, StepRed sr = StepRed{});
+             int* nparts, StepRed sr = StepRed{}, const cudaEvent_t* peer_ev = nullptr);
 int csr_passes(const fab_ctx* c);
 int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* const* xin, double* const* z,
-                   cudaStream_t st, int64_t* launches, int* nparts, const double* xi, StepRed sr = StepRed{});
+                   cudaStream_t st, int64_t* launches, int* nparts, const double* xi, StepRed sr = StepRed{},
+                   const cudaEvent_t* peer_ev = nullptr);
 int csr_interleave(fab_ctx* c, int p, const double* const* x, double* xi, cudaStream_t st, int64_t* launches);
 bool csr_interleave_fits(const fab_ctx* c, int p);
 constexpr int kBatchMaxCtx = 4;              // fab_basis_batch: contexts per call

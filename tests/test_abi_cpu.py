@@ -26,9 +26,35 @@ def test_library_exports_every_declared_symbol():
     assert set(names) == set(_lib.EXPORTS)
 
 
+def test_struct_layouts_match_header(tmp_path):
+    """The ctypes mirrors of fab_operator / fab_opts / fab_lsqr_opts /
+    fab_info have the C compiler's size and every field's offset (gcc on
+    include/fab.h), so the binding marshals exactly what the ABI declares."""
+    import subprocess
+    from paper_2212_12758_b200 import _lib
+    structs = {"fab_operator": _lib.FabOperator, "fab_opts": _lib.FabOpts, "fab_lsqr_opts": _lib.FabLsqrOpts,
+               "fab_info": _lib.FabInfo}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "fab.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ["return 0; }"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {tuple(ln.split()[:2]): int(ln.split()[2]) for ln in out if ln.strip()}
+    for cname, py in structs.items():
+        assert got[(cname, "sizeof")] == C.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert got[(cname, fname)] == getattr(py, fname).offset, (cname, fname)
+
+
 def test_version_and_strerror():
     from paper_2212_12758_b200 import _lib
-    assert _lib.lib.fab_version() == 1
+    assert _lib.lib.fab_version() == 2
     for code in (0, 1, 2, 3, -1, -2, -3, -4, -5, -6, -7, -8, -9):
         assert len(_lib.lib.fab_strerror(code)) > 0
     assert _lib.lib.fab_strerror(12345) == b"unknown status"

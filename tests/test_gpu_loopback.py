@@ -159,6 +159,30 @@ def test_loopback_partitioned_parity(name, kw, P, csr):
         assert res[0]["info"]["m_eff"] == ref["m_eff"]
 
 
+@pytest.mark.parametrize("name,kw,P", [("c3", dict(g=32, m=60, s=120), 4), ("c1", {}, 3),
+                                       ("c5", dict(n=20000 + 77, m=40, s=80), 3),
+                                       ("c4", dict(n=1 << 15, m=20, s=40), 4)])
+def test_loopback_halo_overlap_split(name, kw, P, monkeypatch):
+    """C1 overlapped with K1.  Stencil: the halo on a side stream while K1
+    runs the interior rows, then the boundary slabs.  CSR: the all-gather as
+    R-1 pipelined steps on a side stream, K1's column blocks ordered by the
+    owning rank (own columns first), each waiting only for its slice.  The
+    same solve as the serialised C1 up to the grouping of partial sums."""
+    p = fp.make(name, **kw)
+    monkeypatch.setenv("FAB_HALO_OVERLAP", "0")
+    _, r0 = run_partitioned(p, P, "blendenpik")
+    monkeypatch.setenv("FAB_HALO_OVERLAP", "1")
+    _, r1 = run_partitioned(p, P, "blendenpik")
+    y0 = np.concatenate([r["y"] for r in r0])
+    y1 = np.concatenate([r["y"] for r in r1])
+    assert rel(y1, y0) <= 1e-12
+    assert rel(r1[0]["H"], r0[0]["H"]) <= 1e-12
+    check_replicated(r1, ["H", "SV", "C", "yls"])
+    ref = ofab.solve(p.scipy(), p.b, p.m, p.k, p.s, p.sketch_seed, mode="blendenpik", f=p.f, alpha=p.alpha,
+                     sigma=p.sigma, lsqr_iters=40)
+    assert rel(y1, ref["f_m"]) <= 1e-10
+
+
 def test_loopback_other_bases_and_sign():
     """Algorithm 1 (+ Algorithm 3), full Arnoldi (+ FOM) and sign(A) b (the
     squared operator: halo / all-gather of t = A w) over loopback ranks."""
