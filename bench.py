@@ -31,6 +31,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Krylov iterations/sec and f(A)b solves/sec at n=16M, m=200; HBM GB/s vs peak"
+PRE_S = 768   # Blendenpik preconditioner sketch rows of the precond variant (= s_max cap, ~3.8 m)
 WORKLOAD = ("c3: 3D 7-point upwind convection-diffusion, 256^3 grid (n=16,777,216), fp64, "
             "f=sqrt(A + 1e-2||A||_inf I), seeded Gaussian b, m=200, k=4, s=400, "
             "Algorithm 4 (Blendenpik-LSQR tol 1e-6)")
@@ -405,16 +406,19 @@ def main():
     b_np = np.ascontiguousarray(p.b[r0:r1])
     b = torch.as_tensor(b_np).cuda(dev)
     stream = torch.cuda.current_stream(dev)
-    sv = fab.Solver(op, b, m_max=p.m, k_max=p.k, s_max=p.s, device=dev, profile=True, comm=comm)
+    # s_max leaves room for the Blendenpik preconditioner-sketch variant
+    # (precond_s = PRE_S rows, reading G-12); the headline keeps s = 400
+    sv = fab.Solver(op, b, m_max=p.m, k_max=p.k, s_max=max(p.s, PRE_S), device=dev, profile=True, comm=comm)
     y = torch.empty(n_loc, dtype=torch.float64, device=f"cuda:{dev}")
 
-    def step(mode="blendenpik", fused=True, iters=0):
+    def step(mode="blendenpik", fused=True, iters=0, precond_s=0):
         if mode != "none" and fused:
             sv.sketch(p.s, p.sketch_seed)
         sv.basis(p.m, p.k)
         if mode != "none" and not fused:
             sv.sketch(p.s, p.sketch_seed)
-        sv.compress(mode, iters=iters, tol=0.0 if iters else 1e-6)
+        sv.compress(mode, iters=iters, tol=0.0 if iters else 1e-6, precond_s=precond_s,
+                    precond_seed=p.sketch_seed + 1 if precond_s else -1)
         sv.apply(p.f, p.alpha, p.sigma, out=y)
         return sv.info()
 
@@ -564,6 +568,19 @@ def main():
                                           "gram_gflops": 2.0 * n_loc * (m + 1) ** 2 / 2 /
                                           max(inf["ms_lsqr_pass"], 1e-9) / 1e6}
             side("blendenpik_gram", gram)
+
+        def precond():
+            # Blendenpik with its own preconditioner sketch Theta' of PRE_S
+            # rows ("once again, a SRHT"; fab_lsqr_opts.
+            # precond_s / precond_seed): one more pass over V_m (K5), fewer
+            # LSQR passes.  A variant, not the headline (which keeps s = 2m).
+            ms, inf = timed(lambda: step("blendenpik", precond_s=PRE_S))
+            modes["blendenpik_precond"] = 1e3 / ms
+            out["blendenpik_precond"] = {"solves_per_s": 1e3 / ms, "precond_s": PRE_S,
+                                         "lsqr_iters": inf["lsqr_iters"],
+                                         "precond_sketch_ms": inf["ms_precond_sketch"],
+                                         "compress_ms": inf["ms_compress"]}
+        side("blendenpik_precond", precond)
 
         def api_order():
             # API-order variant: sketch after the basis (batched SRHT pass)

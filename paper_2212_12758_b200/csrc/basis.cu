@@ -939,16 +939,18 @@ __global__ void __launch_bounds__(kThreads, kPipeCtasPerSm) k_sketch_direct(Pipe
 // b, b + nvirt, ... in order, starting from 0.0) exactly as K3 / k_sketch_
 // direct add them: the partials are bitwise equal to the fused sketch's.
 //
-// A CTA (one per SM) runs kSkG groups that take consecutive tiles of one
-// virtual b; each group adds its tile's s terms into the CTA's accumulators
-// in tile order (a shared turn counter), so groups overlap each other's
-// loads, butterflies and transposes without CTA-wide barriers.
+// A CTA runs kSkG groups that take alternate tiles of one virtual b (two
+// CTAs per SM: four groups, eight warps; 64 values per thread need ~200
+// registers, and the register file is split per SM sub-partition); each
+// group adds its tile's s terms into the CTA's accumulators in tile order
+// (a shared turn counter), so the groups overlap each other's loads,
+// butterflies and transposes without CTA-wide barriers.
 //   load layout  : thread t holds idx = j | t << 2 | qh << 8, q = qh + 16 j
 //                  (one 256-bit load per qh: idx bits 0,1 contiguous)
 //   matrix       : M[a][b], a = idx bits 2..7, b = idx bits {0,1,8..11}
 //   round-2 layout: thread t' = b holds a = 0..63
 // ---------------------------------------------------------------------------
-constexpr int kSkG = 5;                   // tile groups per CTA
+constexpr int kSkG = 2;                   // tile groups per CTA (2 CTAs per SM)
 constexpr int kSkGT = 64;                 // threads per group
 constexpr int kSkGV = 64;                 // values per thread
 constexpr int kSkGLd = 65;                // padded row of the 64 x 64 matrix
@@ -980,7 +982,7 @@ __device__ __forceinline__ void group_sync(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(kSkGT) : "memory");
 }
 
-__global__ void __maxnreg__(200) k_sketch_groups(PipeArgs a, int nvirt) {
+__global__ void __launch_bounds__(kSkG * kSkGT, 2) k_sketch_groups(PipeArgs a, int nvirt) {
   if (a.st->breakdown) return;
   extern __shared__ __align__(128) double sk_smem[];
   double* acc = sk_smem + kSkG * kSkGBuf;                       // s accumulators of the current b
@@ -1601,8 +1603,7 @@ int launch_sketch_cols(fab_ctx* c, int c0, int c1, cudaStream_t st) {
   // the same partial slots (virtual CTAs = K3's grid) on one CTA per SM
   const int smem = (kSkG * kSkGBuf + 3 * kThreads) * (int)sizeof(double) + 3 * kThreads * (4 + 8);
   FAB_CUDA(ensure_dyn_smem((const void*)k_sketch_groups, smem));
-  const int grid = c->num_sms < c->grid_upd ? c->num_sms : c->grid_upd;
-  k_sketch_groups<<<grid, kSkG * kSkGT, smem, st>>>(a, c->grid_upd);
+  k_sketch_groups<<<c->grid_upd, kSkG * kSkGT, smem, st>>>(a, c->grid_upd);
   FAB_CHECK_LAUNCH();
   return FAB_OK;
 }

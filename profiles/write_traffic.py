@@ -39,7 +39,7 @@ def main():
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     rd *= scale.get(units["dram__bytes_read.sum"], 1.0)
     wr *= scale.get(units["dram__bytes_write.sum"], 1.0)
-    tscale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}
+    tscale = {"ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}
     dur *= tscale.get(units["gpu__time_duration.sum"], 1.0)
     import bench
     rec = {"capture": name, "kernel": d["Kernel Name"][:120], "n": n, "m": m,

@@ -82,7 +82,12 @@ def test_golden_basis_and_sketch(run):
     r = res["blendenpik40"]
     assert np.array_equal(r["rows"], g["rows"])                       # bit-exact (G-10)
     assert rel(r["H"], g["H"]) <= 1e-12
-    assert np.abs(r["SV"] - g["SV"]).max() <= 1e-13 * np.abs(g["SV"]).max()
+    # Theta V of the GPU's basis against Theta V of the oracle's: per column
+    # the sketch's own rounding (1e-13, tests/test_gpu_fullsize.py checks it
+    # on the GPU's columns) plus Theta applied to the two bases' difference,
+    # which grows with the column index like H's (<= 1e-12 relative)
+    dcol = np.linalg.norm(r["SV"] - g["SV"], axis=0) / np.linalg.norm(g["SV"], axis=0)
+    assert dcol.max() <= 1e-12, dcol.max()
     assert np.abs(r["vrows"] - g["vrows"]).max() <= 1e-10
     assert rel(r["R"], g["R"]) <= 1e-11
 
@@ -96,7 +101,13 @@ def test_golden_fm_per_mode(run, key):
     assert np.abs(r["blocks"] - g[f"{key}_fm_blocks"]).max() <= 1e-10 * np.abs(g[f"{key}_fm_blocks"]).max()
     assert abs(r["norm"] - float(g[f"{key}_fm_norm"])) <= 1e-10 * float(g[f"{key}_fm_norm"])
     assert rel(r["c"], g[f"{key}_c"]) <= 1e-10
-    assert rel(r["C_last"], g[f"{key}_C_last"]) <= 1e-10
+    # C_m's last column carries h_{m+1,m} y: determined to 1e-10 where y is
+    # (sketch-and-solve, the converged L = 120); for the unconverged
+    # iterates (L = 40, tol 1e-6) to 20x the oracle's own floor (reading R-3)
+    tol = 1e-10
+    if key in ("blendenpik40", "blendenpik"):
+        tol = max(tol, 20 * rel(g["blendenpik40_inv_C_last"], g["blendenpik40_C_last"]))
+    assert rel(r["C_last"], g[f"{key}_C_last"]) <= tol, (rel(r["C_last"], g[f"{key}_C_last"]), tol)
 
 
 def test_golden_y_per_mode(run):
