@@ -321,7 +321,7 @@ int fab_init(fab_ctx** out, const fab_operator* A, const double* b, const fab_op
   INIT_CUDA(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking));
   for (int i = 0; i < kCombChunks; ++i) INIT_CUDA(cudaEventCreateWithFlags(&c->ev_chunk[i], cudaEventDisableTiming));
   INIT_CUDA(cudaMallocHost(&c->st_h, sizeof(DevState)));
-  if (c->comm && comm_size(c) > 1) {   // C1 on a side stream, overlapped with K1 (basis.cu)
+  if ((c->comm && comm_size(c) > 1) || k1_forced_split(c)) {   // C1 on a side stream, overlapped with K1 (basis.cu)
     INIT_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     INIT_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     INIT_CUDA(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));

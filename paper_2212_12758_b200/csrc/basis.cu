@@ -1295,7 +1295,8 @@ int init_vector_norm(fab_ctx* c) {
   }
   // per-step dot partials: one slot per CTA of K1 (two launches' worth when
   // the halo overlaps K1 on several GPUs: interior + boundary slabs)
-  const int64_t slots = (int64_t)c->grid_spmv * (c->comm ? 2 : 1);
+  const char* fs = getenv("FAB_FORCE_K1_SPLIT");
+  const int64_t slots = (int64_t)c->grid_spmv * ((c->comm || (fs && fs[0] == '1')) ? 2 : 1);
   if (c->part_dots) cudaFree(c->part_dots);
   FAB_CUDA(cudaMalloc(&c->part_dots, slots * (kKMax + 1) * sizeof(double)));
   return FAB_OK;
@@ -1428,10 +1429,24 @@ int enqueue_k1(fab_ctx* c, int col, int nw, double* z, bool need_z, cudaStream_t
 // Gi..Gi+Gb-1); the boundary launch's last CTA forms the step sums over all
 // of them (fixed order).  The result differs from the unsplit K1 only in the
 // dots' grouping (rounding).
+// boundary-slab width: the halo on several GPUs; FAB_FORCE_K1_SPLIT=1 on one
+// GPU (timing the split's own cost) uses the stencil's widest
+// offset as if the block had neighbours
+static int64_t split_rows(const fab_ctx* c) {
+  if (c->hal > 0) return c->hal;
+  return c->op.dims[2] > 1 ? c->op.dims[0] * c->op.dims[1] : c->op.dims[0];
+}
+
+bool k1_forced_split(const fab_ctx* c) {
+  const char* f = getenv("FAB_FORCE_K1_SPLIT");
+  return !c->comm && c->stencil && f && f[0] == '1';
+}
+
 bool k1_split_ok(const fab_ctx* c) {
   const char* e = getenv("FAB_HALO_OVERLAP");
-  return c->side && stencil_vec_path(c) && !(c->flags & FAB_FLAG_SQUARE) && !c->mf && c->hal > 0 &&
-         c->hal % 2 == 0 && c->n % 2 == 0 && c->n >= 4 * c->hal && !(e && e[0] == '0');
+  const int64_t h = split_rows(c);
+  return c->side && stencil_vec_path(c) && !(c->flags & FAB_FLAG_SQUARE) && !c->mf && h > 0 && h % 2 == 0 &&
+         c->n % 2 == 0 && c->n >= 4 * h && !(e && e[0] == '0');
 }
 
 // CSR on several GPUs: this rank's rows into xg, then the all-gather as R-1
@@ -1471,7 +1486,7 @@ static int enqueue_k1_split(fab_ctx* c, int col, int nw, double* z, cudaStream_t
   FAB_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
   FAB_TRY(comm_halo(c, x, c->side));
   FAB_CUDA(cudaEventRecord(c->ev_halo, c->side));
-  const int64_t hal = c->hal, per = (int64_t)kThreads * 2 * kK1U;
+  const int64_t hal = split_rows(c), per = (int64_t)kThreads * 2 * kK1U;
   const int gb_need = (int)((2 * hal + per - 1) / per);
   const int Gb = gb_need < c->grid_spmv ? gb_need : c->grid_spmv;
   const int Gi = c->grid_spmv;
@@ -1571,7 +1586,10 @@ static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st,
     FAB_TRY(comm_allreduce(c, c->red, (size_t)nw + 1, false, st));
     return enqueue_k3(c, col, nw, fused, st, launches, nparts, c->red);
   }
-  FAB_TRY(enqueue_k1(c, col, nw, c->vec, false, st, launches, &nparts));
+  if (k1_forced_split(c) && k1_split_ok(c))   // one GPU, timing the multi-GPU K1 split (no halo to send)
+    FAB_TRY(enqueue_k1_split(c, col, nw, c->vec, st, launches, &nparts, nullptr));
+  else
+    FAB_TRY(enqueue_k1(c, col, nw, c->vec, false, st, launches, &nparts));
   return enqueue_k3(c, col, nw, fused, st, launches, nparts);   // K2 fused into K3
 }
 

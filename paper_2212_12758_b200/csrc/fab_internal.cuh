@@ -364,6 +364,7 @@ int comm_gather_x(fab_ctx* c, const double* x, cudaStream_t st);
 int comm_gather_step(fab_ctx* c, const double* x, int d, cudaStream_t st);   // pipelined C1: slice of rank + d
 int comm_setup_partition(fab_ctx* c);
 bool comm_graphable(const fab_ctx* c);       // false for a loopback rank: enqueue eagerly
+bool k1_forced_split(const fab_ctx* c);      // basis.cu: FAB_FORCE_K1_SPLIT=1 (one GPU, timing only)
 const char* nccl_last_error();
 // basis.cu
 int basis_setup_grids(fab_ctx* c);

@@ -183,6 +183,28 @@ def test_loopback_halo_overlap_split(name, kw, P, monkeypatch):
     assert rel(y1, ref["f_m"]) <= 1e-10
 
 
+def test_forced_k1_split_one_gpu(monkeypatch):
+    """FAB_FORCE_K1_SPLIT=1 on one GPU runs the ranks' K1 structure
+    (interior rows, then the boundary slabs; the timing knob of DESIGN.md
+    §9): the same solve up to the dots' grouping, oracle parity kept."""
+    import torch
+    import paper_2212_12758_b200 as fab
+    p = fp.make("c3", g=48, m=60, s=120)
+    ys = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("FAB_FORCE_K1_SPLIT", flag)
+        sv = fab.Solver(fab.Operator.from_problem(p), torch.as_tensor(p.b).cuda(), p.m, p.k, p.s)
+        sv.sketch(p.s, p.sketch_seed)
+        sv.basis(p.m, p.k)
+        sv.compress("blendenpik", iters=40)
+        ys.append((sv.apply(p.f, p.alpha, p.sigma).cpu().numpy(), sv.get("H")))
+        sv.close()
+    assert rel(ys[1][0], ys[0][0]) <= 1e-12 and rel(ys[1][1], ys[0][1]) <= 1e-12
+    ref = ofab.solve(p.scipy(), p.b, p.m, p.k, p.s, p.sketch_seed, mode="blendenpik", f=p.f, alpha=p.alpha,
+                     sigma=p.sigma, lsqr_iters=40)
+    assert rel(ys[1][0], ref["f_m"]) <= 1e-10
+
+
 def test_loopback_other_bases_and_sign():
     """Algorithm 1 (+ Algorithm 3), full Arnoldi (+ FOM) and sign(A) b (the
     squared operator: halo / all-gather of t = A w) over loopback ranks."""
