@@ -104,7 +104,20 @@ enum {
      workspace, the second fuses the window dots); fab_init (and fab_set of a
      new b) replaces b by A b, so gamma_b = ||A b||.  fab_apply(FAB_SIGN, 1, 0)
      then returns sign(A) b.  The breakdown threshold is 1e-14 ||A||_inf^2. */
-  FAB_FLAG_SQUARE = 2
+  FAB_FLAG_SQUARE = 2,
+  /* Asynchronous Algorithm 2 + compression (only fab_apply
+     synchronizes).  fab_basis and fab_compress enqueue their work on
+     opts->stream and return FAB_OK without waiting; their status -- a
+     breakdown (m_eff), cond(R) (ILLCOND / ESINGULAR), the LSQR outcome
+     (NOTCONV), the phase times -- is resolved at the next synchronizing call
+     (fab_apply, fab_get*, fab_sketch, fab_set, another fab_basis), which
+     returns it.  fab_compress assumes m_eff = m; if the basis broke down,
+     the resolution re-runs the compression synchronously on the m_eff
+     columns, so the result is the synchronous one.  Applies on one GPU
+     (no communicator) without FAB_FLAG_PROFILE and for the modes
+     BLENDENPIK / SKETCH_SOLVE / NONE / LSQR (GRAM decides its path on the
+     host: synchronous); otherwise the calls behave synchronously. */
+  FAB_FLAG_ASYNC = 4
 };
 
 typedef struct fab_ctx fab_ctx;

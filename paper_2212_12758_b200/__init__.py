@@ -87,12 +87,14 @@ class Operator:
 
 class Solver:
     def __init__(self, op: Operator, b, m_max, k_max=2, s_max=0, stream=None, device=None,
-                 workspace=True, profile=False, comm=None, square=False):
+                 workspace=True, profile=False, comm=None, square=False, asynchronous=False):
         """b: this rank's rows (numpy host array or CUDA float64 tensor).
         comm: dist.Comm for a row-partitioned multi-GPU solve (every rank
         makes the same calls in the same order), None on one GPU.
         square: Krylov space of A^2 started from A b (FAB_FLAG_SQUARE), so
-        apply("sign") = (A^2)^{-1/2} (A b) = sign(A) b."""
+        apply("sign") = (A^2)^{-1/2} (A b) = sign(A) b.
+        asynchronous: FAB_FLAG_ASYNC -- basis() and compress() only enqueue;
+        their status is resolved (and returned) by apply() / get()."""
         torch = _torch()
         self.op = op
         self.torch = torch
@@ -104,7 +106,8 @@ class Solver:
         o.device = dev
         o.m_max, o.k_max, o.s_max = m_max, k_max, s_max
         o.b_location = _lib.FAB_DEVICE
-        o.flags = (_lib.FAB_FLAG_PROFILE if profile else 0) | (_lib.FAB_FLAG_SQUARE if square else 0)
+        o.flags = ((_lib.FAB_FLAG_PROFILE if profile else 0) | (_lib.FAB_FLAG_SQUARE if square else 0)
+                   | (_lib.FAB_FLAG_ASYNC if asynchronous else 0))
         self.comm = comm
         o.comm = comm.handle.value if comm is not None else None
         if isinstance(b, np.ndarray):
@@ -185,7 +188,8 @@ class Solver:
         else:
             y = torch.empty(self.n, dtype=torch.float64, device=f"cuda:{self.device}") if out is None else out
             ptr, loc = y.data_ptr(), _lib.FAB_DEVICE
-        check(lib.fab_apply(self.ctx, FUNCS[f], float(alpha), float(sigma), C.c_void_p(ptr), loc), "fab_apply")
+        st = check(lib.fab_apply(self.ctx, FUNCS[f], float(alpha), float(sigma), C.c_void_p(ptr), loc), "fab_apply")
+        self.status["apply"] = st
         return y
 
     # --- results ------------------------------------------------------------

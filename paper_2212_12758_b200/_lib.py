@@ -18,7 +18,7 @@ FAB_OP_CSR, FAB_OP_STENCIL = 0, 1
 FAB_DEVICE, FAB_HOST = 0, 1
 GET = dict(info=0, H=1, V=2, SV=3, rows=4, signs=5, y=6, C=7, fc=8, R=9, beta=10)
 FAB_SET_POLY, FAB_SET_B_HOST, FAB_SET_B_DEVICE = 100, 101, 102
-FAB_FLAG_PROFILE, FAB_FLAG_SQUARE = 1, 2
+FAB_FLAG_PROFILE, FAB_FLAG_SQUARE, FAB_FLAG_ASYNC = 1, 2, 4
 
 MODES = {"blendenpik": FAB_BLENDENPIK, "sketch_solve": FAB_SKETCH_SOLVE, "none": FAB_NONE, "lsqr": FAB_LSQR,
          "blendenpik_gram": FAB_BLENDENPIK_GRAM}

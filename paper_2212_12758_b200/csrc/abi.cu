@@ -201,6 +201,9 @@ static void free_ctx(fab_ctx* c) {
   if (c->part_dots) cudaFree(c->part_dots);
   if (c->own_ws && c->ws) cudaFree(c->ws);
   if (c->st_h) cudaFreeHost(c->st_h);
+  if (c->stats_h) cudaFreeHost(c->stats_h);
+  if (c->ev_b0) cudaEventDestroy(c->ev_b0);
+  if (c->ev_b1) cudaEventDestroy(c->ev_b1);
   if (c->cap) cudaStreamDestroy(c->cap);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -321,6 +324,9 @@ int fab_init(fab_ctx** out, const fab_operator* A, const double* b, const fab_op
   INIT_CUDA(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking));
   for (int i = 0; i < kCombChunks; ++i) INIT_CUDA(cudaEventCreateWithFlags(&c->ev_chunk[i], cudaEventDisableTiming));
   INIT_CUDA(cudaMallocHost(&c->st_h, sizeof(DevState)));
+  INIT_CUDA(cudaMallocHost(&c->stats_h, 4 * sizeof(double)));
+  INIT_CUDA(cudaEventCreate(&c->ev_b0));
+  INIT_CUDA(cudaEventCreate(&c->ev_b1));
   if ((c->comm && comm_size(c) > 1) || k1_forced_split(c)) {   // C1 on a side stream, overlapped with K1 (basis.cu)
     INIT_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     INIT_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
@@ -403,6 +409,57 @@ static int basis_finish(fab_ctx* c, int m, int k, double ms) {
   c->info.basis_alg = 2;
   return c->breakdown ? FAB_BREAKDOWN : FAB_OK;
 }
+
+static bool async_ok(const fab_ctx* c) {
+  return (c->flags & FAB_FLAG_ASYNC) && !(c->flags & FAB_FLAG_PROFILE) && !c->comm;
+}
+
+// FAB_FLAG_ASYNC: resolve the work fab_basis / fab_compress enqueued without
+// waiting (one stream synchronisation); returns the worst warning, or the
+// error, they would have returned
+static int resolve_pending(fab_ctx* c) {
+  int worst = FAB_OK;
+  if (c->basis_pending) {
+    c->basis_pending = false;
+    FAB_CUDA(cudaEventSynchronize(c->ev_b1));
+    float t = 0.f;
+    FAB_CUDA(cudaEventElapsedTime(&t, c->ev_b0, c->ev_b1));
+    const bool comp = c->compressed;
+    int rc = basis_finish(c, c->m, c->k, t);
+    if (rc < 0) return rc;
+    c->compressed = comp;
+    worst = rc;
+    if (c->breakdown && c->compress_pending) {
+      // the compression assumed m_eff = m: rerun it synchronously on the
+      // m_eff columns of the broken-down basis
+      c->compress_pending = false;
+      const unsigned fl = c->flags;
+      c->flags &= ~(unsigned)FAB_FLAG_ASYNC;
+      int w = FAB_OK;
+      rc = run_compress(c, c->pend_mode, c->pend_opts_set ? &c->pend_opts : nullptr, &w);
+      c->flags = fl;
+      if (rc != FAB_OK) {
+        c->compressed = false;
+        return rc;
+      }
+      FAB_CUDA(cudaStreamSynchronize(c->stream));
+      if (w > worst) worst = w;
+    }
+  }
+  if (c->compress_pending) {
+    c->compress_pending = false;
+    int w = FAB_OK;
+    const int rc = compress_resolve(c, &w);
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, c->ev0, c->ev1) == cudaSuccess) c->info.ms_compress = t;
+    if (rc != FAB_OK) {
+      c->compressed = false;
+      return rc;
+    }
+    if (w > worst) worst = w;
+  }
+  return worst;
+}
 }  // namespace fab
 
 int fab_basis(fab_ctx* c, int m, int k) {
@@ -410,8 +467,25 @@ int fab_basis(fab_ctx* c, int m, int k) {
   if (!c) return FAB_EINVAL;
   if (k < 1 || k > c->k_max || m < 1 || m > c->m_max || m >= c->n_global) return FAB_EINVAL;
   if (c->sketch_ready && c->s < m + 1) return FAB_EINVAL;
+  int rc = resolve_pending(c);
+  if (rc < 0) return rc;
+  if (async_ok(c)) {
+    // enqueue only: the basis' status is resolved at the next synchronizing call
+    FAB_CUDA(cudaEventRecord(c->ev_b0, c->stream));
+    if ((rc = run_basis(c, m, k)) != FAB_OK) return rc;
+    FAB_CUDA(cudaEventRecord(c->ev_b1, c->stream));
+    c->basis_pending = true;
+    c->m = m;
+    c->k = k;
+    c->m_eff = m;                  // assumed until resolved (a breakdown reruns the compression)
+    c->breakdown = false;
+    c->basis_ready = true;
+    c->compressed = false;
+    c->sketch_in_V = c->sketch_ready;
+    return FAB_OK;
+  }
   FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
-  int rc = run_basis(c, m, k);
+  rc = run_basis(c, m, k);
   if (rc != FAB_OK) return rc;
   double ms = 0;
   if ((rc = timed_end(c, &ms)) != FAB_OK) return rc;
@@ -422,6 +496,11 @@ int fab_basis_batch(fab_ctx** cs, int p, int m, int k) {
   NvtxRange nvtx__("fab_basis_batch");
   if (!cs || p < 1 || p > kBatchMaxCtx) return FAB_EINVAL;
   fab_ctx* c = cs[0];
+  for (int i = 0; i < p; ++i)
+    if (cs[i]) {
+      const int pr__ = resolve_pending(cs[i]);   // FAB_FLAG_ASYNC
+      if (pr__ < 0) return pr__;
+    }
   for (int i = 0; i < p; ++i) {
     fab_ctx* d = cs[i];
     if (!d) return FAB_EINVAL;
@@ -464,6 +543,10 @@ int fab_basis_batch(fab_ctx** cs, int p, int m, int k) {
 int fab_basis_arnoldi(fab_ctx* c, int m) {
   NvtxRange nvtx__("fab_basis_arnoldi");
   if (!c) return FAB_EINVAL;
+  {
+    const int pr__ = resolve_pending(c);   // FAB_FLAG_ASYNC: finish enqueued basis / compression
+    if (pr__ < 0) return pr__;
+  }
   if (m < 1 || m > c->m_max || m >= c->n_global) return FAB_EINVAL;
   FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
   int rc = run_basis_arnoldi(c, m);
@@ -496,6 +579,10 @@ int fab_basis_arnoldi(fab_ctx* c, int m) {
 int fab_basis_whiten(fab_ctx* c, int m, int k, double cond_max) {
   NvtxRange nvtx__("fab_basis_whiten");
   if (!c) return FAB_EINVAL;
+  {
+    const int pr__ = resolve_pending(c);   // FAB_FLAG_ASYNC: finish enqueued basis / compression
+    if (pr__ < 0) return pr__;
+  }
   if (!c->sketch_ready) return FAB_EORDER;   // the monitor and Algorithm 1 need Theta
   if (k < 1 || k > c->k_max || m < 1 || m > c->m_max || m >= c->n_global || c->s < m + 1) return FAB_EINVAL;
   if (!(cond_max >= 0.0)) return FAB_EINVAL;
@@ -534,6 +621,10 @@ int fab_basis_whiten(fab_ctx* c, int m, int k, double cond_max) {
 int fab_basis_sgs(fab_ctx* c, int m) {
   NvtxRange nvtx__("fab_basis_sgs");
   if (!c) return FAB_EINVAL;
+  {
+    const int pr__ = resolve_pending(c);   // FAB_FLAG_ASYNC: finish enqueued basis / compression
+    if (pr__ < 0) return pr__;
+  }
   if (!c->sketch_ready) return FAB_EORDER;   // Algorithm 1 sketches every new vector
   if (m < 1 || m > c->m_max || m >= c->n_global || c->s < m + 1) return FAB_EINVAL;
   FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
@@ -567,6 +658,10 @@ int fab_basis_sgs(fab_ctx* c, int m) {
 int fab_sketch(fab_ctx* c, int s, uint64_t seed) {
   NvtxRange nvtx__("fab_sketch");
   if (!c) return FAB_EINVAL;
+  {
+    const int pr__ = resolve_pending(c);   // FAB_FLAG_ASYNC: finish enqueued basis / compression
+    if (pr__ < 0) return pr__;
+  }
   if (s < 1 || s > c->s_max || (int64_t)s > c->N) return FAB_EINVAL;
   if (c->basis_ready && s < (c->breakdown ? c->m_eff : c->m + 1)) return FAB_EINVAL;
   FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
@@ -603,6 +698,14 @@ int fab_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o) {
       (o->precond_s < c->m_eff || o->precond_s > c->s_max || (int64_t)o->precond_s > c->N))
     return FAB_EINVAL;
   int rc;
+  if (c->compress_pending) {   // an earlier asynchronous compression: resolve it first
+    if ((rc = resolve_pending(c)) < 0) return rc;
+  }
+  // API order needs the basis' final state (resolve it); an asynchronous
+  // basis followed by the fused sketch does not
+  if (c->basis_pending && (needs_sketch && !c->sketch_in_V)) {
+    if ((rc = resolve_pending(c)) < 0) return rc;
+  }
   const int64_t l0 = c->nlaunch;
   if (needs_sketch && !c->sketch_in_V) {
     // API order (basis before sketch): one batched SRHT pass over V_{m+1}
@@ -620,6 +723,19 @@ int fab_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o) {
   rc = run_compress(c, mode, o, &warn);
   if (rc != FAB_OK) return rc;
   c->info.launches_compress = c->nlaunch - l0;
+  if (async_ok(c) && mode != FAB_BLENDENPIK_GRAM) {
+    // enqueue only: cond(R), the LSQR outcome and the time are resolved at
+    // the next synchronizing call
+    FAB_CUDA(cudaEventRecord(c->ev1, c->stream));
+    c->compress_pending = true;
+    c->pend_mode = mode;
+    c->pend_opts_set = o != nullptr;
+    if (o) c->pend_opts = *o;
+    c->compressed = true;
+    c->mode = mode;
+    c->info.mode = mode;
+    return FAB_OK;
+  }
   double ms = 0;
   if ((rc = timed_end(c, &ms)) != FAB_OK) return rc;
   FAB_CUDA(cudaGetLastError());
@@ -640,6 +756,10 @@ int fab_apply(fab_ctx* c, int f, double alpha, double sigma, double* y, int y_lo
   }
   if (y_location != FAB_DEVICE && y_location != FAB_HOST) return FAB_EINVAL;
   if (!isfinite(alpha) || !isfinite(sigma)) return FAB_EINVAL;
+  // FAB_FLAG_ASYNC: the enqueued basis / compression finish here (their
+  // warning is this call's, their error ends it)
+  const int pend = resolve_pending(c);
+  if (pend < 0) return pend;
   if (!c->compressed) return FAB_EORDER;
   FAB_CUDA(cudaEventRecord(c->ev0, c->stream));
   double* cvec = svec(c, 16);
@@ -662,11 +782,15 @@ int fab_apply(fab_ctx* c, int f, double alpha, double sigma, double* y, int y_lo
   c->info.dense_iters = iters;
   c->info.ms_apply = ms;
   c->info.launches_apply = c->nlaunch - l0;
-  return FAB_OK;
+  return pend;
 }
 
 int fab_get(fab_ctx* c, int what, void* dst, size_t bytes) {
   if (!c || !dst) return FAB_EINVAL;
+  {
+    const int pr__ = resolve_pending(c);   // FAB_FLAG_ASYNC: finish enqueued basis / compression
+    if (pr__ < 0) return pr__;
+  }
   const int me = c->m_eff;
   auto need = [&](size_t b) { return bytes >= b; };
   switch (what) {
@@ -747,6 +871,10 @@ int fab_get(fab_ctx* c, int what, void* dst, size_t bytes) {
 
 int fab_get_column(fab_ctx* c, int j, double* dst) {
   if (!c || !dst) return FAB_EINVAL;
+  {
+    const int pr__ = resolve_pending(c);   // FAB_FLAG_ASYNC: finish enqueued basis / compression
+    if (pr__ < 0) return pr__;
+  }
   if (!c->basis_ready) return FAB_EORDER;
   const int cols = c->breakdown ? c->m_eff : c->m_eff + 1;
   if (j < 0 || j >= cols) return FAB_EINVAL;
@@ -759,6 +887,10 @@ int fab_get_column(fab_ctx* c, int j, double* dst) {
 
 int fab_get_vrows(fab_ctx* c, const int64_t* rows, int nrows, double* dst) {
   if (!c || !dst || !rows || nrows < 0) return FAB_EINVAL;
+  {
+    const int pr__ = resolve_pending(c);   // FAB_FLAG_ASYNC: finish enqueued basis / compression
+    if (pr__ < 0) return pr__;
+  }
   if (!c->basis_ready) return FAB_EORDER;
   const int cols = c->breakdown ? c->m_eff : c->m_eff + 1;
   std::vector<double> bt(cols);
@@ -774,6 +906,10 @@ int fab_get_vrows(fab_ctx* c, const int64_t* rows, int nrows, double* dst) {
 
 int fab_set(fab_ctx* c, int what, const void* src, size_t bytes) {
   if (!c || !src) return FAB_EINVAL;
+  {
+    const int pr__ = resolve_pending(c);   // FAB_FLAG_ASYNC: finish enqueued basis / compression
+    if (pr__ < 0) return pr__;
+  }
   if (what == FAB_SET_POLY) {
     const size_t n = bytes / sizeof(double);
     if (n < 1 || n > (size_t)kPolyMax) return FAB_EINVAL;

@@ -127,7 +127,7 @@ __device__ __forceinline__ int64_t rowq(const CsrArgs& a, int64_t r, uint64_t po
 // P right-hand sides share every entry load (multi-RHS SpMM); per vector the
 // arithmetic and its order are exactly those of P = 1.
 template <int NWM, bool ACC, bool DOTS, int P>
-__global__ void __launch_bounds__(kThreads, P == 1 ? 6 : (P == 2 ? 5 : 4)) k_csr_stream(CsrArgs a) {
+__global__ void __launch_bounds__(kThreads, P == 1 ? 6 : 3) k_csr_stream(CsrArgs a) {
   constexpr int kCsrU = kCsrNB / kThreads;
   pdl_wait();
   pdl_trigger();

@@ -173,6 +173,16 @@ struct fab_ctx {
   int g_arn_m = -1;
   int64_t g_arn_launches = 0;
 
+  // FAB_FLAG_ASYNC: work enqueued by fab_basis / fab_compress whose status
+  // is resolved at the next synchronizing call (abi.cu: resolve_pending)
+  bool basis_pending = false, compress_pending = false;
+  int pend_mode = -1;
+  fab_lsqr_opts pend_opts{};
+  bool pend_opts_set = false;
+  bool pend_graph = false, pend_fixed = false, pend_need_ls = false, pend_rstats = false;
+  cudaEvent_t ev_b0 = nullptr, ev_b1 = nullptr;   // the pending basis' start / end
+  double* stats_h = nullptr;                      // pinned: {min |R_ii|, max |R_ii|, cond_1(R)}
+
   fab_info info{};
   unsigned flags = 0;
   int64_t nlaunch = 0;               // kernels launched outside the basis graph
@@ -404,6 +414,8 @@ int sketch_precond(fab_ctx* c, int s2, uint64_t seed2, int m, double* dst, cudaS
 // lsqr.cu / compress
 int lsqr_setup(fab_ctx* c);
 int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn);
+int lsqr_collect(fab_ctx* c, bool graph_loop, bool fixed, bool prof, int npass, int* warn);
+int compress_resolve(fab_ctx* c, int* warn);   // FAB_FLAG_ASYNC
 // dense.cu
 int dense_fe1(fab_ctx* c, int f, double alpha, double sigma, double* c_out, int* iters);
 int dense_qr_sketch(fab_ctx* c, int m, double* R, double* qtb, cudaStream_t st);

@@ -801,6 +801,13 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
   c->info.ms_precond_sketch = 0.0;
   int64_t launches = 0;
   const bool need_ls = (mode != FAB_NONE) && !c->breakdown;
+  // FAB_FLAG_ASYNC: no host read here; cond(R), the LSQR state and the
+  // warnings are resolved at the next synchronizing call (compress_resolve)
+  const bool async = (c->flags & FAB_FLAG_ASYNC) && !(c->flags & FAB_FLAG_PROFILE) && !c->comm &&
+                     mode != FAB_BLENDENPIK_GRAM;
+  c->pend_need_ls = need_ls;
+  c->pend_rstats = false;
+  c->pend_graph = false;
   if (mode != FAB_NONE && mode != FAB_LSQR && !c->sketch_in_V) return FAB_EORDER;
   if (need_ls && mode == FAB_LSQR) {
     // Algorithm 3 (l.194): plain LSQR on V_m -- the Blendenpik iteration with R = I
@@ -856,12 +863,17 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
     k_transpose<<<(m * m + kThreads - 1) / kThreads, kThreads, 0, st>>>(Rinv, m, RinvT);
     FAB_CHECK_LAUNCH();
     ++launches;
-    double hs[3];
-    FAB_CUDA(cudaMemcpyAsync(hs, stats, sizeof(hs), cudaMemcpyDeviceToHost, st));
-    FAB_CUDA(cudaStreamSynchronize(st));
-    c->info.cond_R = hs[2];
-    if (!(hs[0] >= 1e-14 * hs[1])) return FAB_ESINGULAR;
-    if (hs[2] > 1e8) *warn = FAB_ILLCOND;
+    if (async) {
+      FAB_CUDA(cudaMemcpyAsync(c->stats_h, stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+      c->pend_rstats = true;
+    } else {
+      double hs[3];
+      FAB_CUDA(cudaMemcpyAsync(hs, stats, sizeof(hs), cudaMemcpyDeviceToHost, st));
+      FAB_CUDA(cudaStreamSynchronize(st));
+      c->info.cond_R = hs[2];
+      if (!(hs[0] >= 1e-14 * hs[1])) return FAB_ESINGULAR;
+      if (hs[2] > 1e8) *warn = FAB_ILLCOND;
+    }
   }
   if (need_ls) {
     if (mode == FAB_SKETCH_SOLVE) {
@@ -1084,33 +1096,57 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
         ++launches;
       }
       FAB_CUDA(cudaMemcpyAsync(c->st_h, c->st_d, sizeof(DevState), cudaMemcpyDeviceToHost, st));
-      FAB_CUDA(cudaStreamSynchronize(st));
-      c->info.lsqr_iters = c->st_h->lsqr_iters;
-      // graph replay: reset + init pass + init scalars + finish, and per
-      // iteration (the body ran iters times, once more when it ended on done)
-      // one pass and one step kernel
-      if (graph_loop) c->nlaunch += 4 + 2 * (int64_t)c->st_h->lsqr_iters;
-      // passes after convergence exit immediately; count the ones that ran
-      c->info.lsqr_passes = 1 + c->st_h->lsqr_iters;
-      c->info.ms_lsqr_pass = 0.0;
-      if (prof) {
-        for (int i = 0; i < 1 + c->st_h->lsqr_iters && i < npass; ++i) {
-          float t = 0.f;
-          FAB_CUDA(cudaEventElapsedTime(&t, c->prof_ev[2 * i], c->prof_ev[2 * i + 1]));
-          c->info.ms_lsqr_pass += t;
-        }
+      if (async && graph_loop) {   // the LSQR outcome is read at the resolution
+        c->pend_graph = true;
+        c->pend_fixed = fixed != 0;
+      } else {
+        FAB_TRY(lsqr_collect(c, graph_loop, fixed != 0, prof, npass, warn));
       }
-      c->info.lsqr_converged = c->st_h->lsqr_done;
-      c->info.lsqr_rnorm = c->st_h->rnorm;
-      c->info.lsqr_arnorm = c->st_h->arnorm;
-      c->info.lsqr_anorm = c->st_h->anorm;
-      if (!fixed && !c->st_h->lsqr_done && *warn == FAB_OK) *warn = FAB_NOTCONV;
     }
   }
   k_build_C<<<(m * m + kThreads - 1) / kThreads, kThreads, 0, st>>>(c->H, c->ldH, y, m, need_ls ? 1 : 0, C);
   FAB_CHECK_LAUNCH();
   ++launches;
   if (!need_ls) FAB_CUDA(cudaMemsetAsync(y, 0, m * sizeof(double), st));
+  return FAB_OK;
+}
+
+// the LSQR outcome from the state mirror (synchronises the stream)
+int lsqr_collect(fab_ctx* c, bool graph_loop, bool fixed, bool prof, int npass, int* warn) {
+  FAB_CUDA(cudaStreamSynchronize(c->stream));
+  c->info.lsqr_iters = c->st_h->lsqr_iters;
+  // graph replay: reset + init pass + init scalars + finish, and per
+  // iteration (the body ran iters times, once more when it ended on done)
+  // one pass and one step kernel
+  if (graph_loop) c->nlaunch += 4 + 2 * (int64_t)c->st_h->lsqr_iters;
+  // passes after convergence exit immediately; count the ones that ran
+  c->info.lsqr_passes = 1 + c->st_h->lsqr_iters;
+  c->info.ms_lsqr_pass = 0.0;
+  if (prof) {
+    for (int i = 0; i < 1 + c->st_h->lsqr_iters && i < npass; ++i) {
+      float t = 0.f;
+      FAB_CUDA(cudaEventElapsedTime(&t, c->prof_ev[2 * i], c->prof_ev[2 * i + 1]));
+      c->info.ms_lsqr_pass += t;
+    }
+  }
+  c->info.lsqr_converged = c->st_h->lsqr_done;
+  c->info.lsqr_rnorm = c->st_h->rnorm;
+  c->info.lsqr_arnorm = c->st_h->arnorm;
+  c->info.lsqr_anorm = c->st_h->anorm;
+  if (!fixed && !c->st_h->lsqr_done && *warn == FAB_OK) *warn = FAB_NOTCONV;
+  return FAB_OK;
+}
+
+// FAB_FLAG_ASYNC: the status of an enqueued fab_compress (stream synchronised)
+int compress_resolve(fab_ctx* c, int* warn) {
+  *warn = FAB_OK;
+  FAB_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->pend_rstats) {
+    c->info.cond_R = c->stats_h[2];
+    if (!(c->stats_h[0] >= 1e-14 * c->stats_h[1])) return FAB_ESINGULAR;
+    if (c->stats_h[2] > 1e8) *warn = FAB_ILLCOND;
+  }
+  if (c->pend_graph) FAB_TRY(lsqr_collect(c, true, c->pend_fixed, false, 0, warn));
   return FAB_OK;
 }
 

@@ -1,7 +1,8 @@
 """Solve latency with the host-driven LSQR loop (FAB_LSQR_GRAPH=0: a host
 poll every 4 iterations, one launch per kernel) against the graph-resident
 loop (one CUDA graph, conditional WHILE node, the tolerance test on the
-device), at the small BASELINE configs where latency matters (c1, c2) and at
+device), and the graph loop with FAB_FLAG_ASYNC (fab_basis / fab_compress
+enqueue only; fab_apply resolves), at the small BASELINE configs where latency matters (c1, c2) and at
 c3 for reference.  Blendenpik-LSQR tol 1e-6, fused sketch, A and b resident.
 
     python profiles/lsqr_graph_timing.py > gpurun_out/lsqr_graph.jsonl
@@ -27,11 +28,14 @@ import paper_2212_12758_b200 as fab  # noqa: E402
 
 def run(name, reps, **kw):
     p = fp.make(name, **kw)
-    sv = fab.Solver(fab.Operator.from_problem(p), torch.as_tensor(p.b).cuda(), p.m, p.k, p.s)
     y = torch.empty(p.n, dtype=torch.float64, device="cuda")
     out = {"config": name, "n": p.n, "m": p.m}
-    for flag in ("0", "1"):
-        os.environ["FAB_LSQR_GRAPH"] = flag
+    for flag in ("0", "1", "async"):
+        # host loop / graph loop (synchronous calls) / graph loop with
+        # FAB_FLAG_ASYNC (fab_basis and fab_compress only enqueue)
+        os.environ["FAB_LSQR_GRAPH"] = "0" if flag == "0" else "1"
+        sv = fab.Solver(fab.Operator.from_problem(p), torch.as_tensor(p.b).cuda(), p.m, p.k, p.s,
+                        asynchronous=(flag == "async"))
         walls, comp = [], []
         for i in range(reps + 3):
             torch.cuda.synchronize()
@@ -44,10 +48,10 @@ def run(name, reps, **kw):
             if i >= 3:
                 walls.append((time.perf_counter() - t0) * 1e6)
                 comp.append(sv.info()["ms_compress"] * 1e3)
-        key = "graph" if flag == "1" else "host_loop"
+        key = {"0": "host_loop", "1": "graph", "async": "graph_async"}[flag]
         out[key] = {"us_per_solve": statistics.median(walls), "compress_us": statistics.median(comp),
                     "lsqr_iters": sv.info()["lsqr_iters"]}
-    sv.close()
+        sv.close()
     return out
 
 
