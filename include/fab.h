@@ -32,8 +32,11 @@
  *    default stream).  fab_basis, fab_compress and fab_apply synchronize
  *    that stream before returning (they report device-side status:
  *    breakdown, LSQR convergence, domain errors), and so do fab_init and
- *    fab_sketch (small host<->device copies).  Asynchronous CUDA errors
- *    surface as FAB_ECUDA at the next synchronizing call.
+ *    fab_sketch (small host<->device copies) -- unless the context was
+ *    created with FAB_FLAG_ASYNC: then fab_basis and fab_compress only
+ *    enqueue, and their status is returned by the next synchronizing call
+ *    (fab_apply, fab_get*).  Asynchronous CUDA errors surface as FAB_ECUDA
+ *    at the next synchronizing call.
  *  - Calls must come in order: init, then basis and sketch (either order),
  *    then compress, then apply (repeatable).  Out-of-order -> FAB_EORDER.
  *  - One context per host thread.  No exception crosses the ABI.
