@@ -974,6 +974,61 @@ static int expm_e1(fab_ctx* c, int m, const double* X0, double* c_out, int* iter
 //   Y_{k+1} = mu/2 Y_k (I + mu^-2 M_k^-1),  Z_{k+1} = mu/2 Z_k (I + mu^-2 M_k^-1)
 //   M_{k+1} = 1/2 I + mu^2/4 M_k + mu^-2/4 M_k^-1
 // Y -> X^{1/2}, Z -> X^{-1/2}, M -> I.
+// Coupled Newton-Schulz iteration for the principal square root (Higham,
+// Functions of Matrices, 2008, eq. (6.35)): with A' = X / ||X||_1,
+//   Y_0 = A', Z_0 = I,  T_k = (3I - Z_k Y_k)/2,  Y_{k+1} = Y_k T_k,  Z_{k+1} = T_k Z_k
+// Y_k -> A'^{1/2}, Z_k -> A'^{-1/2} quadratically when ||I - A'|| < 1 --
+// three m x m GEMMs per step and no inverse, where Denman-Beavers needs a
+// Gauss-Jordan inverse (a 2-us-per-pivot chain on the cluster) every step.
+// Convergence is monitored as ||T_k - I||_F; a step that doubles its smallest
+// value so far, a non-finite value or 60 steps mean the matrix is outside the basin
+// (eigenvalues far from the positive real interval, e.g. c4-like or a
+// negative eigenvalue): *ok = false and the caller runs Denman-Beavers,
+// which also reports EDOMAIN.  Same principal root, different rounding.
+static int ns_e1(fab_ctx* c, int m, const double* X0, int want_inv, double* c_out, int* iters, cudaStream_t st,
+                 bool* ok) {
+  *ok = false;
+  double* Y = dmat(c, 6);
+  double* Z = dmat(c, 7);
+  double* T = dmat(c, 10);
+  double* Y2 = dmat(c, 11);
+  double* Z2 = dmat(c, 12);
+  double h[3];
+  FAB_TRY(read_stats(c, X0, m, h, st));
+  if (h[2] != 0.0 || !(h[0] > 0.0) || !isfinite(h[0])) return FAB_OK;
+  const double sc = h[0];
+  FAB_TRY(lincomb(c, m, 1.0 / sc, X0, 0, nullptr, 0, nullptr, 0.0, Y, st));   // Y_0 = X / ||X||_1
+  FAB_TRY(lincomb(c, m, 0, nullptr, 0, nullptr, 0, nullptr, 1.0, Z, st));      // Z_0 = I
+  bool extra = false;
+  double emin = INFINITY;
+  for (int it = 0; it < 60; ++it) {
+    FAB_TRY(gemm(c, m, Z, Y, -0.5, 0.0, nullptr, 1.5, T, st));                // T = (3I - Z Y) / 2
+    FAB_TRY(read_stats(c, T, m, h, st));
+    const double e = h[1];                                                    // ||T - I||_F
+    if (h[2] != 0.0 || !isfinite(e) || e > 2.0 * emin) return FAB_OK;         // outside the basin
+    emin = fmin(emin, e);
+    FAB_TRY(gemm(c, m, Y, T, 1.0, 0.0, nullptr, 0.0, Y2, st));
+    FAB_TRY(gemm(c, m, T, Z, 1.0, 0.0, nullptr, 0.0, Z2, st));
+    double* t = Y;
+    Y = Y2;
+    Y2 = t;
+    t = Z;
+    Z = Z2;
+    Z2 = t;
+    *iters = it + 1;
+    if (extra) break;
+    if (e <= 1e-13 * sqrt((double)m)) extra = true;   // one more step after convergence
+  }
+  if (!extra) return FAB_OK;
+  // c = f(X) e_1: sqrt(X) = sqrt(sc) Y, X^{-1/2} = Z / sqrt(sc)
+  const int g = (m + 127) / 128;
+  k_unit<<<g, 128, 0, st>>>(m, 0.0, c_out);
+  k_axpy_small<<<g, 128, 0, st>>>(m, want_inv ? 1.0 / sqrt(sc) : sqrt(sc), want_inv ? Z : Y, c_out);
+  FAB_CHECK_LAUNCH();
+  *ok = true;
+  return FAB_OK;
+}
+
 static int db_e1(fab_ctx* c, int m, const double* X0, int want_inv, double* c_out, int* iters,
                  cudaStream_t st) {
   double* M = dmat(c, 5);
@@ -1054,9 +1109,17 @@ int dense_fe1(fab_ctx* c, int f, double alpha, double sigma, double* c_out, int*
     case FAB_EXP:
       return expm_e1(c, m, X, c_out, iters, st);
     case FAB_SQRT:
-      return db_e1(c, m, X, 0, c_out, iters, st);
-    case FAB_INVSQRT:
-      return db_e1(c, m, X, 1, c_out, iters, st);
+    case FAB_INVSQRT: {
+      const int inv = (f == FAB_INVSQRT) ? 1 : 0;
+      const char* e = getenv("FAB_DENSE_DB");   // "1": Denman-Beavers only (A/B)
+      if (!(e && e[0] == '1')) {
+        bool ok = false;
+        FAB_TRY(ns_e1(c, m, X, inv, c_out, iters, st, &ok));
+        if (ok) return FAB_OK;
+      }
+      *iters = 0;
+      return db_e1(c, m, X, inv, c_out, iters, st);
+    }
     case FAB_POLY:
       return poly_e1(c, m, X, c_out, st);
     default:
