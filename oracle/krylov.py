@@ -31,15 +31,17 @@ def _norm_inf(A):
 
 
 def truncated_arnoldi(A, b, m: int, k: int, variant: str = "mgs",
-                      breakdown_tol: float = 1e-14):
+                      breakdown_tol: float = 1e-14, V_out=None):
     """Algorithm 2.  Returns dict(V, H, gamma=||b||_2, m_eff, breakdown):
     V is n x (m+1) and H (m+1) x m without breakdown; on breakdown at step
-    i, m_eff = i-1, V = [v_1..v_{m_eff}] and H is (m_eff+1) x m_eff."""
+    i, m_eff = i-1, V = [v_1..v_{m_eff}] and H is (m_eff+1) x m_eff.
+    V_out: optional zero-filled n x (m+1) array to hold V (e.g. a
+    column-major np.memmap when V exceeds host memory, c5); same arithmetic."""
     n = b.shape[0]
     if k < 1 or m < 1:
         raise ValueError("need k >= 1, m >= 1")
     gamma = float(np.linalg.norm(b))
-    V = np.zeros((n, m + 1))
+    V = np.zeros((n, m + 1)) if V_out is None else V_out
     H = np.zeros((m + 1, m))
     V[:, 0] = b / gamma                                   # l.118
     thresh = breakdown_tol * _norm_inf(A)
