@@ -113,6 +113,8 @@ CASES = [
     ("c3", dict(g=32, m=60, s=120), 2, False),
     ("c3", dict(g=32, m=60, s=120), 3, False),
     ("c3", dict(g=32, m=60, s=120), 4, False),
+    # the 8-GPU layout of the scaling run: 8 z-slabs of 8 planes each
+    ("c3", dict(g=64, m=60, s=120), 8, False),
     # c1 2D: 100-row lines are not 32-aligned -> aligned row blocks cut
     # mid-line and mid 4096-row sketch tile (halo = one line)
     ("c1", {}, 3, False),
