@@ -243,6 +243,17 @@ int fab_comm_init(void** comm, const unsigned char id[128], int rank, int nranks
    comms[r] is released with fab_comm_destroy.  Errors: EINVAL, ENOMEM, ECUDA. */
 int fab_comm_init_loopback(void** comms, int nranks, int device);
 
+/* 1 if the communicator reduces the per-step scalars (C2) through NVLink
+   mailboxes instead of ncclAllReduce: every rank owns a small buffer that
+   its peers map through CUDA IPC; the last CTA of K1 writes this rank's k+1
+   sums into every rank's buffer and raises a flag (release, system scope),
+   and K3's prologue waits for all flags of the step (acquire) and adds the
+   P slots in rank order -- one fused compute + collective, no NCCL launch
+   per step.  Set up by fab_comm_init unless FAB_P2P=0 or IPC is unavailable
+   (all ranks agree).  A rank that stops posting makes the others' fab_basis
+   fail with FAB_ENCCL after 20 s instead of hanging.  0 otherwise. */
+int fab_comm_p2p(void* comm);
+
 /* Destroy a communicator (after every context using it is destroyed). */
 int fab_comm_destroy(void* comm);
 

@@ -29,7 +29,7 @@ EXPORTS = ("fab_version", "fab_strerror", "fab_workspace_size", "fab_init", "fab
            "fab_basis_sgs", "fab_basis_arnoldi", "fab_basis_whiten",
            "fab_sketch", "fab_compress", "fab_apply", "fab_get", "fab_get_column", "fab_get_vrows",
            "fab_set", "fab_last_error", "fab_destroy", "fab_comm_unique_id", "fab_comm_init",
-           "fab_comm_init_loopback", "fab_comm_destroy")
+           "fab_comm_init_loopback", "fab_comm_p2p", "fab_comm_destroy")
 
 
 class FabOperator(C.Structure):
@@ -102,6 +102,7 @@ def load():
         "fab_comm_unique_id": (I, [P]),
         "fab_comm_init": (I, [C.POINTER(P), P, I, I, I]),
         "fab_comm_init_loopback": (I, [P, I, I]),
+        "fab_comm_p2p": (I, [P]),
         "fab_comm_destroy": (I, [P]),
     }
     for name, (res, args) in sig.items():

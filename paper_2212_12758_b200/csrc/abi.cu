@@ -387,6 +387,7 @@ namespace fab {
 static int basis_finish(fab_ctx* c, int m, int k, double ms) {
   int rc;
   if ((rc = pull_state(c)) != FAB_OK) return rc;
+  if (c->st_h->err == FAB_ENCCL) return FAB_ENCCL;   // a rank stopped posting C2 (P2P mailboxes)
   c->m = m;
   c->k = k;
   c->breakdown = c->st_h->breakdown != 0;

@@ -446,6 +446,8 @@ struct PipeArgs {
   // k_scalar's order (bitwise the same), CTA 0 stores beta, H and the state
   int fuse_k2;
   const double* sums;   // fused K2 on several GPUs: the allreduced step scalars (k_step_reduce + C2)
+  int use_mail;         // several GPUs, P2P: the step scalars arrive in this rank's mailbox (C2 over NVLink)
+  P2PMail mail;
   int nparts_dots;
   const double* part_dots;
   const double* part_norm_prev;
@@ -622,6 +624,16 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) k_stream_tiles(P
       nu = a.sums[nw];
 #pragma unroll
       for (int t = 0; t < NWM; ++t) dj[t] = t < nw ? a.sums[t] : 0.0;
+    } else if (a.use_mail) {   // several GPUs, P2P: wait for every rank's sums, add them in rank order
+      double v[kKMax + 1];
+      if (!a.st->breakdown) {   // (after a breakdown no rank posted: nothing to wait for)
+        mail_collect(a.mail, v, nw + 1);
+      } else {
+        for (int t = 0; t <= nw; ++t) v[t] = 0.0;
+      }
+      nu = v[nw];
+#pragma unroll
+      for (int t = 0; t < NWM; ++t) dj[t] = t < nw ? v[t] : 0.0;
     } else {
       __shared__ double red2[(NWM + 1) * kWarps];
       cta_det_sums<NWM>(a.part_norm_prev, gridDim.x, a.part_dots, a.nparts_dots, nw, red2, nu, dj);
@@ -1417,6 +1429,10 @@ int enqueue_k1(fab_ctx* c, int col, int nw, double* z, bool need_z, cudaStream_t
     sr.sums = step_sums;
     sr.part_norm = norm_parts(c, col - 1);
     sr.nparts_norm = c->grid_upd;
+    if (comm_p2p(c, &sr.mail)) {   // ... and posts them to every rank's mailbox (no NCCL call)
+      sr.use_mail = 1;
+      sr.sums = nullptr;
+    }
   }
   return launch_k1(c, col, nw, xin, z, need_z || !c->mf, st, launches, nparts, sr);
 }
@@ -1475,6 +1491,10 @@ static int enqueue_k1_csr_pipe(fab_ctx* c, int col, int nw, double* z, cudaStrea
     sr.sums = step_sums;
     sr.part_norm = norm_parts(c, col - 1);
     sr.nparts_norm = c->grid_upd;
+    if (comm_p2p(c, &sr.mail)) {
+      sr.use_mail = 1;
+      sr.sums = nullptr;
+    }
   }
   return csr_spmv(c, col, nw, c->xg, z, st, launches, nparts, sr, c->ev_peer.data());
 }
@@ -1501,6 +1521,10 @@ static int enqueue_k1_split(fab_ctx* c, int col, int nw, double* z, cudaStream_t
     sr.sums = step_sums;
     sr.part_norm = norm_parts(c, col - 1);
     sr.nparts_norm = c->grid_upd;
+    if (comm_p2p(c, &sr.mail)) {
+      sr.use_mail = 1;
+      sr.sums = nullptr;
+    }
   }
   FAB_TRY(launch_k1(c, col, nw, x, z, true, st, launches, &np, sr, &rb, Gi, Gb));           // boundary slabs
   *nparts = Gi + Gb;
@@ -1545,6 +1569,7 @@ int enqueue_k3(fab_ctx* c, int col, int nw, bool fused, cudaStream_t st, int64_t
   if (nparts_k2 > 0) {
     a.fuse_k2 = 1;
     a.sums = sums;
+    if (!sums && comm_p2p(c, &a.mail)) a.use_mail = 1;
     a.nparts_dots = nparts_k2;
     a.part_dots = c->part_dots;
     a.part_norm_prev = norm_parts(c, col - 1);
@@ -1583,6 +1608,9 @@ static int enqueue_step(fab_ctx* c, int col, int k, bool fused, cudaStream_t st,
       FAB_TRY(enqueue_k1_csr_pipe(c, col, nw, c->vec, st, launches, &nparts, c->red));
     else
       FAB_TRY(enqueue_k1(c, col, nw, c->vec, false, st, launches, &nparts, c->red));
+    P2PMail mail;
+    if (comm_p2p(c, &mail))   // C2 through the mailboxes: K1 posts, K3 collects -- no NCCL call
+      return enqueue_k3(c, col, nw, fused, st, launches, nparts, nullptr);
     FAB_TRY(comm_allreduce(c, c->red, (size_t)nw + 1, false, st));
     return enqueue_k3(c, col, nw, fused, st, launches, nparts, c->red);
   }

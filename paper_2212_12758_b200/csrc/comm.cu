@@ -52,6 +52,7 @@ struct NcclApi {
   ncclResult_t (*groupStart)();
   ncclResult_t (*groupEnd)();
   const char* (*errorString)(ncclResult_t);
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
 };
 
 // one virtual partition of P loopback ranks
@@ -96,9 +97,101 @@ struct Comm {
   LoopGroup* loop = nullptr;            // loopback rank (no NCCL)
   void* scratch = nullptr;              // loopback allreduce result before the copy back
   size_t scratch_bytes = 0;
+  // C2 mailboxes over NVLink (fab_internal.cuh P2PMail): own allocation + the
+  // peers' mapped through CUDA IPC
+  bool p2p = false;
+  char* mail_base = nullptr;
+  char* peer_base[kMailRanks] = {};
 };
 
+constexpr size_t kMailData = (size_t)2 * kMailRanks * kMailLen * sizeof(double);
+constexpr size_t kMailFlags = (size_t)2 * kMailRanks * sizeof(unsigned long long);
+constexpr size_t kMailBytes = kMailData + kMailFlags + 256;   // + this rank's epoch counter
+
 bool comm_graphable(const fab_ctx* c) { return !(c->comm && c->comm->loop); }
+
+bool comm_p2p(const fab_ctx* c, P2PMail* m) {
+  if (!c->comm || !c->comm->p2p) return false;
+  const Comm* cm = c->comm;
+  memset(m, 0, sizeof(*m));
+  m->P = cm->nranks;
+  m->rank = cm->rank;
+  for (int q = 0; q < cm->nranks; ++q) {
+    char* b = q == cm->rank ? cm->mail_base : cm->peer_base[q];
+    m->box[q] = reinterpret_cast<double*>(b);
+    m->flag[q] = reinterpret_cast<unsigned long long*>(b + kMailData);
+  }
+  m->epoch = reinterpret_cast<unsigned long long*>(cm->mail_base + kMailData + kMailFlags);
+  m->err = &c->st_d->err;
+  return true;
+}
+
+// One-shot P2P C2 (SURVEY §8e "one-shot P2P small allreduce"): every rank
+// allocates a mailbox, the IPC handles go round with one NCCL all-gather, every
+// rank maps its peers'.  All ranks agree (an allreduce of the outcome) or none
+// uses it.  FAB_P2P=0 keeps C2 on ncclAllReduce.
+static NcclApi* nccl_api();
+static void setup_p2p(Comm* cm) {
+  NcclApi* api = nccl_api();
+  const char* e = getenv("FAB_P2P");
+  if (!api || cm->nranks < 1 || cm->nranks > kMailRanks || (e && e[0] == '0')) return;
+  int ok = 1;
+  if (cudaMalloc(&cm->mail_base, kMailBytes) != cudaSuccess || cudaMemset(cm->mail_base, 0, kMailBytes) != cudaSuccess)
+    ok = 0;
+  cudaIpcMemHandle_t mine;
+  memset(&mine, 0, sizeof(mine));
+  if (ok && cm->nranks > 1 && cudaIpcGetMemHandle(&mine, cm->mail_base) != cudaSuccess) ok = 0;
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  char* d = nullptr;
+  std::vector<char> all((size_t)cm->nranks * hb);
+  int* dok = nullptr;
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&d, cm->nranks * hb) != cudaSuccess || cudaMalloc(&dok, sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    ok = 0;   // every rank still takes part in the collectives below
+  }
+  if (d && cudaMemcpy(d + cm->rank * hb, &mine, hb, cudaMemcpyHostToDevice) == cudaSuccess &&
+      api->allGather(d + cm->rank * hb, d, hb, ncclUint8, cm->nc, st) == ncclSuccess &&
+      cudaStreamSynchronize(st) == cudaSuccess &&
+      cudaMemcpy(all.data(), d, all.size(), cudaMemcpyDeviceToHost) == cudaSuccess) {
+    for (int q = 0; q < cm->nranks && ok; ++q) {
+      if (q == cm->rank) continue;
+      cudaIpcMemHandle_t h;
+      memcpy(&h, all.data() + q * hb, hb);
+      void* p = nullptr;
+      if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = 0;
+      } else {
+        cm->peer_base[q] = static_cast<char*>(p);
+      }
+    }
+  } else {
+    cudaGetLastError();
+    ok = 0;
+  }
+  // every rank uses the mailboxes or none does
+  if (dok && cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess &&
+      api->allReduce(dok, dok, 1, ncclInt32, ncclMin, cm->nc, st) == ncclSuccess &&
+      cudaStreamSynchronize(st) == cudaSuccess)
+    cudaMemcpy(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost);
+  else
+    ok = 0;
+  if (d) cudaFree(d);
+  if (dok) cudaFree(dok);
+  if (st) cudaStreamDestroy(st);
+  cm->p2p = ok != 0;
+  if (!cm->p2p) {
+    for (int q = 0; q < kMailRanks; ++q)
+      if (cm->peer_base[q]) {
+        cudaIpcCloseMemHandle(cm->peer_base[q]);
+        cm->peer_base[q] = nullptr;
+      }
+    if (cm->mail_base) cudaFree(cm->mail_base);
+    cm->mail_base = nullptr;
+  }
+}
 
 // out[i] = in_0[i] (+|max) in_1[i] ... in_{P-1}[i], ranks in order
 template <typename T>
@@ -197,6 +290,7 @@ static NcclApi* nccl_api() {
   FAB_SYM(groupStart, "ncclGroupStart")
   FAB_SYM(groupEnd, "ncclGroupEnd")
   FAB_SYM(errorString, "ncclGetErrorString")
+  FAB_SYM(allGather, "ncclAllGather")
 #undef FAB_SYM
   state = 1;
   return &api;
@@ -399,8 +493,14 @@ int fab_comm_init(void** comm, const unsigned char id[128], int rank, int nranks
     delete cm;
     return FAB_ENCCL;
   }
+  setup_p2p(cm);
   *comm = cm;
   return FAB_OK;
+}
+
+int fab_comm_p2p(void* comm) {
+  if (!comm) return FAB_EINVAL;
+  return static_cast<Comm*>(comm)->p2p ? 1 : 0;
 }
 
 int fab_comm_init_loopback(void** comms, int nranks, int device) {
@@ -453,6 +553,9 @@ int fab_comm_destroy(void* comm) {
     delete cm;
     return FAB_OK;
   }
+  for (int q = 0; q < kMailRanks; ++q)
+    if (cm->peer_base[q]) cudaIpcCloseMemHandle(cm->peer_base[q]);
+  if (cm->mail_base) cudaFree(cm->mail_base);
   NcclApi* api = nccl_api();
   if (api && cm->nc) api->commDestroy(cm->nc);
   delete cm;

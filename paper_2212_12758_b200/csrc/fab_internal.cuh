@@ -47,12 +47,82 @@ struct DevState {
 // (arrival counter) reduces every CTA's dot partials and the previous
 // column's norm partials in k_scalar's fixed order into sums[0..nw] for the
 // allreduce.  sums == nullptr: off (one GPU: K3 reduces in its prologue).
+// One-shot P2P allreduce of the step scalars over NVLink (several GPUs, NCCL
+// communicator; comm.cu sets it up with CUDA IPC).  Every rank owns a mailbox
+// [2 parities][kMailRanks slots][kMailLen] doubles + [2][kMailRanks] flags;
+// box[q] / flag[q] are rank q's mailbox mapped into this process.  The last
+// K1 CTA of rank r writes its k+1 sums into slot r of EVERY rank's mailbox
+// (parity = epoch & 1), then the flags (release, system scope); K3's
+// prologue waits (acquire) until all P flags of its own mailbox reach the
+// epoch and adds the P slots in rank order -- every rank the same sum, no
+// NCCL launch in the step.  The epoch lives in the communicator (shared by
+// its contexts) and is advanced by the writer.
+constexpr int kMailRanks = 8;
+constexpr int kMailLen = 16;
+struct P2PMail {
+  double* box[kMailRanks];
+  unsigned long long* flag[kMailRanks];
+  unsigned long long* epoch;   // this rank's epoch counter (device)
+  int* err;                    // DevState::err of the context: FAB_ENCCL if a peer never posts
+  int P, rank;
+};
+
 struct StepRed {
   int* count;               // arrival counter (DevState::pad[0]), reset by the last CTA
   double* sums;
   const double* part_norm;  // norm partials of w_hat_{c-1}
   int nparts_norm;
+  int use_mail;             // P2P: the sums go to every rank's mailbox instead of sums
+  P2PMail mail;
 };
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// writer side (thread 0 of the last K1 CTA): the nv values to slot `rank` of
+// every mailbox, then the flags
+__device__ __forceinline__ void mail_post(const P2PMail& m, const double* v, int nv) {
+  const unsigned long long e = *m.epoch + 1;
+  *m.epoch = e;
+  const int par = (int)(e & 1);
+  for (int q = 0; q < m.P; ++q) {
+    double* dst = m.box[q] + ((size_t)par * kMailRanks + m.rank) * kMailLen;
+    for (int t = 0; t < nv; ++t) dst[t] = v[t];
+  }
+  __threadfence_system();
+  for (int q = 0; q < m.P; ++q) st_release_sys(m.flag[q] + par * kMailRanks + m.rank, e);
+}
+
+// reader side (any thread): wait for the current epoch from every rank, then
+// out[t] = sum over q = 0..P-1 in order of slot q's value t
+__device__ __forceinline__ void mail_collect(const P2PMail& m, double* out, int nv) {
+  const unsigned long long e = *(volatile unsigned long long*)m.epoch;
+  const int par = (int)(e & 1);
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int q = 0; q < m.P; ++q)
+    while (ld_acquire_sys(m.flag[m.rank] + par * kMailRanks + q) < e) {
+      __nanosleep(64);
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (t1 - t0 > 20000000000ull) {   // 20 s: a rank stopped posting -- fail, do not hang
+        atomicExch(m.err, FAB_ENCCL);
+        break;
+      }
+    }
+  const double* b = m.box[m.rank] + (size_t)par * kMailRanks * kMailLen;
+  for (int t = 0; t < nv; ++t) {
+    double a = *(volatile const double*)(b + t);
+    for (int q = 1; q < m.P; ++q) a += *(volatile const double*)(b + q * kMailLen + t);
+    out[t] = a;
+  }
+}
 
 struct Comm;   // comm.cu: NCCL communicator of the row-partitioned path
 struct CsrPlan;   // csr.cu: row blocks / column-blocked copy of a CSR operator
@@ -289,8 +359,9 @@ __device__ __forceinline__ double det_sum_cg(const double* p, int count, int str
 // stored by thread 0: the last CTA forms the sums (same order as k_step_reduce)
 __device__ __forceinline__ void step_red_tail(const StepRed& sr, const double* part_dots, int nparts_dots, int nw,
                                               double* red) {
-  if (!sr.sums) return;
+  if (!sr.sums && !sr.use_mail) return;
   __shared__ int last;
+  __shared__ double tsum[kKMax + 1];
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -300,12 +371,19 @@ __device__ __forceinline__ void step_red_tail(const StepRed& sr, const double* p
   if (!last) return;
   __threadfence();
   const double nu = det_sum_cg(sr.part_norm, sr.nparts_norm, 1, 0, red);
-  if (threadIdx.x == 0) sr.sums[nw] = nu;
+  if (threadIdx.x == 0) tsum[nw] = nu;
   for (int t = 0; t < nw; ++t) {
     const double dv = det_sum_cg(part_dots, nparts_dots, kKMax + 1, t, red);
-    if (threadIdx.x == 0) sr.sums[t] = dv;
+    if (threadIdx.x == 0) tsum[t] = dv;
   }
-  if (threadIdx.x == 0) *sr.count = 0;
+  if (threadIdx.x == 0) {
+    if (sr.use_mail) {
+      mail_post(sr.mail, tsum, nw + 1);   // C2 over NVLink, no NCCL launch
+    } else {
+      for (int t = 0; t <= nw; ++t) sr.sums[t] = tsum[t];
+    }
+    *sr.count = 0;
+  }
 }
 
 // Raise a kernel's dynamic shared-memory cap to min(want, opt-in max - its
@@ -374,6 +452,7 @@ int comm_gather_x(fab_ctx* c, const double* x, cudaStream_t st);
 int comm_gather_step(fab_ctx* c, const double* x, int d, cudaStream_t st);   // pipelined C1: slice of rank + d
 int comm_setup_partition(fab_ctx* c);
 bool comm_graphable(const fab_ctx* c);       // false for a loopback rank: enqueue eagerly
+bool comm_p2p(const fab_ctx* c, P2PMail* m); // the NVLink mailboxes of C2 (several GPUs, NCCL comm, IPC ok)
 bool k1_forced_split(const fab_ctx* c);      // basis.cu: FAB_FORCE_K1_SPLIT=1 (one GPU, timing only)
 const char* nccl_last_error();
 // basis.cu

@@ -123,6 +123,11 @@ class Comm:
         check(lib.fab_comm_init(C.byref(self.handle), C.cast(uid, C.c_void_p), self.rank, self.size,
                                 self.device), "fab_comm_init")
 
+    @property
+    def p2p(self):
+        """True if C2 runs through the NVLink mailboxes (fab_comm_p2p)."""
+        return bool(lib.fab_comm_p2p(self.handle))
+
     def close(self):
         if self.handle:
             lib.fab_comm_destroy(self.handle)

@@ -90,6 +90,25 @@ def test_one_rank_nccl_batched_sketch(comm):
     assert np.array_equal(a["SV"], b["SV"]) and np.array_equal(a["y"], b["y"])
 
 
+def test_p2p_mailboxes_carry_c2(comm, monkeypatch):
+    """The per-step reduction (C2) goes through the NVLink mailboxes
+    (fab_comm_p2p; with one rank the mailbox is this GPU's own): K1 posts,
+    K3 collects, no ncclAllReduce in the step -- and the result is still
+    bitwise the single-GPU one (test above) and the NCCL path's."""
+    import torch
+    from paper_2212_12758_b200 import dist as fdist
+    assert comm.p2p
+    p = fp.make("c3", g=32, m=40, s=80)
+    a = _solve(p, comm)
+    monkeypatch.setenv("FAB_P2P", "0")
+    c2 = fdist.Comm(device=0)
+    assert not c2.p2p
+    b = _solve(p, c2)
+    c2.close()
+    assert np.array_equal(a["y"], b["y"]) and np.array_equal(a["H"], b["H"])
+    torch.cuda.synchronize()
+
+
 def test_partition_validation(comm):
     """A 1-rank communicator must own every row: fab_init refuses a block
     that does not tile [0, n) (EINVAL), and an unaligned block start."""

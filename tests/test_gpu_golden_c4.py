@@ -12,7 +12,7 @@ determined by the data (reading G-24); f_m is, and has converged:
   * f_m per mode (Algorithm 5, sketch-and-solve, Blendenpik tol 1e-6) on
     every 1024th row, on the sums of all 4096 blocks of 1024 rows and its
     norm: 1e-10 against the oracle, 1e-12 against the exact exp(A) b;
-  * the first 20 columns of underline-H_m (determined there): 1e-12.
+  * the first 15 columns of underline-H_m (determined there): 1e-12.
 """
 import json
 import os
@@ -79,6 +79,9 @@ def test_c4_fm_per_mode(run, key):
 
 def test_c4_basis_and_rows(run):
     p, g, meta, res = run
+    # the first 15 columns are determined (the oracle's MGS and CGS bases
+    # agree there to 1.5e-15; by column 20 the saturating Krylov space has
+    # amplified rounding to 2e-10, by 30 to 0.5)
     H = res["sketch_solve"]["H"]
-    assert rel(H[:21, :20], g["H"][:21, :20]) <= 1e-12
+    assert rel(H[:16, :15], g["H"][:16, :15]) <= 1e-12
     assert np.array_equal(res["sketch_solve"]["rows"], g["rows"])
