@@ -384,14 +384,24 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    # FAB_BENCH_COMM=1 (testing): run the multi-GPU code path with ONE rank
+    # (NCCL communicator, row-block operator, P2P mailboxes) on one GPU
+    use_comm = world > 1 or os.environ.get("FAB_BENCH_COMM") == "1"
+    if use_comm:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        if world > 1:
+            dist.init_process_group("nccl")
+        else:
+            import socket
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                port = so.getsockname()[1]
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
     dev = local
 
     p = fp.make("c3", g=args.g)
     comm = None
-    if world > 1:
+    if use_comm:
         # ONE solve over all GPUs: z-slabs of the grid, halo
         # exchange + one allreduce per Krylov step over NCCL (strong scaling)
         from paper_2212_12758_b200 import dist as fdist

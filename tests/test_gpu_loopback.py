@@ -185,6 +185,43 @@ def test_loopback_halo_overlap_split(name, kw, P, monkeypatch):
     assert rel(y1, ref["f_m"]) <= 1e-10
 
 
+def test_loopback_precond_sketch_and_api_order():
+    """Blendenpik's own preconditioner sketch Theta' (C3 for Theta'V_m) and
+    the API-order sketch (K5 after the basis) over rank boundaries."""
+    import torch
+    import paper_2212_12758_b200 as fab
+    from paper_2212_12758_b200 import dist as fdist
+    p = fp.make("c5", n=20000 + 77, m=40, s=80)
+    cuts = cuts_for(p, 3)
+    grp = fdist.LoopbackGroup(3, 0)
+
+    def body(r, comm, st):
+        r0, r1 = int(cuts[r]), int(cuts[r + 1])
+        op = fdist.local_operator(p, r0, r1)
+        b = torch.as_tensor(np.ascontiguousarray(p.b[r0:r1])).cuda()
+        sv = fab.Solver(op, b, m_max=p.m, k_max=p.k, s_max=160, stream=st, comm=comm)
+        sv.basis(p.m, p.k)
+        sv.sketch(p.s, p.sketch_seed)                         # API order: K5 at compress
+        sv.compress("blendenpik", iters=120, precond_s=160, precond_seed=77)
+        y = sv.apply(p.f, p.alpha, p.sigma)
+        st.synchronize()
+        out = dict(y=y.cpu().numpy(), SV=sv.get("SV"), info=sv.info())
+        sv.close()
+        return out
+
+    try:
+        res = grp.run(body)
+    finally:
+        grp.close()
+    y = np.concatenate([r["y"] for r in res])
+    ref = ofab.solve(p.scipy(), p.b, p.m, p.k, p.s, p.sketch_seed, mode="blendenpik", f=p.f, alpha=p.alpha,
+                     sigma=p.sigma, lsqr_iters=120, precond=(160, 77))
+    assert rel(y, ref["f_m"]) <= 1e-10
+    assert res[0]["info"]["precond_fresh"] == 1
+    check_replicated(res, ["SV"])
+    assert np.abs(res[0]["SV"] - ref["SV"]).max() <= 1e-13 * np.abs(ref["SV"]).max()
+
+
 def test_forced_k1_split_one_gpu(monkeypatch):
     """FAB_FORCE_K1_SPLIT=1 on one GPU runs the ranks' K1 structure
     (interior rows, then the boundary slabs; the timing knob of DESIGN.md
