@@ -41,6 +41,13 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+JSON_OUT = sys.stdout   # main() points it at the original stdout and sends fd 1 to stderr
+
+
+def emit(obj):
+    print(json.dumps(obj), file=JSON_OUT, flush=True)
+
+
 def workload_config(p, world):
     """The config dict of BOTH arms (the driver compares them)."""
     return {"workload": WORKLOAD, "n": p.n, "m": p.m, "k": p.k, "s": p.s,
@@ -289,7 +296,7 @@ def run_reference(args):
                          "sample": desc},
         "e2e": {"value": val, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(out), flush=True)
+    emit(out)
     return 0
 
 
@@ -367,7 +374,12 @@ def main():
     args = parse()
     world_env = os.environ.get("WORLD_SIZE")
     if args.gpus > 1 and world_env is None:
-        return relaunch_distributed(args)
+        return relaunch_distributed(args)   # the ranks print the line (rank 0)
+    # stdout carries the ONE JSON line only: anything else written to fd 1
+    # (NCCL's version banner, library prints) goes to stderr
+    global JSON_OUT
+    JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     if world_env is not None and int(world_env) != args.gpus:
         log(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world_env}: launch one rank per GPU "
             f"(torchrun --nproc-per-node {args.gpus}) or drop --gpus")
@@ -648,7 +660,7 @@ def main():
     if comm is not None:
         comm.close()
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        emit(out)
     if dist:
         dist.destroy_process_group()
     return 0
