@@ -198,16 +198,19 @@ __global__ void __launch_bounds__(kThreads, P == 1 ? 6 : 3) k_csr_stream(CsrArgs
       continue;
     }
     const int nrows = (int)(r1 - r0);
+    const int icnt = (int)cnt;   // <= kCsrNB: 32-bit bounds from here on
     // stream: row pointers and products of the block's entries to shared memory
     for (int q = tid; q <= nrows; q += kThreads) rps[q] = (int)(rowq(a, r0 + q, pf) - q0);
     {
       int col[kCsrU];
       double v[kCsrU], xv[kCsrU][P];
+      const int32_t* cb = a.ci + q0;
+      const double* vb = a.vals ? a.vals + q0 : nullptr;
 #pragma unroll
       for (int u = 0; u < kCsrU; ++u) {
         const int q = tid + kThreads * u;
-        col[u] = q < cnt ? ld_s32(a.ci + q0 + q, pf) : -1;
-        v[u] = (a.vals && q < cnt) ? ld_sf(a.vals + q0 + q, pf) : 1.0;
+        col[u] = q < icnt ? ld_s32(cb + q, pf) : -1;
+        v[u] = (vb && q < icnt) ? ld_sf(vb + q, pf) : 1.0;
       }
 #pragma unroll
       for (int u = 0; u < kCsrU; ++u) {
@@ -221,17 +224,17 @@ __global__ void __launch_bounds__(kThreads, P == 1 ? 6 : 3) k_csr_stream(CsrArgs
 #pragma unroll
       for (int u = 0; u < kCsrU; ++u) {
         const int q = tid + kThreads * u;
-        if (q < cnt) {
+        if (q < icnt) {
 #pragma unroll
           for (int i = 0; i < P; ++i) prod[i][q] = v[u] * xv[u][i];
         }
       }
     }
     __syncthreads();
-    // reduce: G lanes per row, fixed order
-    const int64_t avg = cnt / nrows;
-    int G = 1;
-    while (G < 32 && 4 * G < avg) G <<= 1;
+    // reduce: G lanes per row, fixed order; G = the least power of two with
+    // 4 G >= the mean row length, 1..32
+    const int avg = icnt / nrows;
+    const int G = avg <= 4 ? 1 : min(32, 1 << (32 - __clz(((avg + 3) >> 2) - 1)));
     const int R = kThreads / G;
     for (int rb = 0; rb < nrows; rb += R) {
       const int rl = rb + tid / G, sub = tid & (G - 1);
