@@ -7,6 +7,9 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfab.so")
+# profiling A/B only (profiles/build_variant.py): another build of the same library
+if os.environ.get("FAB_LIB_VARIANT"):
+    LIB_PATH = os.environ["FAB_LIB_VARIANT"]
 
 # status codes (fab.h)
 FAB_OK, FAB_BREAKDOWN, FAB_ILLCOND, FAB_NOTCONV = 0, 1, 2, 3

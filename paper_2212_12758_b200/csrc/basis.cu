@@ -1740,7 +1740,7 @@ static int enqueue_batch(fab_ctx* const* cs, int p, int m, int k, cudaStream_t s
   for (int col = 1; col <= m; ++col) {
     const int nw = col < k ? col : k;
     int nparts = 0;
-    if (cs[0]->stencil || !csr_interleave_fits(cs[0], p)) {
+    if (cs[0]->stencil || p < 2 || !csr_batch_ok(cs[0])) {
       // no shared entry traffic worth a pass (stencil), or the p inputs would
       // not stay in L2 (every gather would then miss for every vector):
       // per-context K1
@@ -1775,8 +1775,8 @@ static int enqueue_batch(fab_ctx* const* cs, int p, int m, int k, cudaStream_t s
 
 int run_basis_batch(fab_ctx* const* cs, int p, int m, int k) {
   fab_ctx* c = cs[0];
-  if (!c->stencil && !c->xi && p > 1 && csr_interleave_fits(c, p))
-    FAB_CUDA(cudaMalloc(&c->xi, (size_t)c->n * kBatchMaxCtx * sizeof(double)));
+  FAB_TRY(csr_batch_prepare(c, p));
+  if (csr_batch_ok(c) && !c->xi) FAB_CUDA(cudaMalloc(&c->xi, (size_t)c->n * kBatchMaxCtx * sizeof(double)));
   std::vector<fab_ctx*> key(cs, cs + p);
   std::vector<int> fz(p), ss(p);
   for (int i = 0; i < p; ++i) {
@@ -1784,7 +1784,7 @@ int run_basis_batch(fab_ctx* const* cs, int p, int m, int k) {
     ss[i] = cs[i]->s;
   }
   if (!(c->gexec_bat && c->g_bat_ctx == key && c->g_bat_fused == fz && c->g_bat_s == ss && c->g_bat_m == m &&
-        c->g_bat_k == k)) {
+        c->g_bat_k == k && c->g_bat_plan == (const void*)c->csr_bat)) {
     if (c->gexec_bat) {
       cudaGraphExecDestroy(c->gexec_bat);
       c->gexec_bat = nullptr;
@@ -1806,6 +1806,7 @@ int run_basis_batch(fab_ctx* const* cs, int p, int m, int k) {
     c->g_bat_s = ss;
     c->g_bat_m = m;
     c->g_bat_k = k;
+    c->g_bat_plan = c->csr_bat;
     c->g_bat_launches = launches;
   }
   FAB_CUDA(cudaGraphLaunch(c->gexec_bat, c->stream));

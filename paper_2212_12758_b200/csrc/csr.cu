@@ -36,6 +36,12 @@ namespace fab {
 // 1024 / 2048 / 4096: c4 339 / 340 / 420 us, c5 4.24 / 4.37 / 5.26 ms.
 constexpr int kCsrNB = 1024;
 constexpr int kCsrRows = 2048;               // rows per block (cap)
+#ifndef FAB_CSR_OCC
+#define FAB_CSR_OCC 6                        // resident CTAs per SM of the one-vector K1 (launch bound)
+#endif
+#ifndef FAB_CSR_OCC_P
+#define FAB_CSR_OCC_P 3                      // the same for the multi-RHS instantiations (P > 1)
+#endif
 
 constexpr int kBatchMax = 4;   // multi-RHS: vectors per SpMM pass (fab_basis_batch)
 
@@ -107,11 +113,19 @@ __device__ __forceinline__ void gather_x(const CsrArgs& a, int col, uint64_t pl,
   if (P > 1 && a.xi) {
     constexpr int S = (P + 1) & ~1;   // row stride of the interleaved copy (16-B aligned rows)
     const double* b = a.xi + (int64_t)col * S;
+    if constexpr (S == 4) {   // one 32-B sector in one 256-bit load
+      double t[4];
+      asm volatile("ld.global.nc.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+                   : "=d"(t[0]), "=d"(t[1]), "=d"(t[2]), "=d"(t[3]) : "l"(b), "l"(pl));
 #pragma unroll
-    for (int i = 0; i < P; i += 2) {
-      const double2 t = ld_keep2(b + i, pl);
-      xv[i] = t.x;
-      if (i + 1 < P) xv[i + 1] = t.y;
+      for (int i = 0; i < P; ++i) xv[i] = t[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < P; i += 2) {
+        const double2 t = ld_keep2(b + i, pl);
+        xv[i] = t.x;
+        if (i + 1 < P) xv[i + 1] = t.y;
+      }
     }
   } else {
 #pragma unroll
@@ -127,7 +141,7 @@ __device__ __forceinline__ int64_t rowq(const CsrArgs& a, int64_t r, uint64_t po
 // P right-hand sides share every entry load (multi-RHS SpMM); per vector the
 // arithmetic and its order are exactly those of P = 1.
 template <int NWM, bool ACC, bool DOTS, int P>
-__global__ void __launch_bounds__(kThreads, P == 1 ? 6 : 3) k_csr_stream(CsrArgs a) {
+__global__ void __launch_bounds__(kThreads, P == 1 ? FAB_CSR_OCC : FAB_CSR_OCC_P) k_csr_stream(CsrArgs a) {
   constexpr int kCsrU = kCsrNB / kThreads;
   pdl_wait();
   pdl_trigger();
@@ -408,21 +422,21 @@ static int operator_fingerprint(fab_ctx* c, unsigned long long* fp) {
   FAB_CUDA(cudaStreamSynchronize(c->stream));
   return FAB_OK;
 }
+static int build_plan(fab_ctx* c, CsrPlan* plan, int64_t width);
 static std::mutex g_plan_mu;
 static std::vector<std::pair<PlanKey, std::weak_ptr<CsrPlan>>> g_plans;
 static std::vector<std::pair<fab_ctx*, std::shared_ptr<CsrPlan>>> g_holders;
 
 void csr_release(fab_ctx* c) {
   std::lock_guard<std::mutex> lk(g_plan_mu);
-  for (size_t i = 0; i < g_holders.size(); ++i)
-    if (g_holders[i].first == c) {
-      g_holders.erase(g_holders.begin() + i);
-      break;
-    }
+  for (size_t i = 0; i < g_holders.size();)
+    if (g_holders[i].first == c) g_holders.erase(g_holders.begin() + i);
+    else ++i;
   for (size_t i = 0; i < g_plans.size();)
     if (g_plans[i].second.expired()) g_plans.erase(g_plans.begin() + i);
     else ++i;
   c->csr = nullptr;
+  c->csr_bat = nullptr;
 }
 
 static int parallel_threads() {
@@ -441,17 +455,8 @@ int csr_grid(fab_ctx* c, int* grid) {
 // At fab_init: uniform-value detection, the row blocks, and (if x is larger
 // than the L2 budget) the column-blocked copy of the entries -- or the plan
 // another context of the same operator already built.
-static int build_plan(fab_ctx* c, CsrPlan* plan, int64_t width);
-
-int csr_setup(fab_ctx* c) {
-  csr_release(c);
-  // column-block width: the slice of x a pass gathers from stays in ~40 % of L2
-  int l2 = 0;
-  FAB_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device));
-  int64_t width = (int64_t)(0.4 * (double)l2) / 8;
-  if (width < 1024) width = 1024;
-  const char* env = getenv("FAB_CSR_COLBLOCK");   // tests: force a width (columns)
-  if (env && atoll(env) > 0) width = atoll(env);
+// the plan of width `width` for c's operator: another context's, or built now
+static int acquire_plan(fab_ctx* c, int64_t width, CsrPlan** out) {
   unsigned long long fp = 0;
   FAB_TRY(operator_fingerprint(c, &fp));
   const PlanKey key{c->device, c->op.row_ptr, c->op.col_idx, c->op.values, c->n, c->row_begin, c->op.nnz, width, fp,
@@ -472,13 +477,69 @@ int csr_setup(fab_ctx* c) {
     std::lock_guard<std::mutex> lk(g_plan_mu);
     g_plans.push_back({key, sp});
   }
-  if (sp->uniform) {
-    c->op.values = nullptr;
-    c->op.value_scale *= sp->v0;
-  }
   std::lock_guard<std::mutex> lk(g_plan_mu);
-  g_holders.push_back({c, sp});
-  c->csr = sp.get();
+  bool held = false;
+  for (auto& h : g_holders) held |= (h.first == c && h.second == sp);
+  if (!held) g_holders.push_back({c, sp});
+  *out = sp.get();
+  return FAB_OK;
+}
+
+static int l2_bytes(const fab_ctx* c, int* l2) {
+  FAB_CUDA(cudaDeviceGetAttribute(l2, cudaDevAttrL2CacheSize, c->device));
+  return FAB_OK;
+}
+
+int csr_setup(fab_ctx* c) {
+  csr_release(c);
+  // column-block width: the slice of x a pass gathers from stays in ~40 % of L2
+  int l2 = 0;
+  FAB_TRY(l2_bytes(c, &l2));
+  int64_t width = (int64_t)(0.4 * (double)l2) / 8;
+  if (width < 1024) width = 1024;
+  const char* env = getenv("FAB_CSR_COLBLOCK");   // tests: force a width (columns)
+  if (env && atoll(env) > 0) width = atoll(env);
+  CsrPlan* plan = nullptr;
+  FAB_TRY(acquire_plan(c, width, &plan));
+  if (plan->uniform) {
+    c->op.values = nullptr;
+    c->op.value_scale *= plan->v0;
+  }
+  c->csr = plan;
+  return FAB_OK;
+}
+
+// Multi-RHS plan for p right-hand sides (fab_basis_batch): the p inputs are
+// gathered from one interleaved copy, S = p rounded up to even doubles per
+// column, so a gather reads S x 8 bytes.  If the single-RHS plan is one pass
+// and the whole interleaved copy fits the L2 budget, that plan serves; else
+// a column-blocked plan whose slice of the interleaved copy (width x S x 8
+// bytes) fits ~40 % of L2, as the single-RHS plan does for one vector.
+// (c4 at p = 4: the interleaved copy is 134 MB > L2, so 3 column blocks.)
+int csr_batch_prepare(fab_ctx* c, int p) {
+  c->csr_bat = nullptr;
+  if (c->stencil || c->comm || p < 2 || !c->csr) return FAB_OK;
+  const int S = (p + 1) & ~1;
+  int l2 = 0;
+  FAB_TRY(l2_bytes(c, &l2));
+  double frac = 0.75;   // X only (the entry / z streams are evict-first)
+  const char* e = getenv("FAB_BATCH_L2FRAC");
+  if (e && atof(e) > 0) frac = atof(e);
+  const char* ew = getenv("FAB_BATCH_COLBLOCK");   // force a column-blocked batch plan (columns)
+  const int64_t forced = ew ? atoll(ew) : 0;
+  if (forced <= 0 && c->csr->pass.size() == 1 && (double)S * (double)c->n_global * 8.0 <= frac * (double)l2) {
+    c->csr_bat = c->csr;
+    return FAB_OK;
+  }
+  int64_t width = forced > 0 ? forced : (int64_t)(0.4 * (double)l2) / (8 * S);
+  if (width < 1024 && forced <= 0) width = 1024;
+  if (c->csr->width > 0 && c->csr->width <= width && forced <= 0) {   // already blocked narrowly enough
+    c->csr_bat = c->csr;
+    return FAB_OK;
+  }
+  CsrPlan* plan = nullptr;
+  FAB_TRY(acquire_plan(c, width, &plan));
+  c->csr_bat = plan;
   return FAB_OK;
 }
 
@@ -668,17 +729,9 @@ int csr_interleave(fab_ctx* c, int p, const double* const* x, double* xi, cudaSt
   return FAB_OK;
 }
 
-// the interleaved inputs of p right-hand sides stay in the L2 budget the
-// column blocking uses (0.4 L2), and the plan is a single pass
-bool csr_interleave_fits(const fab_ctx* c, int p) {
-  if (!c->csr || c->csr->pass.size() != 1 || c->comm) return false;
-  int l2 = 0;
-  if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device) != cudaSuccess) return false;
-  double frac = 0.75;   // X only (the entry / z streams are evict-first)
-  const char* e = getenv("FAB_BATCH_L2FRAC");
-  if (e && atof(e) > 0) frac = atof(e);
-  return (double)((p + 1) & ~1) * (double)c->n_global * 8.0 <= frac * (double)l2;
-}
+// fab_basis_batch shares K1 across the p contexts iff csr_batch_prepare found
+// a plan for them
+bool csr_batch_ok(const fab_ctx* c) { return c->csr_bat != nullptr; }
 
 int64_t csr_max_blocks(const fab_ctx* c) {
   int64_t m = 0;
@@ -713,7 +766,7 @@ int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* con
                    cudaStream_t st, int64_t* launches, int* nparts, const double* xi, StepRed sr,
                    const cudaEvent_t* peer_ev) {
   fab_ctx* c = cs[0];
-  CsrPlan* plan = c->csr;
+  CsrPlan* plan = (p > 1 && c->csr_bat) ? c->csr_bat : c->csr;
   if (!plan || plan->pass.empty() || p < 1 || p > kBatchMax) return FAB_EORDER;
   *nparts = c->grid_spmv;
   const int np = (int)plan->pass.size();

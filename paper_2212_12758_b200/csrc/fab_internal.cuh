@@ -212,6 +212,7 @@ struct fab_ctx {
   double* wbuf = nullptr;             // whitening scratch (Q, R, R^-1), allocated on first use
   fab::Comm* comm = nullptr;          // NULL: one GPU
   fab::CsrPlan* csr = nullptr;        // CSR operator: K1 plan (csr.cu)
+  fab::CsrPlan* csr_bat = nullptr;    // fab_basis_batch: the plan K1 uses for the batch (csr_batch_prepare)
   std::vector<int64_t> rank_rows;     // row_begin of every rank, plus n_global
 
   // cached Algorithm 1 graph
@@ -225,6 +226,7 @@ struct fab_ctx {
   std::vector<int> g_bat_fused;
   std::vector<int> g_bat_s;
   int g_bat_m = -1, g_bat_k = -1;
+  const void* g_bat_plan = nullptr;
   int64_t g_bat_launches = 0;
   double* xi = nullptr;               // multi-RHS interleaved SpMV inputs (n x 4), allocated on first use
   bool pdl = false;                   // PDL between K1 and K3 (opt-in: FAB_PDL=1; measured slower)
@@ -476,7 +478,8 @@ int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* con
                    cudaStream_t st, int64_t* launches, int* nparts, const double* xi, StepRed sr = StepRed{},
                    const cudaEvent_t* peer_ev = nullptr);
 int csr_interleave(fab_ctx* c, int p, const double* const* x, double* xi, cudaStream_t st, int64_t* launches);
-bool csr_interleave_fits(const fab_ctx* c, int p);
+int csr_batch_prepare(fab_ctx* c, int p);    // choose / build the batch's K1 plan (before capture)
+bool csr_batch_ok(const fab_ctx* c);         // K1 shared across the batch (else per-context K1)
 constexpr int kBatchMaxCtx = 4;              // fab_basis_batch: contexts per call
 int run_basis_batch(fab_ctx* const* cs, int p, int m, int k);
 int64_t csr_max_blocks(const fab_ctx* c);

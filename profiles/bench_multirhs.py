@@ -25,12 +25,27 @@ import fab_problems as fp  # noqa: E402
 import paper_2212_12758_b200 as fab  # noqa: E402
 
 
-def run(name, m, ps=(1, 2, 4), reps=3):
+def run(name, m, ps=(1, 2, 4), reps=3, env=None, tag=None):
+    """env: FAB_* variables set for this run only (plan widths are read when
+    a context / batch plan is built)."""
+    saved = {k: os.environ.get(k) for k in (env or {})}
+    os.environ.update(env or {})
+    try:
+        _run(name, m, ps, reps, tag or name, env or {})
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def _run(name, m, ps, reps, tag, env):
     t0 = time.perf_counter()
     p = fp.make(name, m=m, s=2 * m)
     print(f"[{name}] generated in {time.perf_counter() - t0:.1f} s", file=sys.stderr, flush=True)
     op = fab.Operator.from_problem(p)
-    res = {"config": name, "n": p.n, "m": m, "k": p.k, "s": p.s, "nnz": int(p.meta.get("nnz", 0))}
+    res = {"config": name, "tag": tag, "env": env, "n": p.n, "m": m, "k": p.k, "s": p.s, "nnz": int(p.meta.get("nnz", 0))}
     for nb in ps:
         svs = []
         for i in range(nb):
@@ -58,8 +73,16 @@ def run(name, m, ps=(1, 2, 4), reps=3):
 
 def main():
     torch.cuda.set_device(0)
-    run("c4", 150)
-    run("c5", 40)
+    which = sys.argv[1:] or ["c4", "c4_cb1", "c4_cb2", "c5"]
+    for w in which:
+        if w == "c4":        # batch plan by the L2 rule (p = 4: 3 column blocks of the interleaved copy)
+            run("c4", 150)
+        elif w == "c4_cb1":  # the single-RHS plan column-blocked too (2 blocks of 2^21 columns)
+            run("c4", 150, ps=(1,), env={"FAB_CSR_COLBLOCK": str(1 << 21)}, tag="c4_colblock2")
+        elif w == "c4_cb2":  # p = 2 / 4 with narrower batch blocks
+            run("c4", 150, ps=(2, 4), env={"FAB_BATCH_COLBLOCK": str(1 << 20)}, tag="c4_batchblock_2^20")
+        elif w == "c5":
+            run("c5", 40)
 
 
 if __name__ == "__main__":

@@ -41,14 +41,20 @@ def solvers(p, op, nb, square=False, fused=True):
     return out
 
 
-@pytest.mark.parametrize("name,kw,nb,colblock,square", [
-    ("c5", dict(n=5001, m=15, s=40), 3, None, False),
-    ("c4", dict(n=1 << 14, m=20, s=50), 4, None, False),     # hub rows (long-row path)
-    ("c5", dict(n=5001, m=15, s=40), 2, "1000", False),      # column-blocked passes
-    ("e4", dict(n=5001, m=15, s=40), 3, None, True),         # squared operator: K0 and K1 batched
-    ("c1", dict(m=30), 3, None, False),                       # stencil: per-context K1
+@pytest.mark.parametrize("name,kw,nb,colblock,batchblock,square", [
+    ("c5", dict(n=5001, m=15, s=40), 3, None, None, False),
+    ("c4", dict(n=1 << 14, m=20, s=50), 4, None, None, False),     # hub rows (long-row path)
+    ("c5", dict(n=5001, m=15, s=40), 2, "1000", None, False),      # column-blocked passes
+    ("e4", dict(n=5001, m=15, s=40), 3, None, None, True),         # squared operator: K0 and K1 batched
+    ("c1", dict(m=30), 3, None, None, False),                       # stencil: per-context K1
+    # a column-blocked plan built for the batch only (the contexts' own plan is
+    # one pass): the c4 p = 4 layout at full size, where the interleaved copy
+    # exceeds L2; S = 4 (256-bit gathers) at p = 4 and p = 3, S = 2 at p = 2
+    ("c4", dict(n=1 << 14, m=20, s=50), 4, None, "3001", False),
+    ("c4", dict(n=1 << 14, m=20, s=50), 3, None, "5000", False),
+    ("c5", dict(n=5001, m=15, s=40), 2, None, "1700", False),
 ])
-def test_batch_equals_single_and_oracle(name, kw, nb, colblock, square, monkeypatch):
+def test_batch_equals_single_and_oracle(name, kw, nb, colblock, batchblock, square, monkeypatch):
     import paper_2212_12758_b200 as fab
     if colblock:
         monkeypatch.setenv("FAB_CSR_COLBLOCK", colblock)
@@ -57,21 +63,32 @@ def test_batch_equals_single_and_oracle(name, kw, nb, colblock, square, monkeypa
     f = "sign" if square else p.f
     alpha = 1.0 if square else p.alpha
     batch = solvers(p, op, nb, square)
+    if batchblock:
+        monkeypatch.setenv("FAB_BATCH_COLBLOCK", batchblock)
     fab.basis_batch(batch, p.m, p.k)
+    if batchblock:   # the single solves use the batch's plan width, so bitwise equality is defined
+        monkeypatch.setenv("FAB_CSR_COLBLOCK", batchblock)
     single = solvers(p, op, nb, square)
     for sv in single:
         sv.basis(p.m, p.k)
     A = p.scipy()
     for i in range(nb):
         a, b = batch[i], single[i]
-        assert np.array_equal(a.get("H"), b.get("H"))                   # bitwise
-        assert np.array_equal(a.get("SV"), b.get("SV"))
-        assert np.array_equal(a.get("beta"), b.get("beta"))
+        if batchblock is None:
+            assert np.array_equal(a.get("H"), b.get("H"))                   # bitwise
+            assert np.array_equal(a.get("SV"), b.get("SV"))
+            assert np.array_equal(a.get("beta"), b.get("beta"))
+        else:
+            # same plan, but K1's grid follows each context's own plan (the
+            # dot partials are summed over another CTA count): rounding only
+            assert rel(a.get("H"), b.get("H")) <= 1e-13
+            assert rel(a.get("SV"), b.get("SV")) <= 1e-13
         a.compress("blendenpik", iters=40)
         b.compress("blendenpik", iters=40)
         ya = a.apply(f, alpha, p.sigma).cpu().numpy()
         yb = b.apply(f, alpha, p.sigma).cpu().numpy()
-        assert np.array_equal(ya, yb)
+        if batchblock is None:
+            assert np.array_equal(ya, yb)
         if square:
             ref = ofab.sign(A, rhs(p, i), p.m, p.k, p.s, p.sketch_seed, mode="blendenpik", lsqr_iters=40,
                             keep=False)
