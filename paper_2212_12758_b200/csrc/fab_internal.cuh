@@ -237,6 +237,7 @@ struct fab_ctx {
   cudaGraphExec_t gexec_lsqr = nullptr;
   cudaStream_t cap2 = nullptr;        // second capture stream (the while body)
   int gl_m = -1, gl_G = -1, gl_ns = -1, gl_fixed = -1, gl_maxit = -1;
+  const void* gl_kern = nullptr;      // the K6 kernel the cached graph launches
   bool gl_pipe = false;
   double gl_tol = -1.0;
 

@@ -16,6 +16,9 @@
 // only polls convergence between chunks of iterations.
 #include <math.h>
 
+#include <mutex>
+#include <vector>
+
 #include "fab_internal.cuh"
 #include "pipe.cuh"
 
@@ -93,25 +96,45 @@ k_lsqr_pass(const double* __restrict__ W, int64_t ld, int m, int64_t n, const do
 // same arithmetic as k_lsqr_pass from shared memory (warp w owns columns
 // w + 16 jj, lane = row).  One named barrier per chunk (double-buffered
 // cross-warp partials of t).  Persistent grid, one CTA per SM.
-constexpr int kLsR = 32;
 constexpr int kLsConsWarps = 16;
 constexpr int kLsCons = kLsConsWarps * 32;
 constexpr int kLsPipeThreads = kLsCons + 32;
 constexpr int kLsMaxStages = 16;
 constexpr int kLsSmemLimit = 226 * 1024;
+constexpr int kLsPipeMaxM = 384;   // k_lsqr_pipe: m <= 24 x 16
 
-template <int JPW, bool KEEP = (JPW <= 13)>
+// RPL rows per lane: a chunk is R = 32 RPL rows, so every column segment a
+// box reads is 256 RPL contiguous bytes.  Measured (profiles/micro_tma_box.cu,
+// pure TMA streaming of n = 2^24 x 200): 32-row boxes 6.54 TB/s, 64-row 7.18,
+// 128-row 7.24-7.29 -- short segments cost DRAM efficiency, so the tallest
+// box that still leaves a two-stage ring is used.
+template <int RPL>
+__device__ __forceinline__ void lds_rows(const double* p, double (&v)[RPL]) {
+  if constexpr (RPL == 1) {
+    v[0] = *p;
+  } else {
+#pragma unroll
+    for (int q = 0; q < RPL; q += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(p + q);
+      v[q] = t.x;
+      v[q + 1] = t.y;
+    }
+  }
+}
+
+template <int JPW, int RPL, bool KEEP>
 __global__ void __launch_bounds__(kLsPipeThreads, 1)
 k_lsqr_pipe(const __grid_constant__ CUtensorMap tmW, int boxc, int ncopies, int m, int64_t n,
             const double* __restrict__ p, double scal_arg, const double* t_old, double* t_new,
             double* __restrict__ part_g, double* __restrict__ part_tn, const DevState* __restrict__ st,
             int use_state_scal, int nstage) {
+  constexpr int R = 32 * RPL;
   if (st->lsqr_done) return;
   extern __shared__ __align__(128) double ring[];
-  __shared__ double sp[kMaxM];
-  __shared__ double tpart[2][kLsConsWarps][32];
+  __shared__ double sp[kLsPipeMaxM];
+  __shared__ __align__(16) double tpart[2][kLsConsWarps][R];
   const int mpad = boxc * ncopies;      // W columns held per stage (>= m; extra ones zero-filled)
-  const int stage_d = (mpad + 1) * kLsR;   // doubles per stage: W box(es) + the t_old chunk
+  const int stage_d = (mpad + 1) * R;   // doubles per stage: W box(es) + the t_old chunk
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)nstage * stage_d);
   uint64_t* empty = full + nstage;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -125,23 +148,23 @@ k_lsqr_pipe(const __grid_constant__ CUtensorMap tmW, int boxc, int ncopies, int 
   }
   const double scal = use_state_scal ? st->scal : scal_arg;
   __syncthreads();
-  const int64_t nch = (n + kLsR - 1) / kLsR;
+  const int64_t nch = (n + R - 1) / R;
   if (warp == kLsConsWarps) {
     // ---------------- producer warp ----------------
     const uint64_t pol = policy_evict_first();
     RingPos rp;
     for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
-      const int64_t r0 = ch * kLsR;
-      int64_t rows = n - r0 < kLsR ? n - r0 : kLsR;
+      const int64_t r0 = ch * R;
+      int64_t rows = n - r0 < R ? n - r0 : R;
       rows = (rows + 1) & ~(int64_t)1;   // 16-B multiple (inside the padded vector)
       const uint32_t tbytes = (uint32_t)(rows * 8);
       mbar_wait(empty + rp.stage, rp.phase ^ 1u);
       if (lane == 0) {
         double* sb = ring + (size_t)rp.stage * stage_d;
-        mbar_arrive_expect_tx(full + rp.stage, (uint32_t)(mpad * kLsR * 8) + tbytes);
+        mbar_arrive_expect_tx(full + rp.stage, (uint32_t)(mpad * R * 8) + tbytes);
         for (int q = 0; q < ncopies; ++q)
-          tma_load_2d(sb + (size_t)q * boxc * kLsR, &tmW, (int)r0, q * boxc, full + rp.stage, pol);
-        bulk_g2s(sb + (size_t)mpad * kLsR, t_old + r0, tbytes, full + rp.stage, pol);
+          tma_load_2d(sb + (size_t)q * boxc * R, &tmW, (int)r0, q * boxc, full + rp.stage, pol);
+        bulk_g2s(sb + (size_t)mpad * R, t_old + r0, tbytes, full + rp.stage, pol);
       }
       __syncwarp();
       rp.advance(nstage);
@@ -149,6 +172,9 @@ k_lsqr_pipe(const __grid_constant__ CUtensorMap tmW, int boxc, int ncopies, int 
     return;
   }
   // ---------------- consumer warps ----------------
+  // lane owns rows lane RPL + q (q < RPL) of every chunk; warp w owns columns
+  // w + 16 jj.  Per row: t = sum_j w_j p_j (warp partials summed in warp
+  // order) - scal t_old; per column: g_j += w_j t over the lane's rows in order.
   double acc[JPW];
 #pragma unroll
   for (int jj = 0; jj < JPW; ++jj) acc[jj] = 0.0;
@@ -156,45 +182,78 @@ k_lsqr_pipe(const __grid_constant__ CUtensorMap tmW, int boxc, int ncopies, int 
   int buf = 0;
   RingPos rp;
   for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
-    const int64_t r = ch * kLsR + lane;
-    const bool valid = r < n;
+    const int64_t rbase = ch * R + lane * RPL;
     mbar_wait(full + rp.stage, rp.phase);
     const double* sb = ring + (size_t)rp.stage * stage_d;
-    double vr[KEEP ? JPW : 1];
-    double tp = 0.0;
+    double vr[KEEP ? JPW : 1][RPL];
+    double tp[RPL];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) tp[q] = 0.0;
 #pragma unroll
     for (int jj = 0; jj < JPW; ++jj) {
       const int j = warp + kLsConsWarps * jj;
-      const double w = (valid && j < m) ? sb[j * kLsR + lane] : 0.0;
-      if (KEEP) vr[jj] = w;
-      if (j < m) tp = fma(w, sp[j], tp);
+      double w[RPL];
+      if (j < m) {
+        lds_rows<RPL>(sb + j * R + lane * RPL, w);   // rows >= n are zero (OOB fill)
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) tp[q] = fma(w[q], sp[j], tp[q]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) w[q] = 0.0;
+      }
+      if (KEEP) {
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) vr[KEEP ? jj : 0][q] = w[q];
+      }
     }
-    const double told = valid ? sb[mpad * kLsR + lane] : 0.0;
+    double told[RPL];
+    lds_rows<RPL>(sb + mpad * R + lane * RPL, told);
     if (KEEP) {   // the chunk's values stay in registers: release the stage now
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + rp.stage);
       rp.advance(nstage);
     }
-    tpart[buf][warp][lane] = tp;
-    consumer_sync(1, kLsCons);
-    double t = 0.0;
 #pragma unroll
-    for (int w = 0; w < kLsConsWarps; ++w) t += tpart[buf][w][lane];
-    t = fma(-scal, told, t);
-    if (!valid) t = 0.0;
-    if (warp == 0 && valid) {
-      t_new[r] = t;
-      tn = fma(t, t, tn);
+    for (int q = 0; q < RPL; ++q) tpart[buf][warp][lane * RPL + q] = tp[q];
+    consumer_sync(1, kLsCons);
+    double t[RPL];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) t[q] = 0.0;
+#pragma unroll
+    for (int w = 0; w < kLsConsWarps; ++w) {
+      double x[RPL];
+      lds_rows<RPL>(&tpart[buf][w][lane * RPL], x);
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) t[q] += x[q];
+    }
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      t[q] = fma(-scal, told[q], t[q]);
+      if (rbase + q >= n) t[q] = 0.0;
+    }
+    if (warp == 0) {
+#pragma unroll
+      for (int q = 0; q < RPL; ++q)
+        if (rbase + q < n) {
+          t_new[rbase + q] = t[q];
+          tn = fma(t[q], t[q], tn);
+        }
     }
     if (KEEP) {
 #pragma unroll
-      for (int jj = 0; jj < JPW; ++jj) acc[jj] = fma(vr[jj], t, acc[jj]);
+      for (int jj = 0; jj < JPW; ++jj)
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) acc[jj] = fma(vr[KEEP ? jj : 0][q], t[q], acc[jj]);
     } else {      // large m: re-read the chunk from shared memory, then release it
 #pragma unroll
       for (int jj = 0; jj < JPW; ++jj) {
         const int j = warp + kLsConsWarps * jj;
-        const double w = (valid && j < m) ? sb[j * kLsR + lane] : 0.0;
-        acc[jj] = fma(w, t, acc[jj]);
+        if (j < m) {
+          double w[RPL];
+          lds_rows<RPL>(sb + j * R + lane * RPL, w);
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) acc[jj] = fma(w[q], t[q], acc[jj]);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + rp.stage);
@@ -214,33 +273,389 @@ k_lsqr_pipe(const __grid_constant__ CUtensorMap tmW, int boxc, int ncopies, int 
   }
 }
 
+
+// ---- K6 on a CTA pair (cluster of 2): the m columns split in halves --------
+// Rank r of a cluster streams columns [r h, (r+1) h) (h = ceil(m/2)) of the
+// SAME 32 RPL-row chunks as its peer, so each CTA's box is R rows x h
+// columns: with RPL = 2 every column segment is 512 contiguous bytes (the
+// 32-row box's 256-B segments cap a pure TMA stream at 6.54 TB/s; 64-row
+// boxes reach 7.13-7.18, profiles/r02/micro_tma_box.jsonl) and the ring
+// still holds 4 stages, and the chunk's values of a warp's columns (h / 16
+// per warp x RPL rows) stay in registers.  Per chunk each CTA forms its
+// half of t = W p (warp partials summed in warp order), stores it into the
+// peer's shared memory (DSMEM) and signals the peer's mbarrier (32 lanes,
+// release at cluster scope); both then form t = T_0 + T_1 (rank order, so
+// both CTAs hold the same t bitwise) - scal t_old, and update g for their
+// own columns.  Rank 0 writes t_new and ||t||^2.  Partials: one row of
+// part_g (all m columns, each CTA its half) and one part_tn per cluster.
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cl_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cl_count() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cl_map(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+// asynchronous remote store that completes transaction bytes on the peer's
+// mbarrier (no fence on the sending side)
+__device__ __forceinline__ void cl_st_async2(uint32_t addr, double a, double b, uint32_t bar_addr) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(addr),
+               "d"(a), "d"(b), "r"(bar_addr)
+               : "memory");
+}
+__device__ __forceinline__ void cl_st_async1(uint32_t addr, double a, uint32_t bar_addr) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(addr), "d"(a),
+               "r"(bar_addr)
+               : "memory");
+}
+__device__ __forceinline__ void cl_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+constexpr int kClX = 4;   // exchange buffers per CTA (see the flow-control note below)
+
+template <int JPW, int RPL>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLsPipeThreads, 1)
+k_lsqr_pipe_cl(const __grid_constant__ CUtensorMap tmW, int h, int m, int64_t n, const double* __restrict__ p,
+               double scal_arg, const double* t_old, double* t_new, double* __restrict__ part_g,
+               double* __restrict__ part_tn, const DevState* __restrict__ st, int use_state_scal, int nstage) {
+  constexpr int R = 32 * RPL;
+  constexpr int RW = R / kLsConsWarps;   // rows a warp reduces (2 RPL)
+  static_assert(RPL == 1 || RPL == 2, "RPL");
+  if (st->lsqr_done) return;   // (uniform over the grid: both CTAs of a pair return)
+  extern __shared__ __align__(128) double ring[];
+  __shared__ double sp[kLsPipeMaxM / 2];
+  __shared__ __align__(16) double tpart[2][kLsConsWarps][R + 2];   // warp partials (rows padded: B reads a column)
+  __shared__ __align__(16) double tl_s[kClX][R];              // this CTA's half of W p
+  __shared__ __align__(16) double xpart[kClX][R];             // the peer's half (written by the peer)
+  __shared__ __align__(8) uint64_t xfull[kClX];
+  const uint32_t rank = cl_rank(), peer = rank ^ 1u;
+  const int cid = (int)cl_id(), ncl = (int)cl_count();
+  const int c0 = (int)rank * h;                          // first global column of this CTA
+  const int mloc = m - c0 < h ? m - c0 : h;              // its columns (the last may be one short)
+  const int stage_d = (h + 1) * R;                       // doubles per stage: W box + the t_old chunk
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)nstage * stage_d);
+  uint64_t* empty = full + nstage;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int j = tid; j < mloc; j += blockDim.x) sp[j] = p[c0 + j];
+  if (tid == 0) {
+    for (int i = 0; i < nstage; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, kLsConsWarps);
+    }
+    for (int i = 0; i < kClX; ++i) mbar_init(xfull + i, 1);   // armed per chunk with R x 8 transaction bytes
+    fence_barrier_init();
+  }
+  const double scal = use_state_scal ? st->scal : scal_arg;
+  __syncthreads();
+  cl_sync_all();   // the peer's barriers are initialised before anyone signals them
+  const int64_t nch = (n + R - 1) / R;
+  if (warp == kLsConsWarps) {
+    // ---------------- producer warp ----------------
+    const uint64_t pol = policy_evict_first();
+    RingPos rp;
+    for (int64_t ch = cid; ch < nch; ch += ncl) {
+      const int64_t r0 = ch * R;
+      int64_t rows = n - r0 < R ? n - r0 : R;
+      rows = (rows + 1) & ~(int64_t)1;   // 16-B multiple (inside the padded vector)
+      const uint32_t tbytes = (uint32_t)(rows * 8);
+      mbar_wait(empty + rp.stage, rp.phase ^ 1u);
+      if (lane == 0) {
+        double* sb = ring + (size_t)rp.stage * stage_d;
+        mbar_arrive_expect_tx(full + rp.stage, (uint32_t)(h * R * 8) + tbytes);
+        tma_load_2d(sb, &tmW, (int)r0, c0, full + rp.stage, pol);
+        bulk_g2s(sb + (size_t)h * R, t_old + r0, tbytes, full + rp.stage, pol);
+      }
+      __syncwarp();
+      rp.advance(nstage);
+    }
+  } else {
+    // ---------------- consumer warps ----------------
+    // Chunk i runs in two halves one iteration apart, so the exchange with
+    // the peer is off the critical path:
+    //   A(i): tp = this CTA's columns of W p for the lane's rows (from the
+    //         stage), warp partials to tpart, named barrier;
+    //   B(i): warp w sums the 16 partials of its RW rows (lane = partial x
+    //         row pair, shuffle tree in fixed order) -> tl_s and the peer's
+    //         xpart (DSMEM) + one release-arrive per sending lane;
+    //   C(i-1): wait for the peer's half of chunk i-1, t = T_0 + T_1 - scal
+    //         t_old, g += W^T t re-reading chunk i-1 from its stage, release it.
+    // Flow control of xpart: the peer overwrites buffer x of chunk i in its
+    // B(i + kClX); it gets there only after its C(i + 2) received our
+    // B(i + 2), and our C(i) precedes our B(i + 2) -- so kClX = 4 buffers.
+    double acc[JPW];
+#pragma unroll
+    for (int jj = 0; jj < JPW; ++jj) acc[jj] = 0.0;
+    double tn = 0.0;
+    const uint32_t xremote = cl_map(&xpart[0][0], peer);
+    const uint32_t xbar_remote = cl_map(&xfull[0], peer);
+    RingPos rp;        // stage of chunk i (A)
+    RingPos rq;        // stage of chunk i - 1 (C)
+    int it = 0;        // local chunk counter
+    // C for the chunk `ich` (local index) whose stage is rq: see above
+    auto finish = [&](int ich, int64_t chg) {
+      const int xb = ich % kClX;
+      mbar_wait(&xfull[xb], (uint32_t)((ich / kClX) & 1));
+      const double* sb = ring + (size_t)rq.stage * stage_d;
+      const int64_t rbase = chg * R + lane * RPL;
+      double tl[RPL], tr[RPL], told[RPL], t[RPL];
+      lds_rows<RPL>(&tl_s[xb][lane * RPL], tl);
+      lds_rows<RPL>(&xpart[xb][lane * RPL], tr);
+      lds_rows<RPL>(sb + h * R + lane * RPL, told);
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        t[q] = rank == 0 ? tl[q] + tr[q] : tr[q] + tl[q];
+        t[q] = fma(-scal, told[q], t[q]);
+        if (rbase + q >= n) t[q] = 0.0;
+      }
+      if (warp == 0 && rank == 0) {
+#pragma unroll
+        for (int q = 0; q < RPL; ++q)
+          if (rbase + q < n) {
+            t_new[rbase + q] = t[q];
+            tn = fma(t[q], t[q], tn);
+          }
+      }
+#pragma unroll
+      for (int jj = 0; jj < JPW; ++jj) {
+        const int j = warp + kLsConsWarps * jj;
+        if (j < mloc) {
+          double w[RPL];
+          lds_rows<RPL>(sb + j * R + lane * RPL, w);
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) acc[jj] = fma(w[q], t[q], acc[jj]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + rq.stage);
+      rq.advance(nstage);
+    };
+    int64_t prev = -1;
+    for (int64_t ch = cid; ch < nch; ch += ncl, ++it) {
+      const int buf = it & 1;
+      // A(i); arm this chunk's exchange barrier (its previous phase, chunk
+      // i - kClX, completed before this thread's finish(i - kClX) returned)
+      if (tid == 0) mbar_arrive_expect_tx(&xfull[it % kClX], (uint32_t)(R * sizeof(double)));
+      mbar_wait(full + rp.stage, rp.phase);
+      {
+        const double* sb = ring + (size_t)rp.stage * stage_d;
+        double tp[RPL];
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) tp[q] = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < JPW; ++jj) {
+          const int j = warp + kLsConsWarps * jj;
+          if (j < mloc) {
+            double w[RPL];
+            lds_rows<RPL>(sb + j * R + lane * RPL, w);   // rows >= n are zero (OOB fill)
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) tp[q] = fma(w[q], sp[j], tp[q]);
+          }
+        }
+        if constexpr (RPL == 1) tpart[buf][warp][lane] = tp[0];
+        else *reinterpret_cast<double2*>(&tpart[buf][warp][lane * 2]) = make_double2(tp[0], tp[1]);
+      }
+      rp.advance(nstage);
+      consumer_sync(1, kLsCons);
+      // B(i): lane = (partial pw = lane & 15, row pair rp2 = lane >> 4); warp w
+      // reduces rows w RW + {0..RW-1}
+      {
+        const int pw = lane & 15, half = lane >> 4;
+        double v[RPL];
+        if constexpr (RPL == 1) v[0] = tpart[buf][pw][warp * RW + half];
+        else lds_rows<2>(&tpart[buf][pw][warp * RW + 2 * half], v);
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1)
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+        const int xb = it % kClX;
+        if (pw == 0) {   // lanes 0 and 16 of each warp: R x 8 bytes per chunk in all
+          const int row = warp * RW + RPL * half;
+          const uint32_t dst = xremote + (uint32_t)((xb * R + row) * sizeof(double));
+          const uint32_t bar = xbar_remote + (uint32_t)(xb * sizeof(uint64_t));
+          if constexpr (RPL == 1) {
+            tl_s[xb][row] = v[0];
+            cl_st_async1(dst, v[0], bar);
+          } else {
+            *reinterpret_cast<double2*>(&tl_s[xb][row]) = make_double2(v[0], v[1]);
+            cl_st_async2(dst, v[0], v[1], bar);
+          }
+        }
+      }
+      // C(i-1)
+      if (prev >= 0) finish(it - 1, prev);
+      prev = ch;
+    }
+    if (prev >= 0) {
+      consumer_sync(1, kLsCons);   // every warp's tl_s of the last chunk is written
+      finish(it - 1, prev);
+    }
+#pragma unroll
+    for (int jj = 0; jj < JPW; ++jj) {
+      const int j = warp + kLsConsWarps * jj;
+      const double a = warp_sum(acc[jj]);
+      if (lane == 0 && j < mloc) part_g[(int64_t)cid * m + c0 + j] = a;
+    }
+    if (warp == 0 && rank == 0) {
+      const double a = warp_sum(tn);
+      if (lane == 0) part_tn[cid] = a;
+    }
+  }
+  cl_sync_all();   // no CTA leaves while its peer may still signal it
+}
+
 typedef void (*LsqrPipeFn)(const CUtensorMap, int, int, int, int64_t, const double*, double, const double*,
                            double*, double*, double*, const DevState*, int, int);
 
-static LsqrPipeFn pick_pipe(int m) {
-  const int need = (m + kLsConsWarps - 1) / kLsConsWarps;
-#define FAB_PICK(J) \
-  if (need <= J) return k_lsqr_pipe<J>;
-  FAB_PICK(2) FAB_PICK(4) FAB_PICK(8) FAB_PICK(13) FAB_PICK(16) FAB_PICK(19) FAB_PICK(24)
-#undef FAB_PICK
+// KEEP: the chunk's JPW x RPL values stay in registers between the two uses
+// (else re-read from shared memory, large m)
+// (FAB_LSQR_KEEP=0/1 overrides, measurement only)
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);   // read per call: tests switch variants inside one process
+  return e ? atoi(e) : dflt;
+}
+static int keep_override() { return env_int("FAB_LSQR_KEEP", -1); }
+template <int JPW, int RPL>
+LsqrPipeFn pipe_fn() {
+  const int o = keep_override();
+  const bool keep = o >= 0 ? o != 0 : (JPW * RPL <= 26);
+  return keep ? k_lsqr_pipe<JPW, RPL, true> : k_lsqr_pipe<JPW, RPL, false>;
+}
+
+typedef void (*LsqrPipeClFn)(const CUtensorMap, int, int, int64_t, const double*, double, const double*, double*,
+                             double*, double*, const DevState*, int, int);
+
+// the K6 configuration for m columns: kernel, rows per lane, boxes, ring
+// (cl: the CTA-pair kernel, boxc = h columns per CTA)
+struct PipeCfg {
+  LsqrPipeFn fn = nullptr;
+  LsqrPipeClFn cl = nullptr;
+  int rpl = 1, R = 32, boxc = 0, ncopies = 0, nstage = 0;
+  size_t smem = 0;
+  explicit operator bool() const { return fn || cl; }
+};
+
+static LsqrPipeClFn pick_pipe_cl_fn(int jpw, int rpl) {
+  if (jpw == 4 && rpl == 2) return k_lsqr_pipe_cl<4, 2>;
+  if (jpw == 8 && rpl == 2) return k_lsqr_pipe_cl<8, 2>;
+  if (jpw == 8 && rpl == 1) return k_lsqr_pipe_cl<8, 1>;
+  if (jpw == 12 && rpl == 2) return k_lsqr_pipe_cl<12, 2>;
+  if (jpw == 12 && rpl == 1) return k_lsqr_pipe_cl<12, 1>;
   return nullptr;
 }
 
-// W box: 32 rows x boxc columns, ncopies boxes per chunk (TMA box dims <= 256)
+static size_t pipe_cl_static(int rpl) {
+  return sizeof(double) * (kLsPipeMaxM / 2 + 2 * kLsConsWarps * (32 * rpl + 2) + 2 * kClX * 32 * rpl) +
+         kClX * sizeof(uint64_t);
+}
+
+static int pipe_cl_stages(int h, int rpl, size_t* smem) {
+  const size_t stage = (size_t)(h + 1) * 32 * rpl * sizeof(double);
+  int ns = (int)((kLsSmemLimit - pipe_cl_static(rpl) - 1024) / (stage + 16));
+  if (ns > kLsMaxStages) ns = kLsMaxStages;
+  *smem = (size_t)ns * stage + 2 * ns * sizeof(uint64_t);
+  return ns;
+}
+
+static LsqrPipeFn pick_pipe_fn(int jpw, int rpl) {
+#define FAB_PJ(J)                                        \
+  if (jpw == J) {                                        \
+    if (rpl == 1) return pipe_fn<J, 1>();                \
+    if (rpl == 2 && J <= 13) return pipe_fn<J, 2>();     \
+    if (rpl == 4 && J <= 8) return pipe_fn<J, 4>();      \
+    return nullptr;                                      \
+  }
+  FAB_PJ(2) FAB_PJ(4) FAB_PJ(8) FAB_PJ(13) FAB_PJ(16) FAB_PJ(19) FAB_PJ(24)
+#undef FAB_PJ
+  return nullptr;
+}
+
+static int pipe_jpw(int m) {
+  const int need = (m + kLsConsWarps - 1) / kLsConsWarps;
+  for (int J : {2, 4, 8, 13, 16, 19, 24})
+    if (need <= J) return J;
+  return 0;
+}
+
+// W box: R rows x boxc columns, ncopies boxes per chunk (TMA box dims <= 256)
 static void lsqr_boxes(int m, int* boxc, int* ncopies) {
   *ncopies = (m + 255) / 256;
   *boxc = (m + *ncopies - 1) / *ncopies;
 }
 
-static int lsqr_pipe_stages(int m, size_t* smem) {
+static int pipe_stages(int m, int rpl, size_t* smem) {
   int boxc, ncopies;
   lsqr_boxes(m, &boxc, &ncopies);
-  const size_t stage = (size_t)(boxc * ncopies + 1) * kLsR * sizeof(double);
-  const size_t fixed = sizeof(double) * (kMaxM + 2 * kLsConsWarps * 32) + 1024;
+  const size_t stage = (size_t)(boxc * ncopies + 1) * 32 * rpl * sizeof(double);
+  const size_t fixed = sizeof(double) * (kLsPipeMaxM + 2 * kLsConsWarps * 32 * rpl) + 1024;
   int ns = (int)((kLsSmemLimit - fixed) / (stage + 16));
   if (ns > kLsMaxStages) ns = kLsMaxStages;
   *smem = (size_t)ns * stage + 2 * ns * sizeof(uint64_t);
   return ns;
+}
+
+// 32-row boxes, or 64-row boxes where they pay (see below);
+// FAB_LSQR_RPL=1/2/4 forces one (measurement)
+static PipeCfg pick_pipe(int m, int64_t n, int num_sms) {
+  PipeCfg cfg;
+  const int jpw = pipe_jpw(m);
+  if (!jpw || m > kLsPipeMaxM) return cfg;
+  const int forced = env_int("FAB_LSQR_RPL", 0);
+  // the CTA pair: opt-in (FAB_LSQR_CLUSTER=1), measured slower under the
+  // sustained power cap
+  if (env_int("FAB_LSQR_CLUSTER", 0) == 1 && m >= 2) {
+    const int h = (m + 1) / 2;
+    const int cj = h <= 64 ? 4 : h <= 128 ? 8 : 12;
+    for (int rpl : {2, 1}) {
+      if (forced && rpl != forced) continue;
+      LsqrPipeClFn fn = pick_pipe_cl_fn(cj, rpl);
+      if (!fn) continue;
+      size_t smem = 0;
+      const int ns = pipe_cl_stages(h, rpl, &smem);
+      if (ns < 3) continue;
+      cfg.cl = fn;
+      cfg.rpl = rpl;
+      cfg.R = 32 * rpl;
+      cfg.boxc = h;
+      cfg.ncopies = 1;
+      cfg.nstage = ns;
+      cfg.smem = smem;
+      return cfg;
+    }
+  }
+  for (int rpl : {4, 2, 1}) {
+    if (forced ? rpl != forced : rpl == 4) continue;   // 128-row boxes: measured slower (c2)
+    LsqrPipeFn fn = pick_pipe_fn(jpw, rpl);
+    if (!fn) continue;
+    size_t smem = 0;
+    const int ns = pipe_stages(m, rpl, &smem);
+    // 64-row boxes only with a ring of >= 4 stages and the chunk in registers
+    // and >= 16 chunks per CTA (c2, m = 100: 2.88 vs 3.28 ms per pass; at
+    // m = 200 the two-stage ring is slower; c1 is too short:
+    // profiles/r02/k6_box_ab.jsonl)
+    if (ns < 2 || (!forced && rpl == 2 && (ns < 4 || jpw > 8 || n < (int64_t)64 * 16 * num_sms))) continue;
+    cfg.fn = fn;
+    cfg.rpl = rpl;
+    cfg.R = 32 * rpl;
+    cfg.nstage = ns;
+    cfg.smem = smem;
+    lsqr_boxes(m, &cfg.boxc, &cfg.ncopies);
+    return cfg;
+  }
+  return cfg;
 }
 
 // Tensor map over the first ncols columns of a column-major n x ncols fp64
@@ -250,7 +665,6 @@ static int lsqr_pipe_stages(int m, size_t* smem) {
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
 int make_tmap_cols(const double* base, int64_t n, int ncols, int64_t ld, int box_rows, int box_cols,
                    CUtensorMap* out) {
   static EncodeTiledFn fn = nullptr;
@@ -272,10 +686,19 @@ int make_tmap_cols(const double* base, int64_t n, int ncols, int64_t ld, int box
 }
 
 int lsqr_setup(fab_ctx* c) {
-  static const LsqrPipeFn fns[] = {k_lsqr_pipe<2>, k_lsqr_pipe<4>, k_lsqr_pipe<8>, k_lsqr_pipe<13>,
-                                   k_lsqr_pipe<16>, k_lsqr_pipe<19>, k_lsqr_pipe<24>};
-  const int dyn = kLsSmemLimit - (int)(sizeof(double) * (kMaxM + 2 * kLsConsWarps * 32));
-  for (LsqrPipeFn f : fns) FAB_CUDA(set_max_dyn_smem((const void*)f, dyn));
+  for (int J : {4, 8, 12})
+    for (int rpl : {1, 2}) {
+      LsqrPipeClFn f = pick_pipe_cl_fn(J, rpl);
+      if (!f) continue;
+      FAB_CUDA(set_max_dyn_smem((const void*)f, kLsSmemLimit - (int)pipe_cl_static(rpl)));
+    }
+  for (int J : {2, 4, 8, 13, 16, 19, 24})
+    for (int rpl : {1, 2, 4}) {
+      LsqrPipeFn f = pick_pipe_fn(J, rpl);
+      if (!f) continue;
+      const int dyn = kLsSmemLimit - (int)(sizeof(double) * (kLsPipeMaxM + 2 * kLsConsWarps * 32 * rpl));
+      FAB_CUDA(set_max_dyn_smem((const void*)f, dyn));
+    }
   return FAB_OK;
 }
 
@@ -439,6 +862,59 @@ static int launch_gemv_rows(fab_ctx* c, int ncols, const double* p, double scal,
   return FAB_OK;
 }
 
+// tensor map + launch of the chosen K6 kernel; *nparts = rows of partials
+static int make_pipe_map(fab_ctx* c, const PipeCfg& pc, int ncols, CUtensorMap* tm) {
+  return make_tmap_cols(c->V, c->n, ncols, c->ld, pc.R, pc.boxc, tm);
+}
+// CTA pairs that can be resident at once (a pair needs two SMs of one GPC,
+// so this can be below num_sms / 2): the persistent grid is sized to it
+static int max_pairs(const PipeCfg& pc, int num_sms) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, size_t>, int>> memo;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : memo)
+    if (e.first.first == (const void*)pc.cl && e.first.second == pc.smem) return e.second;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(2 * (num_sms / 2), 1, 1);
+  cfg.blockDim = dim3(kLsPipeThreads, 1, 1);
+  cfg.dynamicSmemBytes = pc.smem;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nc = 0;
+  if (cudaOccupancyMaxActiveClusters(&nc, (const void*)pc.cl, &cfg) != cudaSuccess || nc < 1) {
+    cudaGetLastError();
+    nc = num_sms / 2;
+  }
+  static bool said = false;
+  if (!said && getenv("FAB_VERBOSE")) {
+    fprintf(stderr, "[fab] K6 CTA pairs resident: %d (SMs %d)\n", nc, num_sms);
+    said = true;
+  }
+  memo.push_back({{(const void*)pc.cl, pc.smem}, nc});
+  return nc;
+}
+
+static int pipe_grid(const fab_ctx* c, const PipeCfg& pc) {
+  const int64_t nch = (c->n + pc.R - 1) / pc.R;
+  const int64_t cap = pc.cl ? max_pairs(pc, c->num_sms) : c->num_sms;
+  return (int)(nch < cap ? nch : cap);
+}
+static void launch_pipe(const PipeCfg& pc, const CUtensorMap& tm, int G, int ncols, int64_t n, const double* p,
+                        double scal, const double* t_old, double* t_new, double* part_g, double* part_tn,
+                        const DevState* st_d, int use_state, cudaStream_t st) {
+  if (pc.cl)
+    pc.cl<<<2 * G, kLsPipeThreads, pc.smem, st>>>(tm, pc.boxc, ncols, n, p, scal, t_old, t_new, part_g, part_tn,
+                                                  st_d, use_state, pc.nstage);
+  else
+    pc.fn<<<G, kLsPipeThreads, pc.smem, st>>>(tm, pc.boxc, pc.ncopies, ncols, n, p, scal, t_old, t_new, part_g,
+                                              part_tn, st_d, use_state, pc.nstage);
+}
+
 // One streaming pass over the first ncols stored columns W of V (K6):
 // t_new = W p - scal t_old (scal from st->scal if use_state_scal), with the
 // g = W^T t_new, ||t_new||^2 partials into part_g / part_tn.  Used by LSQR
@@ -459,19 +935,13 @@ int launch_tall_gemv(fab_ctx* c, int ncols, const double* p, double scal, int us
     if (ncols <= 32) return launch_gemv_rows<32>(c, ncols, p, scal, use_state_scal, t_old, t_new, st, nparts_out);
     return launch_gemv_rows<64>(c, ncols, p, scal, use_state_scal, t_old, t_new, st, nparts_out);
   }
-  LsqrPipeFn pipe = pick_pipe(ncols);
-  size_t smem = 0;
-  const int ns = lsqr_pipe_stages(ncols, &smem);
-  if (ns < 2) pipe = nullptr;
+  const PipeCfg pc = pick_pipe(ncols, c->n, c->num_sms);
+  bool pipe = (bool)pc;
   CUtensorMap tm;
-  int boxc = 0, ncopies = 0;
-  lsqr_boxes(ncols, &boxc, &ncopies);
-  if (pipe && make_tmap_cols(c->V, c->n, ncols, c->ld, kLsR, boxc, &tm) != FAB_OK) pipe = nullptr;
+  if (pipe && make_pipe_map(c, pc, ncols, &tm) != FAB_OK) pipe = false;
   if (pipe) {
-    const int64_t nch = (c->n + kLsR - 1) / kLsR;
-    const int G = (int)(nch < c->num_sms ? nch : c->num_sms);
-    pipe<<<G, kLsPipeThreads, smem, st>>>(tm, boxc, ncopies, ncols, c->n, p, scal, t_old, t_new, c->part_g,
-                                         c->part_tn, c->st_d, use_state_scal, ns);
+    const int G = pipe_grid(c, pc);
+    launch_pipe(pc, tm, G, ncols, c->n, p, scal, t_old, t_new, c->part_g, c->part_tn, c->st_d, use_state_scal, st);
     if (nparts_out) *nparts_out = G;
   } else {
     int jpw = 0;
@@ -919,17 +1389,14 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
     } else {
       int jpw = 0;
       LsqrPassFn pass = pick_pass(m, &jpw);
-      LsqrPipeFn pipe = pick_pipe(m);
-      size_t pipe_smem = 0;
-      const int pipe_ns = lsqr_pipe_stages(m, &pipe_smem);
-      if (pipe_ns < 2) pipe = nullptr;
+      const PipeCfg pc = pick_pipe(m, c->n, c->num_sms);
+      bool pipe = (bool)pc;
       if (!pass && !pipe) return FAB_EINVAL;
       CUtensorMap tmW;
-      int boxc = 0, ncopies = 0;
-      lsqr_boxes(m, &boxc, &ncopies);
-      if (pipe && make_tmap_cols(c->V, c->n, m, c->ld, kLsR, boxc, &tmW) != FAB_OK) pipe = nullptr;
-      const int64_t nchunks = (c->n + kLsR - 1) / kLsR;
-      const int G = pipe ? (int)(nchunks < c->num_sms ? nchunks : c->num_sms) : c->grid_lsqr;
+      if (pipe && make_pipe_map(c, pc, m, &tmW) != FAB_OK) pipe = false;
+      const int G = pipe ? pipe_grid(c, pc) : c->grid_lsqr;
+      const int pipe_ns = pc.nstage;
+      const void* pipe_kern = pc.cl ? (const void*)pc.cl : (const void*)pc.fn;
       // one streaming pass over V_m: t_new = W p - scal t_old, g = W^T t_new, ||t_new||^2 (launch_pass_on)
       const int fixed = (o && o->iters > 0) ? o->iters : 0;
       const double tol = (o && o->tol > 0) ? o->tol : 1e-6;
@@ -960,8 +1427,7 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
       };
       auto launch_pass_on = [&](double scal, const double* t_old, int use_state) {
         if (pipe)
-          pipe<<<G, kLsPipeThreads, pipe_smem, ls>>>(tmW, boxc, ncopies, m, c->n, L.p, scal, t_old, c->vec,
-                                                    c->part_g, c->part_tn, c->st_d, use_state, pipe_ns);
+          launch_pipe(pc, tmW, G, m, c->n, L.p, scal, t_old, c->vec, c->part_g, c->part_tn, c->st_d, use_state, ls);
         else
           pass<<<G, kLsqrThreads, 0, ls>>>(c->V, c->ld, m, c->n, L.p, scal, t_old, c->vec, c->part_g,
                                            c->part_tn, c->st_d, use_state);
@@ -1008,8 +1474,8 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
       const char* eg = getenv("FAB_LSQR_GRAPH");
       const bool graph_loop = !prof && !c->comm && !(eg && eg[0] == '0');
       if (graph_loop) {
-        const bool hit = c->gexec_lsqr && c->gl_m == m && c->gl_G == G && c->gl_pipe == (pipe != nullptr) &&
-                         c->gl_ns == pipe_ns && c->gl_fixed == fixed && c->gl_maxit == maxit && c->gl_tol == tol;
+        const bool hit = c->gexec_lsqr && c->gl_m == m && c->gl_G == G && c->gl_pipe == pipe &&
+                         c->gl_ns == pipe_ns && c->gl_kern == pipe_kern && c->gl_fixed == fixed && c->gl_maxit == maxit && c->gl_tol == tol;
         if (!hit) {
           if (c->gexec_lsqr) {
             cudaGraphExecDestroy(c->gexec_lsqr);
@@ -1070,8 +1536,9 @@ int run_compress(fab_ctx* c, int mode, const fab_lsqr_opts* o, int* warn) {
           c->nlaunch = nl0;
           c->gl_m = m;
           c->gl_G = G;
-          c->gl_pipe = pipe != nullptr;
+          c->gl_pipe = pipe;
           c->gl_ns = pipe_ns;
+          c->gl_kern = pipe_kern;
           c->gl_fixed = fixed;
           c->gl_maxit = maxit;
           c->gl_tol = tol;

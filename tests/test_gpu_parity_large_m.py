@@ -221,3 +221,27 @@ def test_precond_sketch_parity(name, kw, s2):
     assert abs(L1 - r1["lsqr"]["iters"]) <= 1
     assert L1 < L0, (L1, L0)
     sv.close()
+
+
+@pytest.mark.parametrize("env", [
+    {"FAB_LSQR_CLUSTER": "1"},                           # CTA pair, 64-row boxes (k_lsqr_pipe_cl<8, 2>)
+    {"FAB_LSQR_CLUSTER": "1", "FAB_LSQR_RPL": "1"},      # CTA pair, 32-row boxes (<8, 1>)
+    {"FAB_LSQR_RPL": "2", "FAB_LSQR_KEEP": "0"},         # one CTA, 64-row boxes, chunk re-read
+    {"FAB_LSQR_RPL": "2", "FAB_LSQR_KEEP": "1"},         # one CTA, 64-row boxes in registers
+], ids=["pair_r64", "pair_r32", "r64_reread", "r64_keep"])
+def test_lsqr_pass_variants_converged(env, monkeypatch):
+    """The opt-in K6 layouts (measured, not the defaults: DESIGN §7) compute
+    the same LSQR: at L = 120 (converged, y determined) y, C and f_m match
+    the oracle at 1e-10 on the c5 m = 200 case of CASES."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    name, kw, _ = CASES[0]
+    p = fp.make(name, **kw)
+    y, sv = gpu(p, "blendenpik", iters=120)
+    ref = ofab.solve(p.scipy(), p.b, p.m, p.k, p.s, p.sketch_seed, mode="blendenpik", f=p.f,
+                     alpha=p.alpha, sigma=p.sigma, lsqr_iters=120)
+    assert sv.info()["lsqr_iters"] == 120
+    assert rel(sv.get("y"), ref["y"]) <= 1e-10
+    assert rel(sv.get("C"), ref["C"]) <= 1e-10
+    assert rel(y, ref["f_m"]) <= 1e-10
+    sv.close()
