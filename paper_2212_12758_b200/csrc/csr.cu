@@ -64,6 +64,13 @@ struct CsrArgs {
   double* part[kBatchMax];       // per-CTA dot partials (DOTS)
   const DevState* st[kBatchMax];
   StepRed sr;                    // P == 1 on several GPUs: fused step reduction (last DOTS pass)
+  // warp-block K1 (k_csr_warp): warp block b = {first row, first entry,
+  // rows << 32 | lg G << 24 | entries} at wblk[3b..3b+2], and the rows too long for one
+  // warp (whole CTA each)
+  const int64_t* wblk;
+  int64_t nwblk;
+  const int64_t* lrows;
+  int64_t nlong;
 };
 
 // Cache policy: the entries, row pointers and z stream through once per pass
@@ -300,6 +307,278 @@ __global__ void __launch_bounds__(kThreads, P == 1 ? FAB_CSR_OCC : FAB_CSR_OCC_P
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-block K1 (P == 1): the same products and row sums as k_csr_stream,
+// but a row block belongs to ONE warp (<= kWNB entries, <= kWRows rows), so
+// no CTA-wide barrier separates the stream phase of one block from the
+// reduce phase of another: each warp runs index loads -> gathers -> row
+// sums -> z / dots on its own, and the 48 resident warps of an SM keep the
+// random gathers of x (the bound of a CSR K1 whose x sits in L2: one L2
+// sector request per gathered entry) in flight while others reduce.
+//   warp blocks : b = global warp id + i * (total warps), static;
+//   a row with kWNB < len <= kWLong entries is a warp block of its own,
+//     summed in registers kWNB entries at a time (lane-strided, then a
+//     fixed shuffle tree);
+//   a row with > kWLong entries (power-law hubs) is summed by the whole CTA
+//     first (lrows, CTA-strided), as k_csr_stream does.
+// Every assignment and summation order is fixed: bitwise reproducible.
+#ifndef FAB_CSRW_NB
+#define FAB_CSRW_NB 128
+#endif
+#ifndef FAB_CSRW_ROWS
+#define FAB_CSRW_ROWS 64
+#endif
+#ifndef FAB_CSRW_OCC
+#define FAB_CSRW_OCC FAB_CSR_OCC
+#endif
+#ifndef FAB_CSRW_RPREG
+#define FAB_CSRW_RPREG 1
+#endif
+#ifndef FAB_CSRW_HDR
+#define FAB_CSRW_HDR 1                       // block headers prefetched one block ahead (lanes 0..2)
+#endif
+constexpr int kWNB = FAB_CSRW_NB;      // entries per warp block
+constexpr int kWRows = FAB_CSRW_ROWS;  // rows per warp block (cap)
+constexpr int kWLong = 2048;   // longer rows: whole CTA
+constexpr int kWU = kWNB / 32;
+
+template <int NWM, bool ACC, bool DOTS>
+__device__ __forceinline__ void warp_row_out(const CsrArgs& a, int i, int64_t row, double acc, double zold,
+                                             const double (&wv)[NWM], double (&d)[NWM]) {
+  double zr = acc * a.vscale;
+  if (ACC) zr += zold;
+  a.z[i][row] = zr;
+  if (DOTS) {
+#pragma unroll
+    for (int t = 0; t < NWM; ++t) d[t] = fma(wv[t], zr, d[t]);
+  }
+}
+
+template <int NWM, bool DOTS>
+__device__ __forceinline__ void warp_row_window(const CsrArgs& a, int i, int64_t row, double (&wv)[NWM]) {
+  const int j0 = a.c - a.nw;
+  if (DOTS) {
+#pragma unroll
+    for (int t = 0; t < NWM - 1; ++t) wv[t] = (t < a.nw - 1) ? __ldg(a.V[i] + (int64_t)(j0 + t) * a.ld + row) : 0.0;
+    wv[NWM - 1] = __ldg(a.V[i] + (int64_t)(a.c - 1) * a.ld + row);
+  } else {
+#pragma unroll
+    for (int t = 0; t < NWM; ++t) wv[t] = 0.0;
+  }
+}
+
+// P right-hand sides share every entry load and gather (multi-RHS SpMM, the
+// interleaved x); per vector the arithmetic and its order are those of P = 1
+template <int NWM, bool ACC, bool DOTS, int P>
+__global__ void __launch_bounds__(kThreads, P == 1 ? FAB_CSRW_OCC : FAB_CSR_OCC_P) k_csr_warp(CsrArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  bool live[P];
+  bool any = false;
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    live[i] = !a.st[i]->breakdown;
+    any |= live[i];
+  }
+  if (!any) return;
+  __shared__ double prod[P][kWarps][kWNB];
+  __shared__ int rps[kWarps][kWRows + 1];
+  __shared__ double red[kWarps * (NWM > P ? NWM : P)];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double d[P][NWM];
+#pragma unroll
+  for (int i = 0; i < P; ++i)
+#pragma unroll
+    for (int t = 0; t < NWM; ++t) d[i][t] = 0.0;
+  const uint64_t pf = pol_first(), pl = pol_last();
+
+  // phase 1: rows longer than kWLong, one CTA each (k_csr_stream's long-row path)
+  for (int64_t r = blockIdx.x; r < a.nlong; r += gridDim.x) {
+    const int64_t r0 = a.lrows[r];
+    const int64_t q0 = rowq(a, r0, pf), cnt = rowq(a, r0 + 1, pf) - q0;
+    constexpr int U = kCsrNB / kThreads;
+    double acc[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) acc[i] = 0.0;
+    for (int64_t base = 0; base < cnt; base += kThreads * U) {
+      int col[U];
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t q = base + tid + kThreads * u;
+        col[u] = q < cnt ? ld_s32(a.ci + q0 + q, pf) : -1;
+        v[u] = (a.vals && q < cnt) ? ld_sf(a.vals + q0 + q, pf) : 1.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (col[u] >= 0) {
+          double xg[P];
+          gather_x<P>(a, col[u], pl, xg);
+#pragma unroll
+          for (int i = 0; i < P; ++i) acc[i] = fma(v[u], xg[i], acc[i]);
+        }
+    }
+    double o[P];
+    block_sum<P>(acc, red, o);
+    if (tid == 0) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        if (!live[i]) continue;
+        double wv[NWM];
+        warp_row_window<NWM, DOTS>(a, i, r0, wv);
+        warp_row_out<NWM, ACC, DOTS>(a, i, r0, o[i], ACC ? a.z[i][r0] : 0.0, wv, d[i]);
+      }
+    }
+  }
+
+  // phase 2: warp blocks
+  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+  int* rw = rps[warp];
+  // block headers one block ahead: the header -> entries -> gathers chain
+  // is the latency a warp block pays before its first gather
+  // (lanes 0..2 hold the three header words: one register pair per lane)
+  // (not in the DOTS pass: its window accumulators already fill the 40
+  // registers of 6 CTAs/SM, and the prefetch's two more spill -- measured
+  // c4, one DOTS pass: 344 vs 325 us per step; c5, 5 of 6 passes without
+  // dots: 4.22 vs 4.36 ms)
+  constexpr bool kPref = FAB_CSRW_HDR && !DOTS;
+  int64_t b = (int64_t)blockIdx.x * kWarps + warp;
+  int64_t hv = (kPref && b < a.nwblk && lane < 3) ? __ldg(a.wblk + 3 * b + lane) : 0;
+  for (; b < a.nwblk; b += nwarps) {
+    int64_t r0, q0, h2;
+    if (kPref) {
+      r0 = __shfl_sync(0xffffffffu, hv, 0);
+      q0 = __shfl_sync(0xffffffffu, hv, 1);
+      h2 = __shfl_sync(0xffffffffu, hv, 2);
+      if (b + nwarps < a.nwblk && lane < 3) hv = __ldg(a.wblk + 3 * (b + nwarps) + lane);
+    } else {
+      r0 = __ldg(a.wblk + 3 * b);
+      q0 = __ldg(a.wblk + 3 * b + 1);
+      h2 = __ldg(a.wblk + 3 * b + 2);
+    }
+    const int nrows = (int)(h2 >> 32), cnt = (int)(h2 & 0xffffff);
+    const int32_t* cb = a.ci + q0;
+    const double* vb = a.vals ? a.vals + q0 : nullptr;
+    if (cnt > kWNB) {
+      // one row (r1 == r0 + 1): lane-strided products summed in registers
+      double acc[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) acc[i] = 0.0;
+      for (int base = 0; base < cnt; base += kWNB) {
+        int col[kWU];
+        double v[kWU];
+#pragma unroll
+        for (int u = 0; u < kWU; ++u) {
+          const int q = base + lane + 32 * u;
+          col[u] = q < cnt ? ld_s32(cb + q, pf) : -1;
+          v[u] = (vb && q < cnt) ? ld_sf(vb + q, pf) : 1.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kWU; ++u)
+          if (col[u] >= 0) {
+            double xg[P];
+            gather_x<P>(a, col[u], pl, xg);
+#pragma unroll
+            for (int i = 0; i < P; ++i) acc[i] = fma(v[u], xg[i], acc[i]);
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < P; ++i) acc[i] = warp_sum(acc[i]);
+      if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          if (!live[i]) continue;
+          double wv[NWM];
+          warp_row_window<NWM, DOTS>(a, i, r0, wv);
+          warp_row_out<NWM, ACC, DOTS>(a, i, r0, acc[i], ACC ? ld_sf(a.z[i] + r0, pf) : 0.0, wv, d[i]);
+        }
+      }
+      continue;
+    }
+    {
+      // entries, then the row pointers, then the gathers: every load of the
+      // block is in flight before the first gather waits for its index
+      int col[kWU];
+      double v[kWU], xv[kWU][P];
+#pragma unroll
+      for (int u = 0; u < kWU; ++u) {
+        const int q = lane + 32 * u;
+        col[u] = q < cnt ? ld_s32(cb + q, pf) : -1;
+        v[u] = (vb && q < cnt) ? ld_sf(vb + q, pf) : 1.0;
+      }
+#if FAB_CSRW_RPREG
+      constexpr int kRU = (kWRows + 32) / 32;   // row pointers per lane (nrows + 1 <= kWRows + 1)
+      int rq[kRU];
+#pragma unroll
+      for (int u = 0; u < kRU; ++u) {
+        const int q = lane + 32 * u;
+        rq[u] = q <= nrows ? (int)(rowq(a, r0 + q, pf) - q0) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < kRU; ++u)
+        if (lane + 32 * u <= nrows) rw[lane + 32 * u] = rq[u];
+#else
+      for (int q = lane; q <= nrows; q += 32) rw[q] = (int)(rowq(a, r0 + q, pf) - q0);
+#endif
+#pragma unroll
+      for (int u = 0; u < kWU; ++u) {
+        if (col[u] >= 0) {
+          gather_x<P>(a, col[u], pl, xv[u]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < P; ++i) xv[u][i] = 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kWU; ++u) {
+        const int q = lane + 32 * u;
+        if (q < cnt) {
+#pragma unroll
+          for (int i = 0; i < P; ++i) prod[i][warp][q] = v[u] * xv[u][i];
+        }
+      }
+    }
+    __syncwarp();
+    // G = 2^lg lanes per row (the least power of two with 4 G >= the mean
+    // row length, from the header), R = 32 / G rows per round
+    const int lg = (int)((h2 >> 24) & 7), G = 1 << lg, R = 32 >> lg;
+    for (int rb = 0; rb < nrows; rb += R) {
+      const int rl = rb + (lane >> lg), sub = lane & (G - 1);
+      const bool own = rl < nrows && sub == 0;
+      const int64_t row = r0 + rl;
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        double wv[NWM], zold = 0.0;
+        if (own && live[i]) {   // issue the row's other loads before summing
+          if (ACC) zold = ld_sf(a.z[i] + row, pf);
+          warp_row_window<NWM, DOTS>(a, i, row, wv);
+        }
+        double acc = 0.0;
+        if (rl < nrows) {
+          const int e = rw[rl + 1];
+          for (int q = rw[rl] + sub; q < e; q += G) acc += prod[i][warp][q];
+        }
+        for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (own && live[i]) warp_row_out<NWM, ACC, DOTS>(a, i, row, acc, zold, wv, d[i]);
+      }
+    }
+    __syncwarp();
+  }
+  if (DOTS) {
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      double out[NWM];
+      block_sum<NWM>(d[i], red, out);
+      if (tid == 0 && live[i]) {
+        double* pp = a.part[i] + (int64_t)blockIdx.x * (kKMax + 1);
+        for (int t = 0; t < a.nw - 1; ++t) pp[t] = out[t];
+        pp[a.nw - 1] = out[NWM - 1];
+      }
+    }
+    if (P == 1) step_red_tail(a.sr, a.part[0], gridDim.x, a.nw, red);
+  }
+}
+
 // uniform values: flag stays 1 iff every value equals v0
 __global__ void k_csr_uniform(const double* __restrict__ vals, int64_t nnz, double v0, int* flag) {
   bool same = true;
@@ -318,6 +597,10 @@ struct CsrPass {
   const double* vals = nullptr;
   int64_t* blk = nullptr;   // owned
   int64_t nblk = 0;
+  int64_t* wblk = nullptr;  // owned: warp block headers (k_csr_warp), 3 per block
+  int64_t nwblk = 0;
+  int64_t* lrows = nullptr; // owned: rows with > kWLong entries
+  int64_t nlong = 0;
 };
 
 struct CsrPlan {
@@ -328,8 +611,11 @@ struct CsrPlan {
   bool uniform = false;       // every value equals v0: the value array is dropped
   double v0 = 1.0;
   ~CsrPlan() {
-    for (auto& p : pass)
+    for (auto& p : pass) {
       if (p.blk) cudaFree(p.blk);
+      if (p.wblk) cudaFree(p.wblk);
+      if (p.lrows) cudaFree(p.lrows);
+    }
     for (void* q : owned) cudaFree(q);
   }
 };
@@ -357,6 +643,64 @@ static int upload_blocks(const std::vector<int64_t>& bl, CsrPass* p) {
   FAB_CUDA(cudaMalloc(&p->blk, bl.size() * sizeof(int64_t)));
   FAB_CUDA(cudaMemcpy(p->blk, bl.data(), bl.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
   return FAB_OK;
+}
+
+// warp blocks of k_csr_warp over row pointers q(r): pairs [r0, r1) of
+// <= kWNB entries and <= kWRows rows, a row of kWNB < len <= kWLong entries
+// alone; rows with more entries go to `lr` (whole CTA each)
+struct WarpBlocks {
+  std::vector<int64_t> wb, lr;   // wb: {first row, first entry, rows << 32 | lg G << 24 | entries} per block
+};
+template <typename Q>
+static WarpBlocks build_warp_blocks(int64_t n, Q q) {
+  WarpBlocks o;
+  auto push = [&](int64_t r0, int64_t r1) {
+    o.wb.push_back(r0);
+    o.wb.push_back(q(r0));
+    // rows << 32 | lg G << 24 | entries, G = the least power of two with
+    // 4 G >= the mean row length (1..32)
+    const int64_t cnt = q(r1) - q(r0), avg = cnt / (r1 - r0);
+    int lg = 0;
+    if (avg > 4)
+      while ((4 << lg) < avg && lg < 5) ++lg;
+    o.wb.push_back(((r1 - r0) << 32) | ((int64_t)lg << 24) | cnt);
+  };
+  int64_t r = 0;
+  while (r < n) {
+    const int64_t len = q(r + 1) - q(r);
+    if (len > kWLong) {
+      o.lr.push_back(r++);
+      continue;
+    }
+    if (len > kWNB) {
+      push(r, r + 1);
+      ++r;
+      continue;
+    }
+    const int64_t q0 = q(r), rs = r;
+    while (r < n && q(r + 1) - q0 <= kWNB && r - rs < kWRows) ++r;
+    push(rs, r);
+  }
+  return o;
+}
+
+static int upload_warp_blocks(const WarpBlocks& w, CsrPass* p) {
+  p->nwblk = (int64_t)w.wb.size() / 3;
+  p->nlong = (int64_t)w.lr.size();
+  FAB_CUDA(cudaMalloc(&p->wblk, (w.wb.size() + 3) * sizeof(int64_t)));
+  if (!w.wb.empty())
+    FAB_CUDA(cudaMemcpy(p->wblk, w.wb.data(), w.wb.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  FAB_CUDA(cudaMalloc(&p->lrows, (w.lr.size() + 1) * sizeof(int64_t)));
+  if (!w.lr.empty())
+    FAB_CUDA(cudaMemcpy(p->lrows, w.lr.data(), w.lr.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  return FAB_OK;
+}
+
+// K1 variant: "warp" (k_csr_warp, default) or "cta" (k_csr_stream);
+// FAB_CSR_K1=cta selects the CTA-block kernel (A/B)
+static bool use_warp_k1() {
+  const char* e = getenv("FAB_CSR_K1");
+  return !(e && e[0] == 'c');
 }
 
 // Plans are shared by the contexts of one operator (the multi-RHS batch
@@ -613,6 +957,7 @@ static int build_plan(fab_ctx* c, CsrPlan* plan, int64_t width) {
     p.ci = c->op.col_idx;
     p.vals = values;
     FAB_TRY(upload_blocks(build_blocks(n, kCsrNB, [&](int64_t r) { return rp[r]; }), &p));
+    FAB_TRY(upload_warp_blocks(build_warp_blocks(n, [&](int64_t r) { return rp[r]; }), &p));
     plan->pass.push_back(p);
     plan->ord.push_back(0);
     return FAB_OK;
@@ -686,12 +1031,14 @@ static int build_plan(fab_ctx* c, CsrPlan* plan, int64_t width) {
   }
   plan->width = width;
   std::vector<std::vector<int64_t>> bls(P);
+  std::vector<WarpBlocks> wbs(P);
   {
     std::vector<std::thread> th;
     for (int64_t j = 0; j < P; ++j)
       th.emplace_back([&, j]() {
         const int32_t* rj = rp2.data() + (size_t)j * (n + 1);
         bls[j] = build_blocks(n, kCsrNB, [&](int64_t r) { return (int64_t)rj[r]; });
+        wbs[j] = build_warp_blocks(n, [&](int64_t r) { return (int64_t)rj[r]; });
       });
     for (auto& x : th) x.join();
   }
@@ -703,6 +1050,7 @@ static int build_plan(fab_ctx* c, CsrPlan* plan, int64_t width) {
     p.ci = dci + base[j];
     p.vals = dva ? dva + base[j] : nullptr;
     FAB_TRY(upload_blocks(bls[j], &p));
+    FAB_TRY(upload_warp_blocks(wbs[j], &p));
     plan->pass.push_back(p);
     plan->ord.push_back(ord_of_block(j));
   }
@@ -742,6 +1090,12 @@ int64_t csr_max_blocks(const fab_ctx* c) {
 
 template <int NWM, int P>
 static cudaError_t launch_pass_p(const CsrArgs& a, int grid, bool acc, bool dots, bool pdl, cudaStream_t st) {
+  if (a.wblk) {
+    if (!acc && dots) return launch_pdl(pdl, k_csr_warp<NWM, false, true, P>, grid, kThreads, 0, st, a);
+    if (!acc) return launch_pdl(pdl, k_csr_warp<NWM, false, false, P>, grid, kThreads, 0, st, a);
+    if (dots) return launch_pdl(pdl, k_csr_warp<NWM, true, true, P>, grid, kThreads, 0, st, a);
+    return launch_pdl(pdl, k_csr_warp<NWM, true, false, P>, grid, kThreads, 0, st, a);
+  }
   if (!acc && dots) return launch_pdl(pdl, k_csr_stream<NWM, false, true, P>, grid, kThreads, 0, st, a);
   if (!acc) return launch_pdl(pdl, k_csr_stream<NWM, false, false, P>, grid, kThreads, 0, st, a);
   if (dots) return launch_pdl(pdl, k_csr_stream<NWM, true, true, P>, grid, kThreads, 0, st, a);
@@ -788,6 +1142,12 @@ int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* con
     a.c = col;
     a.nw = nw;
     a.xi = p > 1 ? xi : nullptr;
+    if (use_warp_k1()) {
+      a.wblk = ps.wblk;
+      a.nwblk = ps.nwblk;
+      a.lrows = ps.lrows;
+      a.nlong = ps.nlong;
+    }
     for (int i = 0; i < p; ++i) {
       a.V[i] = cs[i]->V;
       a.xg[i] = xin[i];

@@ -80,7 +80,8 @@ def test_blendenpik_y_C_fm_at_pipe_instantiation(name, kw, inst):
     determine to ~cond(V_m) eps -- y, C and f_m at 1e-10.  At L = 40 the
     iterate is still ~1e-7 from it and, like any unconverged Krylov iterate,
     carries the implementation's rounding (reading R-3): compared at 20x the
-    oracle's own noise floor (R^{-1} by substitution vs explicit inverse)."""
+    oracle's own noise floor (R^{-1} by substitution vs explicit inverse; the
+    MGS vs CGS basis)."""
     p = fp.make(name, **kw)
     y, sv = gpu(p, "blendenpik", iters=120)
     A = p.scipy()
@@ -109,7 +110,13 @@ def test_blendenpik_y_C_fm_at_pipe_instantiation(name, kw, inst):
                     sigma=p.sigma, lsqr_iters=40)
     r2 = ofab.solve(A, p.b, p.m, p.k, p.s, p.sketch_seed, mode="blendenpik", f=p.f, alpha=p.alpha,
                     sigma=p.sigma, lsqr_iters=40, lsqr_rinv="inverse")
-    ny, nf = rel(r2["y"], r1["y"]), rel(r2["f_m"], r1["f_m"])
+    # the iterate's floor (reading R-3): R^{-1} by substitution vs explicit
+    # inverse, and the basis's own rounding (the literal MGS order of Alg 2
+    # line 6 vs CGS) -- the GPU's SpMV sums each row in its own order
+    r3 = ofab.solve(A, p.b, p.m, p.k, p.s, p.sketch_seed, mode="blendenpik", f=p.f, alpha=p.alpha,
+                    sigma=p.sigma, lsqr_iters=40, variant="mgs")
+    ny = max(rel(r2["y"], r1["y"]), rel(r3["y"], r1["y"]))
+    nf = max(rel(r2["f_m"], r1["f_m"]), rel(r3["f_m"], r1["f_m"]))
     assert sv.info()["lsqr_iters"] == 40
     assert abs(sv.info()["lsqr_rnorm"] - r1["lsqr"]["rnorm"]) <= 1e-10 * r1["lsqr"]["rnorm"]
     assert rel(sv.get("y"), r1["y"]) <= max(1e-10, 20 * ny), (rel(sv.get("y"), r1["y"]), ny)
@@ -157,7 +164,8 @@ def test_tolerance_mode_at_pipe_instantiation(name, kw, inst):
     """The headline's mode (MATLAB lsqr tol 1e-6, l.359): the same iteration
     count as the oracle and f_m at its noise floor (reading R-3: an
     intermediate LSQR iterate moves by the oracle's own rounding; measured
-    here as the gap between R^{-1} by substitution and by explicit inverse)."""
+    here as the gap between R^{-1} by substitution and by explicit inverse,
+    and between the MGS and CGS bases)."""
     p = fp.make(name, **kw)
     y, sv = gpu(p, "blendenpik", tol=1e-6)
     inf = sv.info()
@@ -170,8 +178,10 @@ def test_tolerance_mode_at_pipe_instantiation(name, kw, inst):
                     alpha=p.alpha, sigma=p.sigma, lsqr_iters=L)
     r2 = ofab.solve(p.scipy(), p.b, p.m, p.k, p.s, p.sketch_seed, mode="blendenpik", f=p.f,
                     alpha=p.alpha, sigma=p.sigma, lsqr_iters=L, lsqr_rinv="inverse")
-    ny = rel(r2["y"], r1["y"])
-    nf = rel(r2["f_m"], r1["f_m"])
+    r3 = ofab.solve(p.scipy(), p.b, p.m, p.k, p.s, p.sketch_seed, mode="blendenpik", f=p.f,
+                    alpha=p.alpha, sigma=p.sigma, lsqr_iters=L, variant="mgs")
+    ny = max(rel(r2["y"], r1["y"]), rel(r3["y"], r1["y"]))
+    nf = max(rel(r2["f_m"], r1["f_m"]), rel(r3["f_m"], r1["f_m"]))
     assert rel(sv.get("y"), r1["y"]) <= max(1e-10, 20 * ny), (rel(sv.get("y"), r1["y"]), ny)
     assert rel(y, r1["f_m"]) <= max(1e-10, 20 * nf), (rel(y, r1["f_m"]), nf)
     sv.close()
