@@ -54,7 +54,9 @@ def child(name, m, nrhs=1, reps=5):
         if r:
             ts.append(svs[0].info()["ms_basis"])
     ms = statistics.median(ts)
-    return dict(ms_basis=ms, p=nrhs, us_per_step_per_rhs=1e3 * ms / (m * nrhs), all=ts)
+    import hashlib
+    hsh = hashlib.sha256(np.ascontiguousarray(svs[0].get("H")).tobytes()).hexdigest()[:16]
+    return dict(ms_basis=ms, p=nrhs, us_per_step_per_rhs=1e3 * ms / (m * nrhs), all=ts, H_sha=hsh)
 
 
 def main():
