@@ -37,7 +37,7 @@ def run():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     if not os.path.exists(GOLDEN):
-        pytest.skip(f"{GOLDEN} not generated yet: run tests/golden/make_c5_golden.py (oracle only, ~1.5 h)")
+        pytest.fail(f"{GOLDEN} missing: run tests/golden/make_c5_golden.py (oracle only)")
     torch.cuda.set_device(0)
     torch.cuda.empty_cache()
     import paper_2212_12758_b200 as fab
