@@ -1094,41 +1094,13 @@ int64_t csr_max_blocks(const fab_ctx* c) {
   return m;
 }
 
-// k_csr_warp launch: PDL as launch_pdl, plus (column-blocked passes,
-// FAB_CSR_L2PERSIST=1) an L2 access-policy window that marks this pass's
-// slice of x persisting, so the entry / z streams cannot evict it
-static thread_local const cudaAccessPolicyWindow* t_win = nullptr;
-template <typename... KArgs, typename... Args>
-static cudaError_t launch_csr(bool pdl, void (*k)(KArgs...), int grid, cudaStream_t st, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = st;
-  cudaLaunchAttribute at[2];
-  int na = 0;
-  if (pdl) {
-    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[na].val.programmaticStreamSerializationAllowed = 1;
-    ++na;
-  }
-  if (t_win) {
-    at[na].id = cudaLaunchAttributeAccessPolicyWindow;
-    at[na].val.accessPolicyWindow = *t_win;
-    ++na;
-  }
-  cfg.attrs = at;
-  cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
-}
-
 template <int NWM, int P>
 static cudaError_t launch_pass_p(const CsrArgs& a, int grid, bool acc, bool dots, bool pdl, cudaStream_t st) {
   if (a.wblk) {
-    if (!acc && dots) return launch_csr(pdl, k_csr_warp<NWM, false, true, P>, grid, st, a);
-    if (!acc) return launch_csr(pdl, k_csr_warp<NWM, false, false, P>, grid, st, a);
-    if (dots) return launch_csr(pdl, k_csr_warp<NWM, true, true, P>, grid, st, a);
-    return launch_csr(pdl, k_csr_warp<NWM, true, false, P>, grid, st, a);
+    if (!acc && dots) return launch_pdl(pdl, k_csr_warp<NWM, false, true, P>, grid, kThreads, 0, st, a);
+    if (!acc) return launch_pdl(pdl, k_csr_warp<NWM, false, false, P>, grid, kThreads, 0, st, a);
+    if (dots) return launch_pdl(pdl, k_csr_warp<NWM, true, true, P>, grid, kThreads, 0, st, a);
+    return launch_pdl(pdl, k_csr_warp<NWM, true, false, P>, grid, kThreads, 0, st, a);
   }
   if (!acc && dots) return launch_pdl(pdl, k_csr_stream<NWM, false, true, P>, grid, kThreads, 0, st, a);
   if (!acc) return launch_pdl(pdl, k_csr_stream<NWM, false, false, P>, grid, kThreads, 0, st, a);
@@ -1144,22 +1116,6 @@ static cudaError_t launch_pass(const CsrArgs& a, int grid, int p, bool acc, bool
     case 3: return launch_pass_p<NWM, 3>(a, grid, acc, dots, pdl, st);
     default: return launch_pass_p<NWM, 4>(a, grid, acc, dots, pdl, st);
   }
-}
-
-// FAB_CSR_L2PERSIST=1: set aside persisting L2 for the column-blocked
-// passes' x slices (once per process and device: the limit is device-wide)
-static bool l2_persist(fab_ctx* c) {
-  const char* e = getenv("FAB_CSR_L2PERSIST");
-  if (!(e && e[0] == '1')) return false;
-  static std::once_flag once;
-  static bool ok = false;
-  std::call_once(once, [&]() {
-    int mx = 0;
-    if (cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, c->device) == cudaSuccess && mx > 0)
-      ok = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)mx) == cudaSuccess;
-    cudaGetLastError();
-  });
-  return ok;
 }
 
 // z_i = A xin_i (+ the window dots when nw > 0) for the p contexts cs[i]
@@ -1208,27 +1164,9 @@ int csr_spmv_multi(fab_ctx* const* cs, int p, int col, int nw, const double* con
     const bool acc = j > 0, dots = (j == np - 1) && nw > 0;
     a.sr = (dots && p == 1) ? sr : StepRed{};
     const bool pdl = c->pdl && !c->comm;
-    cudaAccessPolicyWindow win = {};
-    t_win = nullptr;
-    if (plan->width > 0 && !c->comm && l2_persist(c)) {
-      const int S = p > 1 ? ((p + 1) & ~1) : 1;
-      const int64_t c0 = (int64_t)j * plan->width;
-      const int64_t nc = std::min<int64_t>(plan->width, c->n_global - c0);
-      const double* base = p > 1 ? xi + c0 * S : xin[0] + c0;
-      // pass j reads column block j unless an empty block was skipped
-      if (nc > 0 && plan->pass.size() == (size_t)((c->n_global + plan->width - 1) / plan->width)) {
-        win.base_ptr = (void*)base;
-        win.num_bytes = (size_t)nc * S * sizeof(double);
-        win.hitRatio = 1.0f;
-        win.hitProp = cudaAccessPropertyPersisting;
-        win.missProp = cudaAccessPropertyStreaming;
-        t_win = &win;
-      }
-    }
     if (c->k_max <= 2) FAB_CUDA(launch_pass<2>(a, c->grid_spmv, p, acc, dots, pdl, st));
     else if (c->k_max <= 4) FAB_CUDA(launch_pass<4>(a, c->grid_spmv, p, acc, dots, pdl, st));
     else FAB_CUDA(launch_pass<8>(a, c->grid_spmv, p, acc, dots, pdl, st));
-    t_win = nullptr;
     FAB_CHECK_LAUNCH();
     ++*launches;
   }
