@@ -673,3 +673,53 @@ def test_csr_long_rows(colblock, monkeypatch):
         assert rel(y, ref["f_m"]) <= 1e-10, rel(y, ref["f_m"])
     for sv in svs + [single]:
         sv.close()
+
+
+# ---- warp-block CSR K1 (k_csr_warp): block boundaries ----------------------
+def _boundary_matrix(n=5000, seed=9191):
+    """Seeded sparse matrix whose row lengths sit on every warp-block
+    boundary of k_csr_warp (csr.cu: kWNB = 128 entries, kWRows = 64 rows,
+    kWLong = 2048): rows of 0, 1, 127, 128, 129, 2047, 2048 and 2049 entries,
+    a run of 300 empty rows (blocks cut by the 64-row cap), a run of rows of
+    exactly 64 entries (two per block) and 3-entry rows elsewhere."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(seed)
+    lens = np.full(n, 3)
+    lens[1000:1300] = 0
+    lens[2000:2100] = 64
+    for r, L in ((5, 0), (6, 1), (7, 127), (8, 128), (9, 129), (400, 2047), (401, 2048), (402, 2049),
+                 (n - 2, 129), (n - 1, 2049)):
+        lens[r] = L
+    rows = np.repeat(np.arange(n), lens)
+    cols = np.concatenate([rng.choice(n, L, replace=False) for L in lens if L > 0])
+    vals = rng.standard_normal(rows.size) / np.sqrt(np.maximum(lens[rows], 1))
+    A = sp.csr_matrix((vals, (rows, cols)), shape=(n, n))
+    A.sort_indices()
+    assert np.array_equal(np.diff(A.indptr), lens)
+    return A, rng.standard_normal(n)
+
+
+@pytest.mark.parametrize("k1", ["warp", "cta"])
+@pytest.mark.parametrize("colblock", [None, "700"])
+def test_csr_warp_block_boundaries(k1, colblock, monkeypatch):
+    """Both CSR K1 kernels (k_csr_warp, default; k_csr_stream under
+    FAB_CSR_K1=cta) against the oracle on rows at every block boundary:
+    H at 1e-12, f_m of the converged Blendenpik solve at 1e-10; unblocked and
+    with forced column blocks (rows split over 8 passes, z += passes)."""
+    import torch
+    import paper_2212_12758_b200 as fab
+    monkeypatch.setenv("FAB_CSR_K1", k1)
+    if colblock:
+        monkeypatch.setenv("FAB_CSR_COLBLOCK", colblock)
+    A, b = _boundary_matrix()
+    m, k, s, seed = 24, 2, 64, 31
+    ref = ofab.solve(A, b, m, k, s, seed, mode="blendenpik", f="exp", alpha=-0.5, lsqr_iters=60, keep=False)
+    sv = fab.Solver(fab.Operator.csr(A.indptr, A.indices, A.data), torch.as_tensor(b).cuda(), m, k, s)
+    sv.sketch(s, seed)
+    sv.basis(m, k)
+    assert sv.info()["m_eff"] == ref["m_eff"]
+    assert rel(sv.get("H"), ref["H"]) <= 1e-12, rel(sv.get("H"), ref["H"])
+    sv.compress("blendenpik", iters=60)
+    y = sv.apply("exp", -0.5, 0.0).cpu().numpy()
+    assert rel(y, ref["f_m"]) <= 1e-10, rel(y, ref["f_m"])
+    sv.close()
