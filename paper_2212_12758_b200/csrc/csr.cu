@@ -341,6 +341,8 @@ constexpr int kWNB = FAB_CSRW_NB;      // entries per warp block
 constexpr int kWRows = FAB_CSRW_ROWS;  // rows per warp block (cap)
 constexpr int kWLong = 2048;   // longer rows: whole CTA
 constexpr int kWU = kWNB / 32;
+static_assert(kWNB % 32 == 0 && kWNB <= kWLong, "warp block: 32 lanes x kWU entries");
+static_assert(kWLong < (1 << 24), "a warp block's entry count is packed in 24 bits of its header");
 
 template <int NWM, bool ACC, bool DOTS>
 __device__ __forceinline__ void warp_row_out(const CsrArgs& a, int i, int64_t row, double acc, double zold,
