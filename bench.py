@@ -401,8 +401,8 @@ def main():
     use_comm = world > 1 or os.environ.get("FAB_BENCH_COMM") == "1"
     if use_comm:
         import torch.distributed as dist
-        if world > 1:
-            dist.init_process_group("nccl")
+        if world > 1 or os.environ.get("TORCHELASTIC_RUN_ID") or os.environ.get("MASTER_PORT"):
+            dist.init_process_group("nccl")   # torchrun (any world size): its env / agent store
         else:
             import socket
             with socket.socket() as so:
