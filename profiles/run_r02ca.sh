@@ -1,0 +1,5 @@
+# session-start validation in a re-created container: GPU suite, smoke, the driver's bench command
+O=gpurun_out/r02ca; mkdir -p $O
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke_rc=$?; tail -1 $O/smoke.log
+timeout 1500 python bench.py --gpus 1 --steps 20 --warmup 5 > $O/bench.json 2> $O/bench.err; echo bench_rc=$?; cat $O/bench.json | head -c 600
+timeout 2700 python -m pytest tests -m gpu -x -q --timeout 1500 > $O/tests.log 2>&1; echo tests_rc=$? >> $O/tests.log; tail -3 $O/tests.log; grep -E "^(FAILED|ERROR)" $O/tests.log | head
