@@ -1118,6 +1118,180 @@ __global__ void __launch_bounds__(kSkG * kSkGT, 2) k_sketch_groups(PipeArgs a, i
   }
 }
 
+// ---------------------------------------------------------------------------
+// K5 v3 (opt-in FAB_SKETCH_K5=3, measured, not the default): one warp per
+// 1024-row sub-tile.
+//
+// H_N = H_{N/T'} (x) H_{T'} holds for every power of two T' <= N, so the
+// sampled rows of H_N D x can be formed from 1024-row transforms as well as
+// from K3's 4096-row ones: (H_N D x)[r] = sum_t (-1)^popcount((r >> 10) & t)
+// (H_1024 (D x)_t)[r mod 1024] over the 1024-row tiles t.  With 32 values per
+// lane a 1024-point FWHT is two radix-32 rounds in registers around ONE
+// exchange through the warp's own shared buffer -- no CTA barrier per tile --
+// against k_sketch_direct's three radix-16 rounds and two CTA-wide transposes
+// (the L1 data pipe bounds K5: ~1740 wavefronts per 4096 rows and column
+// there, ~1330 here).  The gather touches s entries per 1024 rows instead of
+// per 4096 (0.4 adds per row).  Not bitwise equal to the fused K3 partials (a
+// different butterfly tree, same transform): parity is to the oracle.
+//
+// Partial slot b (the same (col, b) slots as K3, finalized by
+// k_sketch_finalize): the rows of 4096-tiles t_first + b + i nvirt; a CTA of
+// 4 warps owns slot b, warp w the sub-tile 4 T4 + w of each of its tiles, so
+// every warp runs the same item sequence and the 4 warps' accumulators are
+// summed in warp order once per column.
+//   load layout  : lane l, register j = b0 + 2 q': idx = 2 l + b0 + 64 q'
+//                  (round 1: idx bits 0, 6..9; one 16-B load per q')
+//   round-2 layout: lane l = b0 + 2 q'', register j2: idx = b0 + 64 q'' + 2 j2
+//                  (idx bits 1..5)
+//   shared slot of idx: idx + 2 (idx >> 6) (both layouts conflict-free)
+// ---------------------------------------------------------------------------
+constexpr int kSwLog = 10;
+constexpr int kSwT = 1 << kSwLog;
+constexpr int kSwWarps = kSkT / kSwT;            // 4 sub-tiles per K3 tile
+constexpr int kSwBuf = kSwT + 2 * (kSwT >> 6);   // padded doubles per warp buffer
+
+__device__ __forceinline__ int sw_addr(int idx) { return idx + 2 * (idx >> 6); }
+
+__device__ __forceinline__ void reg_fwht32(double (&v)[32]) {
+#pragma unroll
+  for (int h = 1; h < 32; h <<= 1) {
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      if ((q & h) == 0) {
+        const double x = v[q], y = v[q + h];
+        v[q] = x + y;
+        v[q + h] = x - y;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ double2 ld128_first(const double* p, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+
+template <int KA>   // sampled rows per lane: s <= 32 KA
+__global__ void __launch_bounds__(kSwWarps * 32, 2) k_sketch_warp(PipeArgs a, int nvirt) {
+  if (a.st->breakdown) return;
+  extern __shared__ __align__(128) double sw_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* buf = sw_smem + warp * kSwBuf;
+  double* red = sw_smem + kSwWarps * kSwBuf;   // [warp][s]
+  const int s = a.s;
+  uint32_t pk[KA];                              // sampled row p = lane + 32 a: (r mod 1024) | (r >> 10) << 10
+#pragma unroll
+  for (int q = 0; q < KA; ++q) {
+    const int p = lane + 32 * q;
+    const int64_t r = p < s ? __ldg(a.rows + p) : 0;
+    pk[q] = (uint32_t)r;
+  }
+  const int64_t n = a.n, rb = a.row_begin;
+  const int64_t t_first = rb >> kSkLogT, t_last = (rb + n - 1) >> kSkLogT;
+  const int ncols = a.col1 - a.col0;
+  const uint64_t pol = policy_evict_first();
+  const bool even = (rb & 1) == 0 && (a.ld & 1) == 0;
+  double x[32];
+  uint32_t ws[16];
+  // item it of slot b: column col0 + it / mine, 4096-tile t_first + b + (it % mine) nvirt
+  auto issue = [&](int64_t b, int64_t mine, int64_t it) {
+    const int col = a.col0 + (int)(it / mine);
+    const int64_t t1 = ((t_first + b + (it % mine) * nvirt) << 2) + warp;   // 1024-row tile
+    const int64_t g0 = t1 << kSwLog, rc0 = g0 - rb;
+    const double* src = a.V + (int64_t)col * a.ld + rc0;
+    const uint32_t* sg = a.signs + (g0 >> 5) + (lane >> 4);
+    if (even && rc0 >= 0 && rc0 + kSwT <= n) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const double2 t = ld128_first(src + 64 * q + 2 * lane, pol);
+        x[2 * q] = t.x;
+        x[2 * q + 1] = t.y;
+        ws[q] = __ldg(sg + 2 * q);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int64_t r0 = rc0 + 64 * q + 2 * lane;
+        const bool in0 = r0 >= 0 && r0 < n, in1 = r0 + 1 >= 0 && r0 + 1 < n;
+        x[2 * q] = in0 ? ld_first(src + 64 * q + 2 * lane, pol) : 0.0;
+        x[2 * q + 1] = in1 ? ld_first(src + 64 * q + 2 * lane + 1, pol) : 0.0;
+        ws[q] = (in0 || in1) ? __ldg(sg + 2 * q) : 0u;
+      }
+    }
+  };
+  const int bs = 2 * (lane & 15);
+  for (int64_t b = blockIdx.x; b < nvirt; b += gridDim.x) {
+    const int64_t mine = t_first + b <= t_last ? (t_last - t_first - b) / nvirt + 1 : 0;
+    if (mine == 0) {   // no tile for this slot: zero partials
+      for (int col = a.col0; col < a.col1; ++col)
+        for (int p = threadIdx.x; p < s; p += blockDim.x) a.part_sk[((int64_t)col * nvirt + b) * s + p] = 0.0;
+      continue;
+    }
+    const int64_t items = mine * ncols;
+    double acc[KA];
+#pragma unroll
+    for (int q = 0; q < KA; ++q) acc[q] = 0.0;
+    issue(b, mine, 0);
+    for (int64_t it = 0; it < items; ++it) {
+      const int64_t ti = it % mine;
+      const int col = a.col0 + (int)(it / mine);
+      const int64_t t1 = ((t_first + b + ti * nvirt) << 2) + warp;
+      double v[32];
+      // D_tt = -1: flip the sign bit; idx = 2 l + b0 + 64 q' is bit 2 (l & 15) + b0 of word ws[q']
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+#pragma unroll
+        for (int b0 = 0; b0 < 2; ++b0) {
+          const uint32_t bit = (ws[q] >> (bs + b0)) & 1u;
+          const double u = x[2 * q + b0];
+          v[2 * q + b0] = __hiloint2double(__double2hiint(u) ^ (int)(bit << 31), __double2loint(u));
+        }
+      }
+      if (it + 1 < items) issue(b, mine, it + 1);   // the next sub-tile's loads overlap this one's FWHT
+      reg_fwht32(v);                                 // idx bits 0, 6, 7, 8, 9
+      __syncwarp();                                  // the previous sub-tile's gather is done
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        *reinterpret_cast<double2*>(buf + 2 * lane + 66 * q) = make_double2(v[2 * q], v[2 * q + 1]);
+      __syncwarp();
+      const int base2 = (lane & 1) + 66 * (lane >> 1);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = buf[base2 + 2 * j];
+      reg_fwht32(v);                                 // idx bits 1..5
+#pragma unroll
+      for (int j = 0; j < 32; ++j) buf[base2 + 2 * j] = v[j];   // the slots this lane read
+      __syncwarp();
+      // gather: term p = (-1)^popcount((r_p >> 10) & t1) * out[r_p mod 1024]
+#pragma unroll
+      for (int q = 0; q < KA; ++q) {
+        if (lane + 32 * q < s) {
+          const double u = buf[sw_addr((int)(pk[q] & (kSwT - 1)))];
+          const uint32_t par = __popc((pk[q] >> kSwLog) & (uint32_t)t1) & 1u;
+          acc[q] += par ? -u : u;
+        }
+      }
+      if (ti == mine - 1) {   // column done: the 4 warps' sums in warp order
+#pragma unroll
+        for (int q = 0; q < KA; ++q) {
+          const int p = lane + 32 * q;
+          if (p < s) red[warp * s + p] = acc[q];
+          acc[q] = 0.0;
+        }
+        __syncthreads();
+        for (int p = threadIdx.x; p < s; p += blockDim.x) {
+          double t = red[p];
+#pragma unroll
+          for (int w = 1; w < kSwWarps; ++w) t += red[w * s + p];
+          a.part_sk[((int64_t)col * nvirt + b) * s + p] = t;
+        }
+        __syncthreads();
+      }
+    }
+  }
+}
+
 static int pipe_stages(int stage_d, bool sketch, size_t* smem) {
   const size_t stage = (size_t)stage_d * sizeof(double);
   const size_t fixed = (sketch ? kSkSmem * sizeof(double) : 0) + 1024;
@@ -1638,7 +1812,25 @@ int launch_sketch_cols(fab_ctx* c, int c0, int c1, cudaStream_t st) {
   a.st = c->st_d;
   const char* re = getenv("FAB_SKETCH_RING");   // the bulk-copy ring version (A/B)
   if (re && re[0] == '1') return launch_stream<false, true, 0>(c, a, st);
-  const char* kv = getenv("FAB_SKETCH_K5");      // "2": k_sketch_groups (A/B); default: k_sketch_direct
+  // default: k_sketch_direct (bitwise the fused K3 partials); A/B: "2":
+  // k_sketch_groups, "3": k_sketch_warp
+  const char* kv = getenv("FAB_SKETCH_K5");
+  const bool k5v = kv && kv[0] == '3' && c->N <= (int64_t(1) << 32);
+  if (k5v) {
+    const int smem = (kSwWarps * kSwBuf + kSwWarps * c->s) * (int)sizeof(double);
+    if (c->s <= 256) {
+      FAB_CUDA(ensure_dyn_smem((const void*)k_sketch_warp<8>, (kSwWarps * kSwBuf + kSwWarps * 256) * 8));
+      k_sketch_warp<8><<<c->grid_upd, kSwWarps * 32, smem, st>>>(a, c->grid_upd);
+    } else if (c->s <= 512) {
+      FAB_CUDA(ensure_dyn_smem((const void*)k_sketch_warp<16>, (kSwWarps * kSwBuf + kSwWarps * 512) * 8));
+      k_sketch_warp<16><<<c->grid_upd, kSwWarps * 32, smem, st>>>(a, c->grid_upd);
+    } else {
+      FAB_CUDA(ensure_dyn_smem((const void*)k_sketch_warp<24>, (kSwWarps * kSwBuf + kSwWarps * 768) * 8));
+      k_sketch_warp<24><<<c->grid_upd, kSwWarps * 32, smem, st>>>(a, c->grid_upd);
+    }
+    FAB_CHECK_LAUNCH();
+    return FAB_OK;
+  }
   if (!(kv && kv[0] == '2')) {
     const int smem = 2 * kSkSmem * (int)sizeof(double);
     FAB_CUDA(ensure_dyn_smem((const void*)k_sketch_direct, smem));

@@ -122,8 +122,8 @@ int sketch_finalize(fab_ctx* c, int ncols, cudaStream_t st) {
 // Blendenpik with its own SRHT Theta' (Blendenpik "computes
 // a random sketch of the basis using, once again, a SRHT"; reading G-12's
 // precond_s / precond_seed): draw Theta' once per (s2, seed2), then K5 over
-// the m columns of V_m with Theta' in place of Theta (the same per-tile
-// algorithm and fixed-order reduction), finalized into dst (s2 x m).  The
+// the m columns of V_m with Theta' in place of Theta (the same kernel and
+// fixed-order reduction), finalized into dst (s2 x m).  The
 // per-CTA partial buffer of the basis sketch is reused (Theta V is already
 // reduced into SV by then).
 int sketch_precond(fab_ctx* c, int s2, uint64_t seed2, int m, double* dst, cudaStream_t st) {
@@ -152,7 +152,8 @@ int sketch_precond(fab_ctx* c, int s2, uint64_t seed2, int m, double* dst, cudaS
 }
 
 // K5: the sketch drawn after the basis -- one batched streaming pass over
-// V_{m_eff+1} with the same per-tile algorithm (identical results).
+// V_{m_eff+1} (k_sketch_bulk: 1024-row FWHTs per warp; the fused K3 sketch
+// uses 4096-row ones -- the same transform, another rounding order).
 int sketch_batched(fab_ctx* c) {
   const int ncols = c->breakdown ? c->m_eff : c->m + 1;
   int rc = launch_sketch_cols(c, 0, ncols, c->stream);

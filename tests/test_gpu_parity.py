@@ -97,8 +97,26 @@ def test_sketch_values_fused_equals_batched():
     SV1, SV2 = s1.get("SV"), s2.get("SV")
     assert np.array_equal(SV1, SV2)                  # same per-tile algorithm, same order
     th = osrht.SRHT(p.n, p.s, p.sketch_seed)
-    ref = th.apply(s1.get("V"))                      # oracle SRHT of the GPU basis
-    assert np.abs(SV1 - ref).max() <= 1e-13 * max(1.0, np.abs(ref).max())
+    for SV, sv in ((SV1, s1), (SV2, s2)):
+        ref = th.apply(sv.get("V"))                  # oracle SRHT of the GPU basis
+        assert np.abs(SV - ref).max() <= 1e-13 * max(1.0, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("kv", ["1", "2", "3"])
+@pytest.mark.parametrize("name,kw", [
+    ("c3", dict(g=24, m=20, k=4, s=40)),     # s <= 256: 8 rows per lane; 3 ragged 1024-row tiles
+    ("c1", dict(g=70, m=24, s=300)),         # s in (256, 512]; n = 4900: ragged last tile
+    ("c5", dict(n=70000, m=12, s=600)),      # s in (512, 768]
+])
+def test_k5_kernels_match_oracle(monkeypatch, kv, name, kw):
+    """K5 (sketch after the basis): k_sketch_direct (default), k_sketch_groups
+    (FAB_SKETCH_K5=2) and k_sketch_warp (=3) against the oracle SRHT of the
+    GPU's own basis (§2.1.1)."""
+    monkeypatch.setenv("FAB_SKETCH_K5", kv)
+    p = fp.make(name, **kw)
+    _, sv = gpu_solve(p, "sketch_solve", fused=False)
+    ref = osrht.SRHT(p.n, p.s, p.sketch_seed).apply(sv.get("V"))
+    assert np.abs(sv.get("SV") - ref).max() <= 1e-13 * max(1.0, np.abs(ref).max())
 
 
 @pytest.mark.parametrize("mode", MODES)
