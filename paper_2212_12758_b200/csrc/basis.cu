@@ -1022,10 +1022,12 @@ __global__ void __launch_bounds__(kSkG * kSkGT, 2) k_sketch_groups(PipeArgs a, i
     const int64_t tile = t_first + b + (it % mine) * nvirt;
     const int64_t g0 = tile << kSkLogT, rc0 = g0 - rb;
     const double* src = a.V + (int64_t)col * a.ld + rc0;
-    const uint32_t* sg = a.signs + (g0 >> 5) + (t >> 3);
+    const int64_t w0 = (g0 >> 5) + (t >> 3);
+    // sign words past the bitmap (N < T) are not read: their rows are padding
 #pragma unroll
-    for (int qh = 0; qh < 16; ++qh) w[qh] = __ldg(sg + (qh << 3));
-    if (rc0 >= 0 && rc0 + kSkT <= n) {
+    for (int qh = 0; qh < 16; ++qh) w[qh] = w0 + (qh << 3) < a.sign_words ? __ldg(a.signs + w0 + (qh << 3)) : 0u;
+    // 256-bit loads need a 32-B aligned tile start (a rank's rows may begin mid-tile)
+    if (rc0 >= 0 && rc0 + kSkT <= n && (reinterpret_cast<uintptr_t>(src) & 31) == 0) {
 #pragma unroll
       for (int qh = 0; qh < 16; ++qh)
         ld256_first(src + (qh << 8) + (t << 2), pol, v[qh], v[qh + 16], v[qh + 32], v[qh + 48]);
@@ -1812,8 +1814,8 @@ int launch_sketch_cols(fab_ctx* c, int c0, int c1, cudaStream_t st) {
   a.st = c->st_d;
   const char* re = getenv("FAB_SKETCH_RING");   // the bulk-copy ring version (A/B)
   if (re && re[0] == '1') return launch_stream<false, true, 0>(c, a, st);
-  // default: k_sketch_direct (bitwise the fused K3 partials); A/B: "2":
-  // k_sketch_groups, "3": k_sketch_warp
+  // default: k_sketch_groups; A/B: "1": k_sketch_direct (both bitwise the
+  // fused K3 partials), "3": k_sketch_warp
   const char* kv = getenv("FAB_SKETCH_K5");
   const bool k5v = kv && kv[0] == '3' && c->N <= (int64_t(1) << 32);
   if (k5v) {
@@ -1831,7 +1833,7 @@ int launch_sketch_cols(fab_ctx* c, int c0, int c1, cudaStream_t st) {
     FAB_CHECK_LAUNCH();
     return FAB_OK;
   }
-  if (!(kv && kv[0] == '2')) {
+  if (kv && kv[0] == '1') {
     const int smem = 2 * kSkSmem * (int)sizeof(double);
     FAB_CUDA(ensure_dyn_smem((const void*)k_sketch_direct, smem));
     k_sketch_direct<<<c->grid_upd, kThreads, smem, st>>>(a);
