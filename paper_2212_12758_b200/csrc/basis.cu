@@ -1175,8 +1175,21 @@ __device__ __forceinline__ double2 ld128_first(const double* p, uint64_t pol) {
   return v;
 }
 
+// Build-time variants for A/B (profiles/build_variant.py):
+// FAB_SW_PF=0 drops the one-item-ahead register prefetch (64 registers),
+// FAB_SW_ACCS=1 keeps the per-lane accumulators in the warp's shared `red` row
+// (32 registers; same summation order), FAB_SW_OCC = resident CTAs per SM.
+#ifndef FAB_SW_PF
+#define FAB_SW_PF 1
+#endif
+#ifndef FAB_SW_ACCS
+#define FAB_SW_ACCS 0
+#endif
+#ifndef FAB_SW_OCC
+#define FAB_SW_OCC 2
+#endif
 template <int KA>   // sampled rows per lane: s <= 32 KA
-__global__ void __launch_bounds__(kSwWarps * 32, 2) k_sketch_warp(PipeArgs a, int nvirt) {
+__global__ void __launch_bounds__(kSwWarps * 32, FAB_SW_OCC) k_sketch_warp(PipeArgs a, int nvirt) {
   if (a.st->breakdown) return;
   extern __shared__ __align__(128) double sw_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1232,12 +1245,21 @@ __global__ void __launch_bounds__(kSwWarps * 32, 2) k_sketch_warp(PipeArgs a, in
       continue;
     }
     const int64_t items = mine * ncols;
+#if FAB_SW_ACCS
+    for (int p = lane; p < s; p += 32) red[warp * s + p] = 0.0;   // this warp's own row
+#else
     double acc[KA];
 #pragma unroll
     for (int q = 0; q < KA; ++q) acc[q] = 0.0;
+#endif
+#if FAB_SW_PF
     issue(b, mine, 0);
+#endif
     for (int64_t it = 0; it < items; ++it) {
       const int64_t ti = it % mine;
+#if !FAB_SW_PF
+      issue(b, mine, it);
+#endif
       const int col = a.col0 + (int)(it / mine);
       const int64_t t1 = ((t_first + b + ti * nvirt) << 2) + warp;
       double v[32];
@@ -1251,7 +1273,9 @@ __global__ void __launch_bounds__(kSwWarps * 32, 2) k_sketch_warp(PipeArgs a, in
           v[2 * q + b0] = __hiloint2double(__double2hiint(u) ^ (int)(bit << 31), __double2loint(u));
         }
       }
+#if FAB_SW_PF
       if (it + 1 < items) issue(b, mine, it + 1);   // the next sub-tile's loads overlap this one's FWHT
+#endif
       reg_fwht32(v);                                 // idx bits 0, 6, 7, 8, 9
       __syncwarp();                                  // the previous sub-tile's gather is done
 #pragma unroll
@@ -1271,16 +1295,22 @@ __global__ void __launch_bounds__(kSwWarps * 32, 2) k_sketch_warp(PipeArgs a, in
         if (lane + 32 * q < s) {
           const double u = buf[sw_addr((int)(pk[q] & (kSwT - 1)))];
           const uint32_t par = __popc((pk[q] >> kSwLog) & (uint32_t)t1) & 1u;
+#if FAB_SW_ACCS
+          red[warp * s + lane + 32 * q] += par ? -u : u;
+#else
           acc[q] += par ? -u : u;
+#endif
         }
       }
       if (ti == mine - 1) {   // column done: the 4 warps' sums in warp order
+#if !FAB_SW_ACCS
 #pragma unroll
         for (int q = 0; q < KA; ++q) {
           const int p = lane + 32 * q;
           if (p < s) red[warp * s + p] = acc[q];
           acc[q] = 0.0;
         }
+#endif
         __syncthreads();
         for (int p = threadIdx.x; p < s; p += blockDim.x) {
           double t = red[p];
@@ -1289,6 +1319,9 @@ __global__ void __launch_bounds__(kSwWarps * 32, 2) k_sketch_warp(PipeArgs a, in
           a.part_sk[((int64_t)col * nvirt + b) * s + p] = t;
         }
         __syncthreads();
+#if FAB_SW_ACCS
+        for (int p = lane; p < s; p += 32) red[warp * s + p] = 0.0;
+#endif
       }
     }
   }
