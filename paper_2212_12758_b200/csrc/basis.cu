@@ -1188,6 +1188,9 @@ __device__ __forceinline__ double2 ld128_first(const double* p, uint64_t pol) {
 #ifndef FAB_SW_OCC
 #define FAB_SW_OCC 2
 #endif
+#ifndef FAB_SW_TIMING   // 0 = the product kernel; 1, 2 = timing-only diagnostics (see the kernel body)
+#define FAB_SW_TIMING 0
+#endif
 template <int KA>   // sampled rows per lane: s <= 32 KA
 __global__ void __launch_bounds__(kSwWarps * 32, FAB_SW_OCC) k_sketch_warp(PipeArgs a, int nvirt) {
   if (a.st->breakdown) return;
@@ -1276,7 +1279,19 @@ __global__ void __launch_bounds__(kSwWarps * 32, FAB_SW_OCC) k_sketch_warp(PipeA
 #if FAB_SW_PF
       if (it + 1 < items) issue(b, mine, it + 1);   // the next sub-tile's loads overlap this one's FWHT
 #endif
+#if FAB_SW_TIMING == 2   // timing-only diagnostic (wrong values): loads + gather, no transform, no exchange
+      {
+        double t = v[0];
+#pragma unroll
+        for (int j = 1; j < 32; ++j) t += v[j];
+        __syncwarp();
+        buf[sw_addr(lane)] = t;
+        __syncwarp();
+      }
+#else
+#if FAB_SW_TIMING != 1     // 1: timing-only diagnostic (wrong values): the exchange without the butterflies
       reg_fwht32(v);                                 // idx bits 0, 6, 7, 8, 9
+#endif
       __syncwarp();                                  // the previous sub-tile's gather is done
 #pragma unroll
       for (int q = 0; q < 16; ++q)
@@ -1285,10 +1300,13 @@ __global__ void __launch_bounds__(kSwWarps * 32, FAB_SW_OCC) k_sketch_warp(PipeA
       const int base2 = (lane & 1) + 66 * (lane >> 1);
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = buf[base2 + 2 * j];
+#if FAB_SW_TIMING != 1
       reg_fwht32(v);                                 // idx bits 1..5
+#endif
 #pragma unroll
       for (int j = 0; j < 32; ++j) buf[base2 + 2 * j] = v[j];   // the slots this lane read
       __syncwarp();
+#endif
       // gather: term p = (-1)^popcount((r_p >> 10) & t1) * out[r_p mod 1024]
 #pragma unroll
       for (int q = 0; q < KA; ++q) {
