@@ -1188,6 +1188,9 @@ __device__ __forceinline__ double2 ld128_first(const double* p, uint64_t pol) {
 #ifndef FAB_SW_OCC
 #define FAB_SW_OCC 2
 #endif
+#ifndef FAB_SW_WSLATE   // 1: the sign words are loaded when used (L1 hits) instead of with the prefetch (16 registers)
+#define FAB_SW_WSLATE 0
+#endif
 #ifndef FAB_SW_TIMING   // 0 = the product kernel; 1, 2 = timing-only diagnostics (see the kernel body)
 #define FAB_SW_TIMING 0
 #endif
@@ -1226,7 +1229,9 @@ __global__ void __launch_bounds__(kSwWarps * 32, FAB_SW_OCC) k_sketch_warp(PipeA
         const double2 t = ld128_first(src + 64 * q + 2 * lane, pol);
         x[2 * q] = t.x;
         x[2 * q + 1] = t.y;
+#if !FAB_SW_WSLATE
         ws[q] = __ldg(sg + 2 * q);
+#endif
       }
     } else {
 #pragma unroll
@@ -1235,7 +1240,9 @@ __global__ void __launch_bounds__(kSwWarps * 32, FAB_SW_OCC) k_sketch_warp(PipeA
         const bool in0 = r0 >= 0 && r0 < n, in1 = r0 + 1 >= 0 && r0 + 1 < n;
         x[2 * q] = in0 ? ld_first(src + 64 * q + 2 * lane, pol) : 0.0;
         x[2 * q + 1] = in1 ? ld_first(src + 64 * q + 2 * lane + 1, pol) : 0.0;
+#if !FAB_SW_WSLATE
         ws[q] = (in0 || in1) ? __ldg(sg + 2 * q) : 0u;
+#endif
       }
     }
   };
@@ -1267,11 +1274,21 @@ __global__ void __launch_bounds__(kSwWarps * 32, FAB_SW_OCC) k_sketch_warp(PipeA
       const int64_t t1 = ((t_first + b + ti * nvirt) << 2) + warp;
       double v[32];
       // D_tt = -1: flip the sign bit; idx = 2 l + b0 + 64 q' is bit 2 (l & 15) + b0 of word ws[q']
+#if FAB_SW_WSLATE
+      const int64_t rc0c = (t1 << kSwLog) - rb;
+      const uint32_t* sgc = a.signs + ((t1 << kSwLog) >> 5) + (lane >> 4);
+#endif
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
+#if FAB_SW_WSLATE
+        const int64_t r0c = rc0c + 64 * q + 2 * lane;
+        const uint32_t wsq = (r0c + 1 >= 0 && r0c < n) ? __ldg(sgc + 2 * q) : 0u;
+#else
+        const uint32_t wsq = ws[q];
+#endif
 #pragma unroll
         for (int b0 = 0; b0 < 2; ++b0) {
-          const uint32_t bit = (ws[q] >> (bs + b0)) & 1u;
+          const uint32_t bit = (wsq >> (bs + b0)) & 1u;
           const double u = x[2 * q + b0];
           v[2 * q + b0] = __hiloint2double(__double2hiint(u) ^ (int)(bit << 31), __double2loint(u));
         }
